@@ -1,0 +1,174 @@
+/*
+ * sgsf.h -- C ABI of the B200-native Swarm-Gen safety filter (libsgsf.so).
+ *
+ * Plain pointers and sizes only; no torch types.  Every entry point that
+ * touches the GPU is stream-ordered on the caller's `cudaStream_t` (passed as
+ * `void*`, NULL = legacy default stream).  Device buffers are caller-owned.
+ *
+ * Reference interfaces replaced (paths relative to /root/reference/pkg/src/swarmfilter):
+ *   sgsf_create / sgsf_destroy   SafetyFilter.__init__ + KktFactorization cache   solver.py:232-249,
+ *                                assembly.py:154-184, 325-339 (one handle per (problem, degree, rho))
+ *   sgsf_solve                   SafetyFilter.batch_solve -> solve (the AM loop)  solver.py:286-407
+ *   sgsf_solve_host              same, host buffers in/out (the reference's numpy-in / numpy-out call)
+ *   sgsf_verdict                 metrics.feasible_results -> check_original_constraints
+ *                                metrics.py:57-69, assembly.py:437-487
+ *   sgsf_trajectory              basis.coeffs_to_trajectory                        basis.py:149-160
+ *   sgsf_svars                   SolveResult.svars (last spherical step)           solver.py:142-174, 358
+ *   sgsf_spherical_project       kernels.spherical_project (backend contract)      kernels/__init__.py:46-50,
+ *                                                                                  _speedups.pyx:18-73
+ *   sgsf_apply_F / sgsf_apply_FT PairwiseOperator.apply / apply_transpose          assembly.py:285-310
+ *   sgsf_kkt_step                KktFactorization.solve                            assembly.py:186-219
+ */
+#ifndef SGSF_H
+#define SGSF_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* whole-call status codes */
+#define SGSF_OK              0
+#define SGSF_ERR_INVALID     1   /* bad argument / shape            -> DimensionMismatch / ValueError */
+#define SGSF_ERR_CUDA        2   /* CUDA runtime error              -> RuntimeError */
+#define SGSF_ERR_UNSUPPORTED 3   /* size outside what this build handles (e.g. n > max robots) */
+#define SGSF_ERR_SINGULAR    4   /* KKT precompute failed           -> SingularKKT */
+
+/* per-sample status written to outputs.status[b] */
+#define SGSF_SAMPLE_OK           0
+#define SGSF_SAMPLE_SINGULAR_KKT 1   /* endpoint residual above tol_eq (assembly.py:213-217) */
+
+/* term precision of the iteration (state and xi-step are always FP64) */
+#define SGSF_PRECISION_LEAN   0  /* FP32 pair/workspace terms, positions, W^T projection */
+#define SGSF_PRECISION_STRICT 1  /* FP64 everywhere */
+
+typedef struct sgsf_handle_s sgsf_handle_t;
+
+/* FP64 host constants for one (problem, degree, rho); see precompute.py. Row-major. */
+typedef struct {
+    int n;            /* robots */
+    int samples;      /* S = H + 1 */
+    int m1;           /* degree + 1 */
+    double rho;
+    double lat, vert;           /* robot safety spheroid semiaxes a, b */
+    double ws_lat, ws_vert;     /* workspace semiaxes a_w, b_w */
+    double center[3];           /* workspace centre */
+    const double* W;            /* S x m1   value basis */
+    const double* Wd;           /* S x m1   velocity basis */
+    const double* Wdd;          /* S x m1   acceleration basis */
+    const double* B;            /* 6 x m1   endpoint rows (p0 v0 a0 pT vT aT) */
+    const double* rhs;          /* 3 x n x 6 */
+    const double* PBt;          /* m1 x 6   B^T (B B^T)^-1 */
+    const double* Km11;         /* m1 x m1  mean-KKT inverse, top-left */
+    const double* Kd11;         /* m1 x m1  deviation-KKT inverse, top-left */
+    const double* Mm;           /* m1 x m1  rho Km11 G */
+    const double* Md;           /* m1 x m1  rho (n+1) Kd11 G */
+    const double* cconst;       /* 3 x n x m1 */
+} sgsf_problem_t;
+
+typedef struct {
+    int max_iters;
+    double tol_residual;
+    double tol_eq;
+    int early_stop;
+    int precision;        /* SGSF_PRECISION_* */
+    int want_prev;        /* also write coefficients of iteration K-1 (for svars) */
+    int slots_per_block;  /* 0 = auto (smem/thread budget) */
+    int grid;             /* 0 = auto (persistent: #SM x CTAs/SM) */
+} sgsf_config_t;
+
+/* Per-sample outputs, device pointers, caller-owned. dim = 3 n m1. */
+typedef struct {
+    double* coeffs;         /* B x dim */
+    double* multipliers;    /* B x dim */
+    double* res_inf;        /* B x max_iters (entries >= iterations untouched) */
+    double* res_l2;         /* B x max_iters */
+    int32_t* iterations;    /* B */
+    uint8_t* converged;     /* B */
+    double* displacement;   /* B: ||coeffs - xi_bar||_2 */
+    int32_t* status;        /* B: SGSF_SAMPLE_* */
+    double* eq_err;         /* B: ||A xi - b||_inf of the returned iterate */
+    double* coeffs_prev;    /* B x dim, nullable (needs cfg.want_prev) */
+} sgsf_outputs_t;
+
+/* Verdict outputs (check_original_constraints at tol), device pointers. */
+typedef struct {
+    uint8_t* ok;              /* B: no violation */
+    uint8_t* feasible;        /* B: ok && converged[b] (converged may be NULL -> ok) */
+    double* pair_margin_min;  /* B (+inf when n == 1) */
+    double* ws_margin_max;    /* B */
+    int32_t* pair_viol;       /* B */
+    int32_t* ws_viol;         /* B */
+} sgsf_verdict_t;
+
+typedef struct {
+    void* start;   /* cudaEvent_t recorded just before the main solve kernel (nullable) */
+    void* stop;    /* cudaEvent_t recorded just after it */
+} sgsf_timing_t;
+
+const char* sgsf_version(void);
+const char* sgsf_last_error(void);
+/* number of kernels this library has launched since load (evidence for bench.py gpu_launches) */
+uint64_t sgsf_launch_count(void);
+/* largest n this build solves */
+int sgsf_max_robots(void);
+
+int sgsf_create(const sgsf_problem_t* problem, sgsf_handle_t** out);
+void sgsf_destroy(sgsf_handle_t* h);
+
+/* bytes of device workspace sgsf_solve needs (sample queue) */
+size_t sgsf_workspace_bytes(void);
+
+/*
+ * Run the safety filter on a batch.  xi_bar: B x dim (device).  init_mode: B bytes or NULL
+ * (0 = boundary projection of xi_bar with zero multipliers, 1 = warm start from xi0/lam0 rows).
+ */
+int sgsf_solve(sgsf_handle_t* h, int batch, const double* xi_bar, const double* xi0,
+               const double* lam0, const uint8_t* init_mode, const sgsf_config_t* cfg,
+               sgsf_outputs_t* out, void* workspace, const sgsf_timing_t* timing, void* stream);
+
+/* Same with HOST buffers (pageable or pinned): copies in, solves, verdicts, copies out, syncs. */
+int sgsf_solve_host(sgsf_handle_t* h, int batch, const double* xi_bar, const double* xi0,
+                    const double* lam0, const uint8_t* init_mode, const sgsf_config_t* cfg,
+                    double* coeffs, double* multipliers, double* res_inf, double* res_l2,
+                    int32_t* iterations, uint8_t* converged, uint8_t* feasible,
+                    double* displacement, int32_t* status, void* stream);
+
+int sgsf_verdict(sgsf_handle_t* h, int batch, const double* coeffs, const uint8_t* converged,
+                 double tol, sgsf_verdict_t* out, void* stream);
+
+/* pos/vel/acc: B x n x S x 3 (device); any may be NULL */
+int sgsf_trajectory(sgsf_handle_t* h, int batch, const double* coeffs, double* pos, double* vel,
+                    double* acc, void* stream);
+
+/* spherical variables of positions C W^T: pair_* B x P x S, ws_* B x n x S (device) */
+int sgsf_svars(sgsf_handle_t* h, int batch, const double* coeffs, double* pair_az, double* pair_pol,
+               double* pair_rad, double* ws_az, double* ws_pol, double* ws_rad, void* stream);
+
+/*
+ * Unit entry point for the spherical block update (kernels contract).  mode:
+ *   0 = the solver's lean path (FP32 trig-free target, FP64 trig fallback on zero components)
+ *   1 = the solver's strict path (FP64 trig-free target + fallback)
+ *   2 = reference trig formula in FP64
+ * Angles/radial always come from the FP64 reference formula.  Any output may be NULL.
+ */
+int sgsf_spherical_project(int count, const double* dx, const double* dy, const double* dz,
+                           double lat, double vert, double lo, double hi, int mode,
+                           double* az, double* pol, double* rad, double* tx, double* ty, double* tz,
+                           void* stream);
+
+/* FP64 operator applications for the step API (tests / step functions). */
+int sgsf_apply_F(sgsf_handle_t* h, int batch, const double* xi, double* out, void* stream);
+int sgsf_apply_FT(sgsf_handle_t* h, int batch, const double* v, double* out, void* stream);
+/* literal coefficient step from eta (3 x n x m1 per sample): C_i = Km11 eta_bar + Kd11 (eta_i - eta_bar) + cconst_i */
+int sgsf_kkt_step(sgsf_handle_t* h, int batch, const double* eta, double* out, double* eq_err, void* stream);
+
+/* FP32 FFMA throughput microbenchmark (roofline denominator); returns TFLOP/s in *tflops */
+int sgsf_fp32_peak(double* tflops, double* ms, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SGSF_H */

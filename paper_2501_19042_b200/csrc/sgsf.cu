@@ -1,0 +1,455 @@
+// sgsf.cu -- C ABI (include/sgsf.h) over the sm_100a kernels.
+//
+// One handle per (problem, degree, rho): it owns only immutable device
+// constants, like the reference's rho-keyed KKT cache (assembly.py:325-339),
+// so it is safe to share across threads and streams.  Every launch is
+// stream-ordered on the caller's stream; nothing here synchronises except
+// sgsf_solve_host (host buffers in/out) and sgsf_fp32_peak.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/sgsf.h"
+#include "sf_aux.cuh"
+#include "sf_device.cuh"
+#include "sf_persistent.cuh"
+
+using namespace sgsf;
+
+namespace {
+
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_launches{0};
+
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                      \
+    do {                                                                                    \
+        cudaError_t _e = (expr);                                                            \
+        if (_e != cudaSuccess)                                                              \
+            return fail(SGSF_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
+constexpr int kMaxRobots = 16;
+
+}  // namespace
+
+struct sgsf_handle_s {
+    int n, S, m1, P;
+    double rho, lat, vert, ws_lat, ws_vert, center[3];
+    double *W, *Wd, *Wdd, *KMm, *KMd, *Km11, *Kd11, *cconst, *B6, *rhs, *PBt;
+    int device, sm_count;
+};
+
+static AuxParams aux_params(const sgsf_handle_t* h) {
+    AuxParams a;
+    a.n = h->n;
+    a.S = h->S;
+    a.m1 = h->m1;
+    a.P = h->P;
+    a.lat = h->lat;
+    a.vert = h->vert;
+    a.ws_lat = h->ws_lat;
+    a.ws_vert = h->ws_vert;
+    a.cx = h->center[0];
+    a.cy = h->center[1];
+    a.cz = h->center[2];
+    a.W = h->W;
+    a.Wd = h->Wd;
+    a.Wdd = h->Wdd;
+    a.Km11 = h->Km11;
+    a.Kd11 = h->Kd11;
+    a.cconst = h->cconst;
+    a.B6 = h->B6;
+    a.rhs = h->rhs;
+    return a;
+}
+
+extern "C" {
+
+const char* sgsf_version(void) { return "sgsf 0.1 (sm_100a)"; }
+const char* sgsf_last_error(void) { return g_last_error.c_str(); }
+uint64_t sgsf_launch_count(void) { return g_launches.load(); }
+int sgsf_max_robots(void) { return kMaxRobots; }
+size_t sgsf_workspace_bytes(void) { return 256; }
+
+static int upload(double** dst, const double* src, size_t count) {
+    if (!src) return fail(SGSF_ERR_INVALID, "null constant pointer");
+    CUDA_TRY(cudaMalloc(dst, count * sizeof(double)));
+    CUDA_TRY(cudaMemcpy(*dst, src, count * sizeof(double), cudaMemcpyHostToDevice));
+    return SGSF_OK;
+}
+
+void sgsf_destroy(sgsf_handle_t* h) {
+    if (!h) return;
+    double* ptrs[] = {h->W, h->Wd, h->Wdd, h->KMm, h->KMd, h->Km11, h->Kd11, h->cconst, h->B6, h->rhs, h->PBt};
+    for (double* q : ptrs)
+        if (q) cudaFree(q);
+    delete h;
+}
+
+int sgsf_create(const sgsf_problem_t* pr, sgsf_handle_t** out) {
+    if (!pr || !out) return fail(SGSF_ERR_INVALID, "null argument");
+    if (pr->n < 1 || pr->samples < 2 || pr->m1 < 2)
+        return fail(SGSF_ERR_INVALID, "need n >= 1, samples >= 2, m1 >= 2");
+    if (pr->m1 > KMAX) return fail(SGSF_ERR_UNSUPPORTED, "degree + 1 above 16 is not supported");
+    sgsf_handle_t* h = new sgsf_handle_t();
+    std::memset(h, 0, sizeof(*h));
+    h->n = pr->n;
+    h->S = pr->samples;
+    h->m1 = pr->m1;
+    h->P = pr->n * (pr->n - 1) / 2;
+    h->rho = pr->rho;
+    h->lat = pr->lat;
+    h->vert = pr->vert;
+    h->ws_lat = pr->ws_lat;
+    h->ws_vert = pr->ws_vert;
+    for (int i = 0; i < 3; ++i) h->center[i] = pr->center[i];
+    const int m1 = pr->m1, n = pr->n, S = pr->samples;
+    std::vector<double> kmm(m1 * 2 * m1), kmd(m1 * 2 * m1);
+    for (int q = 0; q < m1; ++q)
+        for (int q2 = 0; q2 < m1; ++q2) {
+            kmm[q * 2 * m1 + q2] = pr->Mm[q * m1 + q2];
+            kmm[q * 2 * m1 + m1 + q2] = pr->Km11[q * m1 + q2];
+            kmd[q * 2 * m1 + q2] = pr->Md[q * m1 + q2];
+            kmd[q * 2 * m1 + m1 + q2] = pr->Kd11[q * m1 + q2];
+        }
+    int rc = SGSF_OK;
+    if ((rc = upload(&h->W, pr->W, (size_t)S * m1)) || (rc = upload(&h->Wd, pr->Wd, (size_t)S * m1)) ||
+        (rc = upload(&h->Wdd, pr->Wdd, (size_t)S * m1)) || (rc = upload(&h->KMm, kmm.data(), kmm.size())) ||
+        (rc = upload(&h->KMd, kmd.data(), kmd.size())) || (rc = upload(&h->Km11, pr->Km11, (size_t)m1 * m1)) ||
+        (rc = upload(&h->Kd11, pr->Kd11, (size_t)m1 * m1)) ||
+        (rc = upload(&h->cconst, pr->cconst, (size_t)3 * n * m1)) || (rc = upload(&h->B6, pr->B, (size_t)6 * m1)) ||
+        (rc = upload(&h->rhs, pr->rhs, (size_t)3 * n * 6)) || (rc = upload(&h->PBt, pr->PBt, (size_t)m1 * 6))) {
+        sgsf_destroy(h);
+        return rc;
+    }
+    cudaGetDevice(&h->device);
+    cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, h->device);
+    *out = h;
+    return SGSF_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- launch plumbing for K1
+namespace {
+
+template <typename T, int NB, int MAXT>
+int launch_persistent(const sgsf_handle_t* h, SolveParams& p, const sgsf_config_t* cfg,
+                      const sgsf_timing_t* timing, cudaStream_t stream) {
+    auto kern = sf_persistent_kernel<T, NB, MAXT>;
+    int dev_smem = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
+    // slots per CTA: as many as smem and the thread budget allow (a CTA runs one slot per S threads)
+    int spb = cfg->slots_per_block;
+    if (spb <= 0) {
+        spb = 0;
+        for (int s = 1; s * h->S <= MAXT; ++s) {
+            SmemLayout L = make_layout<T, NB>(h->n, h->S, h->m1, p.MP, s, p.want_prev);
+            if (L.total > (size_t)dev_smem) break;
+            spb = s;
+        }
+        // small batches: spread samples over SMs instead of packing them into few CTAs
+        const int spread = (p.batch + h->sm_count - 1) / h->sm_count;
+        if (spb > spread) spb = spread > 0 ? spread : 1;
+    }
+    if (spb <= 0) return fail(SGSF_ERR_UNSUPPORTED, "problem too large for one CTA (samples or smem)");
+    int threads = ((spb * h->S + 31) / 32) * 32;
+    if (threads < 64) threads = 64;
+    if (threads > MAXT) return fail(SGSF_ERR_UNSUPPORTED, "slots_per_block * samples exceeds the CTA size");
+    p.spb = spb;
+    SmemLayout L = make_layout<T, NB>(h->n, h->S, h->m1, p.MP, spb, p.want_prev);
+    if (L.total > (size_t)dev_smem) return fail(SGSF_ERR_UNSUPPORTED, "shared memory budget exceeded");
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
+    int per_sm = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, L.total));
+    if (per_sm < 1) per_sm = 1;
+    int grid = cfg->grid > 0 ? cfg->grid : h->sm_count * per_sm;
+    const int need = (p.batch + spb - 1) / spb;
+    if (grid > need) grid = need;
+    if (timing && timing->start) CUDA_TRY(cudaEventRecord((cudaEvent_t)timing->start, stream));
+    kern<<<grid, threads, L.total, stream>>>(p);
+    g_launches.fetch_add(1);
+    CUDA_TRY(cudaGetLastError());
+    if (timing && timing->stop) CUDA_TRY(cudaEventRecord((cudaEvent_t)timing->stop, stream));
+    return SGSF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sgsf_solve(sgsf_handle_t* h, int batch, const double* xi_bar, const double* xi0, const double* lam0,
+               const uint8_t* init_mode, const sgsf_config_t* cfg, sgsf_outputs_t* out, void* workspace,
+               const sgsf_timing_t* timing, void* stream_) {
+    if (!h || !cfg || !out || !workspace) return fail(SGSF_ERR_INVALID, "null argument");
+    if (batch < 0) return fail(SGSF_ERR_INVALID, "negative batch");
+    if (cfg->max_iters < 1) return fail(SGSF_ERR_INVALID, "max_iters must be >= 1");
+    if (!(cfg->tol_residual > 0) || !(cfg->tol_eq > 0)) return fail(SGSF_ERR_INVALID, "tolerances must be positive");
+    if (batch == 0) return SGSF_OK;
+    if (!xi_bar || !out->coeffs || !out->multipliers || !out->res_inf || !out->res_l2 || !out->iterations ||
+        !out->converged || !out->displacement || !out->status || !out->eq_err)
+        return fail(SGSF_ERR_INVALID, "null input/output buffer");
+    if (init_mode && (!xi0 || !lam0)) return fail(SGSF_ERR_INVALID, "init_mode given without xi0/lam0");
+    if (cfg->want_prev && !out->coeffs_prev) return fail(SGSF_ERR_INVALID, "want_prev needs coeffs_prev");
+    if (h->n > kMaxRobots) return fail(SGSF_ERR_UNSUPPORTED, "n above sgsf_max_robots() is not supported yet");
+    cudaStream_t stream = (cudaStream_t)stream_;
+
+    SolveParams p;
+    std::memset(&p, 0, sizeof(p));
+    p.n = h->n;
+    p.S = h->S;
+    p.m1 = h->m1;
+    p.MP = (h->m1 + 3) & ~3;
+    p.batch = batch;
+    p.max_iters = cfg->max_iters;
+    p.early_stop = cfg->early_stop ? 1 : 0;
+    p.want_prev = cfg->want_prev ? 1 : 0;
+    p.rho = h->rho;
+    p.tol_res = cfg->tol_residual;
+    p.tol_eq = cfg->tol_eq;
+    p.lat = h->lat;
+    p.vert = h->vert;
+    p.ws_lat = h->ws_lat;
+    p.ws_vert = h->ws_vert;
+    p.cx = h->center[0];
+    p.cy = h->center[1];
+    p.cz = h->center[2];
+    p.W = h->W;
+    p.KMm = h->KMm;
+    p.KMd = h->KMd;
+    p.cconst = h->cconst;
+    p.B6 = h->B6;
+    p.rhs = h->rhs;
+    p.PBt = h->PBt;
+    p.xi_bar = xi_bar;
+    p.xi0 = xi0;
+    p.lam0 = lam0;
+    p.init_mode = init_mode;
+    p.coeffs = out->coeffs;
+    p.mult = out->multipliers;
+    p.res_inf = out->res_inf;
+    p.res_l2 = out->res_l2;
+    p.iterations = out->iterations;
+    p.converged = out->converged;
+    p.displacement = out->displacement;
+    p.status = out->status;
+    p.eq_err = out->eq_err;
+    p.coeffs_prev = out->coeffs_prev;
+    p.queue = (int*)workspace;
+    CUDA_TRY(cudaMemsetAsync(workspace, 0, sizeof(int), stream));
+
+    const bool strict = cfg->precision == SGSF_PRECISION_STRICT;
+    const int n = h->n;
+    if (!strict) {
+        if (n <= 4) return launch_persistent<float, 4, 512>(h, p, cfg, timing, stream);
+        if (n <= 8) return launch_persistent<float, 8, 384>(h, p, cfg, timing, stream);
+        return launch_persistent<float, 16, 320>(h, p, cfg, timing, stream);
+    }
+    if (n <= 4) return launch_persistent<double, 4, 384>(h, p, cfg, timing, stream);
+    if (n <= 8) return launch_persistent<double, 8, 256>(h, p, cfg, timing, stream);
+    return launch_persistent<double, 16, 256>(h, p, cfg, timing, stream);
+}
+
+int sgsf_verdict(sgsf_handle_t* h, int batch, const double* coeffs, const uint8_t* converged, double tol,
+                 sgsf_verdict_t* out, void* stream) {
+    if (!h || !out || (batch > 0 && !coeffs)) return fail(SGSF_ERR_INVALID, "null argument");
+    if (batch == 0) return SGSF_OK;
+    const int threads = 256;
+    const size_t smem = (size_t)(3 * h->n * h->m1 + 3 * h->n * h->S) * sizeof(double) +
+                        threads * (2 * sizeof(double) + 2 * sizeof(int));
+    CUDA_TRY(cudaFuncSetAttribute(verdict_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    verdict_kernel<<<batch, threads, smem, (cudaStream_t)stream>>>(aux_params(h), batch, coeffs, converged, tol,
+                                                                    out->ok, out->feasible, out->pair_margin_min,
+                                                                    out->ws_margin_max, out->pair_viol,
+                                                                    out->ws_viol);
+    g_launches.fetch_add(1);
+    CUDA_TRY(cudaGetLastError());
+    return SGSF_OK;
+}
+
+int sgsf_trajectory(sgsf_handle_t* h, int batch, const double* coeffs, double* pos, double* vel, double* acc,
+                    void* stream) {
+    if (!h || (batch > 0 && !coeffs)) return fail(SGSF_ERR_INVALID, "null argument");
+    if (batch == 0) return SGSF_OK;
+    const size_t total = (size_t)batch * h->n * h->S;
+    int blocks = (int)((total + 255) / 256);
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    trajectory_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(aux_params(h), batch, coeffs, pos, vel, acc);
+    g_launches.fetch_add(1);
+    CUDA_TRY(cudaGetLastError());
+    return SGSF_OK;
+}
+
+int sgsf_svars(sgsf_handle_t* h, int batch, const double* coeffs, double* paz, double* ppol, double* prad,
+               double* waz, double* wpol, double* wrad, void* stream) {
+    if (!h || (batch > 0 && (!coeffs || !waz || !wpol || !wrad))) return fail(SGSF_ERR_INVALID, "null argument");
+    if (h->P > 0 && batch > 0 && (!paz || !ppol || !prad)) return fail(SGSF_ERR_INVALID, "null pair output");
+    if (batch == 0) return SGSF_OK;
+    const size_t smem = (size_t)(3 * h->n * h->m1 + 3 * h->n * h->S) * sizeof(double);
+    CUDA_TRY(cudaFuncSetAttribute(svars_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    svars_kernel<<<batch, 256, smem, (cudaStream_t)stream>>>(aux_params(h), batch, coeffs, paz, ppol, prad, waz,
+                                                              wpol, wrad);
+    g_launches.fetch_add(1);
+    CUDA_TRY(cudaGetLastError());
+    return SGSF_OK;
+}
+
+int sgsf_spherical_project(int count, const double* dx, const double* dy, const double* dz, double lat,
+                           double vert, double lo, double hi, int mode, double* az, double* pol, double* rad,
+                           double* tx, double* ty, double* tz, void* stream) {
+    if (count < 0) return fail(SGSF_ERR_INVALID, "negative count");
+    if (count == 0) return SGSF_OK;
+    if (!dx || !dy || !dz) return fail(SGSF_ERR_INVALID, "null input");
+    if (mode < 0 || mode > 2) return fail(SGSF_ERR_INVALID, "mode must be 0, 1 or 2");
+    int blocks = (count + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    spherical_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(count, dx, dy, dz, lat, vert, lo, hi, mode, az, pol,
+                                                                rad, tx, ty, tz);
+    g_launches.fetch_add(1);
+    CUDA_TRY(cudaGetLastError());
+    return SGSF_OK;
+}
+
+int sgsf_apply_F(sgsf_handle_t* h, int batch, const double* xi, double* out, void* stream) {
+    if (!h || (batch > 0 && (!xi || !out))) return fail(SGSF_ERR_INVALID, "null argument");
+    if (batch == 0) return SGSF_OK;
+    const size_t total = (size_t)batch * 3 * (h->P + h->n) * h->S;
+    int blocks = (int)((total + 255) / 256);
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    apply_F_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(aux_params(h), batch, xi, out);
+    g_launches.fetch_add(1);
+    CUDA_TRY(cudaGetLastError());
+    return SGSF_OK;
+}
+
+int sgsf_apply_FT(sgsf_handle_t* h, int batch, const double* v, double* out, void* stream) {
+    if (!h || (batch > 0 && (!v || !out))) return fail(SGSF_ERR_INVALID, "null argument");
+    if (batch == 0) return SGSF_OK;
+    const size_t smem = (size_t)3 * h->n * h->S * sizeof(double);
+    CUDA_TRY(cudaFuncSetAttribute(apply_FT_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    apply_FT_kernel<<<batch, 256, smem, (cudaStream_t)stream>>>(aux_params(h), batch, v, out);
+    g_launches.fetch_add(1);
+    CUDA_TRY(cudaGetLastError());
+    return SGSF_OK;
+}
+
+int sgsf_kkt_step(sgsf_handle_t* h, int batch, const double* eta, double* out, double* eq_err, void* stream) {
+    if (!h || (batch > 0 && (!eta || !out))) return fail(SGSF_ERR_INVALID, "null argument");
+    if (batch == 0) return SGSF_OK;
+    if (h->m1 > KMAX_AUX) return fail(SGSF_ERR_UNSUPPORTED, "degree too large");
+    const size_t smem = (size_t)(3 * h->m1 + 3 * h->n) * sizeof(double);
+    kkt_step_kernel<<<batch, 128, smem, (cudaStream_t)stream>>>(aux_params(h), batch, eta, out, eq_err);
+    g_launches.fetch_add(1);
+    CUDA_TRY(cudaGetLastError());
+    return SGSF_OK;
+}
+
+int sgsf_solve_host(sgsf_handle_t* h, int batch, const double* xi_bar, const double* xi0, const double* lam0,
+                    const uint8_t* init_mode, const sgsf_config_t* cfg, double* coeffs, double* multipliers,
+                    double* res_inf, double* res_l2, int32_t* iterations, uint8_t* converged, uint8_t* feasible,
+                    double* displacement, int32_t* status, void* stream_) {
+    if (!h || !cfg) return fail(SGSF_ERR_INVALID, "null argument");
+    if (batch <= 0) return batch == 0 ? SGSF_OK : fail(SGSF_ERR_INVALID, "negative batch");
+    cudaStream_t stream = (cudaStream_t)stream_;
+    const size_t dim = (size_t)3 * h->n * h->m1, B = (size_t)batch, MI = (size_t)cfg->max_iters;
+    // one device arena for inputs + outputs
+    const size_t doubles = B * dim * (3 + (init_mode ? 2 : 0)) + 2 * B * MI + 2 * B;
+    const size_t bytes = doubles * sizeof(double) + B * (4 + 4 + 1 + 1 + 1) + 512;
+    char* arena = nullptr;
+    CUDA_TRY(cudaMallocAsync((void**)&arena, bytes, stream));
+    size_t off = 0;
+    auto take = [&](size_t nbytes) {
+        char* q = arena + off;
+        off += (nbytes + 255) & ~size_t(255);
+        return (void*)q;
+    };
+    double* d_xb = (double*)take(B * dim * 8);
+    double* d_x0 = init_mode ? (double*)take(B * dim * 8) : nullptr;
+    double* d_l0 = init_mode ? (double*)take(B * dim * 8) : nullptr;
+    uint8_t* d_mode = init_mode ? (uint8_t*)take(B) : nullptr;
+    sgsf_outputs_t o;
+    std::memset(&o, 0, sizeof(o));
+    o.coeffs = (double*)take(B * dim * 8);
+    o.multipliers = (double*)take(B * dim * 8);
+    o.res_inf = (double*)take(B * MI * 8);
+    o.res_l2 = (double*)take(B * MI * 8);
+    o.iterations = (int32_t*)take(B * 4);
+    o.converged = (uint8_t*)take(B);
+    o.displacement = (double*)take(B * 8);
+    o.status = (int32_t*)take(B * 4);
+    o.eq_err = (double*)take(B * 8);
+    uint8_t* d_feas = (uint8_t*)take(B);
+    void* ws = take(sgsf_workspace_bytes());
+    (void)bytes;
+    CUDA_TRY(cudaMemcpyAsync(d_xb, xi_bar, B * dim * 8, cudaMemcpyHostToDevice, stream));
+    if (init_mode) {
+        CUDA_TRY(cudaMemcpyAsync(d_x0, xi0, B * dim * 8, cudaMemcpyHostToDevice, stream));
+        CUDA_TRY(cudaMemcpyAsync(d_l0, lam0, B * dim * 8, cudaMemcpyHostToDevice, stream));
+        CUDA_TRY(cudaMemcpyAsync(d_mode, init_mode, B, cudaMemcpyHostToDevice, stream));
+    }
+    sgsf_config_t c = *cfg;
+    c.want_prev = 0;
+    int rc = sgsf_solve(h, batch, d_xb, d_x0, d_l0, d_mode, &c, &o, ws, nullptr, stream);
+    if (rc == SGSF_OK) {
+        sgsf_verdict_t v;
+        std::memset(&v, 0, sizeof(v));
+        v.feasible = d_feas;
+        rc = sgsf_verdict(h, batch, o.coeffs, o.converged, 1e-3, &v, stream);
+    }
+    if (rc == SGSF_OK) {
+        if (coeffs) CUDA_TRY(cudaMemcpyAsync(coeffs, o.coeffs, B * dim * 8, cudaMemcpyDeviceToHost, stream));
+        if (multipliers)
+            CUDA_TRY(cudaMemcpyAsync(multipliers, o.multipliers, B * dim * 8, cudaMemcpyDeviceToHost, stream));
+        if (res_inf) CUDA_TRY(cudaMemcpyAsync(res_inf, o.res_inf, B * MI * 8, cudaMemcpyDeviceToHost, stream));
+        if (res_l2) CUDA_TRY(cudaMemcpyAsync(res_l2, o.res_l2, B * MI * 8, cudaMemcpyDeviceToHost, stream));
+        if (iterations) CUDA_TRY(cudaMemcpyAsync(iterations, o.iterations, B * 4, cudaMemcpyDeviceToHost, stream));
+        if (converged) CUDA_TRY(cudaMemcpyAsync(converged, o.converged, B, cudaMemcpyDeviceToHost, stream));
+        if (feasible) CUDA_TRY(cudaMemcpyAsync(feasible, d_feas, B, cudaMemcpyDeviceToHost, stream));
+        if (displacement)
+            CUDA_TRY(cudaMemcpyAsync(displacement, o.displacement, B * 8, cudaMemcpyDeviceToHost, stream));
+        if (status) CUDA_TRY(cudaMemcpyAsync(status, o.status, B * 4, cudaMemcpyDeviceToHost, stream));
+    }
+    cudaFreeAsync(arena, stream);
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    return rc;
+}
+
+int sgsf_fp32_peak(double* tflops, double* ms, void* stream_) {
+    cudaStream_t stream = (cudaStream_t)stream_;
+    int dev = 0, sms = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    float* sink = nullptr;
+    CUDA_TRY(cudaMallocAsync((void**)&sink, 16, stream));
+    const int blocks = sms * 8, threads = 256, iters = 4096;
+    cudaEvent_t a, b;
+    CUDA_TRY(cudaEventCreate(&a));
+    CUDA_TRY(cudaEventCreate(&b));
+    ffma_peak_kernel<<<blocks, threads, 0, stream>>>(sink, 64, 1.0f);   // warm-up
+    CUDA_TRY(cudaEventRecord(a, stream));
+    ffma_peak_kernel<<<blocks, threads, 0, stream>>>(sink, iters, 1.0f);
+    CUDA_TRY(cudaEventRecord(b, stream));
+    g_launches.fetch_add(2);
+    CUDA_TRY(cudaEventSynchronize(b));
+    float t = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&t, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFreeAsync(sink, stream);
+    const double flops = 2.0 * 8.0 * 16.0 * iters * (double)blocks * threads;
+    if (ms) *ms = t;
+    if (tflops) *tflops = flops / (t * 1e-3) / 1e12;
+    return SGSF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,500 @@
+"""Safety-filter API: the reference's call signature over the sm_100a kernels.
+
+Drop-in for ``swarmfilter.solver`` (``solver.py:42-458``): ``SolverConfig``,
+``SolveResult``, ``BatchResult``, ``SafetyFilter(problem, degree, config,
+validate).solve / .batch_solve``, module-level ``solve`` / ``batch_solve`` and
+the step functions ``spherical_step`` / ``multiplier_update`` /
+``coefficient_step``.  Results are the reference's types, so reporting code
+keeps working.
+
+Underneath, one ``batch_solve`` is ONE launch of the persistent kernel over
+the whole batch (``sgsf_solve``) plus one verdict launch; ``threads`` is
+accepted and recorded but has no effect.  ``SafetyFilter.solve_batched`` is
+the tensor-native fast path (device tensors in and out, no per-sample Python).
+
+Extra knobs (keyword fields with defaults, so reference code is unaffected):
+``SolverConfig.precision`` -- "lean" (FP32 term work, FP64 state; default) or
+"strict" (FP64 everywhere) -- and ``SolverConfig.svars`` (fill
+``SolveResult.svars`` in ``solve``/``batch_solve``; the reference always does).
+"""
+from __future__ import annotations
+
+import csv
+import time
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import native
+from .basis import BasisMatrices, build_basis
+from .errors import DimensionMismatch, SingularKKT, SwarmFilterError
+from .precompute import DeviceConstants, EqualitySystem, build_equality, device_constants
+from .problem import validate_problem
+
+_PRECISIONS = {"lean": native.PRECISION_LEAN, "strict": native.PRECISION_STRICT}
+
+
+@dataclass(frozen=True)
+class SolverConfig:
+    rho: float = 1.0
+    max_iters: int = 200
+    tol_residual: float = 1e-3
+    tol_eq: float = 1e-8
+    early_stop: bool = True
+    precision: str = "lean"
+    svars: bool = True
+
+    def __post_init__(self):
+        if not self.rho > 0:
+            raise ValueError(f"rho must be positive, got {self.rho}")
+        if self.max_iters < 1:
+            raise ValueError(f"max_iters must be >= 1, got {self.max_iters}")
+        if not self.tol_residual > 0:
+            raise ValueError(f"tol_residual must be positive, got {self.tol_residual}")
+        if not self.tol_eq > 0:
+            raise ValueError(f"tol_eq must be positive, got {self.tol_eq}")
+        if self.precision not in _PRECISIONS:
+            raise ValueError(f"precision must be one of {sorted(_PRECISIONS)}, got {self.precision!r}")
+
+
+@dataclass(frozen=True)
+class SphericalVars:
+    """Spherical variables of the last iteration; pair arrays (P, S), workspace (n, S)."""
+
+    pair_azimuth: np.ndarray
+    pair_polar: np.ndarray
+    pair_radial: np.ndarray
+    ws_azimuth: np.ndarray
+    ws_polar: np.ndarray
+    ws_radial: np.ndarray
+
+
+@dataclass
+class SolveResult:
+    coeffs: np.ndarray | None
+    multipliers: np.ndarray | None
+    residual_inf: np.ndarray
+    residual_l2: np.ndarray
+    iterations: int
+    converged: bool
+    displacement: float
+    solve_time: float
+    svars: SphericalVars | None = None
+    error: str | None = None
+
+    @property
+    def final_residual_inf(self) -> float:
+        return float(self.residual_inf[-1]) if self.iterations else np.inf
+
+    def to_jsonable(self, n: int | None = None) -> dict:
+        if self.coeffs is None:
+            coeffs = None
+        elif n is None:
+            coeffs = self.coeffs.tolist()
+        else:
+            coeffs = self.coeffs.reshape(3, n, -1).transpose(1, 0, 2).tolist()
+        return {"converged": self.converged, "iterations": self.iterations, "displacement": self.displacement,
+                "solve_time": self.solve_time, "residual_inf": np.asarray(self.residual_inf).tolist(),
+                "residual_l2": np.asarray(self.residual_l2).tolist(), "coefficients": coeffs,
+                "multipliers": None if self.multipliers is None else self.multipliers.tolist(),
+                "error": self.error}
+
+
+def _failed_result(message: str, elapsed: float) -> SolveResult:
+    return SolveResult(None, None, np.empty(0), np.empty(0), 0, False, np.nan, elapsed, error=message)
+
+
+@dataclass
+class BatchResult:
+    results: list
+    wall_time: float
+    threads: int = 1
+
+    @property
+    def n_converged(self) -> int:
+        return sum(1 for r in self.results if r.converged)
+
+    @property
+    def n_failed(self) -> int:
+        return sum(1 for r in self.results if r.error is not None)
+
+
+@dataclass
+class DeviceBatch:
+    """Outputs of :meth:`SafetyFilter.solve_batched` (device tensors, batch-major)."""
+
+    coeffs: torch.Tensor          # (B, dim) f64
+    multipliers: torch.Tensor     # (B, dim) f64
+    residual_inf: torch.Tensor    # (B, max_iters) f64, valid up to iterations[b]
+    residual_l2: torch.Tensor
+    iterations: torch.Tensor      # (B,) i32
+    converged: torch.Tensor       # (B,) u8
+    feasible: torch.Tensor | None  # (B,) u8: converged and passes the original constraints
+    displacement: torch.Tensor    # (B,) f64
+    status: torch.Tensor          # (B,) i32: 0 ok, 1 SingularKKT
+    eq_err: torch.Tensor          # (B,) f64: ||A xi - b||_inf of the returned iterate
+    coeffs_prev: torch.Tensor | None = None
+
+
+class Operator:
+    """Stand-in for the reference's PairwiseOperator (``assembly.py:222-339``).
+
+    Holds the problem/basis and the per-(device, rho) native handles; its
+    ``apply``/``apply_transpose`` run the FP64 operator kernels.
+    """
+
+    def __init__(self, problem, basis: BasisMatrices, equality: EqualitySystem):
+        self.problem = problem
+        self.n = problem.n
+        self.basis = basis
+        self.equality = equality
+        self.pair_i, self.pair_j = np.triu_indices(problem.n, k=1)
+        self._handles: dict = {}
+
+    n_pairs = property(lambda self: int(self.pair_i.size))
+    samples = property(lambda self: self.basis.samples)
+    pair_rows = property(lambda self: self.n_pairs * self.samples)
+    ws_rows = property(lambda self: self.n * self.samples)
+    axis_rows = property(lambda self: self.pair_rows + self.ws_rows)
+    rows = property(lambda self: 3 * self.axis_rows)
+    coeff_dim = property(lambda self: 3 * self.n * (self.basis.degree + 1))
+
+    def constants(self, rho: float) -> DeviceConstants:
+        return device_constants(self.problem, self.basis, self.equality, rho)
+
+    def handle(self, rho: float, device: torch.device | None = None):
+        if not torch.cuda.is_available():
+            raise native.NativeError("the safety filter needs a CUDA device (B200); none is visible")
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        key = (dev.index if dev.index is not None else torch.cuda.current_device(), float(rho))
+        h = self._handles.get(key)
+        if h is None:
+            k = self.constants(rho)
+            keep = [np.ascontiguousarray(a, dtype=np.float64) for a in
+                    (k.W, k.Wd, k.Wdd, k.B, k.rhs, k.PBt, k.Km11, k.Kd11, k.Mm, k.Md, k.cconst)]
+            ptrs = [a.ctypes.data_as(native._dp) for a in keep]
+            pr = native.Problem(k.n, k.samples, k.m1, k.rho, k.lat, k.vert, k.ws_lat, k.ws_vert,
+                                (native.C.c_double * 3)(*k.center), *ptrs)
+            out = native.C.c_void_p()
+            with torch.cuda.device(key[0]):
+                native.check(native.load().sgsf_create(native.C.byref(pr), native.C.byref(out)), "sgsf_create")
+            h = _Handle(out.value)
+            self._handles[key] = h
+        return h.value
+
+    # flat-vector operators on the device (FP64); used by the step functions
+    def apply(self, coeffs) -> np.ndarray:
+        xi = _to_dev(np.asarray(coeffs, dtype=float).reshape(1, -1))
+        out = torch.empty((1, self.rows), dtype=torch.float64, device=xi.device)
+        native.check(native.load().sgsf_apply_F(self.handle(1.0), 1, xi.data_ptr(), out.data_ptr(), _stream()),
+                     "sgsf_apply_F")
+        return out.cpu().numpy().ravel()
+
+    def apply_transpose(self, values) -> np.ndarray:
+        v = np.asarray(values, dtype=float).ravel()
+        if v.size != self.rows:
+            raise DimensionMismatch(f"vector has length {v.size}, expected {self.rows}")
+        vd = _to_dev(v.reshape(1, -1))
+        out = torch.empty((1, self.coeff_dim), dtype=torch.float64, device=vd.device)
+        native.check(native.load().sgsf_apply_FT(self.handle(1.0), 1, vd.data_ptr(), out.data_ptr(), _stream()),
+                     "sgsf_apply_FT")
+        return out.cpu().numpy().ravel()
+
+
+class _Handle:
+    def __init__(self, value):
+        self.value = value
+
+    def __del__(self):
+        try:
+            if self.value and native._lib is not None:
+                native._lib.sgsf_destroy(self.value)
+        except Exception:
+            pass
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _to_dev(a: np.ndarray) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to("cuda", non_blocking=False)
+
+
+class SafetyFilter:
+    """Reusable filter for one problem (``solver.py:224-407``)."""
+
+    def __init__(self, problem, degree: int = 10, config: SolverConfig | None = None, validate: bool = True):
+        if validate:
+            validate_problem(problem)
+        self.problem = problem
+        self.config = config if config is not None else SolverConfig()
+        self.basis = build_basis(problem.duration, degree=degree, samples=problem.horizon_samples)
+        self.equality = build_equality(problem, self.basis)
+        self.operator = Operator(problem, self.basis, self.equality)
+
+    @property
+    def coeff_dim(self) -> int:
+        return self.operator.coeff_dim
+
+    # ------------------------------------------------------------- validation (host)
+    def _check_vector(self, vec, what) -> np.ndarray:
+        arr = np.asarray(vec, dtype=float).ravel()
+        if arr.size != self.coeff_dim:
+            raise DimensionMismatch(f"{what} has length {arr.size}, expected {self.coeff_dim} "
+                                    f"(n={self.problem.n}, degree={self.basis.degree})")
+        return arr
+
+    def _normalize_init(self, init):
+        """None -> None; otherwise (xi0, lam0) arrays (solver.py:264-284)."""
+        if init is None:
+            return None
+        if hasattr(init, "coeffs") and hasattr(init, "multipliers"):
+            if init.coeffs is None:
+                raise SwarmFilterError("cannot warm start from a failed result")
+            init = (init.coeffs, init.multipliers)
+        elif hasattr(init, "xi0"):
+            init = (init.xi0, init.lambda0)
+        c0, m0 = init
+        return (self._check_vector(c0, "initial coefficients").copy(),
+                self._check_vector(m0, "initial multipliers").copy())
+
+    def initial_state(self, proposal, init=None):
+        from .proposals import project_to_boundary
+        xi_bar = self._check_vector(proposal, "proposal")
+        st = self._normalize_init(init)
+        if st is None:
+            return project_to_boundary(xi_bar, self.equality), np.zeros(self.coeff_dim)
+        return st
+
+    # ------------------------------------------------------------- device fast path
+    def solve_batched(self, xi_bar: torch.Tensor, xi0: torch.Tensor | None = None,
+                      lam0: torch.Tensor | None = None, init_mode: torch.Tensor | None = None,
+                      config: SolverConfig | None = None, want_prev: bool = False, verdict: bool = True,
+                      verdict_tol: float = 1e-3, timing=None, slots_per_block: int = 0,
+                      grid: int = 0) -> DeviceBatch:
+        """Filter a (B, dim) float64 CUDA tensor of proposals with one kernel launch.
+
+        ``xi0``/``lam0`` (B, dim) warm-start the rows where ``init_mode`` (B,) uint8 is 1
+        (all rows when ``init_mode`` is None and ``xi0`` is given); other rows start
+        from the boundary projection of the proposal with zero multipliers.
+        ``timing`` = (start, stop) CUDA events recorded around the solve kernel.
+        """
+        cfg = config if config is not None else self.config
+        if xi_bar.dim() != 2 or xi_bar.shape[1] != self.coeff_dim:
+            raise DimensionMismatch(f"proposals must be (B, {self.coeff_dim}), got {tuple(xi_bar.shape)}")
+        if not xi_bar.is_cuda or xi_bar.dtype != torch.float64:
+            raise DimensionMismatch("proposals must be a float64 CUDA tensor")
+        dev = xi_bar.device
+        B = int(xi_bar.shape[0])
+        xi_bar = xi_bar.contiguous()
+        if xi0 is not None:
+            if lam0 is None:
+                lam0 = torch.zeros_like(xi0)
+            if init_mode is None:
+                init_mode = torch.ones(B, dtype=torch.uint8, device=dev)
+            xi0, lam0 = xi0.contiguous(), lam0.contiguous()
+            init_mode = init_mode.to(device=dev, dtype=torch.uint8).contiguous()
+        else:
+            init_mode = None
+        dim, mi = self.coeff_dim, cfg.max_iters
+        f64 = dict(dtype=torch.float64, device=dev)
+        out = DeviceBatch(
+            coeffs=torch.empty((B, dim), **f64), multipliers=torch.empty((B, dim), **f64),
+            residual_inf=torch.empty((B, mi), **f64), residual_l2=torch.empty((B, mi), **f64),
+            iterations=torch.empty(B, dtype=torch.int32, device=dev),
+            converged=torch.empty(B, dtype=torch.uint8, device=dev),
+            feasible=torch.empty(B, dtype=torch.uint8, device=dev) if verdict else None,
+            displacement=torch.empty(B, **f64), status=torch.empty(B, dtype=torch.int32, device=dev),
+            eq_err=torch.empty(B, **f64),
+            coeffs_prev=torch.empty((B, dim), **f64) if want_prev else None,
+        )
+        if B == 0:
+            return out
+        lib = native.load()
+        handle = self.operator.handle(cfg.rho, dev)
+        ccfg = native.Config(int(mi), float(cfg.tol_residual), float(cfg.tol_eq), int(bool(cfg.early_stop)),
+                             _PRECISIONS[cfg.precision], int(bool(want_prev)), int(slots_per_block), int(grid))
+        o = native.Outputs(out.coeffs.data_ptr(), out.multipliers.data_ptr(), out.residual_inf.data_ptr(),
+                           out.residual_l2.data_ptr(), out.iterations.data_ptr(), out.converged.data_ptr(),
+                           out.displacement.data_ptr(), out.status.data_ptr(), out.eq_err.data_ptr(),
+                           out.coeffs_prev.data_ptr() if want_prev else None)
+        ws = torch.empty(int(lib.sgsf_workspace_bytes()), dtype=torch.uint8, device=dev)
+        tm = None
+        if timing is not None:
+            tm = native.Timing(timing[0].cuda_event, timing[1].cuda_event)
+        with torch.cuda.device(dev):
+            stream = _stream()
+            rc = lib.sgsf_solve(handle, B, xi_bar.data_ptr(), native.ptr(xi0), native.ptr(lam0),
+                                native.ptr(init_mode), native.C.byref(ccfg), native.C.byref(o), ws.data_ptr(),
+                                native.C.byref(tm) if tm is not None else None, stream)
+            native.check(rc, "sgsf_solve")
+            if verdict:
+                v = native.Verdict(None, out.feasible.data_ptr(), None, None, None, None)
+                native.check(lib.sgsf_verdict(handle, B, out.coeffs.data_ptr(), out.converged.data_ptr(),
+                                              float(verdict_tol), native.C.byref(v), stream), "sgsf_verdict")
+        return out
+
+    def svars_of(self, coeffs: torch.Tensor) -> list:
+        """Spherical variables of positions C W^T for each row (K2b), as SphericalVars."""
+        B = int(coeffs.shape[0])
+        n, S, P = self.problem.n, self.basis.samples, self.operator.n_pairs
+        dev = coeffs.device
+        f64 = dict(dtype=torch.float64, device=dev)
+        pa, pp, pr = (torch.empty((B, P, S), **f64) for _ in range(3))
+        wa, wp, wr = (torch.empty((B, n, S), **f64) for _ in range(3))
+        if B:
+            native.check(native.load().sgsf_svars(self.operator.handle(self.config.rho, dev), B,
+                                                  coeffs.contiguous().data_ptr(), pa.data_ptr(), pp.data_ptr(),
+                                                  pr.data_ptr(), wa.data_ptr(), wp.data_ptr(), wr.data_ptr(),
+                                                  _stream()), "sgsf_svars")
+        arrs = [t.cpu().numpy() for t in (pa, pp, pr, wa, wp, wr)]
+        return [SphericalVars(*(a[b] for a in arrs)) for b in range(B)]
+
+    # ------------------------------------------------------------- reference-compatible API
+    def solve(self, proposal, init=None, config: SolverConfig | None = None) -> SolveResult:
+        """Filter one proposal; raises on bad input or SingularKKT (solver.py:286-359)."""
+        res = self._run([proposal], [init], config, raise_errors=True)
+        return res[0]
+
+    def _solve_guarded(self, proposal, init, config) -> SolveResult:
+        return self._run([proposal], [init], config, raise_errors=False)[0]
+
+    def batch_solve(self, proposals, inits=None, threads: int = 1, config: SolverConfig | None = None) -> BatchResult:
+        """Filter every proposal in one launch; failures are isolated per item (solver.py:368-407)."""
+        proposals = list(proposals)
+        if inits is None:
+            inits = [None] * len(proposals)
+        else:
+            inits = list(inits)
+            if len(inits) != len(proposals):
+                raise DimensionMismatch(f"got {len(inits)} warm starts for {len(proposals)} proposals")
+        start = time.perf_counter()
+        results = self._run(proposals, inits, config, raise_errors=False)
+        return BatchResult(results=results, wall_time=time.perf_counter() - start, threads=max(1, threads))
+
+    def _run(self, proposals, inits, config, raise_errors: bool) -> list:
+        cfg = config if config is not None else self.config
+        t0 = time.perf_counter()
+        B = len(proposals)
+        results: list = [None] * B
+        rows, xb, x0, l0, mode = [], [], [], [], []
+        for idx, (prop, init) in enumerate(zip(proposals, inits)):
+            try:
+                xi_bar = self._check_vector(prop, "proposal")
+                st = self._normalize_init(init)
+            except (SwarmFilterError, ValueError) as exc:
+                if raise_errors:
+                    raise
+                results[idx] = _failed_result(f"{type(exc).__name__}: {exc}", time.perf_counter() - t0)
+                continue
+            rows.append(idx)
+            xb.append(xi_bar)
+            if st is None:
+                x0.append(np.zeros(self.coeff_dim))
+                l0.append(np.zeros(self.coeff_dim))
+                mode.append(0)
+            else:
+                x0.append(st[0])
+                l0.append(st[1])
+                mode.append(1)
+        if rows:
+            xbd = _to_dev(np.stack(xb))
+            warm = any(mode)
+            out = self.solve_batched(
+                xbd, xi0=_to_dev(np.stack(x0)) if warm else None, lam0=_to_dev(np.stack(l0)) if warm else None,
+                init_mode=torch.tensor(mode, dtype=torch.uint8, device=xbd.device) if warm else None,
+                config=cfg, want_prev=bool(cfg.svars), verdict=False)
+            svars = self.svars_of(out.coeffs_prev) if cfg.svars else [None] * len(rows)
+            h = {k: getattr(out, k).cpu().numpy() for k in
+                 ("coeffs", "multipliers", "residual_inf", "residual_l2", "iterations", "converged",
+                  "displacement", "status", "eq_err")}
+            per = (time.perf_counter() - t0) / max(1, len(rows))
+            for r, idx in enumerate(rows):
+                if h["status"][r] == native.SAMPLE_SINGULAR_KKT:
+                    msg = (f"endpoint conditions missed by {h['eq_err'][r]:.3e} after refinement "
+                           f"(tolerance {cfg.tol_eq:.3e})")
+                    if raise_errors:
+                        raise SingularKKT(msg)
+                    results[idx] = _failed_result(f"SingularKKT: {msg}", per)
+                    continue
+                its = int(h["iterations"][r])
+                results[idx] = SolveResult(
+                    coeffs=h["coeffs"][r].copy(), multipliers=h["multipliers"][r].copy(),
+                    residual_inf=h["residual_inf"][r, :its].copy(), residual_l2=h["residual_l2"][r, :its].copy(),
+                    iterations=its, converged=bool(h["converged"][r]), displacement=float(h["displacement"][r]),
+                    solve_time=per, svars=svars[r])
+        return results
+
+
+# ------------------------------------------------------------------ step functions (test API)
+def spherical_step(coeffs, operator: Operator, problem) -> SphericalVars:
+    """Spherical variables for given coefficients (solver.py:177-183), on the device."""
+    sf_basis = operator.basis
+    xi = _to_dev(np.asarray(coeffs, dtype=float).reshape(1, -1))
+    n, S, P = problem.n, sf_basis.samples, operator.n_pairs
+    f64 = dict(dtype=torch.float64, device=xi.device)
+    pa, pp, pr = (torch.empty((1, P, S), **f64) for _ in range(3))
+    wa, wp, wr = (torch.empty((1, n, S), **f64) for _ in range(3))
+    native.check(native.load().sgsf_svars(operator.handle(1.0), 1, xi.data_ptr(), pa.data_ptr(), pp.data_ptr(),
+                                          pr.data_ptr(), wa.data_ptr(), wp.data_ptr(), wr.data_ptr(), _stream()),
+                 "sgsf_svars")
+    return SphericalVars(*(t.cpu().numpy()[0] for t in (pa, pp, pr, wa, wp, wr)))
+
+
+def multiplier_update(multipliers, coeffs, rhs, operator: Operator, rho: float) -> np.ndarray:
+    """lam - rho F^T (F xi - e) (solver.py:186-199); F and F^T run on the device in FP64."""
+    lam = np.asarray(multipliers, dtype=float).ravel()
+    if lam.size != operator.coeff_dim:
+        raise DimensionMismatch(f"multiplier vector has length {lam.size}, expected {operator.coeff_dim}")
+    return lam - rho * operator.apply_transpose(operator.apply(coeffs) - np.asarray(rhs, dtype=float).ravel())
+
+
+def coefficient_step(proposal, rhs, multipliers, equality, operator: Operator, rho: float,
+                     tol_eq: float = 1e-8) -> np.ndarray:
+    """Equality-constrained QP step (solver.py:202-221) with the decoupled device KKT solve."""
+    xi_bar = np.asarray(proposal, dtype=float).ravel()
+    lam = np.asarray(multipliers, dtype=float).ravel()
+    eta = rho * operator.apply_transpose(rhs) + lam + xi_bar
+    ed = _to_dev(eta.reshape(1, -1))
+    out = torch.empty_like(ed)
+    err = torch.empty(1, dtype=torch.float64, device=ed.device)
+    native.check(native.load().sgsf_kkt_step(operator.handle(rho), 1, ed.data_ptr(), out.data_ptr(),
+                                             err.data_ptr(), _stream()), "sgsf_kkt_step")
+    e = float(err.item())
+    if e > tol_eq:
+        raise SingularKKT(f"endpoint conditions missed by {e:.3e} after refinement (tolerance {tol_eq:.3e})")
+    return out.cpu().numpy().ravel()
+
+
+def write_residuals_csv(path, results, metadata=None) -> None:
+    """Residual histories: proposal_id, iter (1-based), res_inf, res_l2 (solver.py:410-425)."""
+    with open(path, "w", newline="") as fh:
+        for key, value in (metadata or {}).items():
+            fh.write(f"# {key}={value}\n")
+        w = csv.writer(fh)
+        w.writerow(["proposal_id", "iter", "res_inf", "res_l2"])
+        for pid, res in enumerate(results):
+            for k in range(res.iterations):
+                w.writerow([pid, k + 1, repr(float(res.residual_inf[k])), repr(float(res.residual_l2[k]))])
+
+
+def _infer_degree(proposal, problem) -> int:
+    size = np.asarray(proposal).ravel().size
+    per_axis = size // (3 * problem.n)
+    if per_axis * 3 * problem.n != size or per_axis < 1:
+        raise DimensionMismatch(f"proposal length {size} does not factor as 3 * {problem.n} * (degree + 1)")
+    return per_axis - 1
+
+
+def solve(proposal, problem, init=None, config: SolverConfig | None = None) -> SolveResult:
+    return SafetyFilter(problem, degree=_infer_degree(proposal, problem), config=config).solve(proposal, init=init)
+
+
+def batch_solve(proposals, problem, inits=None, threads: int = 1, config: SolverConfig | None = None) -> BatchResult:
+    proposals = list(proposals)
+    if not proposals:
+        return BatchResult(results=[], wall_time=0.0, threads=max(1, threads))
+    sf = SafetyFilter(problem, degree=_infer_degree(proposals[0], problem), config=config)
+    return sf.batch_solve(proposals, inits=inits, threads=threads, config=config)
