@@ -20,7 +20,7 @@ namespace sgsf {
 
 // Reference trig formula in FP64.  Explicit _rn intrinsics keep nvcc from
 // contracting into FMAs so the products round like the reference's scalar C.
-__device__ __noinline__ void ref_spherical(double dx, double dy, double dz, double lat, double vert,
+static __device__ __noinline__ void ref_spherical(double dx, double dy, double dz, double lat, double vert,
                                            double lo, double hi, double* az_o, double* pol_o,
                                            double* rad_o, double* tx, double* ty, double* tz) {
     double az = atan2(dy, dx);

@@ -1,0 +1,96 @@
+// sf_launch.cuh -- host-side launch of K1 for one (T, NB, MP) instantiation.
+// Each kernels_*.cu translation unit instantiates a few of these so the
+// fully-unrolled kernels compile in parallel.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "../../include/sgsf.h"
+#include "sf_persistent.cuh"
+
+namespace sgsf {
+
+struct LaunchInfo {
+    int device, sm_count;
+};
+
+int internal_fail(int code, const std::string& msg);
+void internal_count_launch(int n);
+
+template <typename T, int NB, int MP, int MAXT>
+int launch_persistent(const LaunchInfo& li, SolveParams& p, const sgsf_config_t* cfg, const sgsf_timing_t* timing,
+                      cudaStream_t stream) {
+    auto kern = sf_persistent_kernel<T, NB, MP, MAXT>;
+    int dev_smem = 0;
+    cudaError_t e = cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, li.device);
+    if (e != cudaSuccess) return internal_fail(SGSF_ERR_CUDA, cudaGetErrorString(e));
+    // a slot is a warp group of ceil(S/32) warps with its own named barrier (ids 1..15)
+    const int wps = (p.S + 31) / 32;
+    const int slot_threads = 32 * wps;
+    int spb = cfg->slots_per_block;
+    if (spb <= 0) {
+        spb = 0;
+        for (int s = 1; s * slot_threads <= MAXT && s <= 15; ++s) {
+            if (make_layout<T, NB>(p.n, p.S, MP, s, p.want_prev).total > (size_t)dev_smem) break;
+            spb = s;
+        }
+        // small batches: spread samples over the SMs instead of packing few CTAs
+        const int spread = (p.batch + li.sm_count - 1) / li.sm_count;
+        if (spb > spread) spb = spread > 0 ? spread : 1;
+    }
+    if (spb <= 0) return internal_fail(SGSF_ERR_UNSUPPORTED, "problem too large for one CTA (samples or smem)");
+    if (spb > 15) return internal_fail(SGSF_ERR_UNSUPPORTED, "at most 15 slots per CTA (named barriers)");
+    const int threads = spb * slot_threads;
+    if (threads > MAXT) return internal_fail(SGSF_ERR_UNSUPPORTED, "slots_per_block * samples exceeds the CTA size");
+    p.spb = spb;
+    p.wps = wps;
+    p.MP = MP;
+    const SmemLayout L = make_layout<T, NB>(p.n, p.S, MP, spb, p.want_prev);
+    if (L.total > (size_t)dev_smem) return internal_fail(SGSF_ERR_UNSUPPORTED, "shared memory budget exceeded");
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
+    if (e != cudaSuccess) return internal_fail(SGSF_ERR_CUDA, cudaGetErrorString(e));
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, L.total);
+    if (e != cudaSuccess) return internal_fail(SGSF_ERR_CUDA, cudaGetErrorString(e));
+    if (per_sm < 1) per_sm = 1;
+    int grid = cfg->grid > 0 ? cfg->grid : li.sm_count * per_sm;
+    const int need = (p.batch + spb - 1) / spb;
+    if (grid > need) grid = need;
+    if (timing && timing->start) cudaEventRecord((cudaEvent_t)timing->start, stream);
+    kern<<<grid, threads, L.total, stream>>>(p);
+    internal_count_launch(1);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return internal_fail(SGSF_ERR_CUDA, std::string("sf_persistent launch: ") + cudaGetErrorString(e));
+    if (timing && timing->stop) cudaEventRecord((cudaEvent_t)timing->stop, stream);
+    return SGSF_OK;
+}
+
+// instantiated in kernels_*.cu
+#define SGSF_DECLARE_LAUNCH(T, NB, MP, MAXT)                                                                  \
+    extern template int launch_persistent<T, NB, MP, MAXT>(const LaunchInfo&, SolveParams&, const sgsf_config_t*, \
+                                                           const sgsf_timing_t*, cudaStream_t);
+#define SGSF_DEFINE_LAUNCH(T, NB, MP, MAXT)                                                                    \
+    template int launch_persistent<T, NB, MP, MAXT>(const LaunchInfo&, SolveParams&, const sgsf_config_t*,    \
+                                                    const sgsf_timing_t*, cudaStream_t);
+
+// (T, NB, MAXT): MAXT caps the CTA so ptxas can give the register-resident
+// term pass the registers it needs.
+#define SGSF_FOR_EACH_VARIANT(X) \
+    X(float, 4, 12, 512)         \
+    X(float, 4, 16, 512)         \
+    X(float, 8, 12, 384)         \
+    X(float, 8, 16, 384)         \
+    X(float, 16, 12, 384)        \
+    X(float, 16, 16, 384)        \
+    X(double, 4, 12, 384)        \
+    X(double, 4, 16, 384)        \
+    X(double, 8, 12, 256)        \
+    X(double, 8, 16, 256)        \
+    X(double, 16, 12, 256)       \
+    X(double, 16, 16, 256)
+
+SGSF_FOR_EACH_VARIANT(SGSF_DECLARE_LAUNCH)
+
+}  // namespace sgsf

@@ -5,57 +5,44 @@
 // LU xi-step (assembly.py:186-219) and the boundary projection prologue
 // (projection.py:11-25).
 //
-// Persistent CTAs, one resident CTA per SM.  A CTA owns `spb` sample SLOTS;
-// a slot pulls the next sample index from a global atomic queue whenever its
-// sample finishes, so per-sample iteration-count skew never idles a slot.
+// Persistent CTAs.  A CTA hosts `spb` independent sample SLOTS; a slot is a
+// group of ceil(S/32) warps with its own named barrier, pulling the next
+// sample index from a global atomic queue whenever its sample finishes.
+// Slots never wait for each other, so one slot's serial phases (projection,
+// means, FP64 xi-step) overlap the other slots' term passes.
 //
-// Thread layout in the term phase: thread (slot, t) owns time step t of its
-// slot's sample for ALL robots; the sampled positions of every robot at t live
-// in its registers, so the O(n^2) pair work needs no shared-memory traffic and
-// the scatter F^T is a register accumulation in a fixed order (deterministic,
-// no atomics).  Each round of the CTA runs five phases separated by barriers:
-//
-//   T  positions  p_k(t) = C_k W[t]^T                       (term precision)
-//      for every pair / workspace term:  targets e_k = proj(d_k),
-//        residual r_k = d_k - e_k scattered into R(t);
-//        exit residual of iteration k-1:  d_k - proj(d_{k-1})  -> max / sum sq
-//   G  lam'  = lam - rho R W            (W^T projection, 2 t-halves per row)
-//      one warp per slot: history, early-stop / SingularKKT decision
-//   M  finished slots: write outputs, claim next sample;  others: C_bar, u_bar
-//   M2 mean part  Mm C_bar + Km11 u_bar;  freshly claimed slots: load + project
-//   X  xi-step  C_i = mean part + Md (C_i - C_bar) + Kd11 (u_i - u_bar) + cconst_i,
-//      ||A xi - b||_inf check, lam <- lam'
-//
-// u = 2 lam' - lam + xi_bar (residual identity, precompute.py).  State (C,
-// lam, xi_bar) and the xi-step are FP64; T is float ("lean") or double
-// ("strict") for positions, term math and the W^T projection.
+// Term pass: thread t of a slot owns time step t of its sample for ALL
+// robots; the positions of every robot at t live in its registers.  Per
+// iteration k it
+//   1. evaluates p_k(t) = C_k W[t]^T,
+//   2. scans all pair and workspace terms: interior test (q = a^2 r^2 against
+//      a^2) and exactly-zero components -- ~10 instructions per pair,
+//   3. if every term is interior now and at the previous iterate ("quiet"):
+//      the targets equal the differences, the scattered residual is 0 and the
+//      exit residual of each term is its change Dp_i - Dp_j; its inf-norm is
+//      the per-axis range of Dp and its l2-norm a per-axis sum (O(n));
+//      otherwise a masked pass evaluates Dp_i - Dp_j per pair and takes the
+//      exact slow path only for the flagged terms (target recompute, scatter
+//      of d - e into the thread's residual row R),
+//   4. terms with an exactly-zero component rerun on the careful path, which
+//      uses the FP64 reference trig formula.
+// Then   G  lam' = lam - rho R W   (skipped when the slot had no active term)
+//        M  swarm means / finalize,  M2 mean part of the xi-step,
+//        X  decoupled FP64 xi-step  C_i = Mm Cb + Km11 ub + Md (C_i - Cb)
+//           + Kd11 (u_i - ub) + cconst_i, u = 2 lam' - lam + xi_bar, with the
+//           ||A xi - b||_inf check (assembly.py:198-217).
+// T is float ("lean") or double ("strict") for positions and term math;
+// state and xi-step are FP64.
 #pragma once
 
 #include "sf_device.cuh"
 
 namespace sgsf {
 
-enum { SLOT_EMPTY = 0, SLOT_ACTIVE = 1 };
 enum { SAMPLE_OK = 0, SAMPLE_SINGULAR_KKT = 1 };
 
-struct SlotState {
-    int sample;
-    int k;       // xi-steps taken so far
-    int state;
-    int pad;
-};
-
-struct SlotScratch {   // phase-to-phase messages within one round
-    int done;
-    int failed;
-    int pending;
-    int pad;
-    double last_inf;
-    double eqmax;
-};
-
 struct SolveParams {
-    int n, S, m1, MP, batch, max_iters, early_stop, want_prev, spb;
+    int n, S, m1, MP, batch, max_iters, early_stop, want_prev, spb, wps;
     double rho, tol_res, tol_eq;
     double lat, vert, ws_lat, ws_vert, cx, cy, cz;
     const double* W;       // S x m1
@@ -82,57 +69,75 @@ struct SolveParams {
     int* queue;
 };
 
+// per-slot scalars (written by one thread, read by the slot after a slot barrier)
+struct SlotShared {
+    int sample;
+    int done;
+    int failed;
+    int active;   // some term had an active constraint in this iteration's term pass
+    double last_inf;
+    double eqmax;
+};
+
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
+template <int NB> struct RowStride { static constexpr int value = 3 * NB + 1; };
+
+// Shared-memory map.  Coefficient-space arrays are padded to MP (m1 rounded
+// up to a multiple of 4) columns with zeros, so every loop over the degree
+// runs to the compile-time MP with no guards and vector loads.  P0/P1 hold
+// the positions of iterates k (old) and k+1 (new) as [t][3 NB + 1] rows
+// (thread t owns row t; odd stride -> distinct banks); after the term pass
+// the dead old row is reused for the thread's scattered residual R, valid
+// where rflag[t] is set.
 struct SmemLayout {
-    size_t W, KMm, KMd, cconst, B6, rhs, PBt, st0, st1, sc;
+    size_t W, KMm, KMd, cconst, B6, rhs, PBt;
     size_t slot0, slot_stride;
-    size_t C, Cp, lam, lamN, xb, means, mpart, eqerr, psq, R, posold, Cf, pinf;
+    size_t C, Cp, lam, lamN, xb, means, mpart, eqerr, psq, P0, P1, rflag, Cf, pinf, sh;
     size_t total;
 };
 
 template <typename T, int NB>
-__host__ __device__ inline SmemLayout make_layout(int n, int S, int m1, int MP, int spb, int want_prev) {
-    const int RS = 3 * NB + 1;
+__host__ __device__ inline SmemLayout make_layout(int n, int S, int MP, int spb, int want_prev) {
+    const int RS = RowStride<NB>::value;
     SmemLayout L;
     size_t o = 0;
     const size_t d = sizeof(double), ts = sizeof(T);
-    const int R3 = 3 * n, dim = R3 * m1;
+    const int R3 = 3 * n, dimp = R3 * MP;
     L.W = o;      o = align16(o + (size_t)S * MP * ts);
-    L.KMm = o;    o = align16(o + (size_t)m1 * 2 * m1 * d);
-    L.KMd = o;    o = align16(o + (size_t)m1 * 2 * m1 * d);
-    L.cconst = o; o = align16(o + (size_t)dim * d);
-    L.B6 = o;     o = align16(o + (size_t)6 * m1 * d);
+    L.KMm = o;    o = align16(o + (size_t)MP * 2 * MP * d);
+    L.KMd = o;    o = align16(o + (size_t)MP * 2 * MP * d);
+    L.cconst = o; o = align16(o + (size_t)dimp * d);
+    L.B6 = o;     o = align16(o + (size_t)6 * MP * d);
     L.rhs = o;    o = align16(o + (size_t)R3 * 6 * d);
-    L.PBt = o;    o = align16(o + (size_t)m1 * 6 * d);
-    L.st0 = o;    o = align16(o + (size_t)spb * sizeof(SlotState));
-    L.st1 = o;    o = align16(o + (size_t)spb * sizeof(SlotState));
-    L.sc = o;     o = align16(o + (size_t)spb * sizeof(SlotScratch));
+    L.PBt = o;    o = align16(o + (size_t)MP * 6 * d);
     L.slot0 = o;
     size_t q = 0;
-    L.C = q;      q = align16(q + (size_t)dim * d);
-    L.Cp = q;     q = align16(q + (want_prev ? (size_t)dim * d : 0));
-    L.lam = q;    q = align16(q + (size_t)dim * d);
-    L.lamN = q;   q = align16(q + (size_t)dim * d);
-    L.xb = q;     q = align16(q + (size_t)dim * d);
-    L.means = q;  q = align16(q + (size_t)6 * m1 * d);
-    L.mpart = q;  q = align16(q + (size_t)3 * m1 * d);
+    L.C = q;      q = align16(q + (size_t)dimp * d);
+    L.Cp = q;     q = align16(q + (want_prev ? (size_t)dimp * d : 0));
+    L.lam = q;    q = align16(q + (size_t)dimp * d);
+    L.lamN = q;   q = align16(q + (size_t)dimp * d);
+    L.xb = q;     q = align16(q + (size_t)dimp * d);
+    L.means = q;  q = align16(q + (size_t)6 * MP * d);
+    L.mpart = q;  q = align16(q + (size_t)3 * MP * d);
     L.eqerr = q;  q = align16(q + (size_t)R3 * d);
     L.psq = q;    q = align16(q + (size_t)S * d);
-    L.R = q;      q = align16(q + (size_t)RS * S * ts);
-    L.posold = q; q = align16(q + (size_t)RS * S * ts);
+    L.P0 = q;     q = align16(q + (size_t)RS * S * ts);
+    L.P1 = q;     q = align16(q + (size_t)RS * S * ts);
+    L.rflag = q;  q = align16(q + (size_t)S * sizeof(int));
     L.Cf = q;     q = align16(q + (size_t)R3 * MP * ts);
     L.pinf = q;   q = align16(q + (size_t)S * ts);
+    L.sh = q;     q = align16(q + sizeof(SlotShared));
     L.slot_stride = q;
     L.total = o + (size_t)spb * q;
     return L;
 }
 
-constexpr int KMAX = 16;   // max degree + 1 handled by the register-unrolled loops
-
 struct SlotPtrs {
     double *C, *Cp, *lam, *lamN, *xb, *means, *mpart, *eqerr, *psq;
-    void *R, *posold, *Cf, *pinf;
+    void *P0, *P1, *Cf, *pinf;
+    int* rflag;
+    SlotShared* sh;
 };
 
 __device__ __forceinline__ SlotPtrs slot_ptrs(unsigned char* smem, const SmemLayout& L, int s) {
@@ -147,131 +152,420 @@ __device__ __forceinline__ SlotPtrs slot_ptrs(unsigned char* smem, const SmemLay
     P.mpart = (double*)(b + L.mpart);
     P.eqerr = (double*)(b + L.eqerr);
     P.psq = (double*)(b + L.psq);
-    P.R = (void*)(b + L.R);
-    P.posold = (void*)(b + L.posold);
+    P.P0 = (void*)(b + L.P0);
+    P.P1 = (void*)(b + L.P1);
+    P.rflag = (int*)(b + L.rflag);
     P.Cf = (void*)(b + L.Cf);
     P.pinf = (void*)(b + L.pinf);
+    P.sh = (SlotShared*)(b + L.sh);
     return P;
 }
 
-// ---------------------------------------------------------------- T phase
-// Per-thread buffers R (scattered residual) and posold (positions of the
-// previous iterate) are [t][RS] with RS = 3 NB + 1: thread t touches only
-// its own row, at compile-time offsets, and the odd row stride keeps the
-// warp's accesses on distinct banks.
-template <int NB> struct RowStride { static constexpr int value = 3 * NB + 1; };
-
-// Returns false (and writes nothing) when the fast pass met an exactly-zero
-// component; the caller then reruns the time step with CAREFUL = true.
-template <typename T, int NB, bool CAREFUL>
-__device__ __forceinline__ bool term_pass(const SolveParams& p, const T* __restrict__ Wt, const SlotPtrs& sp,
-                                          int k, int t, const Family<T>& fp, const Family<T>& fw,
-                                          T cx, T cy, T cz) {
-    constexpr int RS = RowStride<NB>::value;
-    const int n = p.n, MP = p.MP;
-    const T* Cf = (const T*)sp.Cf;
-    T* Rrow = (T*)sp.R + t * RS;
-    T* Orow = (T*)sp.posold + t * RS;
-
-    T pos[3 * NB];
-    {
-        T w[KMAX];
-#pragma unroll
-        for (int q = 0; q < KMAX; ++q) w[q] = (q < MP) ? Wt[t * MP + q] : T(0);
-#pragma unroll
-        for (int ax = 0; ax < 3; ++ax) {
-#pragma unroll
-            for (int i = 0; i < NB; ++i) {
-                T s = T(0);
-                if (i < n) {
-                    const T* c = Cf + (ax * n + i) * MP;
-#pragma unroll
-                    for (int q = 0; q < KMAX; ++q)
-                        if (q < MP) s = fma_t<T>(c[q], w[q], s);
-                }
-                pos[ax * NB + i] = s;
-            }
-        }
-    }
-    // k == 0: no previous iterate; "old" := "new" (that exit residual is discarded).
-    // Idempotent, so it is safe even if this fast pass is redone carefully.
-    if (k == 0) {
-#pragma unroll
-        for (int q = 0; q < 3 * NB; ++q)
-            if ((q % NB) < n) Orow[q] = pos[q];
-    }
-
-    T acc[3 * NB];
-#pragma unroll
-    for (int q = 0; q < 3 * NB; ++q) acc[q] = T(0);
-    T inf = T(0), sq = T(0), zmin = T(1);
-
-#pragma unroll
-    for (int i = 0; i < NB; ++i) {
-        if (i < n) {
-            const T pix = pos[i], piy = pos[NB + i], piz = pos[2 * NB + i];
-            const T oix = Orow[i], oiy = Orow[NB + i], oiz = Orow[2 * NB + i];
-#pragma unroll
-            for (int j = i + 1; j < NB; ++j) {
-                if (j < n) {
-                    const T dx = pix - pos[j], dy = piy - pos[NB + j], dz = piz - pos[2 * NB + j];
-                    T rx, ry, rz;
-                    resid<T, true, CAREFUL>(dx, dy, dz, dx, dy, dz, fp, zmin, rx, ry, rz);
-                    acc[i] += rx;
-                    acc[NB + i] += ry;
-                    acc[2 * NB + i] += rz;
-                    acc[j] -= rx;
-                    acc[NB + j] -= ry;
-                    acc[2 * NB + j] -= rz;
-                    const T ox = oix - Orow[j], oy = oiy - Orow[NB + j], oz = oiz - Orow[2 * NB + j];
-                    T xx, xy, xz;
-                    resid<T, true, CAREFUL>(ox, oy, oz, dx, dy, dz, fp, zmin, xx, xy, xz);
-                    inf = fmax(inf, fmax(fabs(xx), fmax(fabs(xy), fabs(xz))));
-                    sq = fma_t<T>(xx, xx, fma_t<T>(xy, xy, fma_t<T>(xz, xz, sq)));
-                }
-            }
-            // workspace containment term of robot i
-            const T rx = pix - cx, ry = piy - cy, rz = piz - cz;
-            T ux, uy, uz;
-            resid<T, false, CAREFUL>(rx, ry, rz, rx, ry, rz, fw, zmin, ux, uy, uz);
-            acc[i] += ux;
-            acc[NB + i] += uy;
-            acc[2 * NB + i] += uz;
-            T xx, xy, xz;
-            resid<T, false, CAREFUL>(oix - cx, oiy - cy, oiz - cz, rx, ry, rz, fw, zmin, xx, xy, xz);
-            inf = fmax(inf, fmax(fabs(xx), fmax(fabs(xy), fabs(xz))));
-            sq = fma_t<T>(xx, xx, fma_t<T>(xy, xy, fma_t<T>(xz, xz, sq)));
-        }
-    }
-    if (!CAREFUL && zmin == T(0)) return false;
-
-#pragma unroll
-    for (int q = 0; q < 3 * NB; ++q) {
-        if ((q % NB) < n) {
-            Rrow[q] = acc[q];
-            Orow[q] = pos[q];
-        }
-    }
-    ((T*)sp.pinf)[t] = inf;
-    sp.psq[t] = (double)sq;
-    return true;
+// Named barrier of one slot.  The non-.aligned form: lanes of a warp may
+// arrive diverged (threads t >= S skip the term pass), which bar.sync
+// (= barrier.sync.aligned) does not allow.
+__device__ __forceinline__ void slot_barrier(int id, int nthreads) {
+    asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-// ---------------------------------------------------------------- load a claimed sample (one row)
+// 16-byte vector of T (float4 / double2) for the row-times-vector loops
+template <typename T> struct Vec16;
+template <> struct Vec16<float> {
+    using type = float4;
+    static constexpr int lanes = 4;
+    __device__ __forceinline__ static void unpack(const float4& v, float* o) {
+        o[0] = v.x;
+        o[1] = v.y;
+        o[2] = v.z;
+        o[3] = v.w;
+    }
+};
+template <> struct Vec16<double> {
+    using type = double2;
+    static constexpr int lanes = 2;
+    __device__ __forceinline__ static void unpack(const double2& v, double* o) {
+        o[0] = v.x;
+        o[1] = v.y;
+    }
+};
+
+template <typename T, int MP>
+__device__ __forceinline__ void load_row16(const T* __restrict__ src, T (&dst)[MP]) {
+    using V = typename Vec16<T>::type;
+    constexpr int L = Vec16<T>::lanes;
+    const V* v = reinterpret_cast<const V*>(src);
+#pragma unroll
+    for (int c = 0; c < MP / L; ++c) Vec16<T>::unpack(v[c], dst + c * L);
+}
+
+// ---------------------------------------------------------------- term pass pieces
+// One bit per term, pairs i<j in loop order then workspace terms.
+template <int NB> struct TermBits {
+    static constexpr int count = NB * (NB - 1) / 2 + NB;
+    static constexpr int words = (count + 31) / 32;
+};
+
+__device__ __forceinline__ bool bit_of(const uint32_t* m, int b) { return (m[b >> 5] >> (b & 31)) & 1u; }
+
+// bit of pair (i < j) and of workspace term i, as closed forms of the loop indices
+// (a loop-carried counter keeps nvcc from fully unrolling the register-indexed loops)
+template <int NB> __host__ __device__ constexpr int pair_bit(int i, int j) { return i * (2 * NB - i - 1) / 2 + (j - i - 1); }
+template <int NB> __host__ __device__ constexpr int ws_bit(int i) { return NB * (NB - 1) / 2 + i; }
+
+// positions of every robot at time step t:  p(t) = C W[t]^T
+template <typename T, int NB, int MP>
+__device__ __forceinline__ void positions_at(const T* __restrict__ Wt, const T* __restrict__ Cf, int t, int n,
+                                             T (&pos)[3 * NB]) {
+    T w[MP];
+    load_row16<T, MP>(Wt + t * MP, w);
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+            T s = T(0);
+            if (i < n) {
+                T c[MP];
+                load_row16<T, MP>(Cf + (ax * n + i) * MP, c);
+#pragma unroll
+                for (int q = 0; q < MP; ++q) s = fma_t<T>(c[q], w[q], s);
+            }
+            pos[ax * NB + i] = s;
+        }
+    }
+}
+
+// Interior bit of every term at the current positions (terms past n count as
+// interior) and min |component| over all differences (0 -> careful path).
+template <typename T, int NB>
+__device__ __forceinline__ void interior_scan(const T (&pos)[3 * NB], int n, const Family<T>& fp,
+                                              const Family<T>& fw, T cx, T cy, T cz,
+                                              uint32_t (&nm)[TermBits<NB>::words], T& zmin) {
+#pragma unroll
+    for (int w = 0; w < TermBits<NB>::words; ++w) nm[w] = 0xffffffffu;
+    T z = T(1);
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+        const T pix = pos[i], piy = pos[NB + i], piz = pos[2 * NB + i];
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {   // constant trip count: nvcc fully unrolls only those
+            const int b = pair_bit<NB>(i, j);
+            if (j > i && j < n) {
+                const T dx = pix - pos[j], dy = piy - pos[NB + j], dz = piz - pos[2 * NB + j];
+                z = fmin(z, fmin(fabs(dx), fmin(fabs(dy), fabs(dz))));
+                const T q = fma_t<T>(dz * fp.beta, dz, fma_t<T>(dy, dy, dx * dx));
+                if (!(q >= fp.lim)) nm[b >> 5] &= ~(1u << (b & 31));
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+        const int b = ws_bit<NB>(i);
+        if (i < n) {
+            const T rx = pos[i] - cx, ry = pos[NB + i] - cy, rz = pos[2 * NB + i] - cz;
+            z = fmin(z, fmin(fabs(rx), fmin(fabs(ry), fabs(rz))));
+            const T q = fma_t<T>(rz * fw.beta, rz, fma_t<T>(ry, ry, rx * rx));
+            if (!(q <= fw.lim)) nm[b >> 5] &= ~(1u << (b & 31));
+        }
+    }
+    zmin = z;
+}
+
+// Exit residual over all terms as if every term were interior at both
+// iterates: x = Dp_i - Dp_j per pair, x = Dp_i per workspace term.  inf =
+// per-axis max(range of Dp, max |Dp|), sq = per-axis n sum (Dp - mean)^2 +
+// sum Dp^2 (O(n) instead of O(n^2)).  Also returns, per axis, the robots
+// attaining the range and the max |Dp| (to validate inf when terms are flagged).
+template <typename T, int NB> struct QuietStats {
+    T inf, sq;
+    T range[3], wmax[3];
+    int imax[3], imin[3], iabs[3];
+};
+
+template <typename T, int NB>
+__device__ __forceinline__ QuietStats<T, NB> quiet_residual(const T (&pos)[3 * NB], const T* __restrict__ Pold, int n) {
+    QuietStats<T, NB> st;
+    T mx = T(0), s2 = T(0);
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+        T lo = T(0), hi = T(0), sum = T(0), am = T(0);
+        int ilo = 0, ihi = 0, iam = 0;
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+            if (i < n) {
+                const T dpi = pos[ax * NB + i] - Pold[ax * NB + i];
+                if (i == 0 || dpi < lo) { lo = dpi; ilo = i; }
+                if (i == 0 || dpi > hi) { hi = dpi; ihi = i; }
+                if (i == 0 || fabs(dpi) > am) { am = fabs(dpi); iam = i; }
+                sum += dpi;
+            }
+        }
+        const T mean = sum / (T)n;
+        T var = T(0), own = T(0);
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+            if (i < n) {
+                const T dpi = pos[ax * NB + i] - Pold[ax * NB + i];
+                const T c = dpi - mean;
+                var = fma_t<T>(c, c, var);
+                own = fma_t<T>(dpi, dpi, own);
+            }
+        }
+        st.range[ax] = hi - lo;
+        st.wmax[ax] = am;
+        st.imax[ax] = ihi;
+        st.imin[ax] = ilo;
+        st.iabs[ax] = iam;
+        mx = fmax(mx, fmax(hi - lo, am));
+        s2 += fma_t<T>((T)n, var, own);
+    }
+    st.inf = mx;
+    st.sq = s2;
+    return st;
+}
+
+// Flagged terms (active now or at the previous iterate), O(#flagged): true
+// exit residual, scatter of d - e for terms active now (into acc), and the
+// corrections of the quiet statistics.  Runtime-indexed data comes from the
+// position rows in shared memory.  Returns true if the max over the
+// unflagged terms needs an exact recompute (a range-attaining pair or
+// max-|Dp| robot is itself flagged).
+template <typename T, int NB>
+__device__ __forceinline__ bool flagged_terms(const T* __restrict__ Pnew, const T* __restrict__ Pold, int n,
+                                              const Family<T>& fp, const Family<T>& fw, T cx, T cy, T cz,
+                                              const uint32_t (&nm)[TermBits<NB>::words],
+                                              const uint32_t (&om)[TermBits<NB>::words],
+                                              const QuietStats<T, NB>& st, T (&acc)[3 * NB], T& flmax, T& dsq,
+                                              bool& act_new) {
+    constexpr int NP = NB * (NB - 1) / 2;
+    bool need_exact = false;
+#pragma unroll
+    for (int w = 0; w < TermBits<NB>::words; ++w) {
+        uint32_t fl = ~(nm[w] & om[w]);
+        while (fl) {
+            const int bit = __ffs(fl) - 1;
+            fl &= fl - 1;
+            const int b = w * 32 + bit;
+            if (b >= TermBits<NB>::count) break;
+            const bool in_new = (nm[w] >> bit) & 1u, in_old = (om[w] >> bit) & 1u;
+            if (b < NP) {
+                int i = 0, rem = b;
+                while (rem >= NB - 1 - i) { rem -= NB - 1 - i; ++i; }
+                const int j = i + 1 + rem;
+                T d[3], o[3], x[3];
+#pragma unroll
+                for (int ax = 0; ax < 3; ++ax) {
+                    const T ni = Pnew[ax * NB + i], nj = Pnew[ax * NB + j];
+                    const T oi = Pold[ax * NB + i], oj = Pold[ax * NB + j];
+                    d[ax] = ni - nj;
+                    o[ax] = oi - oj;
+                    x[ax] = (ni - oi) - (nj - oj);   // Dp_i - Dp_j exactly as in quiet_residual
+                    dsq -= x[ax] * x[ax];
+                    need_exact = need_exact || ((i == st.imax[ax] && j == st.imin[ax]) ||
+                                                (j == st.imax[ax] && i == st.imin[ax]));
+                }
+                if (!in_old) {
+                    const T qo = fma_t<T>(o[2] * fp.beta, o[2], fma_t<T>(o[1], o[1], o[0] * o[0]));
+                    const T so = qo > T(0) ? fp.lat * rsq<T>(qo) : T(0);
+#pragma unroll
+                    for (int ax = 0; ax < 3; ++ax) x[ax] = fma_t<T>(-so, o[ax], d[ax]);
+                }
+                if (!in_new) {
+                    act_new = true;
+                    const T q = fma_t<T>(d[2] * fp.beta, d[2], fma_t<T>(d[1], d[1], d[0] * d[0]));
+                    const T s = fp.lat * rsq<T>(q);
+#pragma unroll
+                    for (int ax = 0; ax < 3; ++ax) {
+                        const T r = fma_t<T>(-s, d[ax], d[ax]);
+#pragma unroll
+                        for (int m = 0; m < NB; ++m) {
+                            if (m == i) acc[ax * NB + m] += r;
+                            if (m == j) acc[ax * NB + m] -= r;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int ax = 0; ax < 3; ++ax) {
+                    flmax = fmax(flmax, fabs(x[ax]));
+                    dsq = fma_t<T>(x[ax], x[ax], dsq);
+                }
+            } else {
+                const int i = b - NP;
+                const T c3[3] = {cx, cy, cz};
+                T d[3], o[3], x[3];
+#pragma unroll
+                for (int ax = 0; ax < 3; ++ax) {
+                    const T ni = Pnew[ax * NB + i], oi = Pold[ax * NB + i];
+                    d[ax] = ni - c3[ax];
+                    o[ax] = oi - c3[ax];
+                    x[ax] = ni - oi;
+                    dsq -= x[ax] * x[ax];
+                    need_exact = need_exact || (i == st.iabs[ax]);
+                }
+                if (!in_old) {
+                    const T qo = fma_t<T>(o[2] * fw.beta, o[2], fma_t<T>(o[1], o[1], o[0] * o[0]));
+                    const T so = qo > T(0) ? fw.lat * rsq<T>(qo) : T(0);
+#pragma unroll
+                    for (int ax = 0; ax < 3; ++ax) x[ax] = fma_t<T>(-so, o[ax], d[ax]);
+                }
+                if (!in_new) {
+                    act_new = true;
+                    const T q = fma_t<T>(d[2] * fw.beta, d[2], fma_t<T>(d[1], d[1], d[0] * d[0]));
+                    const T s = fw.lat * rsq<T>(q);
+#pragma unroll
+                    for (int ax = 0; ax < 3; ++ax) {
+                        const T r = fma_t<T>(-s, d[ax], d[ax]);
+#pragma unroll
+                        for (int m = 0; m < NB; ++m)
+                            if (m == i) acc[ax * NB + m] += r;
+                    }
+                }
+#pragma unroll
+                for (int ax = 0; ax < 3; ++ax) {
+                    flmax = fmax(flmax, fabs(x[ax]));
+                    dsq = fma_t<T>(x[ax], x[ax], dsq);
+                }
+            }
+        }
+    }
+    return need_exact;
+}
+
+// Exact max of |x| over the unflagged terms (x = Dp_i - Dp_j, Dp_i), used
+// only when a range-attaining pair is flagged.
+template <typename T, int NB>
+__device__ __noinline__ T unflagged_max(const T* __restrict__ Pnew, const T* __restrict__ Pold, int n,
+                                        const uint32_t* fl) {
+    T dp[3 * NB];
+#pragma unroll
+    for (int q = 0; q < 3 * NB; ++q) dp[q] = ((q % NB) < n) ? Pnew[q] - Pold[q] : T(0);
+    T mx = T(0);
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+            const int b = pair_bit<NB>(i, j);
+            if (j > i && j < n && !((fl[b >> 5] >> (b & 31)) & 1u))
+                mx = fmax(mx, fmax(fabs(dp[i] - dp[j]), fmax(fabs(dp[NB + i] - dp[NB + j]), fabs(dp[2 * NB + i] - dp[2 * NB + j]))));
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+        const int b = ws_bit<NB>(i);
+        if (i < n && !((fl[b >> 5] >> (b & 31)) & 1u))
+            mx = fmax(mx, fmax(fabs(dp[i]), fmax(fabs(dp[NB + i]), fabs(dp[2 * NB + i]))));
+    }
+    return mx;
+}
+
+// Careful path: every term in the reference orientation, targets of terms
+// with an exactly-zero component from the FP64 trig formula.  Sets the new
+// interior bits (zero-component terms count as active) and whether any zero
+// occurred.  Returns whether some term is active now.  Out of line: it runs
+// only for (time steps of) symmetric scenarios.
+template <typename T, int NB> struct PosPack {
+    T v[3 * NB];
+};
+template <int NB> struct MaskPack {
+    uint32_t w[TermBits<NB>::words];
+};
+template <typename T> struct CarefulOut {
+    T inf, sq;
+    bool zero, active;
+};
+
+// (by-value arguments: taking the address of the caller's register arrays
+// would push them to local memory on the hot path)
+template <typename T, int NB>
+__device__ __noinline__ CarefulOut<T> careful_pass(const PosPack<T, NB> pk, T* __restrict__ Orow, int n,
+                                                   const Family<T> fp, const Family<T> fw, T cx, T cy, T cz,
+                                                   MaskPack<NB>* nmo) {
+    const T* pos = pk.v;
+    MaskPack<NB> nmw;
+    uint32_t* nm = nmw.w;
+    T Rrow[3 * NB];   // accumulated here; written over the (then dead) old row at the end
+#pragma unroll
+    for (int q = 0; q < 3 * NB; ++q) Rrow[q] = T(0);
+#pragma unroll
+    for (int w = 0; w < TermBits<NB>::words; ++w) nm[w] = 0xffffffffu;
+    T mx = T(0), s2 = T(0);
+    bool znow = false, act = false;
+    int b = 0;
+    for (int i = 0; i < NB; ++i) {
+        for (int j = i + 1; j < NB; ++j, ++b) {
+            if (i < n && j < n) {
+                const T dx = pos[i] - pos[j], dy = pos[NB + i] - pos[NB + j], dz = pos[2 * NB + i] - pos[2 * NB + j];
+                T rx, ry, rz, xx, xy, xz;
+                T zu = T(1);
+                resid<T, true, true>(dx, dy, dz, dx, dy, dz, fp, zu, rx, ry, rz);
+                Rrow[i] += rx;
+                Rrow[NB + i] += ry;
+                Rrow[2 * NB + i] += rz;
+                Rrow[j] -= rx;
+                Rrow[NB + j] -= ry;
+                Rrow[2 * NB + j] -= rz;
+                const T ox = Orow[i] - Orow[j], oy = Orow[NB + i] - Orow[NB + j], oz = Orow[2 * NB + i] - Orow[2 * NB + j];
+                resid<T, true, true>(ox, oy, oz, dx, dy, dz, fp, zu, xx, xy, xz);
+                const T q = fma_t<T>(dz * fp.beta, dz, fma_t<T>(dy, dy, dx * dx));
+                const bool zero = (dx == T(0)) || (dy == T(0)) || (dz == T(0));
+                znow = znow || zero;
+                if (!(q >= fp.lim) || zero) {
+                    nm[b >> 5] &= ~(1u << (b & 31));
+                    act = true;
+                }
+                mx = fmax(mx, fmax(fabs(xx), fmax(fabs(xy), fabs(xz))));
+                s2 = fma_t<T>(xx, xx, fma_t<T>(xy, xy, fma_t<T>(xz, xz, s2)));
+            }
+        }
+    }
+    for (int i = 0; i < NB; ++i, ++b) {
+        if (i < n) {
+            const T rx = pos[i] - cx, ry = pos[NB + i] - cy, rz = pos[2 * NB + i] - cz;
+            T ux, uy, uz, xx, xy, xz;
+            T zu = T(1);
+            resid<T, false, true>(rx, ry, rz, rx, ry, rz, fw, zu, ux, uy, uz);
+            Rrow[i] += ux;
+            Rrow[NB + i] += uy;
+            Rrow[2 * NB + i] += uz;
+            resid<T, false, true>(Orow[i] - cx, Orow[NB + i] - cy, Orow[2 * NB + i] - cz, rx, ry, rz, fw, zu, xx, xy,
+                                  xz);
+            const T q = fma_t<T>(rz * fw.beta, rz, fma_t<T>(ry, ry, rx * rx));
+            const bool zero = (rx == T(0)) || (ry == T(0)) || (rz == T(0));
+            znow = znow || zero;
+            if (!(q <= fw.lim) || zero) {
+                nm[b >> 5] &= ~(1u << (b & 31));
+                act = true;
+            }
+            mx = fmax(mx, fmax(fabs(xx), fmax(fabs(xy), fabs(xz))));
+            s2 = fma_t<T>(xx, xx, fma_t<T>(xy, xy, fma_t<T>(xz, xz, s2)));
+        }
+    }
+    for (int q = 0; q < 3 * NB; ++q)
+        if ((q % NB) < n) Orow[q] = Rrow[q];
+    *nmo = nmw;
+    CarefulOut<T> r;
+    r.inf = mx;
+    r.sq = s2;
+    r.zero = znow;
+    r.active = act;
+    return r;
+}
+
+// ---------------------------------------------------------------- load a sample (one coefficient row)
+template <typename T, int MP>
 __device__ __forceinline__ void load_row(const SolveParams& p, const SlotPtrs& sp, int sample, int r,
                                          const double* __restrict__ B6, const double* __restrict__ rhs,
-                                         const double* __restrict__ PBt, bool is_float) {
+                                         const double* __restrict__ PBt) {
     const int m1 = p.m1, dim = 3 * p.n * m1;
     const double* xr = p.xi_bar + (size_t)sample * dim + r * m1;
-    double x[KMAX], c[KMAX], l[KMAX];
+    double x[MP], c[MP], l[MP];
 #pragma unroll
-    for (int q = 0; q < KMAX; ++q) x[q] = (q < m1) ? xr[q] : 0.0;
+    for (int q = 0; q < MP; ++q) x[q] = (q < m1) ? xr[q] : 0.0;
     const int mode = p.init_mode ? p.init_mode[sample] : 0;
     if (mode) {
         const double* cr = p.xi0 + (size_t)sample * dim + r * m1;
         const double* lr = p.lam0 + (size_t)sample * dim + r * m1;
 #pragma unroll
-        for (int q = 0; q < KMAX; ++q) {
+        for (int q = 0; q < MP; ++q) {
             c[q] = (q < m1) ? cr[q] : 0.0;
             l[q] = (q < m1) ? lr[q] : 0.0;
         }
@@ -281,46 +575,40 @@ __device__ __forceinline__ void load_row(const SolveParams& p, const SlotPtrs& s
         for (int cnd = 0; cnd < 6; ++cnd) {
             double e = 0.0;
 #pragma unroll
-            for (int q = 0; q < KMAX; ++q)
-                if (q < m1) e = fma(B6[cnd * m1 + q], x[q], e);
+            for (int q = 0; q < MP; ++q) e = fma(B6[cnd * MP + q], x[q], e);
             res[cnd] = e - rhs[r * 6 + cnd];
         }
 #pragma unroll
-        for (int q = 0; q < KMAX; ++q) {
+        for (int q = 0; q < MP; ++q) {
             double corr = 0.0;
 #pragma unroll
-            for (int cnd = 0; cnd < 6; ++cnd)
-                if (q < m1) corr = fma(PBt[q * 6 + cnd], res[cnd], corr);
+            for (int cnd = 0; cnd < 6; ++cnd) corr = fma(PBt[q * 6 + cnd], res[cnd], corr);
             c[q] = x[q] - corr;
             l[q] = 0.0;
         }
     }
 #pragma unroll
-    for (int q = 0; q < KMAX; ++q) {
-        if (q < m1) {
-            const int idx = r * m1 + q;
-            sp.xb[idx] = x[q];
-            sp.C[idx] = c[q];
-            sp.lam[idx] = l[q];
-            if (p.want_prev) sp.Cp[idx] = c[q];
-        }
-        if (q < p.MP) {
-            if (is_float) ((float*)sp.Cf)[r * p.MP + q] = (q < m1) ? (float)c[q] : 0.f;
-            else ((double*)sp.Cf)[r * p.MP + q] = (q < m1) ? c[q] : 0.0;
-        }
+    for (int q = 0; q < MP; ++q) {
+        const int idx = r * MP + q;
+        sp.xb[idx] = x[q];
+        sp.C[idx] = c[q];
+        sp.lam[idx] = l[q];
+        if (p.want_prev) sp.Cp[idx] = c[q];
+        ((T*)sp.Cf)[idx] = (T)c[q];
     }
 }
 
 // ---------------------------------------------------------------- the kernel
-template <typename T, int NB, int MAXT>
+template <typename T, int NB, int MP, int MAXT>
 __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const SmemLayout L = make_layout<T, NB>(p.n, p.S, p.m1, p.MP, p.spb, p.want_prev);
+    const SmemLayout L = make_layout<T, NB>(p.n, p.S, MP, p.spb, p.want_prev);
     constexpr int RS = RowStride<NB>::value;
-    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
-    const int n = p.n, S = p.S, m1 = p.m1, MP = p.MP, spb = p.spb;
-    const int R3 = 3 * n, dim = R3 * m1, m2 = 2 * m1;
-    const bool is_float = sizeof(T) == 4;
+    constexpr int M2P = 2 * MP;
+    constexpr int NW = TermBits<NB>::words;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int n = p.n, S = p.S, m1 = p.m1;
+    const int R3 = 3 * n, dim = R3 * m1, dimp = R3 * MP;
 
     T* Wt = (T*)(smem + L.W);
     double* KMm = (double*)(smem + L.KMm);
@@ -329,112 +617,179 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
     double* B6 = (double*)(smem + L.B6);
     double* rhs = (double*)(smem + L.rhs);
     double* PBt = (double*)(smem + L.PBt);
-    SlotState* st[2] = {(SlotState*)(smem + L.st0), (SlotState*)(smem + L.st1)};
-    SlotScratch* sc = (SlotScratch*)(smem + L.sc);
 
+    // shared constants, zero-padded to MP columns
     for (int i = tid; i < S * MP; i += nt) {
         const int t = i / MP, q = i % MP;
         Wt[i] = (q < m1) ? (T)p.W[t * m1 + q] : T(0);
     }
-    for (int i = tid; i < m1 * m2; i += nt) {
-        KMm[i] = p.KMm[i];
-        KMd[i] = p.KMd[i];
+    for (int i = tid; i < MP * M2P; i += nt) {
+        const int q = i / M2P, c = i % M2P, half = c / MP, q2 = c % MP;
+        const bool in = q < m1 && q2 < m1;
+        KMm[i] = in ? p.KMm[q * 2 * m1 + half * m1 + q2] : 0.0;
+        KMd[i] = in ? p.KMd[q * 2 * m1 + half * m1 + q2] : 0.0;
     }
-    for (int i = tid; i < dim; i += nt) cconst[i] = p.cconst[i];
-    for (int i = tid; i < 6 * m1; i += nt) B6[i] = p.B6[i];
+    for (int i = tid; i < dimp; i += nt) {
+        const int r = i / MP, q = i % MP;
+        cconst[i] = (q < m1) ? p.cconst[r * m1 + q] : 0.0;
+    }
+    for (int i = tid; i < 6 * MP; i += nt) {
+        const int c = i / MP, q = i % MP;
+        B6[i] = (q < m1) ? p.B6[c * m1 + q] : 0.0;
+    }
     for (int i = tid; i < R3 * 6; i += nt) rhs[i] = p.rhs[i];
-    for (int i = tid; i < m1 * 6; i += nt) PBt[i] = p.PBt[i];
-    if (tid < spb) {
-        sc[tid].pending = atomicAdd(p.queue, 1);
-        sc[tid].done = 1;
-    }
-    __syncthreads();
-    for (int it = tid; it < spb * R3; it += nt) {
-        const int s = it / R3, r = it % R3;
-        if (sc[s].pending < p.batch) load_row(p, slot_ptrs(smem, L, s), sc[s].pending, r, B6, rhs, PBt, is_float);
-    }
-    if (tid < spb) {
-        SlotState z;
-        z.sample = sc[tid].pending;
-        z.k = 0;
-        z.state = (z.sample < p.batch) ? SLOT_ACTIVE : SLOT_EMPTY;
-        z.pad = 0;
-        st[0][tid] = z;
+    for (int i = tid; i < MP * 6; i += nt) {
+        const int q = i / 6;
+        PBt[i] = (q < m1) ? p.PBt[i] : 0.0;
     }
     __syncthreads();
 
-    const int my_slot = tid / S, my_t = tid - (tid / S) * S;
-    const bool term_thread = tid < spb * S;
+    // ---- this thread's slot (an independent warp group)
+    const int gsize = 32 * p.wps;
+    const int slot = tid / gsize, lt = tid - slot * gsize, lane = lt & 31, lwarp = lt >> 5;
+    if (slot >= p.spb) return;
+    const int bar_id = 1 + slot;
+    const SlotPtrs sp = slot_ptrs(smem, L, slot);
     const Family<T> fp = make_family<T>(p.lat, p.vert);
     const Family<T> fw = make_family<T>(p.ws_lat, p.ws_vert);
     const T cx = (T)p.cx, cy = (T)p.cy, cz = (T)p.cz;
     const int half = (S + 1) / 2;
 
-    for (int round = 0;; ++round) {
-        const SlotState* cur = st[round & 1];
-        SlotState* nxt = st[(round + 1) & 1];
-        bool any = false;
-        for (int s = 0; s < spb; ++s) any |= (cur[s].state == SLOT_ACTIVE);
-        if (!any) break;
+    uint32_t imask[NW];
+    bool zprev = false;
 
-        // ---------------- T: term pass
-        if (term_thread && cur[my_slot].state == SLOT_ACTIVE) {
-            const SlotPtrs sp = slot_ptrs(smem, L, my_slot);
-            const int k = cur[my_slot].k;
-            if (!term_pass<T, NB, false>(p, Wt, sp, k, my_t, fp, fw, cx, cy, cz))
-                term_pass<T, NB, true>(p, Wt, sp, k, my_t, fp, fw, cx, cy, cz);
-        }
-        __syncthreads();
+    if (lt == 0) {
+        sp.sh->sample = atomicAdd(p.queue, 1);
+        sp.sh->active = 0;
+    }
+    slot_barrier(bar_id, gsize);
+    int sample = sp.sh->sample;
 
-        // ---------------- G: lam' = lam - rho R W   and the per-slot decision
-        {
-            const int nitems = spb * R3 * 2;
-            for (int it0 = 0; it0 < nitems; it0 += nt) {
-                const int item = it0 + tid;
-                const int s = item / (2 * R3), rem = item - s * (2 * R3), r = rem >> 1, h = rem & 1;
-                const int rreg = (r / n) * NB + (r % n);
-                const bool valid = item < nitems && cur[s].state == SLOT_ACTIVE;
-                T g[KMAX];
+    while (sample < p.batch) {
+        // ---------------- load the sample, default start = boundary projection
+        for (int r = lt; r < R3; r += gsize) load_row<T, MP>(p, sp, sample, r, B6, rhs, PBt);
+        slot_barrier(bar_id, gsize);
+
+        for (int k = 0;; ++k) {
+            // position rows: old = iterate k, new = iterate k+1's input positions; R -> old row
+            T* Prow_old = (T*)((k & 1) ? sp.P1 : sp.P0) + lt * RS;
+            T* Prow_new = (T*)((k & 1) ? sp.P0 : sp.P1) + lt * RS;
+            // ---------------- T: term pass
+            if (lt < S) {
+                T pos[3 * NB];
+                positions_at<T, NB, MP>(Wt, (const T*)sp.Cf, lt, n, pos);
 #pragma unroll
-                for (int q = 0; q < KMAX; ++q) g[q] = T(0);
-                SlotPtrs sp;
-                if (valid) {
-                    sp = slot_ptrs(smem, L, s);
-                    const T* Rr = (const T*)sp.R + rreg;
-                    const int t0 = h ? half : 0, t1 = h ? S : half;
-                    for (int t = t0; t < t1; ++t) {
-                        const T rv = Rr[t * RS];
-                        const T* wr = Wt + t * MP;
+                for (int q = 0; q < 3 * NB; ++q) {
+                    if ((q % NB) < n) {
+                        Prow_new[q] = pos[q];
+                        if (k == 0) Prow_old[q] = pos[q];   // no previous iterate: "old" := "new"
+                    }
+                }
+                if (k == 0) {
 #pragma unroll
-                        for (int q = 0; q < KMAX; ++q)
-                            if (q < MP) g[q] = fma_t<T>(rv, wr[q], g[q]);
+                    for (int w = 0; w < NW; ++w) imask[w] = 0xffffffffu;
+                    zprev = false;
+                }
+                uint32_t nm[NW];
+                T zmin;
+                interior_scan<T, NB>(pos, n, fp, fw, cx, cy, cz, nm, zmin);
+                T inf, sq;
+                bool active = false;
+                if (__builtin_expect(zmin == T(0) || zprev, 0)) {
+                    PosPack<T, NB> pk;
+#pragma unroll
+                    for (int q = 0; q < 3 * NB; ++q) pk.v[q] = pos[q];
+                    MaskPack<NB> mo;
+                    const CarefulOut<T> co = careful_pass<T, NB>(pk, Prow_old, n, fp, fw, cx, cy, cz, &mo);
+#pragma unroll
+                    for (int w = 0; w < NW; ++w) nm[w] = mo.w[w];
+                    inf = co.inf;
+                    sq = co.sq;
+                    active = co.active;
+                    zprev = co.zero;
+                } else {
+                    const QuietStats<T, NB> st = quiet_residual<T, NB>(pos, Prow_old, n);
+                    inf = st.inf;
+                    sq = st.sq;
+                    uint32_t any = 0u;
+#pragma unroll
+                    for (int w = 0; w < NW; ++w) any |= ~(nm[w] & imask[w]);
+                    if (__builtin_expect(any != 0u, 0)) {
+                        T acc[3 * NB];
+#pragma unroll
+                        for (int q = 0; q < 3 * NB; ++q) acc[q] = T(0);
+                        T flmax = T(0), dsq = T(0);
+                        const bool need_exact = flagged_terms<T, NB>(Prow_new, Prow_old, n, fp, fw, cx, cy, cz, nm,
+                                                                     imask, st, acc, flmax, dsq, active);
+                        T base = st.inf;
+                        if (need_exact) {
+                            uint32_t fl[NW];
+#pragma unroll
+                            for (int w = 0; w < NW; ++w) fl[w] = ~(nm[w] & imask[w]);
+                            base = unflagged_max<T, NB>(Prow_new, Prow_old, n, fl);
+                        }
+                        inf = fmax(base, flmax);
+                        sq = fmax(sq + dsq, T(0));
+                        if (active) {   // the old row is dead now: it becomes this thread's R row
+#pragma unroll
+                            for (int q = 0; q < 3 * NB; ++q)
+                                if ((q % NB) < n) Prow_old[q] = acc[q];
+                        }
                     }
                 }
 #pragma unroll
-                for (int q = 0; q < KMAX; ++q) g[q] += __shfl_xor_sync(0xffffffffu, g[q], 1);
-                if (valid) {
-                    const int kh = (m1 + 1) >> 1;
-                    const int q0 = h ? kh : 0, q1 = h ? m1 : kh;
+                for (int w = 0; w < NW; ++w) imask[w] = nm[w];
+                sp.rflag[lt] = active ? 1 : 0;
+                ((T*)sp.pinf)[lt] = inf;
+                sp.psq[lt] = (double)sq;
+                if (active) atomicOr(&sp.sh->active, 1);
+            }
+            slot_barrier(bar_id, gsize);
+
+            // ---------------- G: lam' = lam - rho R W (R is sparse; skipped when nothing is active)
+            const bool any_active = sp.sh->active != 0;
+            for (int it0 = 0; it0 < 2 * R3; it0 += gsize) {
+                const int item = it0 + lt;
+                const bool valid = item < 2 * R3;
+                const int r = item >> 1, h = item & 1;
+                T g[MP];
 #pragma unroll
-                    for (int q = 0; q < KMAX; ++q)
-                        if (q >= q0 && q < q1)
-                            sp.lamN[r * m1 + q] = sp.lam[r * m1 + q] - p.rho * (double)g[q];
+                for (int q = 0; q < MP; ++q) g[q] = T(0);
+                if (valid && any_active) {
+                    const T* Rr = (const T*)((k & 1) ? sp.P1 : sp.P0) + (r / n) * NB + (r % n);
+                    const int t0 = h ? half : 0, t1 = h ? S : half;
+                    for (int t = t0; t < t1; ++t) {
+                        if (!sp.rflag[t]) continue;   // R row valid only where a term was active
+                        const T rv = Rr[t * RS];
+                        if (rv != T(0)) {
+                            T w[MP];
+                            load_row16<T, MP>(Wt + t * MP, w);
+#pragma unroll
+                            for (int q = 0; q < MP; ++q) g[q] = fma_t<T>(rv, w[q], g[q]);
+                        }
+                    }
+                }
+                if (any_active) {
+#pragma unroll
+                    for (int q = 0; q < MP; ++q) g[q] += __shfl_xor_sync(0xffffffffu, g[q], 1);
+                }
+                if (valid) {
+#pragma unroll
+                    for (int q = 0; q < MP; ++q)
+                        if ((q & 1) == h) sp.lamN[r * MP + q] = sp.lam[r * MP + q] - p.rho * (double)g[q];
                 }
             }
-            for (int s = warp; s < spb; s += nwarps) {
-                if (cur[s].state != SLOT_ACTIVE) continue;
-                const SlotPtrs sp = slot_ptrs(smem, L, s);
-                const int k = cur[s].k;
+            if (lwarp == 0) {   // decision: exit residual of iteration k-1, early stop, SingularKKT
                 double emax = 0.0;
-                if (k >= 1)
-                    for (int r = lane; r < R3; r += 32) emax = fmax(emax, sp.eqerr[r]);
                 T inf = T(0);
                 double sqs = 0.0;
-                if (k >= 1)
+                if (k >= 1) {
+                    for (int r = lane; r < R3; r += 32) emax = fmax(emax, sp.eqerr[r]);
                     for (int t = lane; t < S; t += 32) {
                         inf = fmax(inf, ((const T*)sp.pinf)[t]);
                         sqs += sp.psq[t];
                     }
+                }
 #pragma unroll
                 for (int off = 16; off > 0; off >>= 1) {
                     emax = fmax(emax, __shfl_xor_sync(0xffffffffu, emax, off));
@@ -445,157 +800,130 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                     const bool failed = (k >= 1) && (emax > p.tol_eq);
                     bool done = failed;
                     if (k >= 1) {
-                        const size_t h = (size_t)cur[s].sample * p.max_iters + (k - 1);
-                        p.res_inf[h] = (double)inf;
-                        p.res_l2[h] = sqrt(sqs);
-                        sc[s].last_inf = (double)inf;
+                        const size_t hix = (size_t)sample * p.max_iters + (k - 1);
+                        p.res_inf[hix] = (double)inf;
+                        p.res_l2[hix] = sqrt(sqs);
+                        sp.sh->last_inf = (double)inf;
                         done = done || (p.early_stop && (double)inf <= p.tol_res) || (k >= p.max_iters);
                     }
-                    sc[s].done = done;
-                    sc[s].failed = failed;
-                    sc[s].eqmax = emax;
+                    sp.sh->done = done;
+                    sp.sh->failed = failed;
+                    sp.sh->eqmax = emax;
+#ifdef SGSF_DEBUG
+                    if (blockIdx.x == 0 && slot == 0 && k < 4)
+                        printf("D k=%d sample=%d inf=%g sqs=%g emax=%g done=%d C0=%g Cf0=%g\n", k, sample, (double)inf, sqs,
+                               emax, (int)done, sp.C[0], (double)((T*)sp.Cf)[0]);
+#endif
                 }
             }
-        }
-        __syncthreads();
+            slot_barrier(bar_id, gsize);
+            if (lt == 0) sp.sh->active = 0;   // every thread has read it; next writes come after a barrier
 
-        // ---------------- M: finalize finished slots / swarm means for the others
-        for (int it = tid; it < spb * dim; it += nt) {
-            const int s = it / dim, e = it - s * dim;
-            if (cur[s].state == SLOT_ACTIVE && sc[s].done && !sc[s].failed) {
-                const SlotPtrs sp = slot_ptrs(smem, L, s);
-                const size_t o = (size_t)cur[s].sample * dim + e;
-                p.coeffs[o] = sp.C[e];
-                p.mult[o] = sp.lam[e];
-                if (p.want_prev && p.coeffs_prev) p.coeffs_prev[o] = sp.Cp[e];
-            }
-        }
-        for (int s = warp; s < spb; s += nwarps) {
-            if (cur[s].state != SLOT_ACTIVE || !sc[s].done) continue;
-            const SlotPtrs sp = slot_ptrs(smem, L, s);
-            double acc = 0.0;
-            for (int e = lane; e < dim; e += 32) {
-                const double dd = sp.C[e] - sp.xb[e];
-                acc = fma(dd, dd, acc);
-            }
+            if (sp.sh->done) {
+                // ---------------- finalize: outputs of the returned iterate, claim the next sample
+                const bool failed = sp.sh->failed;
+                if (!failed) {
+                    for (int e = lt; e < dim; e += gsize) {
+                        const int r = e / m1, q = e - r * m1;
+                        const size_t o = (size_t)sample * dim + e;
+                        p.coeffs[o] = sp.C[r * MP + q];
+                        p.mult[o] = sp.lam[r * MP + q];
+                        if (p.want_prev && p.coeffs_prev) p.coeffs_prev[o] = sp.Cp[r * MP + q];
+                    }
+                }
+                if (lwarp == 0) {
+                    double acc = 0.0;
+                    for (int e = lane; e < dimp; e += 32) {
+                        const double dd = sp.C[e] - sp.xb[e];
+                        acc = fma(dd, dd, acc);
+                    }
 #pragma unroll
-            for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-            if (lane == 0) {
-                const int b = cur[s].sample;
-                const bool failed = sc[s].failed;
-                p.iterations[b] = failed ? 0 : cur[s].k;
-                p.converged[b] = (!failed && sc[s].last_inf <= p.tol_res) ? 1 : 0;
-                p.displacement[b] = failed ? CUDART_NAN : sqrt(acc);
-                p.status[b] = failed ? SAMPLE_SINGULAR_KKT : SAMPLE_OK;
-                p.eq_err[b] = sc[s].eqmax;
-                sc[s].pending = atomicAdd(p.queue, 1);
+                    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+                    if (lane == 0) {
+                        p.iterations[sample] = failed ? 0 : k;
+                        p.converged[sample] = (!failed && sp.sh->last_inf <= p.tol_res) ? 1 : 0;
+                        p.displacement[sample] = failed ? CUDART_NAN : sqrt(acc);
+                        p.status[sample] = failed ? SAMPLE_SINGULAR_KKT : SAMPLE_OK;
+                        p.eq_err[sample] = sp.sh->eqmax;
+                        sp.sh->sample = atomicAdd(p.queue, 1);
+                    }
+                }
+                slot_barrier(bar_id, gsize);
+                sample = sp.sh->sample;
+                break;
             }
-        }
-        for (int it = tid; it < spb * 3 * m1; it += nt) {
-            const int s = it / (3 * m1), rem = it - s * 3 * m1, ax = rem / m1, q = rem - ax * m1;
-            if (cur[s].state != SLOT_ACTIVE || sc[s].done) continue;
-            const SlotPtrs sp = slot_ptrs(smem, L, s);
-            double cs = 0.0, us = 0.0;
-            for (int i = 0; i < n; ++i) {
-                const int idx = (ax * n + i) * m1 + q;
-                cs += sp.C[idx];
-                us += 2.0 * sp.lamN[idx] - sp.lam[idx] + sp.xb[idx];
+
+            // ---------------- M: swarm means of C and u = 2 lam' - lam + xi_bar
+            for (int it = lt; it < 3 * MP; it += gsize) {
+                const int ax = it / MP, q = it - ax * MP;
+                double cs = 0.0, us = 0.0;
+                for (int i = 0; i < n; ++i) {
+                    const int idx = (ax * n + i) * MP + q;
+                    cs += sp.C[idx];
+                    us += 2.0 * sp.lamN[idx] - sp.lam[idx] + sp.xb[idx];
+                }
+                sp.means[ax * MP + q] = cs / n;
+                sp.means[3 * MP + ax * MP + q] = us / n;
             }
-            sp.means[ax * m1 + q] = cs / n;
-            sp.means[3 * m1 + ax * m1 + q] = us / n;
-        }
-        __syncthreads();
+            slot_barrier(bar_id, gsize);
 
-        // ---------------- M2: mean part of the xi-step / load newly claimed samples
-        for (int it = tid; it < spb * 3 * m1; it += nt) {
-            const int s = it / (3 * m1), rem = it - s * 3 * m1, ax = rem / m1, q = rem - ax * m1;
-            if (cur[s].state != SLOT_ACTIVE || sc[s].done) continue;
-            const SlotPtrs sp = slot_ptrs(smem, L, s);
-            const double* cb = sp.means + ax * m1;
-            const double* ub = sp.means + 3 * m1 + ax * m1;
-            const double* row = KMm + q * m2;
-            double acc = 0.0;
-            for (int q2 = 0; q2 < m1; ++q2) acc = fma(row[q2], cb[q2], acc);
-            for (int q2 = 0; q2 < m1; ++q2) acc = fma(row[m1 + q2], ub[q2], acc);
-            sp.mpart[ax * m1 + q] = acc;
-        }
-        for (int it = tid; it < spb * R3; it += nt) {
-            const int s = it / R3, r = it - s * R3;
-            if (cur[s].state == SLOT_ACTIVE && sc[s].done && sc[s].pending < p.batch)
-                load_row(p, slot_ptrs(smem, L, s), sc[s].pending, r, B6, rhs, PBt, is_float);
-        }
-        __syncthreads();
-
-        // ---------------- X: decoupled xi-step, equality check, commit lam'
-        for (int it = tid; it < spb * R3; it += nt) {
-            const int s = it / R3, r = it - s * R3;
-            if (cur[s].state != SLOT_ACTIVE || sc[s].done) continue;
-            const SlotPtrs sp = slot_ptrs(smem, L, s);
-            const int ax = r / n;
-            const double* cb = sp.means + ax * m1;
-            const double* ub = sp.means + 3 * m1 + ax * m1;
-            double dC[KMAX], dU[KMAX], cn[KMAX];
+            // ---------------- M2: mean part  Mm C_bar + Km11 u_bar
+            for (int it = lt; it < 3 * MP; it += gsize) {
+                const int ax = it / MP, q = it - ax * MP;
+                const double* cb = sp.means + ax * MP;
+                const double* ub = sp.means + 3 * MP + ax * MP;
+                const double* row = KMm + q * M2P;
+                double acc = 0.0;
 #pragma unroll
-            for (int q = 0; q < KMAX; ++q) {
-                if (q < m1) {
-                    const int idx = r * m1 + q;
+                for (int q2 = 0; q2 < MP; ++q2) acc = fma(row[q2], cb[q2], acc);
+#pragma unroll
+                for (int q2 = 0; q2 < MP; ++q2) acc = fma(row[MP + q2], ub[q2], acc);
+                sp.mpart[ax * MP + q] = acc;
+            }
+            slot_barrier(bar_id, gsize);
+
+            // ---------------- X: decoupled xi-step, equality check, commit lam'
+            for (int r = lt; r < R3; r += gsize) {
+                const int ax = r / n;
+                const double* cb = sp.means + ax * MP;
+                const double* ub = sp.means + 3 * MP + ax * MP;
+                double dC[MP], dU[MP], cn[MP];
+#pragma unroll
+                for (int q = 0; q < MP; ++q) {
+                    const int idx = r * MP + q;
                     dC[q] = sp.C[idx] - cb[q];
                     dU[q] = (2.0 * sp.lamN[idx] - sp.lam[idx] + sp.xb[idx]) - ub[q];
-                } else {
-                    dC[q] = 0.0;
-                    dU[q] = 0.0;
                 }
-            }
 #pragma unroll
-            for (int q = 0; q < KMAX; ++q) {
-                double acc = 0.0;
-                if (q < m1) {
-                    const double* row = KMd + q * m2;
-                    acc = sp.mpart[ax * m1 + q] + cconst[r * m1 + q];
+                for (int q = 0; q < MP; ++q) {
+                    const double* row = KMd + q * M2P;
+                    double acc = sp.mpart[ax * MP + q] + cconst[r * MP + q];
 #pragma unroll
-                    for (int q2 = 0; q2 < KMAX; ++q2)
-                        if (q2 < m1) acc = fma(row[q2], dC[q2], acc);
+                    for (int q2 = 0; q2 < MP; ++q2) acc = fma(row[q2], dC[q2], acc);
 #pragma unroll
-                    for (int q2 = 0; q2 < KMAX; ++q2)
-                        if (q2 < m1) acc = fma(row[m1 + q2], dU[q2], acc);
+                    for (int q2 = 0; q2 < MP; ++q2) acc = fma(row[MP + q2], dU[q2], acc);
+                    cn[q] = acc;
                 }
-                cn[q] = acc;
-            }
-            double emax = 0.0;
+                double emax = 0.0;
 #pragma unroll
-            for (int cnd = 0; cnd < 6; ++cnd) {
-                double e = -rhs[r * 6 + cnd];
+                for (int cnd = 0; cnd < 6; ++cnd) {
+                    double e = -rhs[r * 6 + cnd];
 #pragma unroll
-                for (int q = 0; q < KMAX; ++q)
-                    if (q < m1) e = fma(B6[cnd * m1 + q], cn[q], e);
-                emax = fmax(emax, fabs(e));
-            }
-            sp.eqerr[r] = emax;
+                    for (int q = 0; q < MP; ++q) e = fma(B6[cnd * MP + q], cn[q], e);
+                    emax = fmax(emax, fabs(e));
+                }
+                sp.eqerr[r] = emax;
 #pragma unroll
-            for (int q = 0; q < KMAX; ++q) {
-                if (q < m1) {
-                    const int idx = r * m1 + q;
+                for (int q = 0; q < MP; ++q) {
+                    const int idx = r * MP + q;
                     if (p.want_prev) sp.Cp[idx] = sp.C[idx];
                     sp.C[idx] = cn[q];
                     sp.lam[idx] = sp.lamN[idx];
-                    ((T*)sp.Cf)[r * MP + q] = (T)cn[q];
+                    ((T*)sp.Cf)[idx] = (T)cn[q];
                 }
             }
+            slot_barrier(bar_id, gsize);
         }
-        if (tid < spb) {
-            SlotState z = cur[tid];
-            if (z.state == SLOT_ACTIVE) {
-                if (sc[tid].done) {
-                    z.sample = sc[tid].pending;
-                    z.k = 0;
-                    z.state = (z.sample < p.batch) ? SLOT_ACTIVE : SLOT_EMPTY;
-                } else {
-                    z.k += 1;
-                }
-            }
-            nxt[tid] = z;
-        }
-        __syncthreads();
     }
 }
 

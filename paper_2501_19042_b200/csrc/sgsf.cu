@@ -17,6 +17,7 @@
 #include "../../include/sgsf.h"
 #include "sf_aux.cuh"
 #include "sf_device.cuh"
+#include "sf_launch.cuh"
 #include "sf_persistent.cuh"
 
 using namespace sgsf;
@@ -100,7 +101,7 @@ int sgsf_create(const sgsf_problem_t* pr, sgsf_handle_t** out) {
     if (!pr || !out) return fail(SGSF_ERR_INVALID, "null argument");
     if (pr->n < 1 || pr->samples < 2 || pr->m1 < 2)
         return fail(SGSF_ERR_INVALID, "need n >= 1, samples >= 2, m1 >= 2");
-    if (pr->m1 > KMAX) return fail(SGSF_ERR_UNSUPPORTED, "degree + 1 above 16 is not supported");
+    if (pr->m1 > 16) return fail(SGSF_ERR_UNSUPPORTED, "degree + 1 above 16 is not supported");
     sgsf_handle_t* h = new sgsf_handle_t();
     std::memset(h, 0, sizeof(*h));
     h->n = pr->n;
@@ -141,50 +142,10 @@ int sgsf_create(const sgsf_problem_t* pr, sgsf_handle_t** out) {
 }  // extern "C"
 
 // ---------------------------------------------------------------- launch plumbing for K1
-namespace {
-
-template <typename T, int NB, int MAXT>
-int launch_persistent(const sgsf_handle_t* h, SolveParams& p, const sgsf_config_t* cfg,
-                      const sgsf_timing_t* timing, cudaStream_t stream) {
-    auto kern = sf_persistent_kernel<T, NB, MAXT>;
-    int dev_smem = 0;
-    CUDA_TRY(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
-    // slots per CTA: as many as smem and the thread budget allow (a CTA runs one slot per S threads)
-    int spb = cfg->slots_per_block;
-    if (spb <= 0) {
-        spb = 0;
-        for (int s = 1; s * h->S <= MAXT; ++s) {
-            SmemLayout L = make_layout<T, NB>(h->n, h->S, h->m1, p.MP, s, p.want_prev);
-            if (L.total > (size_t)dev_smem) break;
-            spb = s;
-        }
-        // small batches: spread samples over SMs instead of packing them into few CTAs
-        const int spread = (p.batch + h->sm_count - 1) / h->sm_count;
-        if (spb > spread) spb = spread > 0 ? spread : 1;
-    }
-    if (spb <= 0) return fail(SGSF_ERR_UNSUPPORTED, "problem too large for one CTA (samples or smem)");
-    int threads = ((spb * h->S + 31) / 32) * 32;
-    if (threads < 64) threads = 64;
-    if (threads > MAXT) return fail(SGSF_ERR_UNSUPPORTED, "slots_per_block * samples exceeds the CTA size");
-    p.spb = spb;
-    SmemLayout L = make_layout<T, NB>(h->n, h->S, h->m1, p.MP, spb, p.want_prev);
-    if (L.total > (size_t)dev_smem) return fail(SGSF_ERR_UNSUPPORTED, "shared memory budget exceeded");
-    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
-    int per_sm = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, L.total));
-    if (per_sm < 1) per_sm = 1;
-    int grid = cfg->grid > 0 ? cfg->grid : h->sm_count * per_sm;
-    const int need = (p.batch + spb - 1) / spb;
-    if (grid > need) grid = need;
-    if (timing && timing->start) CUDA_TRY(cudaEventRecord((cudaEvent_t)timing->start, stream));
-    kern<<<grid, threads, L.total, stream>>>(p);
-    g_launches.fetch_add(1);
-    CUDA_TRY(cudaGetLastError());
-    if (timing && timing->stop) CUDA_TRY(cudaEventRecord((cudaEvent_t)timing->stop, stream));
-    return SGSF_OK;
-}
-
-}  // namespace
+namespace sgsf {
+int internal_fail(int code, const std::string& msg) { return fail(code, msg); }
+void internal_count_launch(int n) { g_launches.fetch_add((uint64_t)n); }
+}  // namespace sgsf
 
 extern "C" {
 
@@ -209,7 +170,6 @@ int sgsf_solve(sgsf_handle_t* h, int batch, const double* xi_bar, const double* 
     p.n = h->n;
     p.S = h->S;
     p.m1 = h->m1;
-    p.MP = (h->m1 + 3) & ~3;
     p.batch = batch;
     p.max_iters = cfg->max_iters;
     p.early_stop = cfg->early_stop ? 1 : 0;
@@ -250,14 +210,20 @@ int sgsf_solve(sgsf_handle_t* h, int batch, const double* xi_bar, const double* 
 
     const bool strict = cfg->precision == SGSF_PRECISION_STRICT;
     const int n = h->n;
+    const bool wide = h->m1 > 12;
+    LaunchInfo li{h->device, h->sm_count};
+#define SGSF_PICK(T, NB, MAXT)                                                  \
+    return wide ? launch_persistent<T, NB, 16, MAXT>(li, p, cfg, timing, stream) \
+                : launch_persistent<T, NB, 12, MAXT>(li, p, cfg, timing, stream)
     if (!strict) {
-        if (n <= 4) return launch_persistent<float, 4, 512>(h, p, cfg, timing, stream);
-        if (n <= 8) return launch_persistent<float, 8, 384>(h, p, cfg, timing, stream);
-        return launch_persistent<float, 16, 320>(h, p, cfg, timing, stream);
+        if (n <= 4) SGSF_PICK(float, 4, 512);
+        if (n <= 8) SGSF_PICK(float, 8, 384);
+        SGSF_PICK(float, 16, 384);
     }
-    if (n <= 4) return launch_persistent<double, 4, 384>(h, p, cfg, timing, stream);
-    if (n <= 8) return launch_persistent<double, 8, 256>(h, p, cfg, timing, stream);
-    return launch_persistent<double, 16, 256>(h, p, cfg, timing, stream);
+    if (n <= 4) SGSF_PICK(double, 4, 384);
+    if (n <= 8) SGSF_PICK(double, 8, 256);
+    SGSF_PICK(double, 16, 256);
+#undef SGSF_PICK
 }
 
 int sgsf_verdict(sgsf_handle_t* h, int batch, const double* coeffs, const uint8_t* converged, double tol,

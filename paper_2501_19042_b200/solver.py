@@ -323,6 +323,9 @@ class SafetyFilter:
         ws = torch.empty(int(lib.sgsf_workspace_bytes()), dtype=torch.uint8, device=dev)
         tm = None
         if timing is not None:
+            for ev in timing:        # torch creates the CUDA event lazily on its first record()
+                if not ev.cuda_event:
+                    ev.record()
             tm = native.Timing(timing[0].cuda_event, timing[1].cuda_event)
         with torch.cuda.device(dev):
             stream = _stream()
