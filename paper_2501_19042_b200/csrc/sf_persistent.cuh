@@ -125,7 +125,7 @@ __host__ __device__ inline SmemLayout make_layout(int n, int S, int MP, int spb,
     L.P0 = q;     q = align16(q + (size_t)RS * S * ts);
     L.P1 = q;     q = align16(q + (size_t)RS * S * ts);
     L.rflag = q;  q = align16(q + (size_t)S * sizeof(int));
-    L.Cf = q;     q = align16(q + (size_t)R3 * MP * ts);
+    L.Cf = q;     q = align16(q + (size_t)3 * MP * NB * ts);
     L.pinf = q;   q = align16(q + (size_t)S * ts);
     L.sh = q;     q = align16(q + sizeof(SlotShared));
     L.slot_stride = q;
@@ -212,115 +212,198 @@ __device__ __forceinline__ bool bit_of(const uint32_t* m, int b) { return (m[b >
 template <int NB> __host__ __device__ constexpr int pair_bit(int i, int j) { return i * (2 * NB - i - 1) / 2 + (j - i - 1); }
 template <int NB> __host__ __device__ constexpr int ws_bit(int i) { return NB * (NB - 1) / 2 + i; }
 
-// positions of every robot at time step t:  p(t) = C W[t]^T
+// positions of every robot at time step t:  p(t) = C W[t]^T.  Cf is stored
+// robot-minor ([ax][q][NB]) so two robots' coefficients form one f32x2
+// operand.  Robots past n become "phantoms" at distinct, far-away positions:
+// every pair term with a phantom is interior and has no zero component, so
+// the O(n^2) scan needs no per-pair guards.
+template <typename T> __device__ __forceinline__ T phantom_pos(int i) { return T(1e30) * T(i + 1); }
+
 template <typename T, int NB, int MP>
 __device__ __forceinline__ void positions_at(const T* __restrict__ Wt, const T* __restrict__ Cf, int t, int n,
                                              T (&pos)[3 * NB]) {
     T w[MP];
     load_row16<T, MP>(Wt + t * MP, w);
+    if constexpr (sizeof(T) == 4 && NB % 4 == 0) {
+        float2 w2[MP];
 #pragma unroll
-    for (int ax = 0; ax < 3; ++ax) {
+        for (int q = 0; q < MP; ++q) w2[q] = make_float2(w[q], w[q]);
 #pragma unroll
-        for (int i = 0; i < NB; ++i) {
-            T s = T(0);
-            if (i < n) {
-                T c[MP];
-                load_row16<T, MP>(Cf + (ax * n + i) * MP, c);
+        for (int ax = 0; ax < 3; ++ax) {
 #pragma unroll
-                for (int q = 0; q < MP; ++q) s = fma_t<T>(c[q], w[q], s);
+            for (int i4 = 0; i4 < NB; i4 += 4) {
+                float2 a01 = make_float2(0.f, 0.f), a23 = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int q = 0; q < MP; ++q) {
+                    const float4 c = *reinterpret_cast<const float4*>(Cf + (ax * MP + q) * NB + i4);
+                    a01 = __ffma2_rn(make_float2(c.x, c.y), w2[q], a01);
+                    a23 = __ffma2_rn(make_float2(c.z, c.w), w2[q], a23);
+                }
+                pos[ax * NB + i4] = a01.x;
+                pos[ax * NB + i4 + 1] = a01.y;
+                pos[ax * NB + i4 + 2] = a23.x;
+                pos[ax * NB + i4 + 3] = a23.y;
             }
-            pos[ax * NB + i] = s;
+        }
+    } else {
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) {
+#pragma unroll
+            for (int i = 0; i < NB; ++i) {
+                T s = T(0);
+#pragma unroll
+                for (int q = 0; q < MP; ++q) s = fma_t<T>(Cf[(ax * MP + q) * NB + i], w[q], s);
+                pos[ax * NB + i] = s;
+            }
         }
     }
+#pragma unroll
+    for (int q = 0; q < 3 * NB; ++q)
+        if ((q % NB) >= n) pos[q] = phantom_pos<T>(q % NB);
 }
 
 // Interior bit of every term at the current positions (terms past n count as
 // interior) and min |component| over all differences (0 -> careful path).
+// Pair terms are scanned only when `pairs` is set (see the motion bound in
+// the kernel); workspace terms always.  Common case: every term interior --
+// the scan then keeps running min(q) over the pairs, max(q) over the
+// workspace terms and min |component|, each split four ways so the
+// accumulations are independent instruction chains; per-term bits are
+// computed in a second pass only when needed.  Returns min q over the pairs.
 template <typename T, int NB>
-__device__ __forceinline__ void interior_scan(const T (&pos)[3 * NB], int n, const Family<T>& fp,
-                                              const Family<T>& fw, T cx, T cy, T cz,
-                                              uint32_t (&nm)[TermBits<NB>::words], T& zmin) {
+__device__ __forceinline__ T interior_scan(const T (&pos)[3 * NB], int n, const Family<T>& fp, const Family<T>& fw,
+                                           T cx, T cy, T cz, bool pairs, uint32_t (&nm)[TermBits<NB>::words],
+                                           T& zmin) {
+    T qm[4], zm[4];
 #pragma unroll
-    for (int w = 0; w < TermBits<NB>::words; ++w) nm[w] = 0xffffffffu;
-    T z = T(1);
+    for (int u = 0; u < 4; ++u) {
+        qm[u] = T(1e38);
+        zm[u] = T(1);
+    }
+    if (pairs) {
 #pragma unroll
-    for (int i = 0; i < NB; ++i) {
-        const T pix = pos[i], piy = pos[NB + i], piz = pos[2 * NB + i];
+        for (int i = 0; i < NB; ++i) {
+            const T pix = pos[i], piy = pos[NB + i], piz = pos[2 * NB + i];
 #pragma unroll
-        for (int j = 0; j < NB; ++j) {   // constant trip count: nvcc fully unrolls only those
-            const int b = pair_bit<NB>(i, j);
-            if (j > i && j < n) {
-                const T dx = pix - pos[j], dy = piy - pos[NB + j], dz = piz - pos[2 * NB + j];
-                z = fmin(z, fmin(fabs(dx), fmin(fabs(dy), fabs(dz))));
-                const T q = fma_t<T>(dz * fp.beta, dz, fma_t<T>(dy, dy, dx * dx));
-                if (!(q >= fp.lim)) nm[b >> 5] &= ~(1u << (b & 31));
+            for (int j = 0; j < NB; ++j) {   // constant trip count: nvcc fully unrolls only those
+                if (j > i) {
+                    const int u = pair_bit<NB>(i, j) & 3;
+                    const T dx = pix - pos[j], dy = piy - pos[NB + j], dz = piz - pos[2 * NB + j];
+                    zm[u] = fmin(zm[u], fmin(fabs(dx), fmin(fabs(dy), fabs(dz))));
+                    qm[u] = fmin(qm[u], fma_t<T>(dz * fp.beta, dz, fma_t<T>(dy, dy, dx * dx)));
+                }
             }
         }
     }
+    T qw = T(0);
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
-        const int b = ws_bit<NB>(i);
         if (i < n) {
             const T rx = pos[i] - cx, ry = pos[NB + i] - cy, rz = pos[2 * NB + i] - cz;
-            z = fmin(z, fmin(fabs(rx), fmin(fabs(ry), fabs(rz))));
-            const T q = fma_t<T>(rz * fw.beta, rz, fma_t<T>(ry, ry, rx * rx));
-            if (!(q <= fw.lim)) nm[b >> 5] &= ~(1u << (b & 31));
+            zm[i & 3] = fmin(zm[i & 3], fmin(fabs(rx), fmin(fabs(ry), fabs(rz))));
+            qw = fmax(qw, fma_t<T>(rz * fw.beta, rz, fma_t<T>(ry, ry, rx * rx)));
         }
     }
-    zmin = z;
+    zmin = fmin(fmin(zm[0], zm[1]), fmin(zm[2], zm[3]));
+#pragma unroll
+    for (int w = 0; w < TermBits<NB>::words; ++w) nm[w] = 0xffffffffu;
+    const T qmin = fmin(fmin(qm[0], qm[1]), fmin(qm[2], qm[3]));
+    if (__builtin_expect(!(qmin >= fp.lim), 0)) {
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+#pragma unroll
+            for (int j = 0; j < NB; ++j) {
+                if (j > i) {
+                    const int b = pair_bit<NB>(i, j);
+                    const T dx = pos[i] - pos[j], dy = pos[NB + i] - pos[NB + j], dz = pos[2 * NB + i] - pos[2 * NB + j];
+                    const T q = fma_t<T>(dz * fp.beta, dz, fma_t<T>(dy, dy, dx * dx));
+                    if (!(q >= fp.lim)) nm[b >> 5] &= ~(1u << (b & 31));
+                }
+            }
+        }
+    }
+    if (__builtin_expect(!(qw <= fw.lim), 0)) {
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+            const int b = ws_bit<NB>(i);
+            if (i < n) {
+                const T rx = pos[i] - cx, ry = pos[NB + i] - cy, rz = pos[2 * NB + i] - cz;
+                const T q = fma_t<T>(rz * fw.beta, rz, fma_t<T>(ry, ry, rx * rx));
+                if (!(q <= fw.lim)) nm[b >> 5] &= ~(1u << (b & 31));
+            }
+        }
+    }
+    return qmin;
 }
 
-// Exit residual over all terms as if every term were interior at both
-// iterates: x = Dp_i - Dp_j per pair, x = Dp_i per workspace term.  inf =
-// per-axis max(range of Dp, max |Dp|), sq = per-axis n sum (Dp - mean)^2 +
-// sum Dp^2 (O(n) instead of O(n^2)).  Also returns, per axis, the robots
-// attaining the range and the max |Dp| (to validate inf when terms are flagged).
 template <typename T, int NB> struct QuietStats {
     T inf, sq;
+    T dmax2;   // max_i a^2 |Dp_i|_s^2 (same quadratic form as q): bounds the motion of every pair
     T range[3], wmax[3];
     int imax[3], imin[3], iabs[3];
 };
 
+// One pass per axis: min, max, max |Dp|, sum and sum of squares of Dp;
+// sq = (n+1) sum Dp^2 - (sum Dp)^2 (= n sum (Dp - mean)^2 + sum Dp^2).
 template <typename T, int NB>
-__device__ __forceinline__ QuietStats<T, NB> quiet_residual(const T (&pos)[3 * NB], const T* __restrict__ Pold, int n) {
+__device__ __forceinline__ QuietStats<T, NB> quiet_residual(const T (&pos)[3 * NB], const T* __restrict__ Pold, int n,
+                                                            T fp_beta) {
     QuietStats<T, NB> st;
     T mx = T(0), s2 = T(0);
+    T dq[NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) dq[i] = T(0);
 #pragma unroll
     for (int ax = 0; ax < 3; ++ax) {
-        T lo = T(0), hi = T(0), sum = T(0), am = T(0);
+        T lo = T(1e38), hi = T(-1e38), am = T(0), s1 = T(0), sq = T(0);
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+            if (i < n) {
+                const T dpi = pos[ax * NB + i] - Pold[ax * NB + i];
+                lo = fmin(lo, dpi);
+                hi = fmax(hi, dpi);
+                am = fmax(am, fabs(dpi));
+                s1 += dpi;
+                sq = fma_t<T>(dpi, dpi, sq);
+                dq[i] = fma_t<T>(ax == 2 ? dpi * fp_beta : dpi, dpi, dq[i]);
+            }
+        }
+        st.range[ax] = hi - lo;
+        st.wmax[ax] = am;
+        mx = fmax(mx, fmax(hi - lo, am));
+        s2 += fmax(fma_t<T>((T)(n + 1), sq, -s1 * s1), sq);
+    }
+    T dm = T(0);
+#pragma unroll
+    for (int i = 0; i < NB; ++i) dm = fmax(dm, dq[i]);
+    st.dmax2 = dm;
+    st.inf = mx;
+    st.sq = s2;
+    return st;
+}
+
+// Robots attaining the per-axis range and max |Dp| (needed only when some
+// term is flagged, to know whether the quiet inf-norm is attained by it).
+template <typename T, int NB>
+__device__ __forceinline__ void quiet_argmax(const T (&pos)[3 * NB], const T* __restrict__ Pold, int n,
+                                             QuietStats<T, NB>& st) {
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+        T lo = T(1e38), hi = T(-1e38), am = T(-1);
         int ilo = 0, ihi = 0, iam = 0;
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
             if (i < n) {
                 const T dpi = pos[ax * NB + i] - Pold[ax * NB + i];
-                if (i == 0 || dpi < lo) { lo = dpi; ilo = i; }
-                if (i == 0 || dpi > hi) { hi = dpi; ihi = i; }
-                if (i == 0 || fabs(dpi) > am) { am = fabs(dpi); iam = i; }
-                sum += dpi;
+                if (dpi < lo) { lo = dpi; ilo = i; }
+                if (dpi > hi) { hi = dpi; ihi = i; }
+                if (fabs(dpi) > am) { am = fabs(dpi); iam = i; }
             }
         }
-        const T mean = sum / (T)n;
-        T var = T(0), own = T(0);
-#pragma unroll
-        for (int i = 0; i < NB; ++i) {
-            if (i < n) {
-                const T dpi = pos[ax * NB + i] - Pold[ax * NB + i];
-                const T c = dpi - mean;
-                var = fma_t<T>(c, c, var);
-                own = fma_t<T>(dpi, dpi, own);
-            }
-        }
-        st.range[ax] = hi - lo;
-        st.wmax[ax] = am;
         st.imax[ax] = ihi;
         st.imin[ax] = ilo;
         st.iabs[ax] = iam;
-        mx = fmax(mx, fmax(hi - lo, am));
-        s2 += fma_t<T>((T)n, var, own);
     }
-    st.inf = mx;
-    st.sq = s2;
-    return st;
 }
 
 // Flagged terms (active now or at the previous iterate), O(#flagged): true
@@ -551,7 +634,7 @@ __device__ __noinline__ CarefulOut<T> careful_pass(const PosPack<T, NB> pk, T* _
 }
 
 // ---------------------------------------------------------------- load a sample (one coefficient row)
-template <typename T, int MP>
+template <typename T, int NB, int MP>
 __device__ __forceinline__ void load_row(const SolveParams& p, const SlotPtrs& sp, int sample, int r,
                                          const double* __restrict__ B6, const double* __restrict__ rhs,
                                          const double* __restrict__ PBt) {
@@ -594,8 +677,10 @@ __device__ __forceinline__ void load_row(const SolveParams& p, const SlotPtrs& s
         sp.C[idx] = c[q];
         sp.lam[idx] = l[q];
         if (p.want_prev) sp.Cp[idx] = c[q];
-        ((T*)sp.Cf)[idx] = (T)c[q];
     }
+    const int ax = r / p.n, i = r - ax * p.n;
+#pragma unroll
+    for (int q = 0; q < MP; ++q) ((T*)sp.Cf)[(ax * MP + q) * NB + i] = (T)c[q];
 }
 
 // ---------------------------------------------------------------- the kernel
@@ -657,6 +742,11 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
 
     uint32_t imask[NW];
     bool zprev = false;
+    // motion bound for skipping the pair scan: every pair had normalised
+    // distance >= rmin at the last scan; since then the pairs moved by at most
+    // cum (sum over iterations of 2 max_i |Dp_i|, normalised).  While
+    // rmin - cum > 1 + margin every pair is provably interior.
+    T rmin = T(0), cum = T(0);
 
     if (lt == 0) {
         sp.sh->sample = atomicAdd(p.queue, 1);
@@ -667,7 +757,7 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
 
     while (sample < p.batch) {
         // ---------------- load the sample, default start = boundary projection
-        for (int r = lt; r < R3; r += gsize) load_row<T, MP>(p, sp, sample, r, B6, rhs, PBt);
+        for (int r = lt; r < R3; r += gsize) load_row<T, NB, MP>(p, sp, sample, r, B6, rhs, PBt);
         slot_barrier(bar_id, gsize);
 
         for (int k = 0;; ++k) {
@@ -690,9 +780,20 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                     for (int w = 0; w < NW; ++w) imask[w] = 0xffffffffu;
                     zprev = false;
                 }
+                // position changes of this step: O(n) statistics, and the motion bound
+                const QuietStats<T, NB> st = quiet_residual<T, NB>(pos, Prow_old, n, fp.beta);
+                cum += T(2) * sqrt(st.dmax2) / fp.lat;
+                bool pairs_prev_in = true;
+#pragma unroll
+                for (int w = 0; w < NW; ++w) pairs_prev_in = pairs_prev_in && (imask[w] == 0xffffffffu);
+                const bool scan_pairs = (k == 0) || zprev || !pairs_prev_in || !(rmin - cum > T(1) + T(1e-3));
                 uint32_t nm[NW];
                 T zmin;
-                interior_scan<T, NB>(pos, n, fp, fw, cx, cy, cz, nm, zmin);
+                const T qmin = interior_scan<T, NB>(pos, n, fp, fw, cx, cy, cz, scan_pairs, nm, zmin);
+                if (scan_pairs) {
+                    rmin = sqrt(qmin) / fp.lat;
+                    cum = T(0);
+                }
                 T inf, sq;
                 bool active = false;
                 if (__builtin_expect(zmin == T(0) || zprev, 0)) {
@@ -708,19 +809,20 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                     active = co.active;
                     zprev = co.zero;
                 } else {
-                    const QuietStats<T, NB> st = quiet_residual<T, NB>(pos, Prow_old, n);
                     inf = st.inf;
                     sq = st.sq;
                     uint32_t any = 0u;
 #pragma unroll
                     for (int w = 0; w < NW; ++w) any |= ~(nm[w] & imask[w]);
                     if (__builtin_expect(any != 0u, 0)) {
+                        QuietStats<T, NB> st2 = st;
+                        quiet_argmax<T, NB>(pos, Prow_old, n, st2);
                         T acc[3 * NB];
 #pragma unroll
                         for (int q = 0; q < 3 * NB; ++q) acc[q] = T(0);
                         T flmax = T(0), dsq = T(0);
                         const bool need_exact = flagged_terms<T, NB>(Prow_new, Prow_old, n, fp, fw, cx, cy, cz, nm,
-                                                                     imask, st, acc, flmax, dsq, active);
+                                                                     imask, st2, acc, flmax, dsq, active);
                         T base = st.inf;
                         if (need_exact) {
                             uint32_t fl[NW];
@@ -883,43 +985,65 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
             slot_barrier(bar_id, gsize);
 
             // ---------------- X: decoupled xi-step, equality check, commit lam'
-            for (int r = lt; r < R3; r += gsize) {
+            // four lanes per coefficient row, MP/4 outputs each; the row is read by all
+            // four lanes before any of them writes it (__syncwarp), the eq-check partial
+            // sums B cn are combined with shuffles.
+            for (int it0 = 0; it0 < 4 * R3; it0 += gsize) {
+                const int item = it0 + lt;
+                const bool valid = item < 4 * R3;
+                const int r = valid ? (item >> 2) : 0, part = item & 3;
+                constexpr int QL = MP / 4;
                 const int ax = r / n;
-                const double* cb = sp.means + ax * MP;
-                const double* ub = sp.means + 3 * MP + ax * MP;
-                double dC[MP], dU[MP], cn[MP];
+                double cn[QL], lamn[QL];
+                double eqp[6];
 #pragma unroll
-                for (int q = 0; q < MP; ++q) {
-                    const int idx = r * MP + q;
-                    dC[q] = sp.C[idx] - cb[q];
-                    dU[q] = (2.0 * sp.lamN[idx] - sp.lam[idx] + sp.xb[idx]) - ub[q];
+                for (int c6 = 0; c6 < 6; ++c6) eqp[c6] = 0.0;
+                if (valid) {
+                    const double* cb = sp.means + ax * MP;
+                    const double* ub = sp.means + 3 * MP + ax * MP;
+                    double dC[MP], dU[MP];
+#pragma unroll
+                    for (int q = 0; q < MP; ++q) {
+                        const int idx = r * MP + q;
+                        dC[q] = sp.C[idx] - cb[q];
+                        dU[q] = (2.0 * sp.lamN[idx] - sp.lam[idx] + sp.xb[idx]) - ub[q];
+                    }
+#pragma unroll
+                    for (int u = 0; u < QL; ++u) {
+                        const int q = part * QL + u;
+                        const double* row = KMd + q * M2P;
+                        double acc = sp.mpart[ax * MP + q] + cconst[r * MP + q];
+#pragma unroll
+                        for (int q2 = 0; q2 < MP; ++q2) acc = fma(row[q2], dC[q2], acc);
+#pragma unroll
+                        for (int q2 = 0; q2 < MP; ++q2) acc = fma(row[MP + q2], dU[q2], acc);
+                        cn[u] = acc;
+                        lamn[u] = sp.lamN[r * MP + q];
+#pragma unroll
+                        for (int c6 = 0; c6 < 6; ++c6) eqp[c6] = fma(B6[c6 * MP + q], acc, eqp[c6]);
+                    }
                 }
-#pragma unroll
-                for (int q = 0; q < MP; ++q) {
-                    const double* row = KMd + q * M2P;
-                    double acc = sp.mpart[ax * MP + q] + cconst[r * MP + q];
-#pragma unroll
-                    for (int q2 = 0; q2 < MP; ++q2) acc = fma(row[q2], dC[q2], acc);
-#pragma unroll
-                    for (int q2 = 0; q2 < MP; ++q2) acc = fma(row[MP + q2], dU[q2], acc);
-                    cn[q] = acc;
-                }
+                __syncwarp();
                 double emax = 0.0;
 #pragma unroll
-                for (int cnd = 0; cnd < 6; ++cnd) {
-                    double e = -rhs[r * 6 + cnd];
-#pragma unroll
-                    for (int q = 0; q < MP; ++q) e = fma(B6[cnd * MP + q], cn[q], e);
-                    emax = fmax(emax, fabs(e));
+                for (int c6 = 0; c6 < 6; ++c6) {
+                    double e = eqp[c6];
+                    e += __shfl_xor_sync(0xffffffffu, e, 1);
+                    e += __shfl_xor_sync(0xffffffffu, e, 2);
+                    emax = fmax(emax, fabs(e - (valid ? rhs[r * 6 + c6] : 0.0)));
                 }
-                sp.eqerr[r] = emax;
+                if (valid) {
+                    if (part == 0) sp.eqerr[r] = emax;
+                    const int i = r - ax * n;
 #pragma unroll
-                for (int q = 0; q < MP; ++q) {
-                    const int idx = r * MP + q;
-                    if (p.want_prev) sp.Cp[idx] = sp.C[idx];
-                    sp.C[idx] = cn[q];
-                    sp.lam[idx] = sp.lamN[idx];
-                    ((T*)sp.Cf)[idx] = (T)cn[q];
+                    for (int u = 0; u < QL; ++u) {
+                        const int q = part * QL + u;
+                        const int idx = r * MP + q;
+                        if (p.want_prev) sp.Cp[idx] = sp.C[idx];
+                        sp.C[idx] = cn[u];
+                        sp.lam[idx] = lamn[u];
+                        ((T*)sp.Cf)[(ax * MP + q) * NB + i] = (T)cn[u];
+                    }
                 }
             }
             slot_barrier(bar_id, gsize);

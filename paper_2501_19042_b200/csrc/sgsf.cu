@@ -328,9 +328,12 @@ int sgsf_solve_host(sgsf_handle_t* h, int batch, const double* xi_bar, const dou
     if (batch <= 0) return batch == 0 ? SGSF_OK : fail(SGSF_ERR_INVALID, "negative batch");
     cudaStream_t stream = (cudaStream_t)stream_;
     const size_t dim = (size_t)3 * h->n * h->m1, B = (size_t)batch, MI = (size_t)cfg->max_iters;
-    // one device arena for inputs + outputs
-    const size_t doubles = B * dim * (3 + (init_mode ? 2 : 0)) + 2 * B * MI + 2 * B;
-    const size_t bytes = doubles * sizeof(double) + B * (4 + 4 + 1 + 1 + 1) + 512;
+    // one device arena for inputs + outputs (sizes rounded to 256 B each)
+    const size_t sizes[] = {B * dim * 8, init_mode ? B * dim * 8 : 0, init_mode ? B * dim * 8 : 0, init_mode ? B : 0,
+                            B * dim * 8, B * dim * 8, B * MI * 8, B * MI * 8, B * 4, B, B * 8, B * 4, B * 8, B,
+                            sgsf_workspace_bytes()};
+    size_t bytes = 0;
+    for (size_t z : sizes) bytes += (z + 255) & ~size_t(255);
     char* arena = nullptr;
     CUDA_TRY(cudaMallocAsync((void**)&arena, bytes, stream));
     size_t off = 0;
@@ -339,24 +342,23 @@ int sgsf_solve_host(sgsf_handle_t* h, int batch, const double* xi_bar, const dou
         off += (nbytes + 255) & ~size_t(255);
         return (void*)q;
     };
-    double* d_xb = (double*)take(B * dim * 8);
-    double* d_x0 = init_mode ? (double*)take(B * dim * 8) : nullptr;
-    double* d_l0 = init_mode ? (double*)take(B * dim * 8) : nullptr;
-    uint8_t* d_mode = init_mode ? (uint8_t*)take(B) : nullptr;
+    double* d_xb = (double*)take(sizes[0]);
+    double* d_x0 = init_mode ? (double*)take(sizes[1]) : nullptr;
+    double* d_l0 = init_mode ? (double*)take(sizes[2]) : nullptr;
+    uint8_t* d_mode = init_mode ? (uint8_t*)take(sizes[3]) : nullptr;
     sgsf_outputs_t o;
     std::memset(&o, 0, sizeof(o));
-    o.coeffs = (double*)take(B * dim * 8);
-    o.multipliers = (double*)take(B * dim * 8);
-    o.res_inf = (double*)take(B * MI * 8);
-    o.res_l2 = (double*)take(B * MI * 8);
-    o.iterations = (int32_t*)take(B * 4);
-    o.converged = (uint8_t*)take(B);
-    o.displacement = (double*)take(B * 8);
-    o.status = (int32_t*)take(B * 4);
-    o.eq_err = (double*)take(B * 8);
-    uint8_t* d_feas = (uint8_t*)take(B);
-    void* ws = take(sgsf_workspace_bytes());
-    (void)bytes;
+    o.coeffs = (double*)take(sizes[4]);
+    o.multipliers = (double*)take(sizes[5]);
+    o.res_inf = (double*)take(sizes[6]);
+    o.res_l2 = (double*)take(sizes[7]);
+    o.iterations = (int32_t*)take(sizes[8]);
+    o.converged = (uint8_t*)take(sizes[9]);
+    o.displacement = (double*)take(sizes[10]);
+    o.status = (int32_t*)take(sizes[11]);
+    o.eq_err = (double*)take(sizes[12]);
+    uint8_t* d_feas = (uint8_t*)take(sizes[13]);
+    void* ws = take(sizes[14]);
     CUDA_TRY(cudaMemcpyAsync(d_xb, xi_bar, B * dim * 8, cudaMemcpyHostToDevice, stream));
     if (init_mode) {
         CUDA_TRY(cudaMemcpyAsync(d_x0, xi0, B * dim * 8, cudaMemcpyHostToDevice, stream));

@@ -218,7 +218,14 @@ def _stream() -> int:
     return torch.cuda.current_stream().cuda_stream
 
 
+def _require_cuda() -> None:
+    if not torch.cuda.is_available():
+        raise native.NativeError("the safety filter runs on a CUDA device (B200); none is visible "
+                                 "(there is no CPU fallback)")
+
+
 def _to_dev(a: np.ndarray) -> torch.Tensor:
+    _require_cuda()
     return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to("cuda", non_blocking=False)
 
 
