@@ -75,6 +75,8 @@ struct SlotShared {
     int done;
     int failed;
     int active;   // some term had an active constraint in this iteration's term pass
+    int scount;   // time steps queued for the cooperative pair scan
+    int pad_;
     double last_inf;
     double eqmax;
 };
@@ -82,6 +84,7 @@ struct SlotShared {
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
 template <int NB> struct RowStride { static constexpr int value = 3 * NB + 1; };
+template <int NB> struct ScanWords { static constexpr int value = (NB * (NB - 1) / 2 + 31) / 32; };
 
 // Shared-memory map.  Coefficient-space arrays are padded to MP (m1 rounded
 // up to a multiple of 4) columns with zeros, so every loop over the degree
@@ -91,9 +94,9 @@ template <int NB> struct RowStride { static constexpr int value = 3 * NB + 1; };
 // the dead old row is reused for the thread's scattered residual R, valid
 // where rflag[t] is set.
 struct SmemLayout {
-    size_t W, KMm, KMd, cconst, B6, rhs, PBt;
+    size_t W, KMm, KMd, cconst, B6, rhs, PBt, ptab;
     size_t slot0, slot_stride;
-    size_t C, Cp, lam, lamN, xb, means, mpart, eqerr, psq, P0, P1, rflag, Cf, pinf, sh;
+    size_t C, Cp, lam, lamN, xb, means, mpart, eqerr, psq, P0, P1, rflag, Cf, pinf, sh, slist, aq, az, anm;
     size_t total;
 };
 
@@ -111,6 +114,7 @@ __host__ __device__ inline SmemLayout make_layout(int n, int S, int MP, int spb,
     L.B6 = o;     o = align16(o + (size_t)6 * MP * d);
     L.rhs = o;    o = align16(o + (size_t)R3 * 6 * d);
     L.PBt = o;    o = align16(o + (size_t)MP * 6 * d);
+    L.ptab = o;   o = align16(o + (size_t)NB * (NB - 1) / 2 * sizeof(int));
     L.slot0 = o;
     size_t q = 0;
     L.C = q;      q = align16(q + (size_t)dimp * d);
@@ -128,6 +132,10 @@ __host__ __device__ inline SmemLayout make_layout(int n, int S, int MP, int spb,
     L.Cf = q;     q = align16(q + (size_t)3 * MP * NB * ts);
     L.pinf = q;   q = align16(q + (size_t)S * ts);
     L.sh = q;     q = align16(q + sizeof(SlotShared));
+    L.slist = q;  q = align16(q + (size_t)S * sizeof(int));
+    L.aq = q;     q = align16(q + (size_t)S * ts);                 // min q over the pairs (as unsigned bits)
+    L.az = q;     q = align16(q + (size_t)S * ts);                 // min |component| over the pairs
+    L.anm = q;    q = align16(q + (size_t)S * ScanWords<NB>::value * sizeof(uint32_t));   // non-interior pair bits
     L.slot_stride = q;
     L.total = o + (size_t)spb * q;
     return L;
@@ -135,8 +143,9 @@ __host__ __device__ inline SmemLayout make_layout(int n, int S, int MP, int spb,
 
 struct SlotPtrs {
     double *C, *Cp, *lam, *lamN, *xb, *means, *mpart, *eqerr, *psq;
-    void *P0, *P1, *Cf, *pinf;
-    int* rflag;
+    void *P0, *P1, *Cf, *pinf, *aq, *az;
+    int *rflag, *slist;
+    uint32_t* anm;
     SlotShared* sh;
 };
 
@@ -158,6 +167,10 @@ __device__ __forceinline__ SlotPtrs slot_ptrs(unsigned char* smem, const SmemLay
     P.Cf = (void*)(b + L.Cf);
     P.pinf = (void*)(b + L.pinf);
     P.sh = (SlotShared*)(b + L.sh);
+    P.slist = (int*)(b + L.slist);
+    P.aq = (void*)(b + L.aq);
+    P.az = (void*)(b + L.az);
+    P.anm = (uint32_t*)(b + L.anm);
     return P;
 }
 
@@ -633,6 +646,82 @@ __device__ __noinline__ CarefulOut<T> careful_pass(const PosPack<T, NB> pk, T* _
     return r;
 }
 
+// ---------------------------------------------------------------- finishing a time step
+// Given the interior bits of every term (nm) and min |component| (zmin), run
+// the careful / quiet / flagged path of time step `lt` and write its outputs:
+// exit-residual partials, R row (over the dead old row) and its flag.
+template <typename T, int NB>
+__device__ __forceinline__ void finish_step(const SlotPtrs& sp, int lt, int n, const T (&pos)[3 * NB],
+                                            T* __restrict__ Prow_old, const T* __restrict__ Prow_new,
+                                            const QuietStats<T, NB>& st, uint32_t (&nm)[TermBits<NB>::words],
+                                            T zmin, uint32_t (&imask)[TermBits<NB>::words], bool& zprev,
+                                            const Family<T>& fp, const Family<T>& fw, T cx, T cy, T cz) {
+    constexpr int NW = TermBits<NB>::words;
+    T inf, sq;
+    bool active = false;
+    if (__builtin_expect(zmin == T(0) || zprev, 0)) {
+        PosPack<T, NB> pk;
+#pragma unroll
+        for (int q = 0; q < 3 * NB; ++q) pk.v[q] = pos[q];
+        MaskPack<NB> mo;
+        const CarefulOut<T> co = careful_pass<T, NB>(pk, Prow_old, n, fp, fw, cx, cy, cz, &mo);
+#pragma unroll
+        for (int w = 0; w < NW; ++w) nm[w] = mo.w[w];
+        inf = co.inf;
+        sq = co.sq;
+        active = co.active;
+        zprev = co.zero;
+    } else {
+        inf = st.inf;
+        sq = st.sq;
+        uint32_t any = 0u;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) any |= ~(nm[w] & imask[w]);
+        if (__builtin_expect(any != 0u, 0)) {
+            QuietStats<T, NB> st2 = st;
+            quiet_argmax<T, NB>(pos, Prow_old, n, st2);
+            T acc[3 * NB];
+#pragma unroll
+            for (int q = 0; q < 3 * NB; ++q) acc[q] = T(0);
+            T flmax = T(0), dsq = T(0);
+            const bool need_exact =
+                flagged_terms<T, NB>(Prow_new, Prow_old, n, fp, fw, cx, cy, cz, nm, imask, st2, acc, flmax, dsq, active);
+            T base = st.inf;
+            if (need_exact) {
+                uint32_t fl[NW];
+#pragma unroll
+                for (int w = 0; w < NW; ++w) fl[w] = ~(nm[w] & imask[w]);
+                base = unflagged_max<T, NB>(Prow_new, Prow_old, n, fl);
+            }
+            inf = fmax(base, flmax);
+            sq = fmax(sq + dsq, T(0));
+            if (active) {   // the old row is dead now: it becomes this thread's R row
+#pragma unroll
+                for (int q = 0; q < 3 * NB; ++q)
+                    if ((q % NB) < n) Prow_old[q] = acc[q];
+            }
+        }
+    }
+#pragma unroll
+    for (int w = 0; w < NW; ++w) imask[w] = nm[w];
+    sp.rflag[lt] = active ? 1 : 0;
+    ((T*)sp.pinf)[lt] = inf;
+    sp.psq[lt] = (double)sq;
+    if (active) atomicOr(&sp.sh->active, 1);
+}
+
+template <typename T> struct UBits;
+template <> struct UBits<float> {
+    using type = unsigned int;
+    __device__ __forceinline__ static unsigned int of(float x) { return __float_as_uint(x); }
+    __device__ __forceinline__ static float val(unsigned int u) { return __uint_as_float(u); }
+};
+template <> struct UBits<double> {
+    using type = unsigned long long;
+    __device__ __forceinline__ static unsigned long long of(double x) { return (unsigned long long)__double_as_longlong(x); }
+    __device__ __forceinline__ static double val(unsigned long long u) { return __longlong_as_double((long long)u); }
+};
+
 // ---------------------------------------------------------------- load a sample (one coefficient row)
 template <typename T, int NB, int MP>
 __device__ __forceinline__ void load_row(const SolveParams& p, const SlotPtrs& sp, int sample, int r,
@@ -727,6 +816,12 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
         const int q = i / 6;
         PBt[i] = (q < m1) ? p.PBt[i] : 0.0;
     }
+    int* ptab = (int*)(smem + L.ptab);   // pair index -> (i | j << 8), lexicographic i < j
+    if (tid == 0) {
+        int b = 0;
+        for (int i = 0; i < NB; ++i)
+            for (int j = i + 1; j < NB; ++j) ptab[b++] = i | (j << 8);
+    }
     __syncthreads();
 
     // ---- this thread's slot (an independent warp group)
@@ -751,6 +846,7 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
     if (lt == 0) {
         sp.sh->sample = atomicAdd(p.queue, 1);
         sp.sh->active = 0;
+        sp.sh->scount = 0;
     }
     slot_barrier(bar_id, gsize);
     int sample = sp.sh->sample;
@@ -764,7 +860,12 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
             // position rows: old = iterate k, new = iterate k+1's input positions; R -> old row
             T* Prow_old = (T*)((k & 1) ? sp.P1 : sp.P0) + lt * RS;
             T* Prow_new = (T*)((k & 1) ? sp.P0 : sp.P1) + lt * RS;
-            // ---------------- T: term pass
+            // ---------------- T1: positions, O(n) statistics, motion bound; quiet steps finish here
+            using UT = typename UBits<T>::type;
+            constexpr int SW = ScanWords<NB>::value;
+            bool need_scan = false;
+            uint32_t nm[NW];
+            T zmin_ws = T(1);
             if (lt < S) {
                 T pos[3 * NB];
                 positions_at<T, NB, MP>(Wt, (const T*)sp.Cf, lt, n, pos);
@@ -780,71 +881,75 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                     for (int w = 0; w < NW; ++w) imask[w] = 0xffffffffu;
                     zprev = false;
                 }
-                // position changes of this step: O(n) statistics, and the motion bound
                 const QuietStats<T, NB> st = quiet_residual<T, NB>(pos, Prow_old, n, fp.beta);
                 cum += T(2) * sqrt(st.dmax2) / fp.lat;
                 bool pairs_prev_in = true;
 #pragma unroll
                 for (int w = 0; w < NW; ++w) pairs_prev_in = pairs_prev_in && (imask[w] == 0xffffffffu);
-                const bool scan_pairs = (k == 0) || zprev || !pairs_prev_in || !(rmin - cum > T(1) + T(1e-3));
-                uint32_t nm[NW];
-                T zmin;
-                const T qmin = interior_scan<T, NB>(pos, n, fp, fw, cx, cy, cz, scan_pairs, nm, zmin);
-                if (scan_pairs) {
-                    rmin = sqrt(qmin) / fp.lat;
-                    cum = T(0);
-                }
-                T inf, sq;
-                bool active = false;
-                if (__builtin_expect(zmin == T(0) || zprev, 0)) {
-                    PosPack<T, NB> pk;
+                need_scan = (k == 0) || zprev || !pairs_prev_in || !(rmin - cum > T(1) + T(1e-3));
+                interior_scan<T, NB>(pos, n, fp, fw, cx, cy, cz, false, nm, zmin_ws);   // workspace terms only
+                if (need_scan) {
+                    const int e = atomicAdd(&sp.sh->scount, 1);
+                    sp.slist[e] = lt;
+                    ((UT*)sp.aq)[lt] = UBits<T>::of(T(1e30));
+                    ((UT*)sp.az)[lt] = UBits<T>::of(T(1));
 #pragma unroll
-                    for (int q = 0; q < 3 * NB; ++q) pk.v[q] = pos[q];
-                    MaskPack<NB> mo;
-                    const CarefulOut<T> co = careful_pass<T, NB>(pk, Prow_old, n, fp, fw, cx, cy, cz, &mo);
-#pragma unroll
-                    for (int w = 0; w < NW; ++w) nm[w] = mo.w[w];
-                    inf = co.inf;
-                    sq = co.sq;
-                    active = co.active;
-                    zprev = co.zero;
+                    for (int w = 0; w < SW; ++w) sp.anm[lt * SW + w] = 0u;
                 } else {
-                    inf = st.inf;
-                    sq = st.sq;
-                    uint32_t any = 0u;
+                    finish_step<T, NB>(sp, lt, n, pos, Prow_old, Prow_new, st, nm, zmin_ws, imask, zprev, fp, fw, cx,
+                                       cy, cz);
+                }
+            }
+            slot_barrier(bar_id, gsize);
+
+            const int L = sp.sh->scount;
+            if (L > 0) {
+                // ---------------- T2: cooperative O(n^2) scan of the queued time steps, 8 pairs per item
+                constexpr int NP = NB * (NB - 1) / 2;
+                constexpr int PPC = 8;
+                constexpr int CH = (NP + PPC - 1) / PPC;
+                const T* Pbase = (const T*)((k & 1) ? sp.P0 : sp.P1);
+                for (int it = lt; it < L * CH; it += gsize) {
+                    const int e = it / CH, c = it - e * CH;
+                    const int t = sp.slist[e];
+                    const T* row = Pbase + t * RS;
+                    T qm = T(1e30), zm = T(1);
+                    uint32_t m = 0u;
 #pragma unroll
-                    for (int w = 0; w < NW; ++w) any |= ~(nm[w] & imask[w]);
-                    if (__builtin_expect(any != 0u, 0)) {
-                        QuietStats<T, NB> st2 = st;
-                        quiet_argmax<T, NB>(pos, Prow_old, n, st2);
-                        T acc[3 * NB];
-#pragma unroll
-                        for (int q = 0; q < 3 * NB; ++q) acc[q] = T(0);
-                        T flmax = T(0), dsq = T(0);
-                        const bool need_exact = flagged_terms<T, NB>(Prow_new, Prow_old, n, fp, fw, cx, cy, cz, nm,
-                                                                     imask, st2, acc, flmax, dsq, active);
-                        T base = st.inf;
-                        if (need_exact) {
-                            uint32_t fl[NW];
-#pragma unroll
-                            for (int w = 0; w < NW; ++w) fl[w] = ~(nm[w] & imask[w]);
-                            base = unflagged_max<T, NB>(Prow_new, Prow_old, n, fl);
-                        }
-                        inf = fmax(base, flmax);
-                        sq = fmax(sq + dsq, T(0));
-                        if (active) {   // the old row is dead now: it becomes this thread's R row
-#pragma unroll
-                            for (int q = 0; q < 3 * NB; ++q)
-                                if ((q % NB) < n) Prow_old[q] = acc[q];
+                    for (int u = 0; u < PPC; ++u) {
+                        const int bb = c * PPC + u;
+                        if (bb < NP) {
+                            const int ij = ptab[bb], i = ij & 0xff, j = ij >> 8;
+                            if (j < n) {
+                                const T dx = row[i] - row[j], dy = row[NB + i] - row[NB + j];
+                                const T dz = row[2 * NB + i] - row[2 * NB + j];
+                                zm = fmin(zm, fmin(fabs(dx), fmin(fabs(dy), fabs(dz))));
+                                const T q = fma_t<T>(dz * fp.beta, dz, fma_t<T>(dy, dy, dx * dx));
+                                qm = fmin(qm, q);
+                                if (!(q >= fp.lim)) m |= 1u << (bb & 31);
+                            }
                         }
                     }
+                    atomicMin(&((UT*)sp.aq)[t], UBits<T>::of(qm));
+                    atomicMin(&((UT*)sp.az)[t], UBits<T>::of(zm));
+                    if (m) atomicOr(&sp.anm[t * SW + ((c * PPC) >> 5)], m);
                 }
+                slot_barrier(bar_id, gsize);
+
+                // ---------------- T3: queued time steps finish with their scan results
+                if (lt < S && need_scan) {
+                    T pos[3 * NB];
 #pragma unroll
-                for (int w = 0; w < NW; ++w) imask[w] = nm[w];
-                sp.rflag[lt] = active ? 1 : 0;
-                ((T*)sp.pinf)[lt] = inf;
-                sp.psq[lt] = (double)sq;
-                if (active) atomicOr(&sp.sh->active, 1);
+                    for (int q = 0; q < 3 * NB; ++q) pos[q] = ((q % NB) < n) ? Prow_new[q] : phantom_pos<T>(q % NB);
+                    const QuietStats<T, NB> st = quiet_residual<T, NB>(pos, Prow_old, n, fp.beta);
+                    rmin = sqrt(UBits<T>::val(((UT*)sp.aq)[lt])) / fp.lat;
+                    cum = T(0);
+                    const T zmin = fmin(zmin_ws, UBits<T>::val(((UT*)sp.az)[lt]));
+#pragma unroll
+                    for (int w = 0; w < SW; ++w) nm[w] &= ~sp.anm[lt * SW + w];
+                    finish_step<T, NB>(sp, lt, n, pos, Prow_old, Prow_new, st, nm, zmin, imask, zprev, fp, fw, cx, cy,
+                                       cz);
+                }
             }
             slot_barrier(bar_id, gsize);
 
@@ -919,7 +1024,10 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                 }
             }
             slot_barrier(bar_id, gsize);
-            if (lt == 0) sp.sh->active = 0;   // every thread has read it; next writes come after a barrier
+            if (lt == 0) {   // every thread has read them; the next writes come after a barrier
+                sp.sh->active = 0;
+                sp.sh->scount = 0;
+            }
 
             if (sp.sh->done) {
                 // ---------------- finalize: outputs of the returned iterate, claim the next sample
