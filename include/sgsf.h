@@ -118,8 +118,8 @@ int sgsf_max_robots(void);
 int sgsf_create(const sgsf_problem_t* problem, sgsf_handle_t** out);
 void sgsf_destroy(sgsf_handle_t* h);
 
-/* bytes of device workspace sgsf_solve needs (sample queue) */
-size_t sgsf_workspace_bytes(void);
+/* bytes of device workspace sgsf_solve needs for `batch` samples (sample queue + longest-first order) */
+size_t sgsf_workspace_bytes(int batch);
 
 /*
  * Run the safety filter on a batch.  xi_bar: B x dim (device).  init_mode: B bytes or NULL

@@ -18,6 +18,8 @@ struct LaunchInfo {
 
 int internal_fail(int code, const std::string& msg);
 void internal_count_launch(int n);
+// longest-first queue order (kernels_order.cu)
+int launch_order(const SolveParams& p, float* score, int* order, cudaStream_t stream);
 
 template <typename T, int NB, int MP, int MAXT>
 int launch_persistent(const LaunchInfo& li, SolveParams& p, const sgsf_config_t* cfg, const sgsf_timing_t* timing,

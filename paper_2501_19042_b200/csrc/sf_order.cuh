@@ -1,0 +1,144 @@
+// sf_order.cuh -- longest-first sample order for the persistent kernel's queue.
+//
+// The persistent kernel hands samples to its slots in queue order.  With a
+// few samples per slot and iteration counts spread over ~2x, plain index
+// order leaves long samples for the end and the last wave idles most SMs.
+// Processing the likely-long samples first (LPT list scheduling) shortens
+// that tail.  The predictor is the total constraint violation of the start
+// iterate, sum over time steps of max(0, 1 - r) over the pair terms and
+// max(0, r - 1) over the workspace terms (r = normalised spheroid radius).
+// Its rank correlation with the iteration count is ~0.7 on the benchmark
+// scenario.  The order only changes which slot runs a sample and when: every
+// sample's result is independent of it.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "sf_persistent.cuh"
+
+namespace sgsf {
+
+// one CTA per sample, thread t = time step; FP32 is plenty for a heuristic
+template <int NB, int MP>
+__global__ void __launch_bounds__(128) start_score_kernel(const SolveParams p, float* __restrict__ score) {
+    __shared__ float Cs[3 * NB * MP];
+    __shared__ float red[4];
+    const int b = blockIdx.x;
+    const int n = p.n, m1 = p.m1, S = p.S, R3 = 3 * n;
+    const int dim = R3 * m1;
+    const bool warm = p.init_mode && p.init_mode[b];
+    for (int r = threadIdx.x; r < R3; r += blockDim.x) {
+        const double* xr = (warm ? p.xi0 : p.xi_bar) + (size_t)b * dim + r * m1;
+        double x[MP];
+#pragma unroll
+        for (int q = 0; q < MP; ++q) x[q] = q < m1 ? xr[q] : 0.0;
+        if (!warm) {   // boundary projection of the proposal (load_row)
+            double res[6];
+#pragma unroll
+            for (int c = 0; c < 6; ++c) {
+                double e = 0.0;
+#pragma unroll
+                for (int q = 0; q < MP; ++q)
+                    if (q < m1) e = fma(p.B6[c * m1 + q], x[q], e);
+                res[c] = e - p.rhs[r * 6 + c];
+            }
+#pragma unroll
+            for (int q = 0; q < MP; ++q) {
+                if (q < m1) {
+                    double corr = 0.0;
+#pragma unroll
+                    for (int c = 0; c < 6; ++c) corr = fma(p.PBt[q * 6 + c], res[c], corr);
+                    x[q] -= corr;
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < MP; ++q) Cs[r * MP + q] = (float)x[q];
+    }
+    __syncthreads();
+    const float ia2 = (float)(1.0 / (p.lat * p.lat)), ib2 = (float)(1.0 / (p.vert * p.vert));
+    const float iw2 = (float)(1.0 / (p.ws_lat * p.ws_lat)), iv2 = (float)(1.0 / (p.ws_vert * p.ws_vert));
+    float v = 0.f;
+    for (int t = threadIdx.x; t < S; t += blockDim.x) {
+        float w[MP];
+#pragma unroll
+        for (int q = 0; q < MP; ++q) w[q] = q < m1 ? (float)p.W[t * m1 + q] : 0.f;
+        float pos[3 * NB];
+#pragma unroll
+        for (int a = 0; a < 3 * NB; ++a) {
+            const int ax = a / NB, i = a % NB;
+            float acc = 0.f;
+            if (i < n) {
+#pragma unroll
+                for (int q = 0; q < MP; ++q) acc = fmaf(Cs[(ax * n + i) * MP + q], w[q], acc);
+            }
+            pos[a] = acc;
+        }
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+            if (i < n) {
+#pragma unroll
+                for (int j = 0; j < NB; ++j) {
+                    if (j > i && j < n) {
+                        const float dx = pos[i] - pos[j], dy = pos[NB + i] - pos[NB + j];
+                        const float dz = pos[2 * NB + i] - pos[2 * NB + j];
+                        v += fmaxf(0.f, 1.f - sqrtf((dx * dx + dy * dy) * ia2 + dz * dz * ib2));
+                    }
+                }
+                const float rx = pos[i] - (float)p.cx, ry = pos[NB + i] - (float)p.cy;
+                const float rz = pos[2 * NB + i] - (float)p.cz;
+                v += fmaxf(0.f, sqrtf((rx * rx + ry * ry) * iw2 + rz * rz * iv2) - 1.f);
+            }
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float s = 0.f;
+        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) s += red[k];
+        score[b] = s;
+    }
+}
+
+// Bucketed counting sort, descending score, one CTA.  Order inside a bucket
+// follows atomic arrival (scheduling only; results do not depend on it).
+constexpr int kOrderBuckets = 2048;
+constexpr int kOrderThreads = 1024;
+
+__global__ void __launch_bounds__(kOrderThreads) lpt_order_kernel(const float* __restrict__ score, int batch,
+                                                                  int* __restrict__ order) {
+    __shared__ unsigned int cnt[kOrderBuckets];
+    __shared__ float smax;
+    for (int k = threadIdx.x; k < kOrderBuckets; k += blockDim.x) cnt[k] = 0u;
+    float mx = 0.f;
+    for (int b = threadIdx.x; b < batch; b += blockDim.x) mx = fmaxf(mx, score[b]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    if (threadIdx.x == 0) smax = 0.f;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) atomicMax((int*)&smax, __float_as_int(mx));   // non-negative floats
+    __syncthreads();
+    const float scale = smax > 0.f ? (float)(kOrderBuckets - 1) / smax : 0.f;
+    auto bucket = [&](float s) {   // bucket 0 = largest scores
+        int k = (int)(fmaxf(s, 0.f) * scale);
+        k = k > kOrderBuckets - 1 ? kOrderBuckets - 1 : k;
+        return kOrderBuckets - 1 - k;
+    };
+    for (int b = threadIdx.x; b < batch; b += blockDim.x) atomicAdd(&cnt[bucket(score[b])], 1u);
+    __syncthreads();
+    if (threadIdx.x == 0) {   // exclusive scan (2048 entries, once per solve)
+        unsigned int run = 0;
+        for (int k = 0; k < kOrderBuckets; ++k) {
+            const unsigned int c = cnt[k];
+            cnt[k] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < batch; b += blockDim.x) order[atomicAdd(&cnt[bucket(score[b])], 1u)] = b;
+}
+
+}  // namespace sgsf

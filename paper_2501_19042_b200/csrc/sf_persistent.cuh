@@ -67,19 +67,33 @@ struct SolveParams {
     double* eq_err;
     double* coeffs_prev;
     int* queue;
+    const int* order;   // queue position -> sample (longest-first), or null for index order
 };
 
-// per-slot scalars (written by one thread, read by the slot after a slot barrier)
+// next sample for a slot: queue position -> sample index
+__device__ __forceinline__ int next_sample(const SolveParams& p) {
+    const int q = atomicAdd(p.queue, 1);
+    return (p.order && q < p.batch) ? p.order[q] : q;
+}
+
+// per-slot scalars.  The per-iteration flags are double-buffered by the
+// iteration parity: iteration k writes buffer k&1 before the term-pass
+// barrier and reads it after; the other buffer was last read before the
+// previous iteration's closing barrier, so one thread clears it during the
+// term pass with no extra barrier.
+constexpr int MAX_SLOT_WORDS = 16;   // time-step bit words (slot size <= 512 threads)
 struct SlotShared {
     int sample;
-    int done;
-    int failed;
-    int active;   // some term had an active constraint in this iteration's term pass
-    int scount;   // time steps queued for the cooperative pair scan
-    int pad_;
-    double last_inf;
-    double eqmax;
+    int active[2];   // some term had an active constraint in the term pass
+    int scount[2];   // time steps queued for the cooperative pair scan
+    uint32_t amask[2][MAX_SLOT_WORDS];   // time steps with an active term (their R row is valid)
 };
+
+__device__ __forceinline__ void clear_flags(SlotShared* sh, int b, int words) {
+    sh->active[b] = 0;
+    sh->scount[b] = 0;
+    for (int w = 0; w < words; ++w) sh->amask[b][w] = 0u;
+}
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
@@ -92,11 +106,11 @@ template <int NB> struct ScanWords { static constexpr int value = (NB * (NB - 1)
 // the positions of iterates k (old) and k+1 (new) as [t][3 NB + 1] rows
 // (thread t owns row t; odd stride -> distinct banks); after the term pass
 // the dead old row is reused for the thread's scattered residual R, valid
-// where rflag[t] is set.
+// where bit t of the slot's active-step mask is set.
 struct SmemLayout {
     size_t W, KMm, KMd, cconst, B6, rhs, PBt, ptab;
     size_t slot0, slot_stride;
-    size_t C, Cp, lam, lamN, xb, means, mpart, eqerr, psq, P0, P1, rflag, Cf, pinf, sh, slist, aq, az, anm;
+    size_t C, Cp, lam, lamN, xb, means, mpart, eqerr, psq, P0, P1, Cf, pinf, sh, slist, aq, az, anm;
     size_t total;
 };
 
@@ -128,7 +142,6 @@ __host__ __device__ inline SmemLayout make_layout(int n, int S, int MP, int spb,
     L.psq = q;    q = align16(q + (size_t)S * d);
     L.P0 = q;     q = align16(q + (size_t)RS * S * ts);
     L.P1 = q;     q = align16(q + (size_t)RS * S * ts);
-    L.rflag = q;  q = align16(q + (size_t)S * sizeof(int));
     L.Cf = q;     q = align16(q + (size_t)3 * MP * NB * ts);
     L.pinf = q;   q = align16(q + (size_t)S * ts);
     L.sh = q;     q = align16(q + sizeof(SlotShared));
@@ -144,7 +157,7 @@ __host__ __device__ inline SmemLayout make_layout(int n, int S, int MP, int spb,
 struct SlotPtrs {
     double *C, *Cp, *lam, *lamN, *xb, *means, *mpart, *eqerr, *psq;
     void *P0, *P1, *Cf, *pinf, *aq, *az;
-    int *rflag, *slist;
+    int* slist;
     uint32_t* anm;
     SlotShared* sh;
 };
@@ -163,7 +176,6 @@ __device__ __forceinline__ SlotPtrs slot_ptrs(unsigned char* smem, const SmemLay
     P.psq = (double*)(b + L.psq);
     P.P0 = (void*)(b + L.P0);
     P.P1 = (void*)(b + L.P1);
-    P.rflag = (int*)(b + L.rflag);
     P.Cf = (void*)(b + L.Cf);
     P.pinf = (void*)(b + L.pinf);
     P.sh = (SlotShared*)(b + L.sh);
@@ -352,8 +364,6 @@ __device__ __forceinline__ T interior_scan(const T (&pos)[3 * NB], int n, const 
 template <typename T, int NB> struct QuietStats {
     T inf, sq;
     T dmax2;   // max_i a^2 |Dp_i|_s^2 (same quadratic form as q): bounds the motion of every pair
-    T range[3], wmax[3];
-    int imax[3], imin[3], iabs[3];
 };
 
 // One pass per axis: min, max, max |Dp|, sum and sum of squares of Dp;
@@ -381,8 +391,6 @@ __device__ __forceinline__ QuietStats<T, NB> quiet_residual(const T (&pos)[3 * N
                 dq[i] = fma_t<T>(ax == 2 ? dpi * fp_beta : dpi, dpi, dq[i]);
             }
         }
-        st.range[ax] = hi - lo;
-        st.wmax[ax] = am;
         mx = fmax(mx, fmax(hi - lo, am));
         s2 += fmax(fma_t<T>((T)(n + 1), sq, -s1 * s1), sq);
     }
@@ -395,162 +403,161 @@ __device__ __forceinline__ QuietStats<T, NB> quiet_residual(const T (&pos)[3 * N
     return st;
 }
 
-// Robots attaining the per-axis range and max |Dp| (needed only when some
-// term is flagged, to know whether the quiet inf-norm is attained by it).
-template <typename T, int NB>
-__device__ __forceinline__ void quiet_argmax(const T (&pos)[3 * NB], const T* __restrict__ Pold, int n,
-                                             QuietStats<T, NB>& st) {
-#pragma unroll
-    for (int ax = 0; ax < 3; ++ax) {
-        T lo = T(1e38), hi = T(-1e38), am = T(-1);
-        int ilo = 0, ihi = 0, iam = 0;
-#pragma unroll
-        for (int i = 0; i < NB; ++i) {
-            if (i < n) {
-                const T dpi = pos[ax * NB + i] - Pold[ax * NB + i];
-                if (dpi < lo) { lo = dpi; ilo = i; }
-                if (dpi > hi) { hi = dpi; ihi = i; }
-                if (fabs(dpi) > am) { am = fabs(dpi); iam = i; }
-            }
-        }
-        st.imax[ax] = ihi;
-        st.imin[ax] = ilo;
-        st.iabs[ax] = iam;
+// by-value packs of register arrays for out-of-line calls
+template <typename T, int NB> struct PosPack {
+    T v[3 * NB];
+};
+template <int NB> struct MaskPack {
+    uint32_t w[TermBits<NB>::words];
+};
+
+// Flagged terms (active now or at the previous iterate) of one time step,
+// O(#flagged): true exit residual, scatter of d - e for terms active now,
+// and the corrections of the quiet statistics (qinf, qsq).  The quiet
+// inf-norm qinf is the max of |Dp_i - Dp_j| (pairs) and |Dp_i| (workspace)
+// over all terms; it stays exact for the unflagged terms unless a flagged
+// term attains it, and only then is the max over the unflagged terms
+// recomputed.  Runtime-indexed data comes from the position rows in shared
+// memory; out of line and not unrolled, so this cold path costs little code
+// next to the hot one.  Writes the R row over the (then dead) old row when a
+// term is active.
+template <typename T> struct StepOut {
+    T inf, sq;
+    bool active;
+};
+
+template <int NB> __device__ __forceinline__ void term_robots(int b, int& i, int& j) {
+    constexpr int NP = NB * (NB - 1) / 2;
+    if (b < NP) {
+        int rem = b;
+        i = 0;
+        while (rem >= NB - 1 - i) { rem -= NB - 1 - i; ++i; }
+        j = i + 1 + rem;
+    } else {
+        i = b - NP;
+        j = -1;
     }
 }
 
-// Flagged terms (active now or at the previous iterate), O(#flagged): true
-// exit residual, scatter of d - e for terms active now (into acc), and the
-// corrections of the quiet statistics.  Runtime-indexed data comes from the
-// position rows in shared memory.  Returns true if the max over the
-// unflagged terms needs an exact recompute (a range-attaining pair or
-// max-|Dp| robot is itself flagged).
 template <typename T, int NB>
-__device__ __forceinline__ bool flagged_terms(const T* __restrict__ Pnew, const T* __restrict__ Pold, int n,
-                                              const Family<T>& fp, const Family<T>& fw, T cx, T cy, T cz,
-                                              const uint32_t (&nm)[TermBits<NB>::words],
-                                              const uint32_t (&om)[TermBits<NB>::words],
-                                              const QuietStats<T, NB>& st, T (&acc)[3 * NB], T& flmax, T& dsq,
-                                              bool& act_new) {
+__device__ __noinline__ StepOut<T> flagged_path(const T* __restrict__ Pnew, T* __restrict__ Pold, int n,
+                                                const Family<T> fp, const Family<T> fw, T cx, T cy, T cz,
+                                                const MaskPack<NB> nm, const MaskPack<NB> om, T qinf, T qsq) {
     constexpr int NP = NB * (NB - 1) / 2;
-    bool need_exact = false;
-#pragma unroll
-    for (int w = 0; w < TermBits<NB>::words; ++w) {
-        uint32_t fl = ~(nm[w] & om[w]);
+    constexpr int NWD = TermBits<NB>::words;
+    const T c3[3] = {cx, cy, cz};
+    T flmax = T(0), dsq = T(0);
+    bool need_exact = false, act_new = false;
+    // pass 1: exit residual of the flagged terms (needs the old row)
+#pragma unroll 1
+    for (int w = 0; w < NWD; ++w) {
+        uint32_t fl = ~(nm.w[w] & om.w[w]);
         while (fl) {
             const int bit = __ffs(fl) - 1;
             fl &= fl - 1;
             const int b = w * 32 + bit;
             if (b >= TermBits<NB>::count) break;
-            const bool in_new = (nm[w] >> bit) & 1u, in_old = (om[w] >> bit) & 1u;
-            if (b < NP) {
-                int i = 0, rem = b;
-                while (rem >= NB - 1 - i) { rem -= NB - 1 - i; ++i; }
-                const int j = i + 1 + rem;
-                T d[3], o[3], x[3];
+            const bool in_old = (om.w[w] >> bit) & 1u;
+            act_new = act_new || !((nm.w[w] >> bit) & 1u);
+            int i, j;
+            term_robots<NB>(b, i, j);
+            const bool pair = j >= 0;
+            const Family<T>& fm = pair ? fp : fw;
+            T d[3], o[3], x[3];
+            T xq = T(0);
 #pragma unroll
-                for (int ax = 0; ax < 3; ++ax) {
-                    const T ni = Pnew[ax * NB + i], nj = Pnew[ax * NB + j];
-                    const T oi = Pold[ax * NB + i], oj = Pold[ax * NB + j];
+            for (int ax = 0; ax < 3; ++ax) {
+                const T ni = Pnew[ax * NB + i], oi = Pold[ax * NB + i];
+                if (pair) {
+                    const T nj = Pnew[ax * NB + j], oj = Pold[ax * NB + j];
                     d[ax] = ni - nj;
                     o[ax] = oi - oj;
                     x[ax] = (ni - oi) - (nj - oj);   // Dp_i - Dp_j exactly as in quiet_residual
-                    dsq -= x[ax] * x[ax];
-                    need_exact = need_exact || ((i == st.imax[ax] && j == st.imin[ax]) ||
-                                                (j == st.imax[ax] && i == st.imin[ax]));
-                }
-                if (!in_old) {
-                    const T qo = fma_t<T>(o[2] * fp.beta, o[2], fma_t<T>(o[1], o[1], o[0] * o[0]));
-                    const T so = qo > T(0) ? fp.lat * rsq<T>(qo) : T(0);
-#pragma unroll
-                    for (int ax = 0; ax < 3; ++ax) x[ax] = fma_t<T>(-so, o[ax], d[ax]);
-                }
-                if (!in_new) {
-                    act_new = true;
-                    const T q = fma_t<T>(d[2] * fp.beta, d[2], fma_t<T>(d[1], d[1], d[0] * d[0]));
-                    const T s = fp.lat * rsq<T>(q);
-#pragma unroll
-                    for (int ax = 0; ax < 3; ++ax) {
-                        const T r = fma_t<T>(-s, d[ax], d[ax]);
-#pragma unroll
-                        for (int m = 0; m < NB; ++m) {
-                            if (m == i) acc[ax * NB + m] += r;
-                            if (m == j) acc[ax * NB + m] -= r;
-                        }
-                    }
-                }
-#pragma unroll
-                for (int ax = 0; ax < 3; ++ax) {
-                    flmax = fmax(flmax, fabs(x[ax]));
-                    dsq = fma_t<T>(x[ax], x[ax], dsq);
-                }
-            } else {
-                const int i = b - NP;
-                const T c3[3] = {cx, cy, cz};
-                T d[3], o[3], x[3];
-#pragma unroll
-                for (int ax = 0; ax < 3; ++ax) {
-                    const T ni = Pnew[ax * NB + i], oi = Pold[ax * NB + i];
+                } else {
                     d[ax] = ni - c3[ax];
                     o[ax] = oi - c3[ax];
                     x[ax] = ni - oi;
-                    dsq -= x[ax] * x[ax];
-                    need_exact = need_exact || (i == st.iabs[ax]);
                 }
-                if (!in_old) {
-                    const T qo = fma_t<T>(o[2] * fw.beta, o[2], fma_t<T>(o[1], o[1], o[0] * o[0]));
-                    const T so = qo > T(0) ? fw.lat * rsq<T>(qo) : T(0);
+                xq = fmax(xq, fabs(x[ax]));
+                dsq -= x[ax] * x[ax];
+            }
+            need_exact = need_exact || (xq >= qinf);
+            if (!in_old) {
+                const T qo = fma_t<T>(o[2] * fm.beta, o[2], fma_t<T>(o[1], o[1], o[0] * o[0]));
+                const T so = qo > T(0) ? fm.lat * rsq<T>(qo) : T(0);
 #pragma unroll
-                    for (int ax = 0; ax < 3; ++ax) x[ax] = fma_t<T>(-so, o[ax], d[ax]);
+                for (int ax = 0; ax < 3; ++ax) x[ax] = fma_t<T>(-so, o[ax], d[ax]);
+            }
+#pragma unroll
+            for (int ax = 0; ax < 3; ++ax) {
+                flmax = fmax(flmax, fabs(x[ax]));
+                dsq = fma_t<T>(x[ax], x[ax], dsq);
+            }
+        }
+    }
+    T base = qinf;
+    if (need_exact) {   // exact max of |x| over the unflagged terms (needs the old row)
+        base = T(0);
+        int b = 0;
+#pragma unroll 1
+        for (int i = 0; i < NB; ++i) {
+#pragma unroll 1
+            for (int j = i + 1; j < NB; ++j, ++b) {
+                if (j < n && bit_of(nm.w, b) && bit_of(om.w, b)) {
+                    T m = T(0);
+#pragma unroll
+                    for (int ax = 0; ax < 3; ++ax)
+                        m = fmax(m, fabs((Pnew[ax * NB + i] - Pold[ax * NB + i]) - (Pnew[ax * NB + j] - Pold[ax * NB + j])));
+                    base = fmax(base, m);
                 }
-                if (!in_new) {
-                    act_new = true;
-                    const T q = fma_t<T>(d[2] * fw.beta, d[2], fma_t<T>(d[1], d[1], d[0] * d[0]));
-                    const T s = fw.lat * rsq<T>(q);
+            }
+        }
+#pragma unroll 1
+        for (int i = 0; i < n; ++i) {
+            if (bit_of(nm.w, NP + i) && bit_of(om.w, NP + i)) {
+                T m = T(0);
 #pragma unroll
-                    for (int ax = 0; ax < 3; ++ax) {
-                        const T r = fma_t<T>(-s, d[ax], d[ax]);
+                for (int ax = 0; ax < 3; ++ax) m = fmax(m, fabs(Pnew[ax * NB + i] - Pold[ax * NB + i]));
+                base = fmax(base, m);
+            }
+        }
+    }
+    if (act_new) {
+        // pass 2: the old row is dead now -- it becomes this thread's R row (d - e of the active terms)
 #pragma unroll
-                        for (int m = 0; m < NB; ++m)
-                            if (m == i) acc[ax * NB + m] += r;
-                    }
-                }
+        for (int q = 0; q < 3 * NB; ++q)
+            if ((q % NB) < n) Pold[q] = T(0);
+#pragma unroll 1
+        for (int w = 0; w < NWD; ++w) {
+            uint32_t ac = ~nm.w[w];
+            while (ac) {
+                const int bit = __ffs(ac) - 1;
+                ac &= ac - 1;
+                const int b = w * 32 + bit;
+                if (b >= TermBits<NB>::count) break;
+                int i, j;
+                term_robots<NB>(b, i, j);
+                const bool pair = j >= 0;
+                const Family<T>& fm = pair ? fp : fw;
+                T d[3];
+#pragma unroll
+                for (int ax = 0; ax < 3; ++ax) d[ax] = Pnew[ax * NB + i] - (pair ? Pnew[ax * NB + j] : c3[ax]);
+                const T q = fma_t<T>(d[2] * fm.beta, d[2], fma_t<T>(d[1], d[1], d[0] * d[0]));
+                const T s = fm.lat * rsq<T>(q);
 #pragma unroll
                 for (int ax = 0; ax < 3; ++ax) {
-                    flmax = fmax(flmax, fabs(x[ax]));
-                    dsq = fma_t<T>(x[ax], x[ax], dsq);
+                    const T r = fma_t<T>(-s, d[ax], d[ax]);
+                    Pold[ax * NB + i] += r;
+                    if (pair) Pold[ax * NB + j] -= r;
                 }
             }
         }
     }
-    return need_exact;
-}
-
-// Exact max of |x| over the unflagged terms (x = Dp_i - Dp_j, Dp_i), used
-// only when a range-attaining pair is flagged.
-template <typename T, int NB>
-__device__ __noinline__ T unflagged_max(const T* __restrict__ Pnew, const T* __restrict__ Pold, int n,
-                                        const uint32_t* fl) {
-    T dp[3 * NB];
-#pragma unroll
-    for (int q = 0; q < 3 * NB; ++q) dp[q] = ((q % NB) < n) ? Pnew[q] - Pold[q] : T(0);
-    T mx = T(0);
-#pragma unroll
-    for (int i = 0; i < NB; ++i) {
-#pragma unroll
-        for (int j = 0; j < NB; ++j) {
-            const int b = pair_bit<NB>(i, j);
-            if (j > i && j < n && !((fl[b >> 5] >> (b & 31)) & 1u))
-                mx = fmax(mx, fmax(fabs(dp[i] - dp[j]), fmax(fabs(dp[NB + i] - dp[NB + j]), fabs(dp[2 * NB + i] - dp[2 * NB + j]))));
-        }
-    }
-#pragma unroll
-    for (int i = 0; i < NB; ++i) {
-        const int b = ws_bit<NB>(i);
-        if (i < n && !((fl[b >> 5] >> (b & 31)) & 1u))
-            mx = fmax(mx, fmax(fabs(dp[i]), fmax(fabs(dp[NB + i]), fabs(dp[2 * NB + i]))));
-    }
-    return mx;
+    StepOut<T> r;
+    r.inf = fmax(base, flmax);
+    r.sq = fmax(qsq + dsq, T(0));
+    r.active = act_new;
+    return r;
 }
 
 // Careful path: every term in the reference orientation, targets of terms
@@ -558,12 +565,6 @@ __device__ __noinline__ T unflagged_max(const T* __restrict__ Pnew, const T* __r
 // interior bits (zero-component terms count as active) and whether any zero
 // occurred.  Returns whether some term is active now.  Out of line: it runs
 // only for (time steps of) symmetric scenarios.
-template <typename T, int NB> struct PosPack {
-    T v[3 * NB];
-};
-template <int NB> struct MaskPack {
-    uint32_t w[TermBits<NB>::words];
-};
 template <typename T> struct CarefulOut {
     T inf, sq;
     bool zero, active;
@@ -649,15 +650,16 @@ __device__ __noinline__ CarefulOut<T> careful_pass(const PosPack<T, NB> pk, T* _
 // ---------------------------------------------------------------- finishing a time step
 // Given the interior bits of every term (nm) and min |component| (zmin), run
 // the careful / quiet / flagged path of time step `lt` and write its outputs:
-// exit-residual partials, R row (over the dead old row) and its flag.
+// exit-residual partials, R row (over the dead old row) and its bit in the
+// active-step mask of parity buffer `par`.
 template <typename T, int NB>
-__device__ __forceinline__ void finish_step(const SlotPtrs& sp, int lt, int n, const T (&pos)[3 * NB],
+__device__ __forceinline__ void finish_step(const SlotPtrs& sp, int lt, int n, int par, const T (&pos)[3 * NB],
                                             T* __restrict__ Prow_old, const T* __restrict__ Prow_new,
                                             const QuietStats<T, NB>& st, uint32_t (&nm)[TermBits<NB>::words],
                                             T zmin, uint32_t (&imask)[TermBits<NB>::words], bool& zprev,
                                             const Family<T>& fp, const Family<T>& fw, T cx, T cy, T cz) {
     constexpr int NW = TermBits<NB>::words;
-    T inf, sq;
+    T inf = st.inf, sq = st.sq;
     bool active = false;
     if (__builtin_expect(zmin == T(0) || zprev, 0)) {
         PosPack<T, NB> pk;
@@ -672,42 +674,30 @@ __device__ __forceinline__ void finish_step(const SlotPtrs& sp, int lt, int n, c
         active = co.active;
         zprev = co.zero;
     } else {
-        inf = st.inf;
-        sq = st.sq;
         uint32_t any = 0u;
 #pragma unroll
         for (int w = 0; w < NW; ++w) any |= ~(nm[w] & imask[w]);
         if (__builtin_expect(any != 0u, 0)) {
-            QuietStats<T, NB> st2 = st;
-            quiet_argmax<T, NB>(pos, Prow_old, n, st2);
-            T acc[3 * NB];
+            MaskPack<NB> nmp, omp;
 #pragma unroll
-            for (int q = 0; q < 3 * NB; ++q) acc[q] = T(0);
-            T flmax = T(0), dsq = T(0);
-            const bool need_exact =
-                flagged_terms<T, NB>(Prow_new, Prow_old, n, fp, fw, cx, cy, cz, nm, imask, st2, acc, flmax, dsq, active);
-            T base = st.inf;
-            if (need_exact) {
-                uint32_t fl[NW];
-#pragma unroll
-                for (int w = 0; w < NW; ++w) fl[w] = ~(nm[w] & imask[w]);
-                base = unflagged_max<T, NB>(Prow_new, Prow_old, n, fl);
+            for (int w = 0; w < NW; ++w) {
+                nmp.w[w] = nm[w];
+                omp.w[w] = imask[w];
             }
-            inf = fmax(base, flmax);
-            sq = fmax(sq + dsq, T(0));
-            if (active) {   // the old row is dead now: it becomes this thread's R row
-#pragma unroll
-                for (int q = 0; q < 3 * NB; ++q)
-                    if ((q % NB) < n) Prow_old[q] = acc[q];
-            }
+            const StepOut<T> o = flagged_path<T, NB>(Prow_new, Prow_old, n, fp, fw, cx, cy, cz, nmp, omp, inf, sq);
+            inf = o.inf;
+            sq = o.sq;
+            active = o.active;
         }
     }
 #pragma unroll
     for (int w = 0; w < NW; ++w) imask[w] = nm[w];
-    sp.rflag[lt] = active ? 1 : 0;
     ((T*)sp.pinf)[lt] = inf;
     sp.psq[lt] = (double)sq;
-    if (active) atomicOr(&sp.sh->active, 1);
+    if (active) {
+        atomicOr(&sp.sh->amask[par][lt >> 5], 1u << (lt & 31));
+        sp.sh->active[par] = 1;
+    }
 }
 
 template <typename T> struct UBits;
@@ -833,7 +823,7 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
     const Family<T> fp = make_family<T>(p.lat, p.vert);
     const Family<T> fw = make_family<T>(p.ws_lat, p.ws_vert);
     const T cx = (T)p.cx, cy = (T)p.cy, cz = (T)p.cz;
-    const int half = (S + 1) / 2;
+    const int SWT = (S + 31) >> 5;   // words of the active-step mask
 
     uint32_t imask[NW];
     bool zprev = false;
@@ -844,9 +834,9 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
     T rmin = T(0), cum = T(0);
 
     if (lt == 0) {
-        sp.sh->sample = atomicAdd(p.queue, 1);
-        sp.sh->active = 0;
-        sp.sh->scount = 0;
+        sp.sh->sample = next_sample(p);
+        clear_flags(sp.sh, 0, SWT);
+        clear_flags(sp.sh, 1, SWT);
     }
     slot_barrier(bar_id, gsize);
     int sample = sp.sh->sample;
@@ -857,6 +847,8 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
         slot_barrier(bar_id, gsize);
 
         for (int k = 0;; ++k) {
+            const int par = k & 1;
+            if (lt == 0) clear_flags(sp.sh, par ^ 1, SWT);   // last read before the previous closing barrier
             // position rows: old = iterate k, new = iterate k+1's input positions; R -> old row
             T* Prow_old = (T*)((k & 1) ? sp.P1 : sp.P0) + lt * RS;
             T* Prow_new = (T*)((k & 1) ? sp.P0 : sp.P1) + lt * RS;
@@ -889,27 +881,27 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                 need_scan = (k == 0) || zprev || !pairs_prev_in || !(rmin - cum > T(1) + T(1e-3));
                 interior_scan<T, NB>(pos, n, fp, fw, cx, cy, cz, false, nm, zmin_ws);   // workspace terms only
                 if (need_scan) {
-                    const int e = atomicAdd(&sp.sh->scount, 1);
+                    const int e = atomicAdd(&sp.sh->scount[par], 1);
                     sp.slist[e] = lt;
                     ((UT*)sp.aq)[lt] = UBits<T>::of(T(1e30));
                     ((UT*)sp.az)[lt] = UBits<T>::of(T(1));
 #pragma unroll
                     for (int w = 0; w < SW; ++w) sp.anm[lt * SW + w] = 0u;
                 } else {
-                    finish_step<T, NB>(sp, lt, n, pos, Prow_old, Prow_new, st, nm, zmin_ws, imask, zprev, fp, fw, cx,
+                    finish_step<T, NB>(sp, lt, n, par, pos, Prow_old, Prow_new, st, nm, zmin_ws, imask, zprev, fp, fw, cx,
                                        cy, cz);
                 }
             }
             slot_barrier(bar_id, gsize);
 
-            const int L = sp.sh->scount;
-            if (L > 0) {
+            const int Lq = sp.sh->scount[par];
+            if (Lq > 0) {
                 // ---------------- T2: cooperative O(n^2) scan of the queued time steps, 8 pairs per item
                 constexpr int NP = NB * (NB - 1) / 2;
                 constexpr int PPC = 8;
                 constexpr int CH = (NP + PPC - 1) / PPC;
                 const T* Pbase = (const T*)((k & 1) ? sp.P0 : sp.P1);
-                for (int it = lt; it < L * CH; it += gsize) {
+                for (int it = lt; it < Lq * CH; it += gsize) {
                     const int e = it / CH, c = it - e * CH;
                     const int t = sp.slist[e];
                     const T* row = Pbase + t * RS;
@@ -947,91 +939,42 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                     const T zmin = fmin(zmin_ws, UBits<T>::val(((UT*)sp.az)[lt]));
 #pragma unroll
                     for (int w = 0; w < SW; ++w) nm[w] &= ~sp.anm[lt * SW + w];
-                    finish_step<T, NB>(sp, lt, n, pos, Prow_old, Prow_new, st, nm, zmin, imask, zprev, fp, fw, cx, cy,
+                    finish_step<T, NB>(sp, lt, n, par, pos, Prow_old, Prow_new, st, nm, zmin, imask, zprev, fp, fw, cx, cy,
                                        cz);
                 }
-            }
-            slot_barrier(bar_id, gsize);
-
-            // ---------------- G: lam' = lam - rho R W (R is sparse; skipped when nothing is active)
-            const bool any_active = sp.sh->active != 0;
-            for (int it0 = 0; it0 < 2 * R3; it0 += gsize) {
-                const int item = it0 + lt;
-                const bool valid = item < 2 * R3;
-                const int r = item >> 1, h = item & 1;
-                T g[MP];
-#pragma unroll
-                for (int q = 0; q < MP; ++q) g[q] = T(0);
-                if (valid && any_active) {
-                    const T* Rr = (const T*)((k & 1) ? sp.P1 : sp.P0) + (r / n) * NB + (r % n);
-                    const int t0 = h ? half : 0, t1 = h ? S : half;
-                    for (int t = t0; t < t1; ++t) {
-                        if (!sp.rflag[t]) continue;   // R row valid only where a term was active
-                        const T rv = Rr[t * RS];
-                        if (rv != T(0)) {
-                            T w[MP];
-                            load_row16<T, MP>(Wt + t * MP, w);
-#pragma unroll
-                            for (int q = 0; q < MP; ++q) g[q] = fma_t<T>(rv, w[q], g[q]);
-                        }
-                    }
-                }
-                if (any_active) {
-#pragma unroll
-                    for (int q = 0; q < MP; ++q) g[q] += __shfl_xor_sync(0xffffffffu, g[q], 1);
-                }
-                if (valid) {
-#pragma unroll
-                    for (int q = 0; q < MP; ++q)
-                        if ((q & 1) == h) sp.lamN[r * MP + q] = sp.lam[r * MP + q] - p.rho * (double)g[q];
-                }
-            }
-            if (lwarp == 0) {   // decision: exit residual of iteration k-1, early stop, SingularKKT
-                double emax = 0.0;
-                T inf = T(0);
-                double sqs = 0.0;
-                if (k >= 1) {
-                    for (int r = lane; r < R3; r += 32) emax = fmax(emax, sp.eqerr[r]);
-                    for (int t = lane; t < S; t += 32) {
-                        inf = fmax(inf, ((const T*)sp.pinf)[t]);
-                        sqs += sp.psq[t];
-                    }
-                }
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) {
-                    emax = fmax(emax, __shfl_xor_sync(0xffffffffu, emax, off));
-                    inf = fmax(inf, __shfl_xor_sync(0xffffffffu, inf, off));
-                    sqs += __shfl_xor_sync(0xffffffffu, sqs, off);
-                }
-                if (lane == 0) {
-                    const bool failed = (k >= 1) && (emax > p.tol_eq);
-                    bool done = failed;
-                    if (k >= 1) {
-                        const size_t hix = (size_t)sample * p.max_iters + (k - 1);
-                        p.res_inf[hix] = (double)inf;
-                        p.res_l2[hix] = sqrt(sqs);
-                        sp.sh->last_inf = (double)inf;
-                        done = done || (p.early_stop && (double)inf <= p.tol_res) || (k >= p.max_iters);
-                    }
-                    sp.sh->done = done;
-                    sp.sh->failed = failed;
-                    sp.sh->eqmax = emax;
-#ifdef SGSF_DEBUG
-                    if (blockIdx.x == 0 && slot == 0 && k < 4)
-                        printf("D k=%d sample=%d inf=%g sqs=%g emax=%g done=%d C0=%g Cf0=%g\n", k, sample, (double)inf, sqs,
-                               emax, (int)done, sp.C[0], (double)((T*)sp.Cf)[0]);
-#endif
-                }
-            }
-            slot_barrier(bar_id, gsize);
-            if (lt == 0) {   // every thread has read them; the next writes come after a barrier
-                sp.sh->active = 0;
-                sp.sh->scount = 0;
+                slot_barrier(bar_id, gsize);
             }
 
-            if (sp.sh->done) {
+            // ---------------- decision (every warp, redundantly): exit residual of iteration k-1, early stop, SingularKKT
+            double emax = 0.0, sqs = 0.0;
+            T inf = T(0);
+            if (k >= 1) {
+                for (int r = lane; r < R3; r += 32) emax = fmax(emax, sp.eqerr[r]);
+                for (int t = lane; t < S; t += 32) {
+                    inf = fmax(inf, ((const T*)sp.pinf)[t]);
+                    sqs += sp.psq[t];
+                }
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                emax = fmax(emax, __shfl_xor_sync(0xffffffffu, emax, off));
+                inf = fmax(inf, __shfl_xor_sync(0xffffffffu, inf, off));
+                sqs += __shfl_xor_sync(0xffffffffu, sqs, off);
+            }
+            // (a sample can only finish at k >= 1, so `inf` is always the last exit residual there)
+            const bool failed = (k >= 1) && (emax > p.tol_eq);
+            bool done = failed;
+            if (k >= 1) {
+                done = done || (p.early_stop && (double)inf <= p.tol_res) || (k >= p.max_iters);
+                if (lt == 0) {
+                    const size_t hix = (size_t)sample * p.max_iters + (k - 1);
+                    p.res_inf[hix] = (double)inf;
+                    p.res_l2[hix] = sqrt(sqs);
+                }
+            }
+
+            if (done) {
                 // ---------------- finalize: outputs of the returned iterate, claim the next sample
-                const bool failed = sp.sh->failed;
                 if (!failed) {
                     for (int e = lt; e < dim; e += gsize) {
                         const int r = e / m1, q = e - r * m1;
@@ -1051,11 +994,14 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                     for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
                     if (lane == 0) {
                         p.iterations[sample] = failed ? 0 : k;
-                        p.converged[sample] = (!failed && sp.sh->last_inf <= p.tol_res) ? 1 : 0;
+                        p.converged[sample] = (!failed && (double)inf <= p.tol_res) ? 1 : 0;
                         p.displacement[sample] = failed ? CUDART_NAN : sqrt(acc);
                         p.status[sample] = failed ? SAMPLE_SINGULAR_KKT : SAMPLE_OK;
-                        p.eq_err[sample] = sp.sh->eqmax;
-                        sp.sh->sample = atomicAdd(p.queue, 1);
+                        p.eq_err[sample] = emax;
+                        sp.sh->sample = next_sample(p);
+                        // nothing reads the flags in a final iteration (scount: only a clear of a zero)
+                        clear_flags(sp.sh, 0, SWT);
+                        clear_flags(sp.sh, 1, SWT);
                     }
                 }
                 slot_barrier(bar_id, gsize);
@@ -1063,95 +1009,120 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                 break;
             }
 
-            // ---------------- M: swarm means of C and u = 2 lam' - lam + xi_bar
-            for (int it = lt; it < 3 * MP; it += gsize) {
-                const int ax = it / MP, q = it - ax * MP;
-                double cs = 0.0, us = 0.0;
-                for (int i = 0; i < n; ++i) {
-                    const int idx = (ax * n + i) * MP + q;
-                    cs += sp.C[idx];
-                    us += 2.0 * sp.lamN[idx] - sp.lam[idx] + sp.xb[idx];
+            // ---------------- G: lam' = lam - rho R W over the active time steps only (ascending t)
+            const bool any_active = sp.sh->active[par] != 0;
+            if (any_active) {
+                const T* Rb = (const T*)(par ? sp.P1 : sp.P0);   // the old rows hold R
+                for (int r = lt; r < R3; r += gsize) {
+                    T g[MP];
+#pragma unroll
+                    for (int q = 0; q < MP; ++q) g[q] = T(0);
+                    const T* Rr = Rb + (r / n) * NB + (r % n);
+                    for (int w = 0; w < SWT; ++w) {
+                        uint32_t bits = sp.sh->amask[par][w];
+                        while (bits) {
+                            const int t = w * 32 + __ffs(bits) - 1;
+                            bits &= bits - 1;
+                            const T rv = Rr[t * RS];
+                            if (rv != T(0)) {
+                                T wr[MP];
+                                load_row16<T, MP>(Wt + t * MP, wr);
+#pragma unroll
+                                for (int q = 0; q < MP; ++q) g[q] = fma_t<T>(rv, wr[q], g[q]);
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int q = 0; q < MP; ++q) sp.lamN[r * MP + q] = sp.lam[r * MP + q] - p.rho * (double)g[q];
                 }
-                sp.means[ax * MP + q] = cs / n;
-                sp.means[3 * MP + ax * MP + q] = us / n;
+                slot_barrier(bar_id, gsize);
             }
-            slot_barrier(bar_id, gsize);
 
-            // ---------------- M2: mean part  Mm C_bar + Km11 u_bar
-            for (int it = lt; it < 3 * MP; it += gsize) {
-                const int ax = it / MP, q = it - ax * MP;
-                const double* cb = sp.means + ax * MP;
-                const double* ub = sp.means + 3 * MP + ax * MP;
-                const double* row = KMm + q * M2P;
-                double acc = 0.0;
+            // ---------------- MX: one warp per axis -- swarm means of C and u = 2 lam' - lam + xi_bar,
+            // mean part Mm Cb + Km11 ub, decoupled xi-step C_i = mean part + Md (C_i - Cb) + Kd11 (u_i - ub)
+            // + cconst_i, ||A xi - b||_inf partials, commit.  Rows of one axis never leave their warp, so
+            // the sub-steps are ordered by __syncwarp alone.
+            {
+                constexpr int LPR = (32 / NB < 4) ? 32 / NB : 4;   // lanes per coefficient row
+                constexpr int QL = MP / LPR;                       // outputs per lane
+                const double* lamU = any_active ? sp.lamN : sp.lam;   // lam' (= lam when nothing was active)
+                for (int ax = lwarp; ax < 3; ax += p.wps) {
+                    double* mn = sp.means + ax * 2 * MP;   // [Cb | ub]
+                    if (lane < MP) {
+                        double cs = 0.0, us = 0.0;
 #pragma unroll
-                for (int q2 = 0; q2 < MP; ++q2) acc = fma(row[q2], cb[q2], acc);
-#pragma unroll
-                for (int q2 = 0; q2 < MP; ++q2) acc = fma(row[MP + q2], ub[q2], acc);
-                sp.mpart[ax * MP + q] = acc;
-            }
-            slot_barrier(bar_id, gsize);
-
-            // ---------------- X: decoupled xi-step, equality check, commit lam'
-            // four lanes per coefficient row, MP/4 outputs each; the row is read by all
-            // four lanes before any of them writes it (__syncwarp), the eq-check partial
-            // sums B cn are combined with shuffles.
-            for (int it0 = 0; it0 < 4 * R3; it0 += gsize) {
-                const int item = it0 + lt;
-                const bool valid = item < 4 * R3;
-                const int r = valid ? (item >> 2) : 0, part = item & 3;
-                constexpr int QL = MP / 4;
-                const int ax = r / n;
-                double cn[QL], lamn[QL];
-                double eqp[6];
-#pragma unroll
-                for (int c6 = 0; c6 < 6; ++c6) eqp[c6] = 0.0;
-                if (valid) {
-                    const double* cb = sp.means + ax * MP;
-                    const double* ub = sp.means + 3 * MP + ax * MP;
-                    double dC[MP], dU[MP];
-#pragma unroll
-                    for (int q = 0; q < MP; ++q) {
-                        const int idx = r * MP + q;
-                        dC[q] = sp.C[idx] - cb[q];
-                        dU[q] = (2.0 * sp.lamN[idx] - sp.lam[idx] + sp.xb[idx]) - ub[q];
+                        for (int i = 0; i < NB; ++i) {
+                            if (i < n) {
+                                const int idx = (ax * n + i) * MP + lane;
+                                cs += sp.C[idx];
+                                us += 2.0 * lamU[idx] - sp.lam[idx] + sp.xb[idx];
+                            }
+                        }
+                        mn[lane] = cs / n;
+                        mn[MP + lane] = us / n;
                     }
+                    __syncwarp();
+                    if (lane < MP) {
+                        const double* row = KMm + lane * M2P;
+                        double acc = 0.0;
 #pragma unroll
-                    for (int u = 0; u < QL; ++u) {
-                        const int q = part * QL + u;
-                        const double* row = KMd + q * M2P;
-                        double acc = sp.mpart[ax * MP + q] + cconst[r * MP + q];
+                        for (int q2 = 0; q2 < MP; ++q2) acc = fma(row[q2], mn[q2], acc);
 #pragma unroll
-                        for (int q2 = 0; q2 < MP; ++q2) acc = fma(row[q2], dC[q2], acc);
-#pragma unroll
-                        for (int q2 = 0; q2 < MP; ++q2) acc = fma(row[MP + q2], dU[q2], acc);
-                        cn[u] = acc;
-                        lamn[u] = sp.lamN[r * MP + q];
-#pragma unroll
-                        for (int c6 = 0; c6 < 6; ++c6) eqp[c6] = fma(B6[c6 * MP + q], acc, eqp[c6]);
+                        for (int q2 = 0; q2 < MP; ++q2) acc = fma(row[MP + q2], mn[MP + q2], acc);
+                        sp.mpart[ax * MP + lane] = acc;
                     }
-                }
-                __syncwarp();
-                double emax = 0.0;
+                    __syncwarp();
+                    const int i = lane / LPR, part = lane - i * LPR;
+                    const bool valid = i < n;
+                    const int r = ax * n + (valid ? i : 0);
+                    double cn[QL];
+                    double eqp[6];
 #pragma unroll
-                for (int c6 = 0; c6 < 6; ++c6) {
-                    double e = eqp[c6];
-                    e += __shfl_xor_sync(0xffffffffu, e, 1);
-                    e += __shfl_xor_sync(0xffffffffu, e, 2);
-                    emax = fmax(emax, fabs(e - (valid ? rhs[r * 6 + c6] : 0.0)));
-                }
-                if (valid) {
-                    if (part == 0) sp.eqerr[r] = emax;
-                    const int i = r - ax * n;
+                    for (int c6 = 0; c6 < 6; ++c6) eqp[c6] = 0.0;
+                    if (valid) {
+                        double dC[MP], dU[MP];
 #pragma unroll
-                    for (int u = 0; u < QL; ++u) {
-                        const int q = part * QL + u;
-                        const int idx = r * MP + q;
-                        if (p.want_prev) sp.Cp[idx] = sp.C[idx];
-                        sp.C[idx] = cn[u];
-                        sp.lam[idx] = lamn[u];
-                        ((T*)sp.Cf)[(ax * MP + q) * NB + i] = (T)cn[u];
+                        for (int q = 0; q < MP; ++q) {
+                            const int idx = r * MP + q;
+                            dC[q] = sp.C[idx] - mn[q];
+                            dU[q] = (2.0 * lamU[idx] - sp.lam[idx] + sp.xb[idx]) - mn[MP + q];
+                        }
+#pragma unroll
+                        for (int u = 0; u < QL; ++u) {
+                            const int q = part * QL + u;
+                            const double* row = KMd + q * M2P;
+                            double acc = sp.mpart[ax * MP + q] + cconst[r * MP + q];
+#pragma unroll
+                            for (int q2 = 0; q2 < MP; ++q2) acc = fma(row[q2], dC[q2], acc);
+#pragma unroll
+                            for (int q2 = 0; q2 < MP; ++q2) acc = fma(row[MP + q2], dU[q2], acc);
+                            cn[u] = acc;
+#pragma unroll
+                            for (int c6 = 0; c6 < 6; ++c6) eqp[c6] = fma(B6[c6 * MP + q], acc, eqp[c6]);
+                        }
                     }
+                    __syncwarp();   // every lane has read its row before any lane writes it
+                    double em = 0.0;
+#pragma unroll
+                    for (int c6 = 0; c6 < 6; ++c6) {
+                        double e = eqp[c6];
+#pragma unroll
+                        for (int off = 1; off < LPR; off <<= 1) e += __shfl_xor_sync(0xffffffffu, e, off);
+                        em = fmax(em, fabs(e - (valid ? rhs[r * 6 + c6] : 0.0)));
+                    }
+                    if (valid) {
+                        if (part == 0) sp.eqerr[r] = em;
+#pragma unroll
+                        for (int u = 0; u < QL; ++u) {
+                            const int q = part * QL + u;
+                            const int idx = r * MP + q;
+                            if (p.want_prev) sp.Cp[idx] = sp.C[idx];
+                            sp.C[idx] = cn[u];
+                            if (any_active) sp.lam[idx] = lamU[idx];
+                            ((T*)sp.Cf)[(ax * MP + q) * NB + i] = (T)cn[u];
+                        }
+                    }
+                    __syncwarp();
                 }
             }
             slot_barrier(bar_id, gsize);

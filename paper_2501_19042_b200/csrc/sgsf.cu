@@ -80,7 +80,12 @@ const char* sgsf_version(void) { return "sgsf 0.1 (sm_100a)"; }
 const char* sgsf_last_error(void) { return g_last_error.c_str(); }
 uint64_t sgsf_launch_count(void) { return g_launches.load(); }
 int sgsf_max_robots(void) { return kMaxRobots; }
-size_t sgsf_workspace_bytes(void) { return 256; }
+// [queue counter | pad to 256 B][score: batch floats][order: batch ints], 256 B aligned
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+size_t sgsf_workspace_bytes(int batch) {
+    const size_t b = batch > 0 ? (size_t)batch : 0;
+    return 256 + 2 * align256(b * 4);
+}
 
 static int upload(double** dst, const double* src, size_t count) {
     if (!src) return fail(SGSF_ERR_INVALID, "null constant pointer");
@@ -207,6 +212,13 @@ int sgsf_solve(sgsf_handle_t* h, int batch, const double* xi_bar, const double* 
     p.coeffs_prev = out->coeffs_prev;
     p.queue = (int*)workspace;
     CUDA_TRY(cudaMemsetAsync(workspace, 0, sizeof(int), stream));
+    if (batch > 1) {   // longest-first queue order (sf_order.cuh)
+        float* score = (float*)((char*)workspace + 256);
+        int* order = (int*)((char*)workspace + 256 + align256((size_t)batch * 4));
+        const int rc = launch_order(p, score, order, stream);
+        if (rc != SGSF_OK) return rc;
+        p.order = order;
+    }
 
     const bool strict = cfg->precision == SGSF_PRECISION_STRICT;
     const int n = h->n;
@@ -331,7 +343,7 @@ int sgsf_solve_host(sgsf_handle_t* h, int batch, const double* xi_bar, const dou
     // one device arena for inputs + outputs (sizes rounded to 256 B each)
     const size_t sizes[] = {B * dim * 8, init_mode ? B * dim * 8 : 0, init_mode ? B * dim * 8 : 0, init_mode ? B : 0,
                             B * dim * 8, B * dim * 8, B * MI * 8, B * MI * 8, B * 4, B, B * 8, B * 4, B * 8, B,
-                            sgsf_workspace_bytes()};
+                            sgsf_workspace_bytes(batch)};
     size_t bytes = 0;
     for (size_t z : sizes) bytes += (z + 255) & ~size_t(255);
     char* arena = nullptr;

@@ -56,7 +56,7 @@ EXPORTS = {
     "sgsf_last_error": (C.c_char_p, []),
     "sgsf_launch_count": (C.c_uint64, []),
     "sgsf_max_robots": (C.c_int, []),
-    "sgsf_workspace_bytes": (C.c_size_t, []),
+    "sgsf_workspace_bytes": (C.c_size_t, [C.c_int]),
     "sgsf_create": (C.c_int, [C.POINTER(Problem), C.POINTER(C.c_void_p)]),
     "sgsf_destroy": (None, [C.c_void_p]),
     "sgsf_solve": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,

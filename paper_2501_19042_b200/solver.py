@@ -327,7 +327,7 @@ class SafetyFilter:
                            out.residual_l2.data_ptr(), out.iterations.data_ptr(), out.converged.data_ptr(),
                            out.displacement.data_ptr(), out.status.data_ptr(), out.eq_err.data_ptr(),
                            out.coeffs_prev.data_ptr() if want_prev else None)
-        ws = torch.empty(int(lib.sgsf_workspace_bytes()), dtype=torch.uint8, device=dev)
+        ws = torch.empty(int(lib.sgsf_workspace_bytes(B)), dtype=torch.uint8, device=dev)
         tm = None
         if timing is not None:
             for ev in timing:        # torch creates the CUDA event lazily on its first record()
