@@ -653,18 +653,18 @@ __device__ __noinline__ CarefulOut<T> careful_pass(const PosPack<T, NB> pk, T* _
 // exit-residual partials, R row (over the dead old row) and its bit in the
 // active-step mask of parity buffer `par`.
 template <typename T, int NB>
-__device__ __forceinline__ void finish_step(const SlotPtrs& sp, int lt, int n, int par, const T (&pos)[3 * NB],
-                                            T* __restrict__ Prow_old, const T* __restrict__ Prow_new,
-                                            const QuietStats<T, NB>& st, uint32_t (&nm)[TermBits<NB>::words],
+__device__ __forceinline__ void finish_step(const SlotPtrs& sp, int lt, int n, int par, T* __restrict__ Prow_old,
+                                            const T* __restrict__ Prow_new, T qinf, T qsq,
+                                            uint32_t (&nm)[TermBits<NB>::words],
                                             T zmin, uint32_t (&imask)[TermBits<NB>::words], bool& zprev,
                                             const Family<T>& fp, const Family<T>& fw, T cx, T cy, T cz) {
     constexpr int NW = TermBits<NB>::words;
-    T inf = st.inf, sq = st.sq;
+    T inf = qinf, sq = qsq;
     bool active = false;
     if (__builtin_expect(zmin == T(0) || zprev, 0)) {
         PosPack<T, NB> pk;
 #pragma unroll
-        for (int q = 0; q < 3 * NB; ++q) pk.v[q] = pos[q];
+        for (int q = 0; q < 3 * NB; ++q) pk.v[q] = ((q % NB) < n) ? Prow_new[q] : phantom_pos<T>(q % NB);
         MaskPack<NB> mo;
         const CarefulOut<T> co = careful_pass<T, NB>(pk, Prow_old, n, fp, fw, cx, cy, cz, &mo);
 #pragma unroll
@@ -857,7 +857,7 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
             constexpr int SW = ScanWords<NB>::value;
             bool need_scan = false;
             uint32_t nm[NW];
-            T zmin_ws = T(1);
+            T zmin_ws = T(1), qinf = T(0), qsq = T(0);   // quiet statistics, kept for T3
             if (lt < S) {
                 T pos[3 * NB];
                 positions_at<T, NB, MP>(Wt, (const T*)sp.Cf, lt, n, pos);
@@ -874,6 +874,8 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                     zprev = false;
                 }
                 const QuietStats<T, NB> st = quiet_residual<T, NB>(pos, Prow_old, n, fp.beta);
+                qinf = st.inf;
+                qsq = st.sq;
                 cum += T(2) * sqrt(st.dmax2) / fp.lat;
                 bool pairs_prev_in = true;
 #pragma unroll
@@ -888,8 +890,8 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
 #pragma unroll
                     for (int w = 0; w < SW; ++w) sp.anm[lt * SW + w] = 0u;
                 } else {
-                    finish_step<T, NB>(sp, lt, n, par, pos, Prow_old, Prow_new, st, nm, zmin_ws, imask, zprev, fp, fw, cx,
-                                       cy, cz);
+                    finish_step<T, NB>(sp, lt, n, par, Prow_old, Prow_new, qinf, qsq, nm, zmin_ws, imask, zprev, fp, fw,
+                                       cx, cy, cz);
                 }
             }
             slot_barrier(bar_id, gsize);
@@ -930,17 +932,13 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
 
                 // ---------------- T3: queued time steps finish with their scan results
                 if (lt < S && need_scan) {
-                    T pos[3 * NB];
-#pragma unroll
-                    for (int q = 0; q < 3 * NB; ++q) pos[q] = ((q % NB) < n) ? Prow_new[q] : phantom_pos<T>(q % NB);
-                    const QuietStats<T, NB> st = quiet_residual<T, NB>(pos, Prow_old, n, fp.beta);
                     rmin = sqrt(UBits<T>::val(((UT*)sp.aq)[lt])) / fp.lat;
                     cum = T(0);
                     const T zmin = fmin(zmin_ws, UBits<T>::val(((UT*)sp.az)[lt]));
 #pragma unroll
                     for (int w = 0; w < SW; ++w) nm[w] &= ~sp.anm[lt * SW + w];
-                    finish_step<T, NB>(sp, lt, n, par, pos, Prow_old, Prow_new, st, nm, zmin, imask, zprev, fp, fw, cx, cy,
-                                       cz);
+                    finish_step<T, NB>(sp, lt, n, par, Prow_old, Prow_new, qinf, qsq, nm, zmin, imask, zprev, fp, fw, cx,
+                                       cy, cz);
                 }
                 slot_barrier(bar_id, gsize);
             }
@@ -1063,12 +1061,15 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                     }
                     __syncwarp();
                     if (lane < MP) {
-                        const double* row = KMm + lane * M2P;
+                        const double2* row = reinterpret_cast<const double2*>(KMm + lane * M2P);
+                        const double2* mv = reinterpret_cast<const double2*>(mn);
                         double acc = 0.0;
 #pragma unroll
-                        for (int q2 = 0; q2 < MP; ++q2) acc = fma(row[q2], mn[q2], acc);
-#pragma unroll
-                        for (int q2 = 0; q2 < MP; ++q2) acc = fma(row[MP + q2], mn[MP + q2], acc);
+                        for (int c = 0; c < MP; ++c) {   // [Mm | Km11] . [Cb | ub], in column order
+                            const double2 a = row[c], m = mv[c];
+                            acc = fma(a.x, m.x, acc);
+                            acc = fma(a.y, m.y, acc);
+                        }
                         sp.mpart[ax * MP + lane] = acc;
                     }
                     __syncwarp();
@@ -1080,22 +1081,32 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
 #pragma unroll
                     for (int c6 = 0; c6 < 6; ++c6) eqp[c6] = 0.0;
                     if (valid) {
-                        double dC[MP], dU[MP];
+                        double dCU[2 * MP];   // [C_i - Cb | u_i - ub]
 #pragma unroll
-                        for (int q = 0; q < MP; ++q) {
-                            const int idx = r * MP + q;
-                            dC[q] = sp.C[idx] - mn[q];
-                            dU[q] = (2.0 * lamU[idx] - sp.lam[idx] + sp.xb[idx]) - mn[MP + q];
+                        for (int c = 0; c < MP / 2; ++c) {
+                            const int idx = r * MP + 2 * c;
+                            const double2 cc = *reinterpret_cast<const double2*>(sp.C + idx);
+                            const double2 lu = *reinterpret_cast<const double2*>(lamU + idx);
+                            const double2 ll = *reinterpret_cast<const double2*>(sp.lam + idx);
+                            const double2 xx = *reinterpret_cast<const double2*>(sp.xb + idx);
+                            const double2 mc = *reinterpret_cast<const double2*>(mn + 2 * c);
+                            const double2 mu = *reinterpret_cast<const double2*>(mn + MP + 2 * c);
+                            dCU[2 * c] = cc.x - mc.x;
+                            dCU[2 * c + 1] = cc.y - mc.y;
+                            dCU[MP + 2 * c] = (2.0 * lu.x - ll.x + xx.x) - mu.x;
+                            dCU[MP + 2 * c + 1] = (2.0 * lu.y - ll.y + xx.y) - mu.y;
                         }
 #pragma unroll
                         for (int u = 0; u < QL; ++u) {
                             const int q = part * QL + u;
-                            const double* row = KMd + q * M2P;
+                            const double2* row = reinterpret_cast<const double2*>(KMd + q * M2P);
                             double acc = sp.mpart[ax * MP + q] + cconst[r * MP + q];
 #pragma unroll
-                            for (int q2 = 0; q2 < MP; ++q2) acc = fma(row[q2], dC[q2], acc);
-#pragma unroll
-                            for (int q2 = 0; q2 < MP; ++q2) acc = fma(row[MP + q2], dU[q2], acc);
+                            for (int c = 0; c < MP; ++c) {   // [Md | Kd11] . [dC | dU], in column order
+                                const double2 a = row[c];
+                                acc = fma(a.x, dCU[2 * c], acc);
+                                acc = fma(a.y, dCU[2 * c + 1], acc);
+                            }
                             cn[u] = acc;
 #pragma unroll
                             for (int c6 = 0; c6 < 6; ++c6) eqp[c6] = fma(B6[c6 * MP + q], acc, eqp[c6]);
