@@ -14,23 +14,30 @@
 // Term pass: thread t of a slot owns time step t of its sample for ALL
 // robots; the positions of every robot at t live in its registers.  Per
 // iteration k it
-//   1. evaluates p_k(t) = C_k W[t]^T,
-//   2. scans all pair and workspace terms: interior test (q = a^2 r^2 against
-//      a^2) and exactly-zero components -- ~10 instructions per pair,
-//   3. if every term is interior now and at the previous iterate ("quiet"):
-//      the targets equal the differences, the scattered residual is 0 and the
-//      exit residual of each term is its change Dp_i - Dp_j; its inf-norm is
-//      the per-axis range of Dp and its l2-norm a per-axis sum (O(n));
-//      otherwise a masked pass evaluates Dp_i - Dp_j per pair and takes the
-//      exact slow path only for the flagged terms (target recompute, scatter
-//      of d - e into the thread's residual row R),
-//   4. terms with an exactly-zero component rerun on the careful path, which
+//   T1 evaluates p_k(t) = C_k W[t]^T, the O(n) statistics of the position
+//      change and the workspace terms, and decides whether the O(n^2) pair
+//      scan is needed: a motion bound (every pair had normalised distance >=
+//      rmin at the last scan and moved by at most cum since) proves all pairs
+//      interior while rmin - cum > 1 + margin,
+//   T2 scans the pairs of the time steps that need it, one step at a time
+//      with all 32 lanes of the owning warp (ballots give the non-interior
+//      pair bits) -- warp-local, so no slot barrier,
+//   T3 finishes every step: if every term is interior now and at the
+//      previous iterate ("quiet"), the targets equal the differences, the
+//      scattered residual is 0 and the exit residual of each term is its
+//      change Dp_i - Dp_j -- its inf-norm is the per-axis range of Dp and its
+//      l2-norm a per-axis sum (O(n)); otherwise the flagged terms take the
+//      exact path (target recompute, scatter of d - e into the R row), and
+//      terms with an exactly-zero component rerun on the careful path, which
 //      uses the FP64 reference trig formula.
-// Then   G  lam' = lam - rho R W   (skipped when the slot had no active term)
-//        M  swarm means / finalize,  M2 mean part of the xi-step,
-//        X  decoupled FP64 xi-step  C_i = Mm Cb + Km11 ub + Md (C_i - Cb)
-//           + Kd11 (u_i - ub) + cconst_i, u = 2 lam' - lam + xi_bar, with the
-//           ||A xi - b||_inf check (assembly.py:198-217).
+// Then every warp takes the stop decision from the per-step partials (no
+// barrier), G forms lam' = lam - rho R W over the active steps only (skipped
+// with its barrier when nothing is active), and MX -- one warp per axis --
+// forms the swarm means and the decoupled FP64 xi-step
+//   C_i = Mm Cb + Km11 ub + Md (C_i - Cb) + Kd11 (u_i - ub) + cconst_i,
+//   u = 2 lam' - lam + xi_bar,
+// with the ||A xi - b||_inf check (assembly.py:198-217).  Two slot barriers
+// per quiet iteration.
 // T is float ("lean") or double ("strict") for positions and term math;
 // state and xi-step are FP64.
 #pragma once
@@ -85,20 +92,17 @@ constexpr int MAX_SLOT_WORDS = 16;   // time-step bit words (slot size <= 512 th
 struct SlotShared {
     int sample;
     int active[2];   // some term had an active constraint in the term pass
-    int scount[2];   // time steps queued for the cooperative pair scan
     uint32_t amask[2][MAX_SLOT_WORDS];   // time steps with an active term (their R row is valid)
 };
 
 __device__ __forceinline__ void clear_flags(SlotShared* sh, int b, int words) {
     sh->active[b] = 0;
-    sh->scount[b] = 0;
     for (int w = 0; w < words; ++w) sh->amask[b][w] = 0u;
 }
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
 template <int NB> struct RowStride { static constexpr int value = 3 * NB + 1; };
-template <int NB> struct ScanWords { static constexpr int value = (NB * (NB - 1) / 2 + 31) / 32; };
 
 // Shared-memory map.  Coefficient-space arrays are padded to MP (m1 rounded
 // up to a multiple of 4) columns with zeros, so every loop over the degree
@@ -110,7 +114,7 @@ template <int NB> struct ScanWords { static constexpr int value = (NB * (NB - 1)
 struct SmemLayout {
     size_t W, KMm, KMd, cconst, B6, rhs, PBt, ptab;
     size_t slot0, slot_stride;
-    size_t C, Cp, lam, lamN, xb, means, mpart, eqerr, psq, P0, P1, Cf, pinf, sh, slist, aq, az, anm;
+    size_t C, Cp, lam, lamN, xb, means, mpart, eqerr, psq, P0, P1, Cf, pinf, sh;
     size_t total;
 };
 
@@ -145,10 +149,6 @@ __host__ __device__ inline SmemLayout make_layout(int n, int S, int MP, int spb,
     L.Cf = q;     q = align16(q + (size_t)3 * MP * NB * ts);
     L.pinf = q;   q = align16(q + (size_t)S * ts);
     L.sh = q;     q = align16(q + sizeof(SlotShared));
-    L.slist = q;  q = align16(q + (size_t)S * sizeof(int));
-    L.aq = q;     q = align16(q + (size_t)S * ts);                 // min q over the pairs (as unsigned bits)
-    L.az = q;     q = align16(q + (size_t)S * ts);                 // min |component| over the pairs
-    L.anm = q;    q = align16(q + (size_t)S * ScanWords<NB>::value * sizeof(uint32_t));   // non-interior pair bits
     L.slot_stride = q;
     L.total = o + (size_t)spb * q;
     return L;
@@ -156,9 +156,7 @@ __host__ __device__ inline SmemLayout make_layout(int n, int S, int MP, int spb,
 
 struct SlotPtrs {
     double *C, *Cp, *lam, *lamN, *xb, *means, *mpart, *eqerr, *psq;
-    void *P0, *P1, *Cf, *pinf, *aq, *az;
-    int* slist;
-    uint32_t* anm;
+    void *P0, *P1, *Cf, *pinf;
     SlotShared* sh;
 };
 
@@ -179,10 +177,6 @@ __device__ __forceinline__ SlotPtrs slot_ptrs(unsigned char* smem, const SmemLay
     P.Cf = (void*)(b + L.Cf);
     P.pinf = (void*)(b + L.pinf);
     P.sh = (SlotShared*)(b + L.sh);
-    P.slist = (int*)(b + L.slist);
-    P.aq = (void*)(b + L.aq);
-    P.az = (void*)(b + L.az);
-    P.anm = (uint32_t*)(b + L.anm);
     return P;
 }
 
@@ -191,6 +185,17 @@ __device__ __forceinline__ SlotPtrs slot_ptrs(unsigned char* smem, const SmemLay
 // (= barrier.sync.aligned) does not allow.
 __device__ __forceinline__ void slot_barrier(int id, int nthreads) {
     asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// warp-wide min of non-negative values: one REDUX on the float bits (which
+// order like the values), shuffles for double
+__device__ __forceinline__ float warp_min_nonneg(float v) {
+    return __uint_as_float(__reduce_min_sync(0xffffffffu, __float_as_uint(v)));
+}
+__device__ __forceinline__ double warp_min_nonneg(double v) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, off));
+    return v;
 }
 
 // 16-byte vector of T (float4 / double2) for the row-times-vector loops
@@ -700,18 +705,6 @@ __device__ __forceinline__ void finish_step(const SlotPtrs& sp, int lt, int n, i
     }
 }
 
-template <typename T> struct UBits;
-template <> struct UBits<float> {
-    using type = unsigned int;
-    __device__ __forceinline__ static unsigned int of(float x) { return __float_as_uint(x); }
-    __device__ __forceinline__ static float val(unsigned int u) { return __uint_as_float(u); }
-};
-template <> struct UBits<double> {
-    using type = unsigned long long;
-    __device__ __forceinline__ static unsigned long long of(double x) { return (unsigned long long)__double_as_longlong(x); }
-    __device__ __forceinline__ static double val(unsigned long long u) { return __longlong_as_double((long long)u); }
-};
-
 // ---------------------------------------------------------------- load a sample (one coefficient row)
 template <typename T, int NB, int MP>
 __device__ __forceinline__ void load_row(const SolveParams& p, const SlotPtrs& sp, int sample, int r,
@@ -825,12 +818,19 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
     const T cx = (T)p.cx, cy = (T)p.cy, cz = (T)p.cz;
     const int SWT = (S + 31) >> 5;   // words of the active-step mask
 
+    constexpr int NP = NB * (NB - 1) / 2;
+    constexpr int NPW = (NP + 31) / 32;   // words holding pair bits
     uint32_t imask[NW];
     bool zprev = false;
-    // motion bound for skipping the pair scan: every pair had normalised
-    // distance >= rmin at the last scan; since then the pairs moved by at most
-    // cum (sum over iterations of 2 max_i |Dp_i|, normalised).  While
-    // rmin - cum > 1 + margin every pair is provably interior.
+    // Verlet-style pair list: the last scan of this time step split the pairs
+    // into "near" (normalised distance < kSkin; their bits in `near`, checked
+    // exactly every iteration) and "far" (distance >= rmin >= kSkin).  Since
+    // the scan every pair moved by at most cum (sum over iterations of
+    // 2 max_i |Dp_i|, normalised), so while rmin - cum > 1 + margin every far
+    // pair is provably interior and needs no test.
+    constexpr float kSkin = 1.5f;
+    const T skin_lim = T(kSkin * kSkin) * fp.lim;
+    uint32_t near[NPW];
     T rmin = T(0), cum = T(0);
 
     if (lt == 0) {
@@ -853,8 +853,6 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
             T* Prow_old = (T*)((k & 1) ? sp.P1 : sp.P0) + lt * RS;
             T* Prow_new = (T*)((k & 1) ? sp.P0 : sp.P1) + lt * RS;
             // ---------------- T1: positions, O(n) statistics, motion bound; quiet steps finish here
-            using UT = typename UBits<T>::type;
-            constexpr int SW = ScanWords<NB>::value;
             bool need_scan = false;
             uint32_t nm[NW];
             T zmin_ws = T(1), qinf = T(0), qsq = T(0);   // quiet statistics, kept for T3
@@ -877,71 +875,75 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                 qinf = st.inf;
                 qsq = st.sq;
                 cum += T(2) * sqrt(st.dmax2) / fp.lat;
-                bool pairs_prev_in = true;
-#pragma unroll
-                for (int w = 0; w < NW; ++w) pairs_prev_in = pairs_prev_in && (imask[w] == 0xffffffffu);
-                need_scan = (k == 0) || zprev || !pairs_prev_in || !(rmin - cum > T(1) + T(1e-3));
+                need_scan = (k == 0) || zprev || !(rmin - cum > T(1) + T(1e-3));
                 interior_scan<T, NB>(pos, n, fp, fw, cx, cy, cz, false, nm, zmin_ws);   // workspace terms only
-                if (need_scan) {
-                    const int e = atomicAdd(&sp.sh->scount[par], 1);
-                    sp.slist[e] = lt;
-                    ((UT*)sp.aq)[lt] = UBits<T>::of(T(1e30));
-                    ((UT*)sp.az)[lt] = UBits<T>::of(T(1));
+                if (!need_scan) {   // near pairs of the last scan, exactly (a pair active before is near)
 #pragma unroll
-                    for (int w = 0; w < SW; ++w) sp.anm[lt * SW + w] = 0u;
-                } else {
-                    finish_step<T, NB>(sp, lt, n, par, Prow_old, Prow_new, qinf, qsq, nm, zmin_ws, imask, zprev, fp, fw,
-                                       cx, cy, cz);
-                }
-            }
-            slot_barrier(bar_id, gsize);
-
-            const int Lq = sp.sh->scount[par];
-            if (Lq > 0) {
-                // ---------------- T2: cooperative O(n^2) scan of the queued time steps, 8 pairs per item
-                constexpr int NP = NB * (NB - 1) / 2;
-                constexpr int PPC = 8;
-                constexpr int CH = (NP + PPC - 1) / PPC;
-                const T* Pbase = (const T*)((k & 1) ? sp.P0 : sp.P1);
-                for (int it = lt; it < Lq * CH; it += gsize) {
-                    const int e = it / CH, c = it - e * CH;
-                    const int t = sp.slist[e];
-                    const T* row = Pbase + t * RS;
-                    T qm = T(1e30), zm = T(1);
-                    uint32_t m = 0u;
-#pragma unroll
-                    for (int u = 0; u < PPC; ++u) {
-                        const int bb = c * PPC + u;
-                        if (bb < NP) {
-                            const int ij = ptab[bb], i = ij & 0xff, j = ij >> 8;
-                            if (j < n) {
-                                const T dx = row[i] - row[j], dy = row[NB + i] - row[NB + j];
-                                const T dz = row[2 * NB + i] - row[2 * NB + j];
-                                zm = fmin(zm, fmin(fabs(dx), fmin(fabs(dy), fabs(dz))));
-                                const T q = fma_t<T>(dz * fp.beta, dz, fma_t<T>(dy, dy, dx * dx));
-                                qm = fmin(qm, q);
-                                if (!(q >= fp.lim)) m |= 1u << (bb & 31);
-                            }
+                    for (int w = 0; w < NPW; ++w) {
+                        uint32_t bits = near[w];
+                        while (bits) {
+                            const int bit = __ffs(bits) - 1;
+                            bits &= bits - 1;
+                            const int ij = ptab[w * 32 + bit], i = ij & 0xff, j = ij >> 8;
+                            const T dx = Prow_new[i] - Prow_new[j], dy = Prow_new[NB + i] - Prow_new[NB + j];
+                            const T dz = Prow_new[2 * NB + i] - Prow_new[2 * NB + j];
+                            zmin_ws = fmin(zmin_ws, fmin(fabs(dx), fmin(fabs(dy), fabs(dz))));
+                            const T q = fma_t<T>(dz * fp.beta, dz, fma_t<T>(dy, dy, dx * dx));
+                            if (!(q >= fp.lim)) nm[w] &= ~(1u << bit);
                         }
                     }
-                    atomicMin(&((UT*)sp.aq)[t], UBits<T>::of(qm));
-                    atomicMin(&((UT*)sp.az)[t], UBits<T>::of(zm));
-                    if (m) atomicOr(&sp.anm[t * SW + ((c * PPC) >> 5)], m);
                 }
-                slot_barrier(bar_id, gsize);
-
-                // ---------------- T3: queued time steps finish with their scan results
-                if (lt < S && need_scan) {
-                    rmin = sqrt(UBits<T>::val(((UT*)sp.aq)[lt])) / fp.lat;
-                    cum = T(0);
-                    const T zmin = fmin(zmin_ws, UBits<T>::val(((UT*)sp.az)[lt]));
-#pragma unroll
-                    for (int w = 0; w < SW; ++w) nm[w] &= ~sp.anm[lt * SW + w];
-                    finish_step<T, NB>(sp, lt, n, par, Prow_old, Prow_new, qinf, qsq, nm, zmin, imask, zprev, fp, fw, cx,
-                                       cy, cz);
-                }
-                slot_barrier(bar_id, gsize);
             }
+
+            // ---------------- T2: warp-local O(n^2) pair scans of this warp's queued time steps: all 32 lanes
+            // take 1/32 of the pairs of one step; ballots give the non-interior pair bits, shuffles the minima
+            T zmin_pairs = T(1);
+            __syncwarp();   // the rows written in T1 are read by the other lanes
+            uint32_t qmask = __ballot_sync(0xffffffffu, lt < S && need_scan);
+            while (qmask) {
+                const int src = __ffs(qmask) - 1;
+                qmask &= qmask - 1;
+                const T* row = Prow_new + (src - lane) * RS;   // row of time step (lt - lane + src)
+                T qm = T(1e30), zm = T(1);   // min q over the far pairs, min |component| over all pairs
+                uint32_t words[NPW], nwords[NPW];
+#pragma unroll
+                for (int u = 0; u < NPW; ++u) {
+                    const int bb = u * 32 + lane;
+                    bool outside = false, is_near = false;
+                    if (bb < NP) {
+                        const int ij = ptab[bb], i = ij & 0xff, j = ij >> 8;
+                        if (j < n) {
+                            const T dx = row[i] - row[j], dy = row[NB + i] - row[NB + j];
+                            const T dz = row[2 * NB + i] - row[2 * NB + j];
+                            zm = fmin(zm, fmin(fabs(dx), fmin(fabs(dy), fabs(dz))));
+                            const T q = fma_t<T>(dz * fp.beta, dz, fma_t<T>(dy, dy, dx * dx));
+                            is_near = !(q >= skin_lim);
+                            if (!is_near) qm = fmin(qm, q);
+                            outside = !(q >= fp.lim);
+                        }
+                    }
+                    words[u] = __ballot_sync(0xffffffffu, outside);
+                    nwords[u] = __ballot_sync(0xffffffffu, is_near);
+                }
+                qm = warp_min_nonneg(qm);
+                zm = warp_min_nonneg(zm);
+                if (lane == src) {
+                    rmin = sqrt(qm) / fp.lat;
+                    cum = T(0);
+                    zmin_pairs = zm;
+#pragma unroll
+                    for (int u = 0; u < NPW; ++u) {
+                        nm[u] &= ~words[u];
+                        near[u] = nwords[u];
+                    }
+                }
+            }
+
+            // ---------------- T3: every time step finishes (quiet / flagged / careful path)
+            if (lt < S)
+                finish_step<T, NB>(sp, lt, n, par, Prow_old, Prow_new, qinf, qsq, nm, fmin(zmin_ws, zmin_pairs), imask,
+                                   zprev, fp, fw, cx, cy, cz);
+            slot_barrier(bar_id, gsize);
 
             // ---------------- decision (every warp, redundantly): exit residual of iteration k-1, early stop, SingularKKT
             double emax = 0.0, sqs = 0.0;
@@ -997,7 +999,7 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                         p.status[sample] = failed ? SAMPLE_SINGULAR_KKT : SAMPLE_OK;
                         p.eq_err[sample] = emax;
                         sp.sh->sample = next_sample(p);
-                        // nothing reads the flags in a final iteration (scount: only a clear of a zero)
+                        // nothing reads the flags in a final iteration
                         clear_flags(sp.sh, 0, SWT);
                         clear_flags(sp.sh, 1, SWT);
                     }
