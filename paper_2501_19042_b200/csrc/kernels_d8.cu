@@ -2,6 +2,6 @@
 #include "sf_launch.cuh"
 
 namespace sgsf {
-SGSF_DEFINE_LAUNCH(double, 8, 12, 256)
-SGSF_DEFINE_LAUNCH(double, 8, 16, 256)
+SGSF_DEFINE_LAUNCH(double, 8, 12, 256, 1)
+SGSF_DEFINE_LAUNCH(double, 8, 16, 256, 1)
 }  // namespace sgsf

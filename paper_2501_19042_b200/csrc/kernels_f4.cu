@@ -2,6 +2,6 @@
 #include "sf_launch.cuh"
 
 namespace sgsf {
-SGSF_DEFINE_LAUNCH(float, 4, 12, 512)
-SGSF_DEFINE_LAUNCH(float, 4, 16, 512)
+SGSF_DEFINE_LAUNCH(float, 4, 12, 512, 1)
+SGSF_DEFINE_LAUNCH(float, 4, 16, 512, 1)
 }  // namespace sgsf

@@ -2,6 +2,6 @@
 #include "sf_launch.cuh"
 
 namespace sgsf {
-SGSF_DEFINE_LAUNCH(float, 8, 12, 384)
-SGSF_DEFINE_LAUNCH(float, 8, 16, 384)
+SGSF_DEFINE_LAUNCH(float, 8, 12, 384, 1)
+SGSF_DEFINE_LAUNCH(float, 8, 16, 384, 1)
 }  // namespace sgsf

@@ -21,15 +21,16 @@ void internal_count_launch(int n);
 // longest-first queue order (kernels_order.cu)
 int launch_order(const SolveParams& p, float* score, int* order, cudaStream_t stream);
 
-template <typename T, int NB, int MP, int MAXT>
+template <typename T, int NB, int MP, int MAXT, int TPS>
 int launch_persistent(const LaunchInfo& li, SolveParams& p, const sgsf_config_t* cfg, const sgsf_timing_t* timing,
                       cudaStream_t stream) {
-    auto kern = sf_persistent_kernel<T, NB, MP, MAXT>;
+    auto kern = sf_persistent_kernel<T, NB, MP, MAXT, TPS>;
     int dev_smem = 0;
     cudaError_t e = cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, li.device);
     if (e != cudaSuccess) return internal_fail(SGSF_ERR_CUDA, cudaGetErrorString(e));
-    // a slot is a warp group of ceil(S/32) warps with its own named barrier (ids 1..15)
-    const int wps = (p.S + 31) / 32;
+    // a slot is a warp group with its own named barrier (ids 1..15): ceil(S/32) warps with one
+    // thread per time step, ceil(S/16) warps with two (TPS = 2: 16 steps per warp)
+    const int wps = TPS == 2 ? (p.S + 15) / 16 : (p.S + 31) / 32;
     const int slot_threads = 32 * wps;
     int spb = cfg->slots_per_block;
     if (spb <= 0) {
@@ -70,28 +71,32 @@ int launch_persistent(const LaunchInfo& li, SolveParams& p, const sgsf_config_t*
 }
 
 // instantiated in kernels_*.cu
-#define SGSF_DECLARE_LAUNCH(T, NB, MP, MAXT)                                                                  \
-    extern template int launch_persistent<T, NB, MP, MAXT>(const LaunchInfo&, SolveParams&, const sgsf_config_t*, \
-                                                           const sgsf_timing_t*, cudaStream_t);
-#define SGSF_DEFINE_LAUNCH(T, NB, MP, MAXT)                                                                    \
-    template int launch_persistent<T, NB, MP, MAXT>(const LaunchInfo&, SolveParams&, const sgsf_config_t*,    \
-                                                    const sgsf_timing_t*, cudaStream_t);
+#define SGSF_DECLARE_LAUNCH(T, NB, MP, MAXT, TPS)                                                   \
+    extern template int launch_persistent<T, NB, MP, MAXT, TPS>(const LaunchInfo&, SolveParams&,         \
+                                                                const sgsf_config_t*, const sgsf_timing_t*, \
+                                                                cudaStream_t);
+#define SGSF_DEFINE_LAUNCH(T, NB, MP, MAXT, TPS)                                                             \
+    template int launch_persistent<T, NB, MP, MAXT, TPS>(const LaunchInfo&, SolveParams&, const sgsf_config_t*, \
+                                                         const sgsf_timing_t*, cudaStream_t);
 
-// (T, NB, MAXT): MAXT caps the CTA so ptxas can give the register-resident
-// term pass the registers it needs.
-#define SGSF_FOR_EACH_VARIANT(X) \
-    X(float, 4, 12, 512)         \
-    X(float, 4, 16, 512)         \
-    X(float, 8, 12, 384)         \
-    X(float, 8, 16, 384)         \
-    X(float, 16, 12, 384)        \
-    X(float, 16, 16, 384)        \
-    X(double, 4, 12, 384)        \
-    X(double, 4, 16, 384)        \
-    X(double, 8, 12, 256)        \
-    X(double, 8, 16, 256)        \
-    X(double, 16, 12, 256)       \
-    X(double, 16, 16, 256)
+// (T, NB, MP, MAXT, TPS): MAXT caps the CTA so ptxas can give the
+// register-resident term pass the registers it needs; TPS = threads per time
+// step.  TPS = 2 (half the robots per lane, 7 warps per slot) compiles but
+// measured slower on B200: the term pass is latency-bound, not
+// work-bound, and the extra warps cap the registers at 80 (spills).
+#define SGSF_FOR_EACH_VARIANT(X)  \
+    X(float, 4, 12, 512, 1)       \
+    X(float, 4, 16, 512, 1)       \
+    X(float, 8, 12, 384, 1)       \
+    X(float, 8, 16, 384, 1)       \
+    X(float, 16, 12, 384, 1)      \
+    X(float, 16, 16, 384, 1)      \
+    X(double, 4, 12, 384, 1)      \
+    X(double, 4, 16, 384, 1)      \
+    X(double, 8, 12, 256, 1)      \
+    X(double, 8, 16, 256, 1)      \
+    X(double, 16, 12, 256, 1)     \
+    X(double, 16, 16, 256, 1)
 
 SGSF_FOR_EACH_VARIANT(SGSF_DECLARE_LAUNCH)
 

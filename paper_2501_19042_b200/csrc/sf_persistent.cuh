@@ -102,7 +102,15 @@ __device__ __forceinline__ void clear_flags(SlotShared* sh, int b, int words) {
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
-template <int NB> struct RowStride { static constexpr int value = 3 * NB + 1; };
+// Position-row stride (elements of T): a whole number of 16-byte units, and an
+// odd number of them, so the per-thread rows are read and written as 16-byte
+// vectors with no bank conflicts (8 consecutive rows hit 8 distinct 16-byte
+// bank groups).
+template <typename T, int NB> struct RowStride {
+    static constexpr int per16 = 16 / (int)sizeof(T);
+    static constexpr int base = (3 * NB + per16 - 1) / per16;   // 16-byte units
+    static constexpr int value = ((base & 1) ? base : base + 1) * per16;
+};
 
 // Shared-memory map.  Coefficient-space arrays are padded to MP (m1 rounded
 // up to a multiple of 4) columns with zeros, so every loop over the degree
@@ -120,7 +128,7 @@ struct SmemLayout {
 
 template <typename T, int NB>
 __host__ __device__ inline SmemLayout make_layout(int n, int S, int MP, int spb, int want_prev) {
-    const int RS = RowStride<NB>::value;
+    const int RS = RowStride<T, NB>::value;
     SmemLayout L;
     size_t o = 0;
     const size_t d = sizeof(double), ts = sizeof(T);
@@ -242,171 +250,251 @@ __device__ __forceinline__ bool bit_of(const uint32_t* m, int b) { return (m[b >
 template <int NB> __host__ __device__ constexpr int pair_bit(int i, int j) { return i * (2 * NB - i - 1) / 2 + (j - i - 1); }
 template <int NB> __host__ __device__ constexpr int ws_bit(int i) { return NB * (NB - 1) / 2 + i; }
 
-// positions of every robot at time step t:  p(t) = C W[t]^T.  Cf is stored
-// robot-minor ([ax][q][NB]) so two robots' coefficients form one f32x2
-// operand.  Robots past n become "phantoms" at distinct, far-away positions:
-// every pair term with a phantom is interior and has no zero component, so
-// the O(n^2) scan needs no per-pair guards.
+// Robots past n become "phantoms" at distinct, far-away positions: every
+// pair term with a phantom is interior and has no zero component.  Cf is
+// stored robot-minor ([ax][q][NB]) so two robots' coefficients form one
+// f32x2 operand.
 template <typename T> __device__ __forceinline__ T phantom_pos(int i) { return T(1e30) * T(i + 1); }
 
-template <typename T, int NB, int MP>
-__device__ __forceinline__ void positions_at(const T* __restrict__ Wt, const T* __restrict__ Cf, int t, int n,
-                                             T (&pos)[3 * NB]) {
+
+// ---- part-wise term pass: a thread owns RH = NB / TPS robots [r0, r0 + RH) of its time step;
+// with TPS = 2 the two halves of a step sit in lanes l and l ^ 16 and combine with shuffles.
+
+// positions of robots [r0, r0 + RH) at time step t (phantoms past n)
+template <typename T, int NB, int RH, int MP>
+__device__ __forceinline__ void positions_part(const T* __restrict__ Wt, const T* __restrict__ Cf, int t, int r0, int n,
+                                               T (&pos)[3 * RH]) {
     T w[MP];
     load_row16<T, MP>(Wt + t * MP, w);
-    if constexpr (sizeof(T) == 4 && NB % 4 == 0) {
+    if constexpr (sizeof(T) == 4 && RH % 4 == 0) {
         float2 w2[MP];
 #pragma unroll
         for (int q = 0; q < MP; ++q) w2[q] = make_float2(w[q], w[q]);
 #pragma unroll
         for (int ax = 0; ax < 3; ++ax) {
 #pragma unroll
-            for (int i4 = 0; i4 < NB; i4 += 4) {
+            for (int i4 = 0; i4 < RH; i4 += 4) {
                 float2 a01 = make_float2(0.f, 0.f), a23 = make_float2(0.f, 0.f);
 #pragma unroll
                 for (int q = 0; q < MP; ++q) {
-                    const float4 c = *reinterpret_cast<const float4*>(Cf + (ax * MP + q) * NB + i4);
+                    const float4 c = *reinterpret_cast<const float4*>(Cf + (ax * MP + q) * NB + r0 + i4);
                     a01 = __ffma2_rn(make_float2(c.x, c.y), w2[q], a01);
                     a23 = __ffma2_rn(make_float2(c.z, c.w), w2[q], a23);
                 }
-                pos[ax * NB + i4] = a01.x;
-                pos[ax * NB + i4 + 1] = a01.y;
-                pos[ax * NB + i4 + 2] = a23.x;
-                pos[ax * NB + i4 + 3] = a23.y;
+                pos[ax * RH + i4] = a01.x;
+                pos[ax * RH + i4 + 1] = a01.y;
+                pos[ax * RH + i4 + 2] = a23.x;
+                pos[ax * RH + i4 + 3] = a23.y;
             }
         }
     } else {
 #pragma unroll
         for (int ax = 0; ax < 3; ++ax) {
 #pragma unroll
-            for (int i = 0; i < NB; ++i) {
+            for (int i = 0; i < RH; ++i) {
                 T s = T(0);
 #pragma unroll
-                for (int q = 0; q < MP; ++q) s = fma_t<T>(Cf[(ax * MP + q) * NB + i], w[q], s);
-                pos[ax * NB + i] = s;
+                for (int q = 0; q < MP; ++q) s = fma_t<T>(Cf[(ax * MP + q) * NB + r0 + i], w[q], s);
+                pos[ax * RH + i] = s;
             }
         }
     }
 #pragma unroll
-    for (int q = 0; q < 3 * NB; ++q)
-        if ((q % NB) >= n) pos[q] = phantom_pos<T>(q % NB);
+    for (int q = 0; q < 3 * RH; ++q)
+        if (r0 + (q % RH) >= n) pos[q] = phantom_pos<T>(r0 + (q % RH));
 }
 
-// Interior bit of every term at the current positions (terms past n count as
-// interior) and min |component| over all differences (0 -> careful path).
-// Pair terms are scanned only when `pairs` is set (see the motion bound in
-// the kernel); workspace terms always.  Common case: every term interior --
-// the scan then keeps running min(q) over the pairs, max(q) over the
-// workspace terms and min |component|, each split four ways so the
-// accumulations are independent instruction chains; per-term bits are
-// computed in a second pass only when needed.  Returns min q over the pairs.
-template <typename T, int NB>
-__device__ __forceinline__ T interior_scan(const T (&pos)[3 * NB], int n, const Family<T>& fp, const Family<T>& fw,
-                                           T cx, T cy, T cz, bool pairs, uint32_t (&nm)[TermBits<NB>::words],
-                                           T& zmin) {
-    T qm[4], zm[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        qm[u] = T(1e38);
-        zm[u] = T(1);
-    }
-    if (pairs) {
-#pragma unroll
-        for (int i = 0; i < NB; ++i) {
-            const T pix = pos[i], piy = pos[NB + i], piz = pos[2 * NB + i];
-#pragma unroll
-            for (int j = 0; j < NB; ++j) {   // constant trip count: nvcc fully unrolls only those
-                if (j > i) {
-                    const int u = pair_bit<NB>(i, j) & 3;
-                    const T dx = pix - pos[j], dy = piy - pos[NB + j], dz = piz - pos[2 * NB + j];
-                    zm[u] = fmin(zm[u], fmin(fabs(dx), fmin(fabs(dy), fabs(dz))));
-                    qm[u] = fmin(qm[u], fma_t<T>(dz * fp.beta, dz, fma_t<T>(dy, dy, dx * dx)));
-                }
-            }
-        }
-    }
-    T qw = T(0);
-#pragma unroll
-    for (int i = 0; i < NB; ++i) {
-        if (i < n) {
-            const T rx = pos[i] - cx, ry = pos[NB + i] - cy, rz = pos[2 * NB + i] - cz;
-            zm[i & 3] = fmin(zm[i & 3], fmin(fabs(rx), fmin(fabs(ry), fabs(rz))));
-            qw = fmax(qw, fma_t<T>(rz * fw.beta, rz, fma_t<T>(ry, ry, rx * rx)));
-        }
-    }
-    zmin = fmin(fmin(zm[0], zm[1]), fmin(zm[2], zm[3]));
-#pragma unroll
-    for (int w = 0; w < TermBits<NB>::words; ++w) nm[w] = 0xffffffffu;
-    const T qmin = fmin(fmin(qm[0], qm[1]), fmin(qm[2], qm[3]));
-    if (__builtin_expect(!(qmin >= fp.lim), 0)) {
-#pragma unroll
-        for (int i = 0; i < NB; ++i) {
-#pragma unroll
-            for (int j = 0; j < NB; ++j) {
-                if (j > i) {
-                    const int b = pair_bit<NB>(i, j);
-                    const T dx = pos[i] - pos[j], dy = pos[NB + i] - pos[NB + j], dz = pos[2 * NB + i] - pos[2 * NB + j];
-                    const T q = fma_t<T>(dz * fp.beta, dz, fma_t<T>(dy, dy, dx * dx));
-                    if (!(q >= fp.lim)) nm[b >> 5] &= ~(1u << (b & 31));
-                }
-            }
-        }
-    }
-    if (__builtin_expect(!(qw <= fw.lim), 0)) {
-#pragma unroll
-        for (int i = 0; i < NB; ++i) {
-            const int b = ws_bit<NB>(i);
-            if (i < n) {
-                const T rx = pos[i] - cx, ry = pos[NB + i] - cy, rz = pos[2 * NB + i] - cz;
-                const T q = fma_t<T>(rz * fw.beta, rz, fma_t<T>(ry, ry, rx * rx));
-                if (!(q <= fw.lim)) nm[b >> 5] &= ~(1u << (b & 31));
-            }
-        }
-    }
-    return qmin;
-}
-
-template <typename T, int NB> struct QuietStats {
-    T inf, sq;
-    T dmax2;   // max_i a^2 |Dp_i|_s^2 (same quadratic form as q): bounds the motion of every pair
-};
-
-// One pass per axis: min, max, max |Dp|, sum and sum of squares of Dp;
-// sq = (n+1) sum Dp^2 - (sum Dp)^2 (= n sum (Dp - mean)^2 + sum Dp^2).
-template <typename T, int NB>
-__device__ __forceinline__ QuietStats<T, NB> quiet_residual(const T (&pos)[3 * NB], const T* __restrict__ Pold, int n,
-                                                            T fp_beta) {
-    QuietStats<T, NB> st;
-    T mx = T(0), s2 = T(0);
-    T dq[NB];
-#pragma unroll
-    for (int i = 0; i < NB; ++i) dq[i] = T(0);
+// 16-byte vector copies of this thread's part of a position row
+template <typename T, int NB, int RH>
+__device__ __forceinline__ void store_part(T* __restrict__ row, int r0, const T (&pos)[3 * RH]) {
+    using V = typename Vec16<T>::type;
+    constexpr int L = Vec16<T>::lanes;
 #pragma unroll
     for (int ax = 0; ax < 3; ++ax) {
-        T lo = T(1e38), hi = T(-1e38), am = T(0), s1 = T(0), sq = T(0);
 #pragma unroll
-        for (int i = 0; i < NB; ++i) {
-            if (i < n) {
-                const T dpi = pos[ax * NB + i] - Pold[ax * NB + i];
-                lo = fmin(lo, dpi);
-                hi = fmax(hi, dpi);
-                am = fmax(am, fabs(dpi));
-                s1 += dpi;
-                sq = fma_t<T>(dpi, dpi, sq);
-                dq[i] = fma_t<T>(ax == 2 ? dpi * fp_beta : dpi, dpi, dq[i]);
-            }
+        for (int c = 0; c < RH / L; ++c) {
+            V v;
+            T* e = reinterpret_cast<T*>(&v);
+#pragma unroll
+            for (int u = 0; u < L; ++u) e[u] = pos[ax * RH + c * L + u];
+            *reinterpret_cast<V*>(row + ax * NB + r0 + c * L) = v;
         }
-        mx = fmax(mx, fmax(hi - lo, am));
-        s2 += fmax(fma_t<T>((T)(n + 1), sq, -s1 * s1), sq);
     }
-    T dm = T(0);
+}
+template <typename T, int NB, int RH>
+__device__ __forceinline__ void load_part(const T* __restrict__ row, int r0, T (&out)[3 * RH]) {
+    using V = typename Vec16<T>::type;
+    constexpr int L = Vec16<T>::lanes;
 #pragma unroll
-    for (int i = 0; i < NB; ++i) dm = fmax(dm, dq[i]);
-    st.dmax2 = dm;
+    for (int ax = 0; ax < 3; ++ax) {
+#pragma unroll
+        for (int c = 0; c < RH / L; ++c) {
+            const V v = *reinterpret_cast<const V*>(row + ax * NB + r0 + c * L);
+            const T* e = reinterpret_cast<const T*>(&v);
+#pragma unroll
+            for (int u = 0; u < L; ++u) out[ax * RH + c * L + u] = e[u];
+        }
+    }
+}
+
+// combine the two halves of a time step (lanes l, l ^ 16); identity for TPS = 1
+template <int TPS, typename V> __device__ __forceinline__ V part_min(V v, unsigned m) {
+    if constexpr (TPS == 2) return fmin(v, __shfl_xor_sync(m, v, 16));
+    return v;
+}
+template <int TPS, typename V> __device__ __forceinline__ V part_max(V v, unsigned m) {
+    if constexpr (TPS == 2) return fmax(v, __shfl_xor_sync(m, v, 16));
+    return v;
+}
+template <int TPS, typename V> __device__ __forceinline__ V part_sum(V v, unsigned m) {
+    if constexpr (TPS == 2) return v + __shfl_xor_sync(m, v, 16);
+    return v;
+}
+template <int TPS> __device__ __forceinline__ uint32_t part_and(uint32_t v, unsigned m) {
+    if constexpr (TPS == 2) return v & __shfl_xor_sync(m, v, 16);
+    return v;
+}
+
+template <typename T> struct PartStats {
+    T inf, sq, dmax2;
+};
+
+// pairwise (tree) reduction of a register array, log2(N) dependent levels
+template <typename T, int N, typename Op> __device__ __forceinline__ T tree_reduce(T (&v)[N], Op op) {
+#pragma unroll
+    for (int w = N / 2; w >= 1; w /= 2) {
+#pragma unroll
+        for (int i = 0; i < w; ++i) v[i] = op(v[i], v[i + w]);
+    }
+    return v[0];
+}
+struct OpMin { template <typename T> __device__ T operator()(T a, T b) const { return fmin(a, b); } };
+struct OpMax { template <typename T> __device__ T operator()(T a, T b) const { return fmax(a, b); } };
+struct OpAdd { template <typename T> __device__ T operator()(T a, T b) const { return a + b; } };
+
+// O(n) statistics of the position change Dp of the whole step, from this
+// thread's robots (Pold: the old row): per axis min, max, sum and sum of
+// squares, combined over the step's lanes.  inf = max over the terms of
+// |Dp_i - Dp_j| (pairs: per-axis range) and |Dp_i| (workspace: max(max, -min));
+// sq = (n+1) sum Dp^2 - (sum Dp)^2 (= n sum (Dp - mean)^2 + sum Dp^2).  FULL:
+// every robot of this part is real (no phantom guards; tree reductions).  All
+// lanes in `m` must call it together.
+template <typename T, int NB, int RH, int TPS, bool FULL>
+__device__ __forceinline__ PartStats<T> quiet_part(const T (&pos)[3 * RH], const T* __restrict__ Pold, int r0, int n,
+                                                   T fp_beta, unsigned m) {
+    T old[3 * RH];
+    load_part<T, NB, RH>(Pold, r0, old);
+    T dp[3 * RH];
+#pragma unroll
+    for (int q = 0; q < 3 * RH; ++q) dp[q] = pos[q] - old[q];   // phantoms: 0 (same far value in both rows)
+    T mx = T(0), s2 = T(0), dm = T(0);
+    if constexpr (FULL) {
+        T dq[RH];
+#pragma unroll
+        for (int i = 0; i < RH; ++i)
+            dq[i] = fma_t<T>(dp[2 * RH + i] * fp_beta, dp[2 * RH + i], fma_t<T>(dp[RH + i], dp[RH + i], dp[i] * dp[i]));
+        dm = tree_reduce(dq, OpMax());
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) {
+            T lo[RH], hi[RH], s1[RH], sq[RH];
+#pragma unroll
+            for (int i = 0; i < RH; ++i) {
+                lo[i] = hi[i] = s1[i] = dp[ax * RH + i];
+                sq[i] = dp[ax * RH + i] * dp[ax * RH + i];
+            }
+            T l = part_min<TPS>(tree_reduce(lo, OpMin()), m), hh = part_max<TPS>(tree_reduce(hi, OpMax()), m);
+            T a1 = part_sum<TPS>(tree_reduce(s1, OpAdd()), m), a2 = part_sum<TPS>(tree_reduce(sq, OpAdd()), m);
+            mx = fmax(mx, fmax(hh - l, fmax(hh, -l)));
+            s2 += fmax(fma_t<T>((T)(n + 1), a2, -a1 * a1), a2);
+        }
+    } else {
+        T dq[RH];
+#pragma unroll
+        for (int i = 0; i < RH; ++i) dq[i] = T(0);
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) {
+            T lo = T(1e38), hi = T(-1e38), s1 = T(0), sq = T(0);
+#pragma unroll
+            for (int i = 0; i < RH; ++i) {
+                if (r0 + i < n) {
+                    const T dpi = dp[ax * RH + i];
+                    lo = fmin(lo, dpi);
+                    hi = fmax(hi, dpi);
+                    s1 += dpi;
+                    sq = fma_t<T>(dpi, dpi, sq);
+                    dq[i] = fma_t<T>(ax == 2 ? dpi * fp_beta : dpi, dpi, dq[i]);
+                }
+            }
+            lo = part_min<TPS>(lo, m);
+            hi = part_max<TPS>(hi, m);
+            s1 = part_sum<TPS>(s1, m);
+            sq = part_sum<TPS>(sq, m);
+            mx = fmax(mx, fmax(hi - lo, fmax(hi, -lo)));
+            s2 += fmax(fma_t<T>((T)(n + 1), sq, -s1 * s1), sq);
+        }
+#pragma unroll
+        for (int i = 0; i < RH; ++i) dm = fmax(dm, dq[i]);
+    }
+    PartStats<T> st;
+    st.dmax2 = part_max<TPS>(dm, m);
     st.inf = mx;
     st.sq = s2;
     return st;
 }
+
+// workspace terms of this thread's robots: a value that is 0 iff some
+// component is exactly zero (FULL: the product of the three components,
+// which can only underflow to a false "zero" -- that just takes the exact
+// careful path), and the non-interior workspace bits cleared in nm (combined
+// over the step's lanes; h = this lane's half)
+template <typename T, int NB, int RH, int TPS, bool FULL>
+__device__ __forceinline__ T ws_part(const T (&pos)[3 * RH], int r0, int h, int n, const Family<T>& fw, T cx, T cy,
+                                     T cz, uint32_t (&nm)[TermBits<NB>::words], unsigned m) {
+    T zm = T(1), qw = T(0);
+    if constexpr (FULL) {
+        T zv[RH], qv[RH];
+#pragma unroll
+        for (int i = 0; i < RH; ++i) {
+            const T rx = pos[i] - cx, ry = pos[RH + i] - cy, rz = pos[2 * RH + i] - cz;
+            zv[i] = fabs(rx * ry * rz);
+            qv[i] = fma_t<T>(rz * fw.beta, rz, fma_t<T>(ry, ry, rx * rx));
+        }
+        zm = tree_reduce(zv, OpMin());
+        qw = tree_reduce(qv, OpMax());
+    } else {
+#pragma unroll
+        for (int i = 0; i < RH; ++i) {
+            if (r0 + i < n) {
+                const T rx = pos[i] - cx, ry = pos[RH + i] - cy, rz = pos[2 * RH + i] - cz;
+                zm = fmin(zm, fmin(fabs(rx), fmin(fabs(ry), fabs(rz))));
+                qw = fmax(qw, fma_t<T>(rz * fw.beta, rz, fma_t<T>(ry, ry, rx * rx)));
+            }
+        }
+    }
+#pragma unroll
+    for (int w = 0; w < TermBits<NB>::words; ++w) nm[w] = 0xffffffffu;
+    if (__builtin_expect(__any_sync(m, !(qw <= fw.lim)), 0)) {
+        uint32_t out = 0u;   // bit i: workspace term of robot r0 + i non-interior
+#pragma unroll
+        for (int i = 0; i < RH; ++i) {
+            if (r0 + i < n) {
+                const T rx = pos[i] - cx, ry = pos[RH + i] - cy, rz = pos[2 * RH + i] - cz;
+                const T q = fma_t<T>(rz * fw.beta, rz, fma_t<T>(ry, ry, rx * rx));
+                if (!(q <= fw.lim)) out |= 1u << i;
+            }
+        }
+        if constexpr (TPS == 2) {
+            const uint32_t other = __shfl_xor_sync(m, out, 16);
+            out = h == 0 ? (out | (other << RH)) : (other | (out << RH));
+        }
+        constexpr int NP = NB * (NB - 1) / 2;
+        const unsigned long long sh = (unsigned long long)out << (NP & 31);
+        nm[NP >> 5] &= ~(uint32_t)sh;
+        if constexpr ((NP & 31) + NB > 32) nm[(NP >> 5) + 1] &= ~(uint32_t)(sh >> 32);
+    }
+    return part_min<TPS>(zm, m);
+}
+
 
 // by-value packs of register arrays for out-of-line calls
 template <typename T, int NB> struct PosPack {
@@ -477,7 +565,7 @@ __device__ __noinline__ StepOut<T> flagged_path(const T* __restrict__ Pnew, T* _
                     const T nj = Pnew[ax * NB + j], oj = Pold[ax * NB + j];
                     d[ax] = ni - nj;
                     o[ax] = oi - oj;
-                    x[ax] = (ni - oi) - (nj - oj);   // Dp_i - Dp_j exactly as in quiet_residual
+                    x[ax] = (ni - oi) - (nj - oj);   // Dp_i - Dp_j exactly as in quiet_part
                 } else {
                     d[ax] = ni - c3[ax];
                     o[ax] = oi - c3[ax];
@@ -756,11 +844,11 @@ __device__ __forceinline__ void load_row(const SolveParams& p, const SlotPtrs& s
 }
 
 // ---------------------------------------------------------------- the kernel
-template <typename T, int NB, int MP, int MAXT>
+template <typename T, int NB, int MP, int MAXT, int TPS>
 __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const SmemLayout L = make_layout<T, NB>(p.n, p.S, MP, p.spb, p.want_prev);
-    constexpr int RS = RowStride<NB>::value;
+    constexpr int RS = RowStride<T, NB>::value;
     constexpr int M2P = 2 * MP;
     constexpr int NW = TermBits<NB>::words;
     const int tid = threadIdx.x, nt = blockDim.x;
@@ -817,9 +905,35 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
     const Family<T> fw = make_family<T>(p.ws_lat, p.ws_vert);
     const T cx = (T)p.cx, cy = (T)p.cy, cz = (T)p.cz;
     const int SWT = (S + 31) >> 5;   // words of the active-step mask
+    // time step of this thread and the part of the robots it owns: TPS = 2 puts the two halves
+    // of a step in lanes l and l ^ 16 (16 steps per warp); the h = 0 lane owns the step's state
+    constexpr int RH = NB / TPS;
+    const int ts = TPS == 2 ? lwarp * 16 + (lane & 15) : lt;
+    const int h = TPS == 2 ? lane >> 4 : 0;
+    const int r0 = h * RH;
+    const bool owner = h == 0;
+    const unsigned smask = __ballot_sync(0xffffffffu, ts < S);   // lanes of this warp with a step
 
     constexpr int NP = NB * (NB - 1) / 2;
     constexpr int NPW = (NP + 31) / 32;   // words holding pair bits
+#ifdef SGSF_PHASE_TIMING
+    // clock64 stamps of slot 0 / thread 0 of CTA 0: [0] loop top (after MX barrier), [5] T1 end,
+    // [6] T2 end, [1] after the term-pass barrier, [2] after decision, [3] after G, [4] after MX barrier
+    long long pt_last = 0, pt_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int pt_prev = -1, pt_iters = 0;
+#define SGSF_PT(ID)                                                                          \
+    do {                                                                                      \
+        if (tid == 0) {                                                                        \
+            const long long now = clock64();                                                  \
+            if (pt_prev >= 0) pt_acc[ID] += now - pt_last;                                    \
+            pt_last = now;                                                                    \
+            pt_prev = ID;                                                                     \
+            if (ID == 0) ++pt_iters;                                                          \
+        }                                                                                     \
+    } while (0)
+#else
+#define SGSF_PT(ID) ((void)0)
+#endif
     uint32_t imask[NW];
     bool zprev = false;
     // Verlet-style pair list: the last scan of this time step split the pairs
@@ -847,63 +961,65 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
         slot_barrier(bar_id, gsize);
 
         for (int k = 0;; ++k) {
+            SGSF_PT(0);
             const int par = k & 1;
             if (lt == 0) clear_flags(sp.sh, par ^ 1, SWT);   // last read before the previous closing barrier
             // position rows: old = iterate k, new = iterate k+1's input positions; R -> old row
-            T* Prow_old = (T*)((k & 1) ? sp.P1 : sp.P0) + lt * RS;
-            T* Prow_new = (T*)((k & 1) ? sp.P0 : sp.P1) + lt * RS;
-            // ---------------- T1: positions, O(n) statistics, motion bound; quiet steps finish here
+            T* const Pbase_new = (T*)((k & 1) ? sp.P0 : sp.P1);
+            T* Prow_old = (T*)((k & 1) ? sp.P1 : sp.P0) + ts * RS;
+            T* Prow_new = Pbase_new + ts * RS;
+            // ---------------- T1: positions, O(n) statistics, workspace terms, motion bound, near pairs
             bool need_scan = false;
             uint32_t nm[NW];
             T zmin_ws = T(1), qinf = T(0), qsq = T(0);   // quiet statistics, kept for T3
-            if (lt < S) {
-                T pos[3 * NB];
-                positions_at<T, NB, MP>(Wt, (const T*)sp.Cf, lt, n, pos);
-#pragma unroll
-                for (int q = 0; q < 3 * NB; ++q) {
-                    if ((q % NB) < n) {
-                        Prow_new[q] = pos[q];
-                        if (k == 0) Prow_old[q] = pos[q];   // no previous iterate: "old" := "new"
-                    }
-                }
+            if (ts < S) {
+                T pos[3 * RH];
+                positions_part<T, NB, RH, MP>(Wt, (const T*)sp.Cf, ts, r0, n, pos);
+                store_part<T, NB, RH>(Prow_new, r0, pos);
                 if (k == 0) {
+                    store_part<T, NB, RH>(Prow_old, r0, pos);   // no previous iterate: "old" := "new"
 #pragma unroll
                     for (int w = 0; w < NW; ++w) imask[w] = 0xffffffffu;
                     zprev = false;
                 }
-                const QuietStats<T, NB> st = quiet_residual<T, NB>(pos, Prow_old, n, fp.beta);
+                const bool full = n == NB;   // uniform: no phantom robots -> guard-free tree reductions
+                const PartStats<T> st = full ? quiet_part<T, NB, RH, TPS, true>(pos, Prow_old, r0, n, fp.beta, smask)
+                                             : quiet_part<T, NB, RH, TPS, false>(pos, Prow_old, r0, n, fp.beta, smask);
                 qinf = st.inf;
                 qsq = st.sq;
                 cum += T(2) * sqrt(st.dmax2) / fp.lat;
                 need_scan = (k == 0) || zprev || !(rmin - cum > T(1) + T(1e-3));
-                interior_scan<T, NB>(pos, n, fp, fw, cx, cy, cz, false, nm, zmin_ws);   // workspace terms only
-                if (!need_scan) {   // near pairs of the last scan, exactly (a pair active before is near)
+                zmin_ws = full ? ws_part<T, NB, RH, TPS, true>(pos, r0, h, n, fw, cx, cy, cz, nm, smask)
+                               : ws_part<T, NB, RH, TPS, false>(pos, r0, h, n, fw, cx, cy, cz, nm, smask);
+            }
+            __syncwarp();   // both halves of every row written before the owners and the scans read them
+            if (ts < S && owner && !need_scan) {   // near pairs of the last scan, exactly (a pair active before is near)
 #pragma unroll
-                    for (int w = 0; w < NPW; ++w) {
-                        uint32_t bits = near[w];
-                        while (bits) {
-                            const int bit = __ffs(bits) - 1;
-                            bits &= bits - 1;
-                            const int ij = ptab[w * 32 + bit], i = ij & 0xff, j = ij >> 8;
-                            const T dx = Prow_new[i] - Prow_new[j], dy = Prow_new[NB + i] - Prow_new[NB + j];
-                            const T dz = Prow_new[2 * NB + i] - Prow_new[2 * NB + j];
-                            zmin_ws = fmin(zmin_ws, fmin(fabs(dx), fmin(fabs(dy), fabs(dz))));
-                            const T q = fma_t<T>(dz * fp.beta, dz, fma_t<T>(dy, dy, dx * dx));
-                            if (!(q >= fp.lim)) nm[w] &= ~(1u << bit);
-                        }
+                for (int w = 0; w < NPW; ++w) {
+                    uint32_t bits = near[w];
+                    while (bits) {
+                        const int bit = __ffs(bits) - 1;
+                        bits &= bits - 1;
+                        const int ij = ptab[w * 32 + bit], i = ij & 0xff, j = ij >> 8;
+                        const T dx = Prow_new[i] - Prow_new[j], dy = Prow_new[NB + i] - Prow_new[NB + j];
+                        const T dz = Prow_new[2 * NB + i] - Prow_new[2 * NB + j];
+                        zmin_ws = fmin(zmin_ws, fmin(fabs(dx), fmin(fabs(dy), fabs(dz))));
+                        const T q = fma_t<T>(dz * fp.beta, dz, fma_t<T>(dy, dy, dx * dx));
+                        if (!(q >= fp.lim)) nm[w] &= ~(1u << bit);
                     }
                 }
             }
 
+            SGSF_PT(5);
             // ---------------- T2: warp-local O(n^2) pair scans of this warp's queued time steps: all 32 lanes
-            // take 1/32 of the pairs of one step; ballots give the non-interior pair bits, shuffles the minima
+            // take 1/32 of the pairs of one step; ballots give the non-interior pair bits, REDUX the minima
             T zmin_pairs = T(1);
-            __syncwarp();   // the rows written in T1 are read by the other lanes
-            uint32_t qmask = __ballot_sync(0xffffffffu, lt < S && need_scan);
+            uint32_t qmask = __ballot_sync(0xffffffffu, ts < S && owner && need_scan);
             while (qmask) {
                 const int src = __ffs(qmask) - 1;
                 qmask &= qmask - 1;
-                const T* row = Prow_new + (src - lane) * RS;   // row of time step (lt - lane + src)
+                const int tsrc = TPS == 2 ? lwarp * 16 + src : lt - lane + src;
+                const T* row = Pbase_new + tsrc * RS;
                 T qm = T(1e30), zm = T(1);   // min q over the far pairs, min |component| over all pairs
                 uint32_t words[NPW], nwords[NPW];
 #pragma unroll
@@ -939,11 +1055,13 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                 }
             }
 
-            // ---------------- T3: every time step finishes (quiet / flagged / careful path)
-            if (lt < S)
-                finish_step<T, NB>(sp, lt, n, par, Prow_old, Prow_new, qinf, qsq, nm, fmin(zmin_ws, zmin_pairs), imask,
+            SGSF_PT(6);
+            // ---------------- T3: every time step finishes (quiet / flagged / careful path), by its owner lane
+            if (ts < S && owner)
+                finish_step<T, NB>(sp, ts, n, par, Prow_old, Prow_new, qinf, qsq, nm, fmin(zmin_ws, zmin_pairs), imask,
                                    zprev, fp, fw, cx, cy, cz);
             slot_barrier(bar_id, gsize);
+            SGSF_PT(1);
 
             // ---------------- decision (every warp, redundantly): exit residual of iteration k-1, early stop, SingularKKT
             double emax = 0.0, sqs = 0.0;
@@ -1009,6 +1127,7 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                 break;
             }
 
+            SGSF_PT(2);
             // ---------------- G: lam' = lam - rho R W over the active time steps only (ascending t)
             const bool any_active = sp.sh->active[par] != 0;
             if (any_active) {
@@ -1038,6 +1157,7 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                 slot_barrier(bar_id, gsize);
             }
 
+            SGSF_PT(3);
             // ---------------- MX: one warp per axis -- swarm means of C and u = 2 lam' - lam + xi_bar,
             // mean part Mm Cb + Km11 ub, decoupled xi-step C_i = mean part + Md (C_i - Cb) + Kd11 (u_i - ub)
             // + cconst_i, ||A xi - b||_inf partials, commit.  Rows of one axis never leave their warp, so
@@ -1139,8 +1259,16 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                 }
             }
             slot_barrier(bar_id, gsize);
+            SGSF_PT(4);
         }
     }
+#ifdef SGSF_PHASE_TIMING
+    if (tid == 0)
+        printf("PT block %d iters %d total %.0f T1 %.0f T2 %.0f T3bar %.0f dec %.0f G %.0f MX %.0f\n", blockIdx.x, pt_iters,
+               (double)(pt_acc[0] + pt_acc[1] + pt_acc[2] + pt_acc[3] + pt_acc[4] + pt_acc[5] + pt_acc[6]),
+               (double)pt_acc[5] / pt_iters, (double)pt_acc[6] / pt_iters, (double)pt_acc[1] / pt_iters,
+               (double)pt_acc[2] / pt_iters, (double)pt_acc[3] / pt_iters, (double)(pt_acc[4] + pt_acc[0]) / pt_iters);
+#endif
 }
 
 }  // namespace sgsf

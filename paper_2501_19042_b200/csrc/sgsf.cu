@@ -224,17 +224,17 @@ int sgsf_solve(sgsf_handle_t* h, int batch, const double* xi_bar, const double* 
     const int n = h->n;
     const bool wide = h->m1 > 12;
     LaunchInfo li{h->device, h->sm_count};
-#define SGSF_PICK(T, NB, MAXT)                                                  \
-    return wide ? launch_persistent<T, NB, 16, MAXT>(li, p, cfg, timing, stream) \
-                : launch_persistent<T, NB, 12, MAXT>(li, p, cfg, timing, stream)
+#define SGSF_PICK(T, NB, MAXT, TPS)                                                       \
+    return wide ? launch_persistent<T, NB, 16, MAXT, TPS>(li, p, cfg, timing, stream) \
+                : launch_persistent<T, NB, 12, MAXT, TPS>(li, p, cfg, timing, stream)
     if (!strict) {
-        if (n <= 4) SGSF_PICK(float, 4, 512);
-        if (n <= 8) SGSF_PICK(float, 8, 384);
-        SGSF_PICK(float, 16, 384);
+        if (n <= 4) SGSF_PICK(float, 4, 512, 1);
+        if (n <= 8) SGSF_PICK(float, 8, 384, 1);
+        SGSF_PICK(float, 16, 384, 1);
     }
-    if (n <= 4) SGSF_PICK(double, 4, 384);
-    if (n <= 8) SGSF_PICK(double, 8, 256);
-    SGSF_PICK(double, 16, 256);
+    if (n <= 4) SGSF_PICK(double, 4, 384, 1);
+    if (n <= 8) SGSF_PICK(double, 8, 256, 1);
+    SGSF_PICK(double, 16, 256, 1);
 #undef SGSF_PICK
 }
 
