@@ -5,6 +5,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdio>
 #include <string>
 
 #include "../../include/sgsf.h"
@@ -67,6 +68,17 @@ int launch_persistent(const LaunchInfo& li, SolveParams& p, const sgsf_config_t*
     e = cudaGetLastError();
     if (e != cudaSuccess) return internal_fail(SGSF_ERR_CUDA, std::string("sf_persistent launch: ") + cudaGetErrorString(e));
     if (timing && timing->stop) cudaEventRecord((cudaEvent_t)timing->stop, stream);
+#ifdef SGSF_PHASE_TIMING
+    {
+        unsigned long long c[8];
+        cudaStreamSynchronize(stream);
+        cudaMemcpyFromSymbol(c, g_sgsf_counts, sizeof(c));
+        printf("COUNTS finish %llu flagged %llu exact %llu careful %llu flagged_terms %llu near_checks %llu scans %llu\n",
+               c[0], c[1], c[2], c[3], c[4], c[5], c[6]);
+        const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        cudaMemcpyToSymbol(g_sgsf_counts, z, sizeof(z));
+    }
+#endif
     return SGSF_OK;
 }
 

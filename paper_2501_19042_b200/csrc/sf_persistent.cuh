@@ -195,6 +195,15 @@ __device__ __forceinline__ void slot_barrier(int id, int nthreads) {
     asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+#ifdef SGSF_PHASE_TIMING
+// event counters of the instrumented build: [0] finish calls, [1] flagged path, [2] exact recompute,
+// [3] careful path, [4] flagged terms, [5] near checks, [6] pair scans, [7] G items with work
+__device__ unsigned long long g_sgsf_counts[8];
+#define SGSF_COUNT(I, V) atomicAdd(&g_sgsf_counts[I], (unsigned long long)(V))
+#else
+#define SGSF_COUNT(I, V) ((void)0)
+#endif
+
 // warp-wide min of non-negative values: one REDUX on the float bits (which
 // order like the values), shuffles for double
 __device__ __forceinline__ float warp_min_nonneg(float v) {
@@ -551,6 +560,7 @@ __device__ __noinline__ StepOut<T> flagged_path(const T* __restrict__ Pnew, T* _
             const int b = w * 32 + bit;
             if (b >= TermBits<NB>::count) break;
             const bool in_old = (om.w[w] >> bit) & 1u;
+            SGSF_COUNT(4, 1);
             act_new = act_new || !((nm.w[w] >> bit) & 1u);
             int i, j;
             term_robots<NB>(b, i, j);
@@ -589,7 +599,9 @@ __device__ __noinline__ StepOut<T> flagged_path(const T* __restrict__ Pnew, T* _
         }
     }
     T base = qinf;
-    if (need_exact) {   // exact max of |x| over the unflagged terms (needs the old row)
+    // the unflagged max is <= qinf; it matters only when the flagged terms' true max stays below qinf
+    if (need_exact && flmax < qinf) {   // exact max of |x| over the unflagged terms (needs the old row)
+        SGSF_COUNT(2, 1);
         base = T(0);
         int b = 0;
 #pragma unroll 1
@@ -754,7 +766,9 @@ __device__ __forceinline__ void finish_step(const SlotPtrs& sp, int lt, int n, i
     constexpr int NW = TermBits<NB>::words;
     T inf = qinf, sq = qsq;
     bool active = false;
+    SGSF_COUNT(0, 1);
     if (__builtin_expect(zmin == T(0) || zprev, 0)) {
+        SGSF_COUNT(3, 1);
         PosPack<T, NB> pk;
 #pragma unroll
         for (int q = 0; q < 3 * NB; ++q) pk.v[q] = ((q % NB) < n) ? Prow_new[q] : phantom_pos<T>(q % NB);
@@ -777,6 +791,7 @@ __device__ __forceinline__ void finish_step(const SlotPtrs& sp, int lt, int n, i
                 nmp.w[w] = nm[w];
                 omp.w[w] = imask[w];
             }
+            SGSF_COUNT(1, 1);
             const StepOut<T> o = flagged_path<T, NB>(Prow_new, Prow_old, n, fp, fw, cx, cy, cz, nmp, omp, inf, sq);
             inf = o.inf;
             sq = o.sq;
@@ -1000,6 +1015,7 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                     while (bits) {
                         const int bit = __ffs(bits) - 1;
                         bits &= bits - 1;
+                        SGSF_COUNT(5, 1);
                         const int ij = ptab[w * 32 + bit], i = ij & 0xff, j = ij >> 8;
                         const T dx = Prow_new[i] - Prow_new[j], dy = Prow_new[NB + i] - Prow_new[NB + j];
                         const T dz = Prow_new[2 * NB + i] - Prow_new[2 * NB + j];
@@ -1018,6 +1034,7 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
             while (qmask) {
                 const int src = __ffs(qmask) - 1;
                 qmask &= qmask - 1;
+                if (lane == 0) SGSF_COUNT(6, 1);
                 const int tsrc = TPS == 2 ? lwarp * 16 + src : lt - lane + src;
                 const T* row = Pbase_new + tsrc * RS;
                 T qm = T(1e30), zm = T(1);   // min q over the far pairs, min |component| over all pairs
