@@ -68,7 +68,7 @@ int launch_persistent(const LaunchInfo& li, SolveParams& p, const sgsf_config_t*
     e = cudaGetLastError();
     if (e != cudaSuccess) return internal_fail(SGSF_ERR_CUDA, std::string("sf_persistent launch: ") + cudaGetErrorString(e));
     if (timing && timing->stop) cudaEventRecord((cudaEvent_t)timing->stop, stream);
-#ifdef SGSF_PHASE_TIMING
+#ifdef SGSF_COUNTERS
     {
         unsigned long long c[8];
         cudaStreamSynchronize(stream);

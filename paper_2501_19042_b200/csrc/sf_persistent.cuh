@@ -148,14 +148,14 @@ __host__ __device__ inline SmemLayout make_layout(int n, int S, int MP, int spb,
     L.lam = q;    q = align16(q + (size_t)dimp * d);
     L.lamN = q;   q = align16(q + (size_t)dimp * d);
     L.xb = q;     q = align16(q + (size_t)dimp * d);
-    L.means = q;  q = align16(q + (size_t)6 * MP * d);
+    L.means = q;  q = align16(q + (size_t)3 * 4 * MP * d);            // per axis [Cb | ub | lamb | xbm]
     L.mpart = q;  q = align16(q + (size_t)3 * MP * d);
-    L.eqerr = q;  q = align16(q + (size_t)R3 * d);
-    L.psq = q;    q = align16(q + (size_t)S * d);
+    L.eqerr = q;  q = align16(q + (size_t)4 * d);                     // per axis max ||A xi - b|| over its rows
+    L.psq = q;    q = align16(q + (size_t)MAX_SLOT_WORDS * d);        // per warp sum of the l2 partials
     L.P0 = q;     q = align16(q + (size_t)RS * S * ts);
     L.P1 = q;     q = align16(q + (size_t)RS * S * ts);
     L.Cf = q;     q = align16(q + (size_t)3 * MP * NB * ts);
-    L.pinf = q;   q = align16(q + (size_t)S * ts);
+    L.pinf = q;   q = align16(q + (size_t)MAX_SLOT_WORDS * ts);       // per warp max of the inf partials
     L.sh = q;     q = align16(q + sizeof(SlotShared));
     L.slot_stride = q;
     L.total = o + (size_t)spb * q;
@@ -195,7 +195,7 @@ __device__ __forceinline__ void slot_barrier(int id, int nthreads) {
     asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-#ifdef SGSF_PHASE_TIMING
+#ifdef SGSF_COUNTERS
 // event counters of the instrumented build: [0] finish calls, [1] flagged path, [2] exact recompute,
 // [3] careful path, [4] flagged terms, [5] near checks, [6] pair scans, [7] G items with work
 __device__ unsigned long long g_sgsf_counts[8];
@@ -212,6 +212,14 @@ __device__ __forceinline__ float warp_min_nonneg(float v) {
 __device__ __forceinline__ double warp_min_nonneg(double v) {
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, off));
+    return v;
+}
+__device__ __forceinline__ float warp_max_nonneg(float v) {
+    return __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(v)));
+}
+__device__ __forceinline__ double warp_max_nonneg(double v) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, off));
     return v;
 }
 
@@ -756,9 +764,13 @@ __device__ __noinline__ CarefulOut<T> careful_pass(const PosPack<T, NB> pk, T* _
 // Given the interior bits of every term (nm) and min |component| (zmin), run
 // the careful / quiet / flagged path of time step `lt` and write its outputs:
 // exit-residual partials, R row (over the dead old row) and its bit in the
-// active-step mask of parity buffer `par`.
+// active-step mask of parity buffer `par`; returns its exit-residual partials.
+template <typename T> struct Partials {
+    T inf, sq;
+};
+
 template <typename T, int NB>
-__device__ __forceinline__ void finish_step(const SlotPtrs& sp, int lt, int n, int par, T* __restrict__ Prow_old,
+__device__ __forceinline__ Partials<T> finish_step(const SlotPtrs& sp, int lt, int n, int par, T* __restrict__ Prow_old,
                                             const T* __restrict__ Prow_new, T qinf, T qsq,
                                             uint32_t (&nm)[TermBits<NB>::words],
                                             T zmin, uint32_t (&imask)[TermBits<NB>::words], bool& zprev,
@@ -800,12 +812,14 @@ __device__ __forceinline__ void finish_step(const SlotPtrs& sp, int lt, int n, i
     }
 #pragma unroll
     for (int w = 0; w < NW; ++w) imask[w] = nm[w];
-    ((T*)sp.pinf)[lt] = inf;
-    sp.psq[lt] = (double)sq;
     if (active) {
         atomicOr(&sp.sh->amask[par][lt >> 5], 1u << (lt & 31));
         sp.sh->active[par] = 1;
     }
+    Partials<T> r;
+    r.inf = inf;
+    r.sq = sq;
+    return r;
 }
 
 // ---------------------------------------------------------------- load a sample (one coefficient row)
@@ -1074,27 +1088,32 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
 
             SGSF_PT(6);
             // ---------------- T3: every time step finishes (quiet / flagged / careful path), by its owner lane
+            Partials<T> pr{T(0), T(0)};
             if (ts < S && owner)
-                finish_step<T, NB>(sp, ts, n, par, Prow_old, Prow_new, qinf, qsq, nm, fmin(zmin_ws, zmin_pairs), imask,
-                                   zprev, fp, fw, cx, cy, cz);
+                pr = finish_step<T, NB>(sp, ts, n, par, Prow_old, Prow_new, qinf, qsq, nm, fmin(zmin_ws, zmin_pairs),
+                                        imask, zprev, fp, fw, cx, cy, cz);
+            {   // per-warp exit-residual partials for the decision (fixed order: deterministic)
+                const T wi = warp_max_nonneg(pr.inf);
+                double wq = (double)pr.sq;
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) wq += __shfl_xor_sync(0xffffffffu, wq, off);
+                if (lane == 0) {
+                    ((T*)sp.pinf)[lwarp] = wi;
+                    sp.psq[lwarp] = wq;
+                }
+            }
             slot_barrier(bar_id, gsize);
             SGSF_PT(1);
 
             // ---------------- decision (every warp, redundantly): exit residual of iteration k-1, early stop, SingularKKT
             double emax = 0.0, sqs = 0.0;
             T inf = T(0);
-            if (k >= 1) {
-                for (int r = lane; r < R3; r += 32) emax = fmax(emax, sp.eqerr[r]);
-                for (int t = lane; t < S; t += 32) {
-                    inf = fmax(inf, ((const T*)sp.pinf)[t]);
-                    sqs += sp.psq[t];
+            if (k >= 1) {   // partials: per axis (MX of iteration k-1), per warp (T3 above)
+                emax = fmax(fmax(sp.eqerr[0], sp.eqerr[1]), sp.eqerr[2]);
+                for (int w = 0; w < p.wps; ++w) {
+                    inf = fmax(inf, ((const T*)sp.pinf)[w]);
+                    sqs += sp.psq[w];
                 }
-            }
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                emax = fmax(emax, __shfl_xor_sync(0xffffffffu, emax, off));
-                inf = fmax(inf, __shfl_xor_sync(0xffffffffu, inf, off));
-                sqs += __shfl_xor_sync(0xffffffffu, sqs, off);
             }
             // (a sample can only finish at k >= 1, so `inf` is always the last exit residual there)
             const bool failed = (k >= 1) && (emax > p.tol_eq);
@@ -1145,58 +1164,83 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
             }
 
             SGSF_PT(2);
-            // ---------------- G: lam' = lam - rho R W over the active time steps only (ascending t)
             const bool any_active = sp.sh->active[par] != 0;
-            if (any_active) {
-                const T* Rb = (const T*)(par ? sp.P1 : sp.P0);   // the old rows hold R
-                for (int r = lt; r < R3; r += gsize) {
-                    T g[MP];
-#pragma unroll
-                    for (int q = 0; q < MP; ++q) g[q] = T(0);
-                    const T* Rr = Rb + (r / n) * NB + (r % n);
-                    for (int w = 0; w < SWT; ++w) {
-                        uint32_t bits = sp.sh->amask[par][w];
-                        while (bits) {
-                            const int t = w * 32 + __ffs(bits) - 1;
-                            bits &= bits - 1;
-                            const T rv = Rr[t * RS];
-                            if (rv != T(0)) {
-                                T wr[MP];
-                                load_row16<T, MP>(Wt + t * MP, wr);
-#pragma unroll
-                                for (int q = 0; q < MP; ++q) g[q] = fma_t<T>(rv, wr[q], g[q]);
-                            }
-                        }
-                    }
-#pragma unroll
-                    for (int q = 0; q < MP; ++q) sp.lamN[r * MP + q] = sp.lam[r * MP + q] - p.rho * (double)g[q];
-                }
-                slot_barrier(bar_id, gsize);
-            }
 
-            SGSF_PT(3);
-            // ---------------- MX: one warp per axis -- swarm means of C and u = 2 lam' - lam + xi_bar,
-            // mean part Mm Cb + Km11 ub, decoupled xi-step C_i = mean part + Md (C_i - Cb) + Kd11 (u_i - ub)
-            // + cconst_i, ||A xi - b||_inf partials, commit.  Rows of one axis never leave their warp, so
-            // the sub-steps are ordered by __syncwarp alone.
+            // ---------------- MX: one warp per axis; rows of an axis never leave their warp, so its
+            // sub-steps are ordered by __syncwarp alone.  Lane (i, part) owns robot i's row of this axis and
+            // outputs q in [part QL, part QL + QL).
+            //   G   lam'_i = lam_i - rho (R W)_i over the active time steps only (ascending t)
+            //   M   swarm means: Cb summed; ub = 2 lamb' - lamb + xbm from the tracked means of lam
+            //       (re-summed only when lam changed) and of xi_bar (summed once per sample)
+            //   X   mean part Mm Cb + Km11 ub, decoupled xi-step
+            //       C_i = mean part + Md (C_i - Cb) + Kd11 (u_i - ub) + cconst_i, u = 2 lam' - lam + xi_bar,
+            //       ||A xi - b||_inf of the axis, commit
             {
                 constexpr int LPR = (32 / NB < 4) ? 32 / NB : 4;   // lanes per coefficient row
                 constexpr int QL = MP / LPR;                       // outputs per lane
                 const double* lamU = any_active ? sp.lamN : sp.lam;   // lam' (= lam when nothing was active)
                 for (int ax = lwarp; ax < 3; ax += p.wps) {
-                    double* mn = sp.means + ax * 2 * MP;   // [Cb | ub]
-                    if (lane < MP) {
-                        double cs = 0.0, us = 0.0;
+                    double* mn = sp.means + ax * 4 * MP;   // [Cb | ub | lamb | xbm]
+                    const int i = lane / LPR, part = lane - i * LPR;
+                    const bool valid = i < n;
+                    const int r = ax * n + (valid ? i : 0);
+                    if (any_active && valid) {   // G for this lane's outputs of row r
+                        T g[QL];
 #pragma unroll
-                        for (int i = 0; i < NB; ++i) {
-                            if (i < n) {
-                                const int idx = (ax * n + i) * MP + lane;
-                                cs += sp.C[idx];
-                                us += 2.0 * lamU[idx] - sp.lam[idx] + sp.xb[idx];
+                        for (int u = 0; u < QL; ++u) g[u] = T(0);
+                        const T* Rr = (const T*)(par ? sp.P1 : sp.P0) + ax * NB + i;   // the old rows hold R
+                        for (int w = 0; w < SWT; ++w) {
+                            uint32_t bits = sp.sh->amask[par][w];
+                            while (bits) {
+                                const int t = w * 32 + __ffs(bits) - 1;
+                                bits &= bits - 1;
+                                const T rv = Rr[t * RS];
+                                if (rv != T(0)) {
+#pragma unroll
+                                    for (int u = 0; u < QL; ++u) g[u] = fma_t<T>(rv, Wt[t * MP + part * QL + u], g[u]);
+                                }
                             }
                         }
-                        mn[lane] = cs / n;
-                        mn[MP + lane] = us / n;
+#pragma unroll
+                        for (int u = 0; u < QL; ++u) {
+                            const int idx = r * MP + part * QL + u;
+                            sp.lamN[idx] = sp.lam[idx] - p.rho * (double)g[u];
+                        }
+                    }
+                    __syncwarp();
+                    {   // means: lane (q, half) sums robots [half NB/2, half NB/2 + NB/2)
+                        const int q = lane & 15, hm = lane >> 4;
+                        double cs = 0.0, ls = 0.0, l0 = 0.0, xs = 0.0;
+                        if (q < MP) {
+#pragma unroll
+                            for (int u = 0; u < NB / 2; ++u) {
+                                const int ii = hm * (NB / 2) + u;
+                                if (ii < n) {
+                                    const int idx = (ax * n + ii) * MP + q;
+                                    cs += sp.C[idx];
+                                    if (any_active) ls += sp.lamN[idx];
+                                    if (k == 0) {
+                                        l0 += sp.lam[idx];
+                                        xs += sp.xb[idx];
+                                    }
+                                }
+                            }
+                        }
+                        cs += __shfl_xor_sync(0xffffffffu, cs, 16);
+                        if (any_active) ls += __shfl_xor_sync(0xffffffffu, ls, 16);
+                        if (k == 0) {
+                            l0 += __shfl_xor_sync(0xffffffffu, l0, 16);
+                            xs += __shfl_xor_sync(0xffffffffu, xs, 16);
+                        }
+                        if (lane < MP) {
+                            const double lb = k == 0 ? l0 / n : mn[2 * MP + lane];
+                            const double xm = k == 0 ? xs / n : mn[3 * MP + lane];
+                            const double lbn = any_active ? ls / n : lb;
+                            mn[lane] = cs / n;
+                            mn[MP + lane] = 2.0 * lbn - lb + xm;
+                            mn[2 * MP + lane] = lbn;
+                            mn[3 * MP + lane] = xm;
+                        }
                     }
                     __syncwarp();
                     if (lane < MP) {
@@ -1212,9 +1256,6 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                         sp.mpart[ax * MP + lane] = acc;
                     }
                     __syncwarp();
-                    const int i = lane / LPR, part = lane - i * LPR;
-                    const bool valid = i < n;
-                    const int r = ax * n + (valid ? i : 0);
                     double cn[QL];
                     double eqp[6];
 #pragma unroll
@@ -1253,15 +1294,17 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                     }
                     __syncwarp();   // every lane has read its row before any lane writes it
                     double em = 0.0;
+                    const double* rr = rhs + r * 6;
 #pragma unroll
                     for (int c6 = 0; c6 < 6; ++c6) {
                         double e = eqp[c6];
 #pragma unroll
                         for (int off = 1; off < LPR; off <<= 1) e += __shfl_xor_sync(0xffffffffu, e, off);
-                        em = fmax(em, fabs(e - (valid ? rhs[r * 6 + c6] : 0.0)));
+                        em = fmax(em, fabs(e - rr[c6]));
                     }
+                    em = warp_max_nonneg(valid ? em : 0.0);
+                    if (lane == 0) sp.eqerr[ax] = em;
                     if (valid) {
-                        if (part == 0) sp.eqerr[r] = em;
 #pragma unroll
                         for (int u = 0; u < QL; ++u) {
                             const int q = part * QL + u;

@@ -1,7 +1,7 @@
 #!/bin/bash
 # (on the GPU box) rebuild with -DSGSF_PHASE_TIMING; per-CTA slot-0 phase cycles -> gpurun_out/pt_*.log
 make -C paper_2501_19042_b200/csrc clean >/dev/null
-make -C paper_2501_19042_b200/csrc -j16 EXTRA=-DSGSF_PHASE_TIMING >/dev/null 2>&1 || exit 1
+make -C paper_2501_19042_b200/csrc -j16 EXTRA="-DSGSF_PHASE_TIMING ${PT_EXTRA}" >/dev/null 2>&1 || exit 1
 mkdir -p gpurun_out
 python - <<'PY'
 import sys, os
