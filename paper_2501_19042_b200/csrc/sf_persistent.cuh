@@ -122,7 +122,7 @@ template <typename T, int NB> struct RowStride {
 struct SmemLayout {
     size_t W, KMm, KMd, cconst, B6, rhs, PBt, ptab;
     size_t slot0, slot_stride;
-    size_t C, Cp, lam, lamN, xb, means, mpart, eqerr, psq, P0, P1, Cf, pinf, sh;
+    size_t C, Cp, lam, gb, U, xb, means, mpart, eqerr, psq, P0, P1, Cf, pinf, sh;
     size_t total;
 };
 
@@ -146,7 +146,8 @@ __host__ __device__ inline SmemLayout make_layout(int n, int S, int MP, int spb,
     L.C = q;      q = align16(q + (size_t)dimp * d);
     L.Cp = q;     q = align16(q + (want_prev ? (size_t)dimp * d : 0));
     L.lam = q;    q = align16(q + (size_t)dimp * d);
-    L.lamN = q;   q = align16(q + (size_t)dimp * d);
+    L.gb = q;     q = align16(q + (size_t)dimp * ts);               // G result: lam' = lam - rho gb
+    L.U = q;      q = align16(q + (size_t)dimp * d);                // u = 2 lam' - lam + xi_bar
     L.xb = q;     q = align16(q + (size_t)dimp * d);
     L.means = q;  q = align16(q + (size_t)3 * 4 * MP * d);            // per axis [Cb | ub | lamb | xbm]
     L.mpart = q;  q = align16(q + (size_t)3 * MP * d);
@@ -163,7 +164,8 @@ __host__ __device__ inline SmemLayout make_layout(int n, int S, int MP, int spb,
 }
 
 struct SlotPtrs {
-    double *C, *Cp, *lam, *lamN, *xb, *means, *mpart, *eqerr, *psq;
+    double *C, *Cp, *lam, *U, *xb, *means, *mpart, *eqerr, *psq;
+    void* gb;
     void *P0, *P1, *Cf, *pinf;
     SlotShared* sh;
 };
@@ -174,7 +176,8 @@ __device__ __forceinline__ SlotPtrs slot_ptrs(unsigned char* smem, const SmemLay
     P.C = (double*)(b + L.C);
     P.Cp = (double*)(b + L.Cp);
     P.lam = (double*)(b + L.lam);
-    P.lamN = (double*)(b + L.lamN);
+    P.gb = (void*)(b + L.gb);
+    P.U = (double*)(b + L.U);
     P.xb = (double*)(b + L.xb);
     P.means = (double*)(b + L.means);
     P.mpart = (double*)(b + L.mpart);
@@ -221,6 +224,14 @@ __device__ __forceinline__ double warp_max_nonneg(double v) {
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, off));
     return v;
+}
+
+// D += A B for one 8x8x4 FP64 tile (DMMA): A (8x4, row) element [lane/4][lane%4],
+// B (4x8, col) element [lane%4][lane/4], D (8x8) elements [lane/4][2 (lane%4) + {0, 1}]
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+        : "+d"(d0), "+d"(d1)
+        : "d"(a), "d"(b));
 }
 
 // 16-byte vector of T (float4 / double2) for the row-times-vector loops
@@ -900,7 +911,8 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
     for (int i = tid; i < MP * M2P; i += nt) {
         const int q = i / M2P, c = i % M2P, half = c / MP, q2 = c % MP;
         const bool in = q < m1 && q2 < m1;
-        KMm[i] = in ? p.KMm[q * 2 * m1 + half * m1 + q2] : 0.0;
+        // [Mm - Md | Km11 - Kd11]: the xi-step takes the raw rows (see MX)
+        KMm[i] = in ? p.KMm[q * 2 * m1 + half * m1 + q2] - p.KMd[q * 2 * m1 + half * m1 + q2] : 0.0;
         KMd[i] = in ? p.KMd[q * 2 * m1 + half * m1 + q2] : 0.0;
     }
     for (int i = tid; i < dimp; i += nt) {
@@ -975,6 +987,7 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
     const T skin_lim = T(kSkin * kSkin) * fp.lim;
     uint32_t near[NPW];
     T rmin = T(0), cum = T(0);
+    bool prev_active = false;   // lam changed in the previous iteration (the U rows are stale)
 
     if (lt == 0) {
         sp.sh->sample = next_sample(p);
@@ -1167,47 +1180,61 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
             const bool any_active = sp.sh->active[par] != 0;
 
             // ---------------- MX: one warp per axis; rows of an axis never leave their warp, so its
-            // sub-steps are ordered by __syncwarp alone.  Lane (i, part) owns robot i's row of this axis and
-            // outputs q in [part QL, part QL + QL).
-            //   G   lam'_i = lam_i - rho (R W)_i over the active time steps only (ascending t)
+            // sub-steps are ordered by __syncwarp alone.
+            //   G   lam'_i = lam_i - rho (R W)_i over the active time steps only (ascending t): lane
+            //       (i, part) forms the outputs [part QL, part QL + QL) of robot i's row
+            //   U   u_i = 2 lam'_i - lam_i + xi_bar_i (only when lam changed now or in the last iteration)
             //   M   swarm means: Cb summed; ub = 2 lamb' - lamb + xbm from the tracked means of lam
             //       (re-summed only when lam changed) and of xi_bar (summed once per sample)
-            //   X   mean part Mm Cb + Km11 ub, decoupled xi-step
-            //       C_i = mean part + Md (C_i - Cb) + Kd11 (u_i - ub) + cconst_i, u = 2 lam' - lam + xi_bar,
-            //       ||A xi - b||_inf of the axis, commit
+            //   X   C_i = Md C_i + Kd11 u_i + (Mm - Md) Cb + (Km11 - Kd11) ub + cconst_i  (= the decoupled
+            //       xi-step Mm Cb + Km11 ub + Md (C_i - Cb) + Kd11 (u_i - ub) + cconst_i) as FP64 tensor-core
+            //       tiles: [robots x (C | u)] . [Md | Kd11]^T, then ||A xi - b||_inf of the new rows
+            //       (B6 C_i - rhs_i, also DMMA), commit
             {
-                constexpr int LPR = (32 / NB < 4) ? 32 / NB : 4;   // lanes per coefficient row
-                constexpr int QL = MP / LPR;                       // outputs per lane
-                const double* lamU = any_active ? sp.lamN : sp.lam;   // lam' (= lam when nothing was active)
+                constexpr int LPR = (32 / NB < 4) ? 32 / NB : 4;   // lanes per coefficient row (G)
+                constexpr int QL = MP / LPR;                       // outputs per lane (G)
+                constexpr int MT = (NB + 7) / 8;                   // 8-robot tiles
+                constexpr int KT = MP / 2;                         // 4-column k-steps over [C | u]
+                constexpr int KC = MP / 4;                         // ... of which over C
+                const bool u_stale = any_active || prev_active || k == 0;
+                const int fr = lane >> 2, fc = lane & 3;           // fragment row / column
                 for (int ax = lwarp; ax < 3; ax += p.wps) {
                     double* mn = sp.means + ax * 4 * MP;   // [Cb | ub | lamb | xbm]
-                    const int i = lane / LPR, part = lane - i * LPR;
-                    const bool valid = i < n;
-                    const int r = ax * n + (valid ? i : 0);
-                    if (any_active && valid) {   // G for this lane's outputs of row r
-                        T g[QL];
+                    const int rb = ax * n;                 // first row of this axis
+                    T* gbuf = (T*)sp.gb;
+                    if (any_active) {   // G
+                        const int i = lane / LPR, part = lane - i * LPR;
+                        if (i < n) {
+                            T g[QL];
 #pragma unroll
-                        for (int u = 0; u < QL; ++u) g[u] = T(0);
-                        const T* Rr = (const T*)(par ? sp.P1 : sp.P0) + ax * NB + i;   // the old rows hold R
-                        for (int w = 0; w < SWT; ++w) {
-                            uint32_t bits = sp.sh->amask[par][w];
-                            while (bits) {
-                                const int t = w * 32 + __ffs(bits) - 1;
-                                bits &= bits - 1;
-                                const T rv = Rr[t * RS];
-                                if (rv != T(0)) {
+                            for (int u = 0; u < QL; ++u) g[u] = T(0);
+                            const T* Rr = (const T*)(par ? sp.P1 : sp.P0) + ax * NB + i;   // the old rows hold R
+                            for (int w = 0; w < SWT; ++w) {
+                                uint32_t bits = sp.sh->amask[par][w];
+                                while (bits) {
+                                    const int t = w * 32 + __ffs(bits) - 1;
+                                    bits &= bits - 1;
+                                    const T rv = Rr[t * RS];
+                                    if (rv != T(0)) {
 #pragma unroll
-                                    for (int u = 0; u < QL; ++u) g[u] = fma_t<T>(rv, Wt[t * MP + part * QL + u], g[u]);
+                                        for (int u = 0; u < QL; ++u)
+                                            g[u] = fma_t<T>(rv, Wt[t * MP + part * QL + u], g[u]);
+                                    }
                                 }
                             }
-                        }
 #pragma unroll
-                        for (int u = 0; u < QL; ++u) {
-                            const int idx = r * MP + part * QL + u;
-                            sp.lamN[idx] = sp.lam[idx] - p.rho * (double)g[u];
+                            for (int u = 0; u < QL; ++u) gbuf[(rb + i) * MP + part * QL + u] = g[u];
+                        }
+                        __syncwarp();
+                    }
+                    if (u_stale) {   // U rows of this axis
+                        for (int e = lane; e < n * MP; e += 32) {
+                            const int idx = rb * MP + e;
+                            const double l = sp.lam[idx];
+                            const double lp = any_active ? l - p.rho * (double)gbuf[idx] : l;
+                            sp.U[idx] = 2.0 * lp - l + sp.xb[idx];
                         }
                     }
-                    __syncwarp();
                     {   // means: lane (q, half) sums robots [half NB/2, half NB/2 + NB/2)
                         const int q = lane & 15, hm = lane >> 4;
                         double cs = 0.0, ls = 0.0, l0 = 0.0, xs = 0.0;
@@ -1216,9 +1243,9 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                             for (int u = 0; u < NB / 2; ++u) {
                                 const int ii = hm * (NB / 2) + u;
                                 if (ii < n) {
-                                    const int idx = (ax * n + ii) * MP + q;
+                                    const int idx = (rb + ii) * MP + q;
                                     cs += sp.C[idx];
-                                    if (any_active) ls += sp.lamN[idx];
+                                    if (any_active) ls += sp.lam[idx] - p.rho * (double)gbuf[idx];
                                     if (k == 0) {
                                         l0 += sp.lam[idx];
                                         xs += sp.xb[idx];
@@ -1243,12 +1270,12 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                         }
                     }
                     __syncwarp();
-                    if (lane < MP) {
+                    if (lane < MP) {   // mean part (Mm - Md) Cb + (Km11 - Kd11) ub
                         const double2* row = reinterpret_cast<const double2*>(KMm + lane * M2P);
                         const double2* mv = reinterpret_cast<const double2*>(mn);
                         double acc = 0.0;
 #pragma unroll
-                        for (int c = 0; c < MP; ++c) {   // [Mm | Km11] . [Cb | ub], in column order
+                        for (int c = 0; c < MP; ++c) {
                             const double2 a = row[c], m = mv[c];
                             acc = fma(a.x, m.x, acc);
                             acc = fma(a.y, m.y, acc);
@@ -1256,67 +1283,95 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                         sp.mpart[ax * MP + lane] = acc;
                     }
                     __syncwarp();
-                    double cn[QL];
-                    double eqp[6];
+                    // X: D[robot][q] = mean part + cconst + sum_c [C | u][robot][c] KMd[q][c]
+                    double dacc[MT][2][2];
 #pragma unroll
-                    for (int c6 = 0; c6 < 6; ++c6) eqp[c6] = 0.0;
-                    if (valid) {
-                        double dCU[2 * MP];   // [C_i - Cb | u_i - ub]
+                    for (int mt = 0; mt < MT; ++mt) {
+                        const int rob = 8 * mt + fr;
 #pragma unroll
-                        for (int c = 0; c < MP / 2; ++c) {
-                            const int idx = r * MP + 2 * c;
-                            const double2 cc = *reinterpret_cast<const double2*>(sp.C + idx);
-                            const double2 lu = *reinterpret_cast<const double2*>(lamU + idx);
-                            const double2 ll = *reinterpret_cast<const double2*>(sp.lam + idx);
-                            const double2 xx = *reinterpret_cast<const double2*>(sp.xb + idx);
-                            const double2 mc = *reinterpret_cast<const double2*>(mn + 2 * c);
-                            const double2 mu = *reinterpret_cast<const double2*>(mn + MP + 2 * c);
-                            dCU[2 * c] = cc.x - mc.x;
-                            dCU[2 * c + 1] = cc.y - mc.y;
-                            dCU[MP + 2 * c] = (2.0 * lu.x - ll.x + xx.x) - mu.x;
-                            dCU[MP + 2 * c + 1] = (2.0 * lu.y - ll.y + xx.y) - mu.y;
-                        }
+                        for (int nt = 0; nt < 2; ++nt) {
 #pragma unroll
-                        for (int u = 0; u < QL; ++u) {
-                            const int q = part * QL + u;
-                            const double2* row = reinterpret_cast<const double2*>(KMd + q * M2P);
-                            double acc = sp.mpart[ax * MP + q] + cconst[r * MP + q];
-#pragma unroll
-                            for (int c = 0; c < MP; ++c) {   // [Md | Kd11] . [dC | dU], in column order
-                                const double2 a = row[c];
-                                acc = fma(a.x, dCU[2 * c], acc);
-                                acc = fma(a.y, dCU[2 * c + 1], acc);
+                            for (int e = 0; e < 2; ++e) {
+                                const int q = 8 * nt + 2 * fc + e;
+                                dacc[mt][nt][e] =
+                                    (rob < n && q < MP) ? sp.mpart[ax * MP + q] + cconst[(rb + rob) * MP + q] : 0.0;
                             }
-                            cn[u] = acc;
-#pragma unroll
-                            for (int c6 = 0; c6 < 6; ++c6) eqp[c6] = fma(B6[c6 * MP + q], acc, eqp[c6]);
                         }
                     }
-                    __syncwarp();   // every lane has read its row before any lane writes it
-                    double em = 0.0;
-                    const double* rr = rhs + r * 6;
 #pragma unroll
-                    for (int c6 = 0; c6 < 6; ++c6) {
-                        double e = eqp[c6];
+                    for (int kk = 0; kk < KT; ++kk) {
+                        const int c = 4 * kk + fc;
+                        double bf[2];
 #pragma unroll
-                        for (int off = 1; off < LPR; off <<= 1) e += __shfl_xor_sync(0xffffffffu, e, off);
-                        em = fmax(em, fabs(e - rr[c6]));
+                        for (int nt = 0; nt < 2; ++nt) {
+                            const int qb = 8 * nt + fr;
+                            bf[nt] = qb < MP ? KMd[qb * M2P + c] : 0.0;
+                        }
+#pragma unroll
+                        for (int mt = 0; mt < MT; ++mt) {
+                            const int rob = 8 * mt + fr;
+                            const double a = rob < n ? (kk < KC ? sp.C[(rb + rob) * MP + c] : sp.U[(rb + rob) * MP + c - MP])
+                                                     : 0.0;
+#pragma unroll
+                            for (int nt = 0; nt < 2; ++nt) dmma884(dacc[mt][nt][0], dacc[mt][nt][1], a, bf[nt]);
+                        }
                     }
-                    em = warp_max_nonneg(valid ? em : 0.0);
-                    if (lane == 0) sp.eqerr[ax] = em;
-                    if (valid) {
+                    if (p.want_prev) {
+                        for (int e = lane; e < n * MP; e += 32) sp.Cp[rb * MP + e] = sp.C[rb * MP + e];
+                    }
+                    __syncwarp();   // every lane has read the rows before any lane writes them
 #pragma unroll
-                        for (int u = 0; u < QL; ++u) {
-                            const int q = part * QL + u;
-                            const int idx = r * MP + q;
-                            if (p.want_prev) sp.Cp[idx] = sp.C[idx];
-                            sp.C[idx] = cn[u];
-                            if (any_active) sp.lam[idx] = lamU[idx];
-                            ((T*)sp.Cf)[(ax * MP + q) * NB + i] = (T)cn[u];
+                    for (int mt = 0; mt < MT; ++mt) {
+                        const int rob = 8 * mt + fr;
+#pragma unroll
+                        for (int nt = 0; nt < 2; ++nt) {
+                            const int q = 8 * nt + 2 * fc;
+                            if (rob < n && q < MP) {
+                                *reinterpret_cast<double2*>(sp.C + (rb + rob) * MP + q) =
+                                    make_double2(dacc[mt][nt][0], dacc[mt][nt][1]);
+                                ((T*)sp.Cf)[(ax * MP + q) * NB + rob] = (T)dacc[mt][nt][0];
+                                ((T*)sp.Cf)[(ax * MP + q + 1) * NB + rob] = (T)dacc[mt][nt][1];
+                            }
+                        }
+                    }
+                    if (any_active) {   // commit lam'
+                        for (int e = lane; e < n * MP; e += 32) {
+                            const int idx = rb * MP + e;
+                            sp.lam[idx] = sp.lam[idx] - p.rho * (double)gbuf[idx];
                         }
                     }
                     __syncwarp();
+                    {   // ||A xi - b||_inf over this axis' new rows: E[robot][c6] = B6[c6] . C_robot - rhs
+                        double eacc[MT][2];
+#pragma unroll
+                        for (int mt = 0; mt < MT; ++mt) {
+                            const int rob = 8 * mt + fr;
+#pragma unroll
+                            for (int e = 0; e < 2; ++e) {
+                                const int c6 = 2 * fc + e;
+                                eacc[mt][e] = (rob < n && c6 < 6) ? -rhs[(rb + rob) * 6 + c6] : 0.0;
+                            }
+                        }
+#pragma unroll
+                        for (int kk = 0; kk < MP / 4; ++kk) {
+                            const int q = 4 * kk + fc;
+                            const double bv = fr < 6 ? B6[fr * MP + q] : 0.0;
+#pragma unroll
+                            for (int mt = 0; mt < MT; ++mt) {
+                                const int rob = 8 * mt + fr;
+                                const double a = rob < n ? sp.C[(rb + rob) * MP + q] : 0.0;
+                                dmma884(eacc[mt][0], eacc[mt][1], a, bv);
+                            }
+                        }
+                        double em = 0.0;
+#pragma unroll
+                        for (int mt = 0; mt < MT; ++mt) em = fmax(em, fmax(fabs(eacc[mt][0]), fabs(eacc[mt][1])));
+                        em = warp_max_nonneg(em);
+                        if (lane == 0) sp.eqerr[ax] = em;
+                    }
+                    __syncwarp();
                 }
+                prev_active = any_active;
             }
             slot_barrier(bar_id, gsize);
             SGSF_PT(4);
