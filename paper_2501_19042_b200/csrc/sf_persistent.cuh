@@ -212,18 +212,22 @@ __device__ unsigned long long g_sgsf_counts[8];
 __device__ __forceinline__ float warp_min_nonneg(float v) {
     return __uint_as_float(__reduce_min_sync(0xffffffffu, __float_as_uint(v)));
 }
+// non-negative doubles order like their (hi, lo) words: REDUX the high words,
+// then the low words of the lanes that hold the winning high word
 __device__ __forceinline__ double warp_min_nonneg(double v) {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, off));
-    return v;
+    const unsigned hi = (unsigned)__double2hiint(v), lo = (unsigned)__double2loint(v);
+    const unsigned mh = __reduce_min_sync(0xffffffffu, hi);
+    const unsigned ml = __reduce_min_sync(0xffffffffu, hi == mh ? lo : 0xffffffffu);
+    return __hiloint2double((int)mh, (int)ml);
 }
 __device__ __forceinline__ float warp_max_nonneg(float v) {
     return __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(v)));
 }
 __device__ __forceinline__ double warp_max_nonneg(double v) {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, off));
-    return v;
+    const unsigned hi = (unsigned)__double2hiint(v), lo = (unsigned)__double2loint(v);
+    const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+    return __hiloint2double((int)mh, (int)ml);
 }
 
 // D += A B for one 8x8x4 FP64 tile (DMMA): A (8x4, row) element [lane/4][lane%4],
@@ -946,6 +950,9 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
     const Family<T> fw = make_family<T>(p.ws_lat, p.ws_vert);
     const T cx = (T)p.cx, cy = (T)p.cy, cz = (T)p.cz;
     const int SWT = (S + 31) >> 5;   // words of the active-step mask
+    const double inv_n = 1.0 / n;
+    // the residual history is written by a warp that has no axis in MX when there is one
+    const int hist_lt = p.wps > 3 ? 32 * (p.wps - 1) : 0;
     // time step of this thread and the part of the robots it owns: TPS = 2 puts the two halves
     // of a step in lanes l and l ^ 16 (16 steps per warp); the h = 0 lane owns the step's state
     constexpr int RH = NB / TPS;
@@ -960,7 +967,7 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
 #ifdef SGSF_PHASE_TIMING
     // clock64 stamps of slot 0 / thread 0 of CTA 0: [0] loop top (after MX barrier), [5] T1 end,
     // [6] T2 end, [1] after the term-pass barrier, [2] after decision, [3] after G, [4] after MX barrier
-    long long pt_last = 0, pt_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long pt_last = 0, pt_acc[16] = {0};
     int pt_prev = -1, pt_iters = 0;
 #define SGSF_PT(ID)                                                                          \
     do {                                                                                      \
@@ -1133,7 +1140,7 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
             bool done = failed;
             if (k >= 1) {
                 done = done || (p.early_stop && (double)inf <= p.tol_res) || (k >= p.max_iters);
-                if (lt == 0) {
+                if (lt == hist_lt) {
                     const size_t hix = (size_t)sample * p.max_iters + (k - 1);
                     p.res_inf[hix] = (double)inf;
                     p.res_l2[hix] = sqrt(sqs);
@@ -1227,6 +1234,7 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                         }
                         __syncwarp();
                     }
+                    SGSF_PT(8);
                     if (u_stale) {   // U rows of this axis
                         for (int e = lane; e < n * MP; e += 32) {
                             const int idx = rb * MP + e;
@@ -1235,6 +1243,7 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                             sp.U[idx] = 2.0 * lp - l + sp.xb[idx];
                         }
                     }
+                    SGSF_PT(9);
                     {   // means: lane (q, half) sums robots [half NB/2, half NB/2 + NB/2)
                         const int q = lane & 15, hm = lane >> 4;
                         double cs = 0.0, ls = 0.0, l0 = 0.0, xs = 0.0;
@@ -1260,16 +1269,17 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                             xs += __shfl_xor_sync(0xffffffffu, xs, 16);
                         }
                         if (lane < MP) {
-                            const double lb = k == 0 ? l0 / n : mn[2 * MP + lane];
-                            const double xm = k == 0 ? xs / n : mn[3 * MP + lane];
-                            const double lbn = any_active ? ls / n : lb;
-                            mn[lane] = cs / n;
+                            const double lb = k == 0 ? l0 * inv_n : mn[2 * MP + lane];
+                            const double xm = k == 0 ? xs * inv_n : mn[3 * MP + lane];
+                            const double lbn = any_active ? ls * inv_n : lb;
+                            mn[lane] = cs * inv_n;
                             mn[MP + lane] = 2.0 * lbn - lb + xm;
                             mn[2 * MP + lane] = lbn;
                             mn[3 * MP + lane] = xm;
                         }
                     }
                     __syncwarp();
+                    SGSF_PT(10);
                     if (lane < MP) {   // mean part (Mm - Md) Cb + (Km11 - Kd11) ub
                         const double2* row = reinterpret_cast<const double2*>(KMm + lane * M2P);
                         const double2* mv = reinterpret_cast<const double2*>(mn);
@@ -1283,6 +1293,7 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                         sp.mpart[ax * MP + lane] = acc;
                     }
                     __syncwarp();
+                    SGSF_PT(11);
                     // X: D[robot][q] = mean part + cconst + sum_c [C | u][robot][c] KMd[q][c]
                     double dacc[MT][2][2];
 #pragma unroll
@@ -1316,6 +1327,7 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                             for (int nt = 0; nt < 2; ++nt) dmma884(dacc[mt][nt][0], dacc[mt][nt][1], a, bf[nt]);
                         }
                     }
+                    SGSF_PT(12);
                     if (p.want_prev) {
                         for (int e = lane; e < n * MP; e += 32) sp.Cp[rb * MP + e] = sp.C[rb * MP + e];
                     }
@@ -1341,6 +1353,7 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                         }
                     }
                     __syncwarp();
+                    SGSF_PT(13);
                     {   // ||A xi - b||_inf over this axis' new rows: E[robot][c6] = B6[c6] . C_robot - rhs
                         double eacc[MT][2];
 #pragma unroll
@@ -1370,6 +1383,7 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                         if (lane == 0) sp.eqerr[ax] = em;
                     }
                     __syncwarp();
+                    SGSF_PT(14);
                 }
                 prev_active = any_active;
             }
@@ -1379,10 +1393,17 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
     }
 #ifdef SGSF_PHASE_TIMING
     if (tid == 0)
-        printf("PT block %d iters %d total %.0f T1 %.0f T2 %.0f T3bar %.0f dec %.0f G %.0f MX %.0f\n", blockIdx.x, pt_iters,
-               (double)(pt_acc[0] + pt_acc[1] + pt_acc[2] + pt_acc[3] + pt_acc[4] + pt_acc[5] + pt_acc[6]),
+        printf("PT block %d iters %d total %.0f T1 %.0f T2 %.0f T3bar %.0f dec %.0f G %.0f MX %.0f "
+               "mxG %.0f mxU %.0f mxM %.0f mxP %.0f mxX %.0f mxC %.0f mxE %.0f\n", blockIdx.x, pt_iters,
+               (double)(pt_acc[0] + pt_acc[1] + pt_acc[2] + pt_acc[3] + pt_acc[4] + pt_acc[5] + pt_acc[6] + pt_acc[8] +
+                        pt_acc[9] + pt_acc[10] + pt_acc[11] + pt_acc[12] + pt_acc[13] + pt_acc[14]),
                (double)pt_acc[5] / pt_iters, (double)pt_acc[6] / pt_iters, (double)pt_acc[1] / pt_iters,
-               (double)pt_acc[2] / pt_iters, (double)pt_acc[3] / pt_iters, (double)(pt_acc[4] + pt_acc[0]) / pt_iters);
+               (double)pt_acc[2] / pt_iters, (double)pt_acc[3] / pt_iters,
+               (double)(pt_acc[4] + pt_acc[0] + pt_acc[8] + pt_acc[9] + pt_acc[10] + pt_acc[11] + pt_acc[12] + pt_acc[13] +
+                        pt_acc[14]) / pt_iters,
+               (double)pt_acc[8] / pt_iters, (double)pt_acc[9] / pt_iters, (double)pt_acc[10] / pt_iters,
+               (double)pt_acc[11] / pt_iters, (double)pt_acc[12] / pt_iters, (double)pt_acc[13] / pt_iters,
+               (double)pt_acc[14] / pt_iters);
 #endif
 }
 
