@@ -122,7 +122,7 @@ template <typename T, int NB> struct RowStride {
 struct SmemLayout {
     size_t W, KMm, KMd, cconst, B6, rhs, PBt, ptab;
     size_t slot0, slot_stride;
-    size_t C, Cp, lam, gb, U, xb, means, mpart, eqerr, psq, P0, P1, Cf, pinf, sh;
+    size_t C, Cp, lam, U, xb, eqerr, psq, P0, P1, Cf, pinf, sh;
     size_t total;
 };
 
@@ -146,11 +146,8 @@ __host__ __device__ inline SmemLayout make_layout(int n, int S, int MP, int spb,
     L.C = q;      q = align16(q + (size_t)dimp * d);
     L.Cp = q;     q = align16(q + (want_prev ? (size_t)dimp * d : 0));
     L.lam = q;    q = align16(q + (size_t)dimp * d);
-    L.gb = q;     q = align16(q + (size_t)dimp * ts);               // G result: lam' = lam - rho gb
     L.U = q;      q = align16(q + (size_t)dimp * d);                // u = 2 lam' - lam + xi_bar
     L.xb = q;     q = align16(q + (size_t)dimp * d);
-    L.means = q;  q = align16(q + (size_t)3 * 4 * MP * d);            // per axis [Cb | ub | lamb | xbm]
-    L.mpart = q;  q = align16(q + (size_t)3 * MP * d);
     L.eqerr = q;  q = align16(q + (size_t)4 * d);                     // per axis max ||A xi - b|| over its rows
     L.psq = q;    q = align16(q + (size_t)MAX_SLOT_WORDS * d);        // per warp sum of the l2 partials
     L.P0 = q;     q = align16(q + (size_t)RS * S * ts);
@@ -164,8 +161,7 @@ __host__ __device__ inline SmemLayout make_layout(int n, int S, int MP, int spb,
 }
 
 struct SlotPtrs {
-    double *C, *Cp, *lam, *U, *xb, *means, *mpart, *eqerr, *psq;
-    void* gb;
+    double *C, *Cp, *lam, *U, *xb, *eqerr, *psq;
     void *P0, *P1, *Cf, *pinf;
     SlotShared* sh;
 };
@@ -176,11 +172,8 @@ __device__ __forceinline__ SlotPtrs slot_ptrs(unsigned char* smem, const SmemLay
     P.C = (double*)(b + L.C);
     P.Cp = (double*)(b + L.Cp);
     P.lam = (double*)(b + L.lam);
-    P.gb = (void*)(b + L.gb);
     P.U = (double*)(b + L.U);
     P.xb = (double*)(b + L.xb);
-    P.means = (double*)(b + L.means);
-    P.mpart = (double*)(b + L.mpart);
     P.eqerr = (double*)(b + L.eqerr);
     P.psq = (double*)(b + L.psq);
     P.P0 = (void*)(b + L.P0);
@@ -951,6 +944,7 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
     const T cx = (T)p.cx, cy = (T)p.cy, cz = (T)p.cz;
     const int SWT = (S + 31) >> 5;   // words of the active-step mask
     const double inv_n = 1.0 / n;
+    const T inv_lat = T(1) / fp.lat;
     // the residual history is written by a warp that has no axis in MX when there is one
     const int hist_lt = p.wps > 3 ? 32 * (p.wps - 1) : 0;
     // time step of this thread and the part of the robots it owns: TPS = 2 puts the two halves
@@ -1036,7 +1030,7 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                                              : quiet_part<T, NB, RH, TPS, false>(pos, Prow_old, r0, n, fp.beta, smask);
                 qinf = st.inf;
                 qsq = st.sq;
-                cum += T(2) * sqrt(st.dmax2) / fp.lat;
+                cum += T(2) * sqrt(st.dmax2) * inv_lat;
                 need_scan = (k == 0) || zprev || !(rmin - cum > T(1) + T(1e-3));
                 zmin_ws = full ? ws_part<T, NB, RH, TPS, true>(pos, r0, h, n, fw, cx, cy, cz, nm, smask)
                                : ws_part<T, NB, RH, TPS, false>(pos, r0, h, n, fw, cx, cy, cz, nm, smask);
@@ -1095,7 +1089,7 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                 qm = warp_min_nonneg(qm);
                 zm = warp_min_nonneg(zm);
                 if (lane == src) {
-                    rmin = sqrt(qm) / fp.lat;
+                    rmin = sqrt(qm) * inv_lat;
                     cum = T(0);
                     zmin_pairs = zm;
 #pragma unroll
@@ -1187,114 +1181,83 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
             const bool any_active = sp.sh->active[par] != 0;
 
             // ---------------- MX: one warp per axis; rows of an axis never leave their warp, so its
-            // sub-steps are ordered by __syncwarp alone.
-            //   G   lam'_i = lam_i - rho (R W)_i over the active time steps only (ascending t): lane
-            //       (i, part) forms the outputs [part QL, part QL + QL) of robot i's row
-            //   U   u_i = 2 lam'_i - lam_i + xi_bar_i (only when lam changed now or in the last iteration)
-            //   M   swarm means: Cb summed; ub = 2 lamb' - lamb + xbm from the tracked means of lam
-            //       (re-summed only when lam changed) and of xi_bar (summed once per sample)
-            //   X   C_i = Md C_i + Kd11 u_i + (Mm - Md) Cb + (Km11 - Kd11) ub + cconst_i  (= the decoupled
-            //       xi-step Mm Cb + Km11 ub + Md (C_i - Cb) + Kd11 (u_i - ub) + cconst_i) as FP64 tensor-core
-            //       tiles: [robots x (C | u)] . [Md | Kd11]^T, then ||A xi - b||_inf of the new rows
-            //       (B6 C_i - rhs_i, also DMMA), commit
+            // sub-steps are ordered by __syncwarp alone.  All products are FP64 tensor-core tiles
+            // (DMMA m8n8k4, rows = robots), with the accumulators D[robot][q] held in registers:
+            //   G   g = R W over the active time steps (k = active step, compacted in ascending t);
+            //       lam' = lam - rho g                                    (only when something was active)
+            //   U   u_i = 2 lam'_i - lam_i + xi_bar_i   (only when lam changed now or in the last iteration)
+            //   X   C_i = Md C_i + Kd11 u_i + cconst_i + (Mm - Md) Cb + (Km11 - Kd11) ub
+            //       (= the decoupled xi-step Mm Cb + Km11 ub + Md (C_i - Cb) + Kd11 (u_i - ub) + cconst_i):
+            //       [robots x (C | u)] . [Md | Kd11]^T, plus the column sums of the same fragments (n Cb,
+            //       n ub) times [Mm - Md | Km11 - Kd11]^T / n for every row
+            //   E   ||A xi - b||_inf over the new rows (B6 C_i - rhs_i), commit
             {
-                constexpr int LPR = (32 / NB < 4) ? 32 / NB : 4;   // lanes per coefficient row (G)
-                constexpr int QL = MP / LPR;                       // outputs per lane (G)
-                constexpr int MT = (NB + 7) / 8;                   // 8-robot tiles
-                constexpr int KT = MP / 2;                         // 4-column k-steps over [C | u]
-                constexpr int KC = MP / 4;                         // ... of which over C
+                constexpr int MT = (NB + 7) / 8;   // 8-robot tiles
+                constexpr int KT = MP / 2;         // 4-column k-steps over [C | u]
+                constexpr int KC = MP / 4;         // ... of which over C
                 const bool u_stale = any_active || prev_active || k == 0;
-                const int fr = lane >> 2, fc = lane & 3;           // fragment row / column
+                const int fr = lane >> 2, fc = lane & 3;   // fragment row / column
                 for (int ax = lwarp; ax < 3; ax += p.wps) {
-                    double* mn = sp.means + ax * 4 * MP;   // [Cb | ub | lamb | xbm]
-                    const int rb = ax * n;                 // first row of this axis
-                    T* gbuf = (T*)sp.gb;
+                    const int rb = ax * n;   // first row of this axis
+                    double gq[MT][2][2];
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                        for (int nt = 0; nt < 2; ++nt) gq[mt][nt][0] = gq[mt][nt][1] = 0.0;
                     if (any_active) {   // G
-                        const int i = lane / LPR, part = lane - i * LPR;
-                        if (i < n) {
-                            T g[QL];
-#pragma unroll
-                            for (int u = 0; u < QL; ++u) g[u] = T(0);
-                            const T* Rr = (const T*)(par ? sp.P1 : sp.P0) + ax * NB + i;   // the old rows hold R
-                            for (int w = 0; w < SWT; ++w) {
-                                uint32_t bits = sp.sh->amask[par][w];
-                                while (bits) {
-                                    const int t = w * 32 + __ffs(bits) - 1;
-                                    bits &= bits - 1;
-                                    const T rv = Rr[t * RS];
-                                    if (rv != T(0)) {
-#pragma unroll
-                                        for (int u = 0; u < QL; ++u)
-                                            g[u] = fma_t<T>(rv, Wt[t * MP + part * QL + u], g[u]);
+                        const uint32_t* am = sp.sh->amask[par];
+                        int na = 0;
+                        for (int w = 0; w < SWT; ++w) na += __popc(am[w]);
+                        const T* Rb = (const T*)(par ? sp.P1 : sp.P0) + ax * NB;   // the old rows hold R
+                        for (int kk = 0; 4 * kk < na; ++kk) {
+                            int rem = 4 * kk + fc, t = -1;   // this lane's k = active step number
+                            if (rem < na) {
+                                for (int w = 0;; ++w) {
+                                    const uint32_t bits = am[w];
+                                    const int c = __popc(bits);
+                                    if (rem < c) {
+                                        t = w * 32 + (int)__fns(bits, 0, rem + 1);
+                                        break;
                                     }
+                                    rem -= c;
                                 }
                             }
+                            double bw[2];
 #pragma unroll
-                            for (int u = 0; u < QL; ++u) gbuf[(rb + i) * MP + part * QL + u] = g[u];
+                            for (int nt = 0; nt < 2; ++nt) {
+                                const int qb = 8 * nt + fr;
+                                bw[nt] = (t >= 0 && qb < MP) ? (double)Wt[t * MP + qb] : 0.0;
+                            }
+#pragma unroll
+                            for (int mt = 0; mt < MT; ++mt) {
+                                const int rob = 8 * mt + fr;
+                                const double a = (t >= 0 && rob < n) ? (double)Rb[t * RS + rob] : 0.0;
+#pragma unroll
+                                for (int nt = 0; nt < 2; ++nt) dmma884(gq[mt][nt][0], gq[mt][nt][1], a, bw[nt]);
+                            }
+                        }
+                    }
+                    if (u_stale) {   // U rows of this axis, element-wise in the accumulator layout
+#pragma unroll
+                        for (int mt = 0; mt < MT; ++mt) {
+                            const int rob = 8 * mt + fr;
+#pragma unroll
+                            for (int nt = 0; nt < 2; ++nt) {
+                                const int q = 8 * nt + 2 * fc;
+                                if (rob < n && q < MP) {
+                                    const int idx = (rb + rob) * MP + q;
+                                    const double2 l = *reinterpret_cast<const double2*>(sp.lam + idx);
+                                    const double2 x = *reinterpret_cast<const double2*>(sp.xb + idx);
+                                    const double lp0 = l.x - p.rho * gq[mt][nt][0], lp1 = l.y - p.rho * gq[mt][nt][1];
+                                    *reinterpret_cast<double2*>(sp.U + idx) =
+                                        make_double2(2.0 * lp0 - l.x + x.x, 2.0 * lp1 - l.y + x.y);
+                                }
+                            }
                         }
                         __syncwarp();
                     }
                     SGSF_PT(8);
-                    if (u_stale) {   // U rows of this axis
-                        for (int e = lane; e < n * MP; e += 32) {
-                            const int idx = rb * MP + e;
-                            const double l = sp.lam[idx];
-                            const double lp = any_active ? l - p.rho * (double)gbuf[idx] : l;
-                            sp.U[idx] = 2.0 * lp - l + sp.xb[idx];
-                        }
-                    }
-                    SGSF_PT(9);
-                    {   // means: lane (q, half) sums robots [half NB/2, half NB/2 + NB/2)
-                        const int q = lane & 15, hm = lane >> 4;
-                        double cs = 0.0, ls = 0.0, l0 = 0.0, xs = 0.0;
-                        if (q < MP) {
-#pragma unroll
-                            for (int u = 0; u < NB / 2; ++u) {
-                                const int ii = hm * (NB / 2) + u;
-                                if (ii < n) {
-                                    const int idx = (rb + ii) * MP + q;
-                                    cs += sp.C[idx];
-                                    if (any_active) ls += sp.lam[idx] - p.rho * (double)gbuf[idx];
-                                    if (k == 0) {
-                                        l0 += sp.lam[idx];
-                                        xs += sp.xb[idx];
-                                    }
-                                }
-                            }
-                        }
-                        cs += __shfl_xor_sync(0xffffffffu, cs, 16);
-                        if (any_active) ls += __shfl_xor_sync(0xffffffffu, ls, 16);
-                        if (k == 0) {
-                            l0 += __shfl_xor_sync(0xffffffffu, l0, 16);
-                            xs += __shfl_xor_sync(0xffffffffu, xs, 16);
-                        }
-                        if (lane < MP) {
-                            const double lb = k == 0 ? l0 * inv_n : mn[2 * MP + lane];
-                            const double xm = k == 0 ? xs * inv_n : mn[3 * MP + lane];
-                            const double lbn = any_active ? ls * inv_n : lb;
-                            mn[lane] = cs * inv_n;
-                            mn[MP + lane] = 2.0 * lbn - lb + xm;
-                            mn[2 * MP + lane] = lbn;
-                            mn[3 * MP + lane] = xm;
-                        }
-                    }
-                    __syncwarp();
-                    SGSF_PT(10);
-                    if (lane < MP) {   // mean part (Mm - Md) Cb + (Km11 - Kd11) ub
-                        const double2* row = reinterpret_cast<const double2*>(KMm + lane * M2P);
-                        const double2* mv = reinterpret_cast<const double2*>(mn);
-                        double acc = 0.0;
-#pragma unroll
-                        for (int c = 0; c < MP; ++c) {
-                            const double2 a = row[c], m = mv[c];
-                            acc = fma(a.x, m.x, acc);
-                            acc = fma(a.y, m.y, acc);
-                        }
-                        sp.mpart[ax * MP + lane] = acc;
-                    }
-                    __syncwarp();
-                    SGSF_PT(11);
-                    // X: D[robot][q] = mean part + cconst + sum_c [C | u][robot][c] KMd[q][c]
+                    // X: D = cconst + [C | u] . KMd^T, column sums of the A fragments for the mean part
                     double dacc[MT][2][2];
 #pragma unroll
                     for (int mt = 0; mt < MT; ++mt) {
@@ -1304,11 +1267,11 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
 #pragma unroll
                             for (int e = 0; e < 2; ++e) {
                                 const int q = 8 * nt + 2 * fc + e;
-                                dacc[mt][nt][e] =
-                                    (rob < n && q < MP) ? sp.mpart[ax * MP + q] + cconst[(rb + rob) * MP + q] : 0.0;
+                                dacc[mt][nt][e] = (rob < n && q < MP) ? cconst[(rb + rob) * MP + q] : 0.0;
                             }
                         }
                     }
+                    double csum[KT];
 #pragma unroll
                     for (int kk = 0; kk < KT; ++kk) {
                         const int c = 4 * kk + fc;
@@ -1318,15 +1281,43 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                             const int qb = 8 * nt + fr;
                             bf[nt] = qb < MP ? KMd[qb * M2P + c] : 0.0;
                         }
+                        csum[kk] = 0.0;
 #pragma unroll
                         for (int mt = 0; mt < MT; ++mt) {
                             const int rob = 8 * mt + fr;
                             const double a = rob < n ? (kk < KC ? sp.C[(rb + rob) * MP + c] : sp.U[(rb + rob) * MP + c - MP])
                                                      : 0.0;
+                            csum[kk] += a;
 #pragma unroll
                             for (int nt = 0; nt < 2; ++nt) dmma884(dacc[mt][nt][0], dacc[mt][nt][1], a, bf[nt]);
                         }
                     }
+                    SGSF_PT(10);
+                    {   // mean part: every row gets (column sums / n) . [Mm - Md | Km11 - Kd11]^T
+                        double dm[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+                        for (int kk = 0; kk < KT; ++kk) {
+                            double cs = csum[kk];
+                            cs += __shfl_xor_sync(0xffffffffu, cs, 4);
+                            cs += __shfl_xor_sync(0xffffffffu, cs, 8);
+                            cs += __shfl_xor_sync(0xffffffffu, cs, 16);
+                            const int c = 4 * kk + fc;
+                            const double a = cs * inv_n;
+#pragma unroll
+                            for (int nt = 0; nt < 2; ++nt) {
+                                const int qb = 8 * nt + fr;
+                                dmma884(dm[nt][0], dm[nt][1], a, qb < MP ? KMm[qb * M2P + c] : 0.0);
+                            }
+                        }
+#pragma unroll
+                        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                            for (int nt = 0; nt < 2; ++nt) {
+                                dacc[mt][nt][0] += dm[nt][0];
+                                dacc[mt][nt][1] += dm[nt][1];
+                            }
+                    }
+                    SGSF_PT(11);
                     SGSF_PT(12);
                     if (p.want_prev) {
                         for (int e = lane; e < n * MP; e += 32) sp.Cp[rb * MP + e] = sp.C[rb * MP + e];
@@ -1339,17 +1330,16 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                         for (int nt = 0; nt < 2; ++nt) {
                             const int q = 8 * nt + 2 * fc;
                             if (rob < n && q < MP) {
-                                *reinterpret_cast<double2*>(sp.C + (rb + rob) * MP + q) =
-                                    make_double2(dacc[mt][nt][0], dacc[mt][nt][1]);
+                                const int idx = (rb + rob) * MP + q;
+                                *reinterpret_cast<double2*>(sp.C + idx) = make_double2(dacc[mt][nt][0], dacc[mt][nt][1]);
                                 ((T*)sp.Cf)[(ax * MP + q) * NB + rob] = (T)dacc[mt][nt][0];
                                 ((T*)sp.Cf)[(ax * MP + q + 1) * NB + rob] = (T)dacc[mt][nt][1];
+                                if (any_active) {   // commit lam'
+                                    const double2 l = *reinterpret_cast<const double2*>(sp.lam + idx);
+                                    *reinterpret_cast<double2*>(sp.lam + idx) =
+                                        make_double2(l.x - p.rho * gq[mt][nt][0], l.y - p.rho * gq[mt][nt][1]);
+                                }
                             }
-                        }
-                    }
-                    if (any_active) {   // commit lam'
-                        for (int e = lane; e < n * MP; e += 32) {
-                            const int idx = rb * MP + e;
-                            sp.lam[idx] = sp.lam[idx] - p.rho * (double)gbuf[idx];
                         }
                     }
                     __syncwarp();
