@@ -950,7 +950,10 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
     // time step of this thread and the part of the robots it owns: TPS = 2 puts the two halves
     // of a step in lanes l and l ^ 16 (16 steps per warp); the h = 0 lane owns the step's state
     constexpr int RH = NB / TPS;
-    const int ts = TPS == 2 ? lwarp * 16 + (lane & 15) : lt;
+    // TPS = 1: steps are dealt to the warps in chunks of 8 (warp w gets chunks w, w + wps, ...), so
+    // every warp covers the whole horizon -- the exact-path work clusters in time (collisions) and
+    // would otherwise load one warp -- while 8 consecutive rows keep 16-byte row access conflict-free
+    const int ts = TPS == 2 ? lwarp * 16 + (lane & 15) : 8 * (lwarp + p.wps * (lane >> 3)) + (lane & 7);
     const int h = TPS == 2 ? lane >> 4 : 0;
     const int r0 = h * RH;
     const bool owner = h == 0;
@@ -1063,7 +1066,7 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                 const int src = __ffs(qmask) - 1;
                 qmask &= qmask - 1;
                 if (lane == 0) SGSF_COUNT(6, 1);
-                const int tsrc = TPS == 2 ? lwarp * 16 + src : lt - lane + src;
+                const int tsrc = TPS == 2 ? lwarp * 16 + src : 8 * (lwarp + p.wps * (src >> 3)) + (src & 7);
                 const T* row = Pbase_new + tsrc * RS;
                 T qm = T(1e30), zm = T(1);   // min q over the far pairs, min |component| over all pairs
                 uint32_t words[NPW], nwords[NPW];
