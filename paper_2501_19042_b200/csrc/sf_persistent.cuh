@@ -544,13 +544,13 @@ template <typename T> struct StepOut {
     bool active;
 };
 
-template <int NB> __device__ __forceinline__ void term_robots(int b, int& i, int& j) {
+// robots of term bit b: pair (i, j) from the lexicographic pair table, or workspace term i (j = -1)
+template <int NB> __device__ __forceinline__ void term_robots(const int* __restrict__ ptab, int b, int& i, int& j) {
     constexpr int NP = NB * (NB - 1) / 2;
     if (b < NP) {
-        int rem = b;
-        i = 0;
-        while (rem >= NB - 1 - i) { rem -= NB - 1 - i; ++i; }
-        j = i + 1 + rem;
+        const int ij = ptab[b];
+        i = ij & 0xff;
+        j = ij >> 8;
     } else {
         i = b - NP;
         j = -1;
@@ -558,9 +558,10 @@ template <int NB> __device__ __forceinline__ void term_robots(int b, int& i, int
 }
 
 template <typename T, int NB>
-__device__ __noinline__ StepOut<T> flagged_path(const T* __restrict__ Pnew, T* __restrict__ Pold, int n,
-                                                const Family<T> fp, const Family<T> fw, T cx, T cy, T cz,
-                                                const MaskPack<NB> nm, const MaskPack<NB> om, T qinf, T qsq) {
+__device__ __forceinline__ StepOut<T> flagged_path(const T* __restrict__ Pnew, T* __restrict__ Pold, int n,
+                                                   const int* __restrict__ ptab, const Family<T>& fp,
+                                                   const Family<T>& fw, T cx, T cy, T cz, const MaskPack<NB>& nm,
+                                                   const MaskPack<NB>& om, T qinf, T qsq) {
     constexpr int NP = NB * (NB - 1) / 2;
     constexpr int NWD = TermBits<NB>::words;
     const T c3[3] = {cx, cy, cz};
@@ -579,7 +580,7 @@ __device__ __noinline__ StepOut<T> flagged_path(const T* __restrict__ Pnew, T* _
             SGSF_COUNT(4, 1);
             act_new = act_new || !((nm.w[w] >> bit) & 1u);
             int i, j;
-            term_robots<NB>(b, i, j);
+            term_robots<NB>(ptab, b, i, j);
             const bool pair = j >= 0;
             const Family<T>& fm = pair ? fp : fw;
             T d[3], o[3], x[3];
@@ -645,9 +646,13 @@ __device__ __noinline__ StepOut<T> flagged_path(const T* __restrict__ Pnew, T* _
     }
     if (act_new) {
         // pass 2: the old row is dead now -- it becomes this thread's R row (d - e of the active terms)
+        using V = typename Vec16<T>::type;
+        constexpr int L = Vec16<T>::lanes;
+        V z;
 #pragma unroll
-        for (int q = 0; q < 3 * NB; ++q)
-            if ((q % NB) < n) Pold[q] = T(0);
+        for (int u = 0; u < L; ++u) reinterpret_cast<T*>(&z)[u] = T(0);
+#pragma unroll
+        for (int c = 0; c < 3 * NB / L; ++c) reinterpret_cast<V*>(Pold)[c] = z;
 #pragma unroll 1
         for (int w = 0; w < NWD; ++w) {
             uint32_t ac = ~nm.w[w];
@@ -657,7 +662,7 @@ __device__ __noinline__ StepOut<T> flagged_path(const T* __restrict__ Pnew, T* _
                 const int b = w * 32 + bit;
                 if (b >= TermBits<NB>::count) break;
                 int i, j;
-                term_robots<NB>(b, i, j);
+                term_robots<NB>(ptab, b, i, j);
                 const bool pair = j >= 0;
                 const Family<T>& fm = pair ? fp : fw;
                 T d[3];
@@ -778,7 +783,8 @@ template <typename T> struct Partials {
 };
 
 template <typename T, int NB>
-__device__ __forceinline__ Partials<T> finish_step(const SlotPtrs& sp, int lt, int n, int par, T* __restrict__ Prow_old,
+__device__ __forceinline__ Partials<T> finish_step(const SlotPtrs& sp, const int* __restrict__ ptab, int lt, int n,
+                                                   int par, T* __restrict__ Prow_old,
                                             const T* __restrict__ Prow_new, T qinf, T qsq,
                                             uint32_t (&nm)[TermBits<NB>::words],
                                             T zmin, uint32_t (&imask)[TermBits<NB>::words], bool& zprev,
@@ -812,7 +818,7 @@ __device__ __forceinline__ Partials<T> finish_step(const SlotPtrs& sp, int lt, i
                 omp.w[w] = imask[w];
             }
             SGSF_COUNT(1, 1);
-            const StepOut<T> o = flagged_path<T, NB>(Prow_new, Prow_old, n, fp, fw, cx, cy, cz, nmp, omp, inf, sq);
+            const StepOut<T> o = flagged_path<T, NB>(Prow_new, Prow_old, n, ptab, fp, fw, cx, cy, cz, nmp, omp, inf, sq);
             inf = o.inf;
             sq = o.sq;
             active = o.active;
@@ -1107,7 +1113,7 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
             // ---------------- T3: every time step finishes (quiet / flagged / careful path), by its owner lane
             Partials<T> pr{T(0), T(0)};
             if (ts < S && owner)
-                pr = finish_step<T, NB>(sp, ts, n, par, Prow_old, Prow_new, qinf, qsq, nm, fmin(zmin_ws, zmin_pairs),
+                pr = finish_step<T, NB>(sp, ptab, ts, n, par, Prow_old, Prow_new, qinf, qsq, nm, fmin(zmin_ws, zmin_pairs),
                                         imask, zprev, fp, fw, cx, cy, cz);
             {   // per-warp exit-residual partials for the decision (fixed order: deterministic)
                 const T wi = warp_max_nonneg(pr.inf);
