@@ -17,7 +17,8 @@ int launch_order(const SolveParams& p, float* score, int* order, cudaStream_t st
     int rc;
     if (p.n <= 4) rc = wide ? launch_score<4, 16>(p, score, stream) : launch_score<4, 12>(p, score, stream);
     else if (p.n <= 8) rc = wide ? launch_score<8, 16>(p, score, stream) : launch_score<8, 12>(p, score, stream);
-    else rc = wide ? launch_score<16, 16>(p, score, stream) : launch_score<16, 12>(p, score, stream);
+    else if (p.n <= 16) rc = wide ? launch_score<16, 16>(p, score, stream) : launch_score<16, 12>(p, score, stream);
+    else rc = wide ? launch_score<32, 16>(p, score, stream) : launch_score<32, 12>(p, score, stream);
     if (rc != SGSF_OK) return rc;
     lpt_order_kernel<<<1, kOrderThreads, 0, stream>>>(score, p.batch, order);
     internal_count_launch(1);

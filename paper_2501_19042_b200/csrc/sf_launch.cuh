@@ -44,7 +44,13 @@ int launch_persistent(const LaunchInfo& li, SolveParams& p, const sgsf_config_t*
         const int spread = (p.batch + li.sm_count - 1) / li.sm_count;
         if (spb > spread) spb = spread > 0 ? spread : 1;
     }
-    if (spb <= 0) return internal_fail(SGSF_ERR_UNSUPPORTED, "problem too large for one CTA (samples or smem)");
+    if (spb <= 0) {
+        const size_t need = make_layout<T, NB>(p.n, p.S, MP, 1, p.want_prev).total;
+        return internal_fail(SGSF_ERR_UNSUPPORTED,
+                             "problem too large for one CTA: one sample slot needs " + std::to_string(need / 1024) +
+                                 " KB of shared memory, the device allows " + std::to_string(dev_smem / 1024) +
+                                 " KB (use precision='lean' or a shorter horizon)");
+    }
     if (spb > 15) return internal_fail(SGSF_ERR_UNSUPPORTED, "at most 15 slots per CTA (named barriers)");
     const int threads = spb * slot_threads;
     if (threads > MAXT) return internal_fail(SGSF_ERR_UNSUPPORTED, "slots_per_block * samples exceeds the CTA size");
@@ -93,9 +99,10 @@ int launch_persistent(const LaunchInfo& li, SolveParams& p, const sgsf_config_t*
 
 // (T, NB, MP, MAXT, TPS): MAXT caps the CTA so ptxas can give the
 // register-resident term pass the registers it needs; TPS = threads per time
-// step.  TPS = 2 (half the robots per lane, 7 warps per slot) compiles but
-// measured slower on B200: the term pass is latency-bound, not
-// work-bound, and the extra warps cap the registers at 80 (spills).
+// step.  Up to 16 robots: TPS = 1 (TPS = 2 measured slower there: the term
+// pass is latency-bound and the extra warps cap the registers at 80).  32
+// robots: TPS = 2, so a lane still owns 16 robots' positions; one slot of
+// ceil(S/16) warps per CTA (the state and the position rows fill the CTA).
 #define SGSF_FOR_EACH_VARIANT(X)  \
     X(float, 4, 12, 512, 1)       \
     X(float, 4, 16, 512, 1)       \
@@ -108,7 +115,11 @@ int launch_persistent(const LaunchInfo& li, SolveParams& p, const sgsf_config_t*
     X(double, 8, 12, 256, 1)      \
     X(double, 8, 16, 256, 1)      \
     X(double, 16, 12, 256, 1)     \
-    X(double, 16, 16, 256, 1)
+    X(double, 16, 16, 256, 1)     \
+    X(float, 32, 12, 256, 2)      \
+    X(float, 32, 16, 256, 2)      \
+    X(double, 32, 12, 256, 2)     \
+    X(double, 32, 16, 256, 2)
 
 SGSF_FOR_EACH_VARIANT(SGSF_DECLARE_LAUNCH)
 

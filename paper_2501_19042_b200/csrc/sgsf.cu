@@ -39,7 +39,7 @@ int fail(int code, const std::string& msg) {
             return fail(SGSF_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
     } while (0)
 
-constexpr int kMaxRobots = 16;
+constexpr int kMaxRobots = 32;
 
 }  // namespace
 
@@ -230,11 +230,13 @@ int sgsf_solve(sgsf_handle_t* h, int batch, const double* xi_bar, const double* 
     if (!strict) {
         if (n <= 4) SGSF_PICK(float, 4, 512, 1);
         if (n <= 8) SGSF_PICK(float, 8, 384, 1);
-        SGSF_PICK(float, 16, 384, 1);
+        if (n <= 16) SGSF_PICK(float, 16, 384, 1);
+        SGSF_PICK(float, 32, 256, 2);
     }
     if (n <= 4) SGSF_PICK(double, 4, 384, 1);
     if (n <= 8) SGSF_PICK(double, 8, 256, 1);
-    SGSF_PICK(double, 16, 256, 1);
+    if (n <= 16) SGSF_PICK(double, 16, 256, 1);
+    SGSF_PICK(double, 32, 256, 2);
 #undef SGSF_PICK
 }
 

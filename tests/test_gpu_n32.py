@@ -1,0 +1,81 @@
+"""32-robot swarms (BASELINE config 3 size) on the GPU.
+
+The 32-robot kernel variant gives each time step two lanes of 16 robots
+(TPS = 2) and runs one slot per CTA.  Parity with the oracle is checked at a
+fixed iteration count (no early stop), so both sides run the same number of
+alternating-minimisation steps; the full config-3 batch is checked through
+the oracle-free properties used for config 2.
+"""
+import dataclasses
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import sf_oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def _setup(n, horizon, seed, count, max_iters, precision):
+    from paper_2501_19042_b200 import SafetyFilter, SolverConfig, sample_proposals
+    from paper_2501_19042_b200.problem import load_problem
+    from paper_2501_19042_b200.scenarios import random_swarm_doc
+    doc = random_swarm_doc(n, horizon, seed)
+    prob = load_problem(doc)
+    cfg = SolverConfig(max_iters=max_iters, early_stop=False, svars=False, precision=precision)
+    sf = SafetyFilter(prob, config=cfg)
+    props = sample_proposals(prob, sf.basis, count, seed=seed).proposals
+    return doc, sf, cfg, props
+
+
+def _oracle(doc, props, max_iters):
+    op = sf_oracle.make_problem(doc, degree=10)
+    return [sf_oracle.solve(op, x, max_iters=max_iters, early_stop=False) for x in props]
+
+
+@pytest.mark.parametrize("precision,horizon,rtol", [("lean", 100, 1e-5), ("strict", 40, 1e-9)])
+def test_n32_matches_oracle_fixed_iterations(precision, horizon, rtol):
+    doc, sf, cfg, props = _setup(32, horizon, 3, 3, 25, precision)
+    out = sf.solve_batched(torch.from_numpy(props).cuda(), config=cfg)
+    ref = _oracle(doc, props, 25)
+    coeffs = out.coeffs.cpu().numpy()
+    rinf = out.residual_inf.cpu().numpy()
+    for b, r in enumerate(ref):
+        scale = np.abs(r.coeffs).max()
+        assert np.abs(coeffs[b] - r.coeffs).max() <= rtol * scale, b
+        np.testing.assert_allclose(rinf[b], r.residual_inf, rtol=1e-3 if precision == "lean" else 1e-7, atol=1e-9)
+    assert (out.iterations.cpu().numpy() == 25).all()
+    assert out.eq_err.max().item() <= 1e-8
+
+
+def test_n32_strict_full_horizon_reports_smem_limit():
+    """Strict (FP64 positions) at 32 robots and H=100 does not fit one CTA: a clean error, no launch."""
+    doc, sf, cfg, props = _setup(32, 100, 3, 2, 5, "strict")
+    with pytest.raises(NotImplementedError, match="shared memory"):
+        sf.solve_batched(torch.from_numpy(props).cuda(), config=cfg)
+
+
+def test_full_size_config3_properties():
+    """BASELINE config 3 (32 drones, H=100) at its full batch of 4096: endpoint conditions to 1e-8,
+    histories consistent with `converged`, verdict within converged, launch-shape invariance."""
+    from paper_2501_19042_b200 import SafetyFilter, SolverConfig, sample_proposals
+    from paper_2501_19042_b200.scenarios import config_problem
+    prob = config_problem(3)
+    cfg = SolverConfig(max_iters=500, svars=False)
+    sf = SafetyFilter(prob, config=cfg)
+    B = 4096
+    xb = torch.from_numpy(sample_proposals(prob, sf.basis, B, seed=0).proposals).cuda()
+    out = sf.solve_batched(xb, config=cfg)
+    its = out.iterations.cpu().numpy()
+    conv = out.converged.cpu().numpy().astype(bool)
+    feas = out.feasible.cpu().numpy().astype(bool)
+    rinf = out.residual_inf.cpu().numpy()
+    assert (out.status.cpu().numpy() == 0).all()
+    assert out.eq_err.max().item() <= 1e-8
+    assert np.all(feas <= conv)
+    last = rinf[np.arange(B), its - 1]
+    assert np.all((last <= 1e-3) == conv)
+    sub = dataclasses.replace(cfg)
+    alt = sf.solve_batched(xb[:300], config=sub, grid=37)
+    assert torch.equal(alt.coeffs, out.coeffs[:300]) and torch.equal(alt.iterations, out.iterations[:300])
