@@ -20,18 +20,62 @@ namespace sgsf {
 
 // Reference trig formula in FP64.  Explicit _rn intrinsics keep nvcc from
 // contracting into FMAs so the products round like the reference's scalar C.
+// This path exists for terms with an exactly-zero component, and there one
+// of the two angles is special (0, +-pi/2, +-pi): its sine and cosine are
+// the values the library returns for those doubles -- e.g. cos(pi/2) =
+// 6.123233995736766e-17, the "leak" that matters -- so only the other angle
+// needs atan2 + sincos.
+constexpr double kHalfPi = 1.5707963267948966, kPi = 3.141592653589793;
+constexpr double kCosHalfPi = 6.123233995736766e-17, kSinPi = 1.2246467991473532e-16;
+
 static __device__ __noinline__ void ref_spherical(double dx, double dy, double dz, double lat, double vert,
                                            double lo, double hi, double* az_o, double* pol_o,
                                            double* rad_o, double* tx, double* ty, double* tz) {
-    double az = atan2(dy, dx);
-    double planar = hypot(dx, dy);
-    double pol;
-    if (planar == 0.0 && dz == 0.0) {
-        pol = 1.5707963267948966;
+    double az, ca, sa, planar;
+    if (dx == 0.0 && dy != 0.0) {   // atan2(+-y, +-0) = +-pi/2
+        az = copysign(kHalfPi, dy);
+        ca = kCosHalfPi;
+        sa = copysign(1.0, dy);
+        planar = fabs(dy);
+    } else if (dy == 0.0 && dx != 0.0) {   // atan2(+-0, x) = +-0 (x > 0) or +-pi (x < 0)
+        if (dx > 0.0) {
+            az = copysign(0.0, dy);
+            ca = 1.0;
+            sa = copysign(0.0, dy);
+        } else {
+            az = copysign(kPi, dy);
+            ca = -1.0;
+            sa = copysign(kSinPi, dy);
+        }
+        planar = fabs(dx);
+    } else {
+        az = atan2(dy, dx);
+        sincos(az, &sa, &ca);
+        planar = hypot(dx, dy);
+    }
+    double pol, sp, cp;
+    if (planar == 0.0 && dz == 0.0) {   // the reference's all-zero convention
+        pol = kHalfPi;
+        sp = 1.0;
+        cp = kCosHalfPi;
+    } else if (planar == 0.0) {   // atan2(+0, x): 0 for x > 0, pi for x < 0
+        if (dz > 0.0) {
+            pol = 0.0;
+            sp = 0.0;
+            cp = 1.0;
+        } else {
+            pol = kPi;
+            sp = kSinPi;
+            cp = -1.0;
+        }
+    } else if (dz == 0.0) {   // atan2(y > 0, +-0) = pi/2
+        pol = kHalfPi;
+        sp = 1.0;
+        cp = kCosHalfPi;
     } else {
         pol = atan2(__ddiv_rn(planar, lat), __ddiv_rn(dz, vert));
+        sincos(pol, &sp, &cp);
     }
-    double sp = sin(pol), cp = cos(pol);
     double ls = __dmul_rn(lat, sp), vc = __dmul_rn(vert, cp);
     double num = __dadd_rn(__dmul_rn(ls, planar), __dmul_rn(vc, dz));
     double den = __dadd_rn(__dmul_rn(ls, ls), __dmul_rn(vc, vc));
@@ -42,8 +86,8 @@ static __device__ __noinline__ void ref_spherical(double dx, double dy, double d
     if (az_o) *az_o = az;
     if (pol_o) *pol_o = pol;
     if (rad_o) *rad_o = rad;
-    if (tx) *tx = __dmul_rn(lr, cos(az));
-    if (ty) *ty = __dmul_rn(lr, sin(az));
+    if (tx) *tx = __dmul_rn(lr, ca);
+    if (ty) *ty = __dmul_rn(lr, sa);
     if (tz) *tz = __dmul_rn(__dmul_rn(vert, rad), cp);
 }
 
