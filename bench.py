@@ -104,9 +104,28 @@ def cpu_model() -> str:
 
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
+    """`nvidia-smi -lms 100` into a CSV.  Started before the warm-up (its start-up queries the driver and
+    must not overlap the timed steps); `mark()` brackets the timed region and the summary uses those rows."""
+
     def __init__(self, path: Path):
         self.path = path
         self.proc = None
+        self.marks = []
+
+    def lines(self) -> int:
+        try:
+            with open(self.path) as fh:
+                return sum(1 for _ in fh)
+        except OSError:
+            return 0
+
+    def wait_first(self, timeout_s: float = 5.0) -> None:
+        t0 = time.perf_counter()
+        while self.proc is not None and self.lines() == 0 and time.perf_counter() - t0 < timeout_s:
+            time.sleep(0.05)
+
+    def mark(self) -> None:
+        self.marks.append(self.lines())
 
     def __enter__(self):
         try:
@@ -129,12 +148,15 @@ class ClockSampler:
     def summary(self, device_index: int) -> dict:
         rows = []
         try:
-            for line in open(self.path):
-                f = [x.strip() for x in line.split(",")]
-                if len(f) >= 9 and f[0] == str(device_index):
-                    rows.append(f)
+            lines = open(self.path).read().splitlines()
         except OSError:
-            pass
+            lines = []
+        if len(self.marks) == 2 and self.marks[1] > self.marks[0]:
+            lines = lines[self.marks[0]:self.marks[1] + 1]   # the timed region (+ the sample just after it)
+        for line in lines:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 9 and f[0] == str(device_index):
+                rows.append(f)
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
@@ -214,40 +236,47 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         gather(out)
         return out
 
+    clocks = ClockSampler(ROOT / "gpurun_out" / f"clocks_rank{rank}.csv") if rank == 0 else None
+    if clocks:
+        (ROOT / "gpurun_out").mkdir(exist_ok=True)
+        clocks.__enter__()
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
+    if clocks:
+        clocks.wait_first()
 
     # ---- device-timed region: inputs resident in HBM
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     feas_counts, its_total = [], []
     launches0 = native.launch_count()
-    clocks = ClockSampler(ROOT / "gpurun_out" / f"clocks_rank{rank}.csv") if rank == 0 else None
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     if clocks:
-        (ROOT / "gpurun_out").mkdir(exist_ok=True)
-        clocks.__enter__()
+        clocks.mark()
     outs = []
     for k in range(args.steps):
         flush.fill_(float(k))
         ev[k][0].record()
         out = step(timing=kev[k])
         ev[k][1].record()
-        outs.append(out)
+        outs.append((out.feasible, out.iterations))   # the rest is freed: the next step reuses its blocks
+        del out
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     if clocks:
+        time.sleep(0.15)   # one more sample after the last step
+        clocks.mark()
         clocks.__exit__()
     launches = native.launch_count() - launches0
     step_ms = [a.elapsed_time(b) for a, b in ev]
     kern_ms = [a.elapsed_time(b) for a, b in kev]
-    for out in outs:
-        feas_counts.append(int(out.feasible.sum().item()))
-        its_total.append(int(out.iterations.sum().item()))
+    for feas, its in outs:
+        feas_counts.append(int(feas.sum().item()))
+        its_total.append(int(its.sum().item()))
     total_ms = sum(step_ms)
     t = torch.tensor([total_ms, float(sum(feas_counts))], dtype=torch.float64, device=dev)
     if world > 1:
