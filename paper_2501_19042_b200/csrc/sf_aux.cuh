@@ -8,6 +8,10 @@
 
 namespace sgsf {
 
+// window of time steps whose positions the per-sample aux kernels keep in shared memory
+constexpr int AUX_TCH = 32;
+
+
 constexpr int KMAX_AUX = 32;   // max degree + 1 for the (test-only) FP64 step kernels
 
 struct AuxParams {
@@ -50,51 +54,54 @@ __global__ void verdict_kernel(AuxParams a, int batch, const double* __restrict_
     extern __shared__ __align__(16) unsigned char sm[];
     const int n = a.n, S = a.S, m1 = a.m1, P = a.P, dim = 3 * n * m1;
     double* C = (double*)sm;
-    double* pos = C + dim;                       // 3 x n x S
-    double* red_min = pos + 3 * n * S;           // blockDim
+    double* pos = C + dim;                       // 3 x n x AUX_TCH (a window of time steps)
+    double* red_min = pos + 3 * n * AUX_TCH;     // blockDim
     double* red_max = red_min + blockDim.x;
     int* red_pc = (int*)(red_max + blockDim.x);
     int* red_wc = red_pc + blockDim.x;
     const int b = blockIdx.x;
     if (b >= batch) return;
     for (int e = threadIdx.x; e < dim; e += blockDim.x) C[e] = coeffs[(size_t)b * dim + e];
-    __syncthreads();
-    for (int e = threadIdx.x; e < 3 * n * S; e += blockDim.x) {
-        const int row = e / S, t = e - row * S;
-        pos[e] = eval_pos(C + row * m1, a.W + t * m1, m1);
-    }
-    __syncthreads();
     const double ia2 = a.lat * a.lat, ib2 = a.vert * a.vert;
     const double wa2 = a.ws_lat * a.ws_lat, wb2 = a.ws_vert * a.ws_vert;
     double pmin = CUDART_INF, wmax = -CUDART_INF;
     int pc = 0, wc = 0;
-    for (int e = threadIdx.x; e < (P + n) * S; e += blockDim.x) {
-        const int term = e / S, t = e - term * S;
-        double dx, dy, dz, a2, b2;
-        if (term < P) {
-            int i, j;
-            pair_of(term, n, i, j);
-            dx = pos[(0 * n + i) * S + t] - pos[(0 * n + j) * S + t];
-            dy = pos[(1 * n + i) * S + t] - pos[(1 * n + j) * S + t];
-            dz = pos[(2 * n + i) * S + t] - pos[(2 * n + j) * S + t];
-            a2 = ia2;
-            b2 = ib2;
-        } else {
-            const int i = term - P;
-            dx = pos[(0 * n + i) * S + t] - a.cx;
-            dy = pos[(1 * n + i) * S + t] - a.cy;
-            dz = pos[(2 * n + i) * S + t] - a.cz;
-            a2 = wa2;
-            b2 = wb2;
+    for (int t0 = 0; t0 < S; t0 += AUX_TCH) {
+        const int tc = min(AUX_TCH, S - t0);
+        __syncthreads();
+        for (int e = threadIdx.x; e < 3 * n * tc; e += blockDim.x) {
+            const int row = e / tc, t = e - row * tc;
+            pos[row * AUX_TCH + t] = eval_pos(C + row * m1, a.W + (t0 + t) * m1, m1);
         }
-        const double m = __dadd_rn(__dadd_rn(__ddiv_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), a2),
-                                             __ddiv_rn(__dmul_rn(dz, dz), b2)), -1.0);
-        if (term < P) {
-            pmin = fmin(pmin, m);
-            pc += (m < -tol);
-        } else {
-            wmax = fmax(wmax, m);
-            wc += (m > tol);
+        __syncthreads();
+        for (int e = threadIdx.x; e < (P + n) * tc; e += blockDim.x) {
+            const int term = e / tc, t = e - term * tc;
+            double dx, dy, dz, a2, b2;
+            if (term < P) {
+                int i, j;
+                pair_of(term, n, i, j);
+                dx = pos[(0 * n + i) * AUX_TCH + t] - pos[(0 * n + j) * AUX_TCH + t];
+                dy = pos[(1 * n + i) * AUX_TCH + t] - pos[(1 * n + j) * AUX_TCH + t];
+                dz = pos[(2 * n + i) * AUX_TCH + t] - pos[(2 * n + j) * AUX_TCH + t];
+                a2 = ia2;
+                b2 = ib2;
+            } else {
+                const int i = term - P;
+                dx = pos[(0 * n + i) * AUX_TCH + t] - a.cx;
+                dy = pos[(1 * n + i) * AUX_TCH + t] - a.cy;
+                dz = pos[(2 * n + i) * AUX_TCH + t] - a.cz;
+                a2 = wa2;
+                b2 = wb2;
+            }
+            const double m = __dadd_rn(__dadd_rn(__ddiv_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), a2),
+                                                 __ddiv_rn(__dmul_rn(dz, dz), b2)), -1.0);
+            if (term < P) {
+                pmin = fmin(pmin, m);
+                pc += (m < -tol);
+            } else {
+                wmax = fmax(wmax, m);
+                wc += (m > tol);
+            }
         }
     }
     red_min[threadIdx.x] = pmin;
@@ -125,39 +132,42 @@ __global__ void svars_kernel(AuxParams a, int batch, const double* __restrict__ 
     extern __shared__ __align__(16) unsigned char sm[];
     const int n = a.n, S = a.S, m1 = a.m1, P = a.P, dim = 3 * n * m1;
     double* C = (double*)sm;
-    double* pos = C + dim;
+    double* pos = C + dim;   // 3 x n x AUX_TCH
     const int b = blockIdx.x;
     if (b >= batch) return;
     for (int e = threadIdx.x; e < dim; e += blockDim.x) C[e] = coeffs[(size_t)b * dim + e];
-    __syncthreads();
-    for (int e = threadIdx.x; e < 3 * n * S; e += blockDim.x) {
-        const int row = e / S, t = e - row * S;
-        pos[e] = eval_pos(C + row * m1, a.W + t * m1, m1);
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < (P + n) * S; e += blockDim.x) {
-        const int term = e / S, t = e - term * S;
-        double az, pol, rad;
-        if (term < P) {
-            int i, j;
-            pair_of(term, n, i, j);
-            ref_spherical(pos[(0 * n + i) * S + t] - pos[(0 * n + j) * S + t],
-                          pos[(1 * n + i) * S + t] - pos[(1 * n + j) * S + t],
-                          pos[(2 * n + i) * S + t] - pos[(2 * n + j) * S + t], a.lat, a.vert, 1.0,
-                          CUDART_INF, &az, &pol, &rad, nullptr, nullptr, nullptr);
-            const size_t o = (size_t)b * P * S + (size_t)term * S + t;
-            paz[o] = az;
-            ppol[o] = pol;
-            prad[o] = rad;
-        } else {
-            const int i = term - P;
-            ref_spherical(pos[(0 * n + i) * S + t] - a.cx, pos[(1 * n + i) * S + t] - a.cy,
-                          pos[(2 * n + i) * S + t] - a.cz, a.ws_lat, a.ws_vert, 0.0, 1.0, &az, &pol, &rad,
-                          nullptr, nullptr, nullptr);
-            const size_t o = (size_t)b * n * S + (size_t)i * S + t;
-            waz[o] = az;
-            wpol[o] = pol;
-            wrad[o] = rad;
+    for (int t0 = 0; t0 < S; t0 += AUX_TCH) {
+        const int tc = min(AUX_TCH, S - t0);
+        __syncthreads();
+        for (int e = threadIdx.x; e < 3 * n * tc; e += blockDim.x) {
+            const int row = e / tc, t = e - row * tc;
+            pos[row * AUX_TCH + t] = eval_pos(C + row * m1, a.W + (t0 + t) * m1, m1);
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < (P + n) * tc; e += blockDim.x) {
+            const int term = e / tc, tl = e - term * tc, t = t0 + tl;
+            double az, pol, rad;
+            if (term < P) {
+                int i, j;
+                pair_of(term, n, i, j);
+                ref_spherical(pos[(0 * n + i) * AUX_TCH + tl] - pos[(0 * n + j) * AUX_TCH + tl],
+                              pos[(1 * n + i) * AUX_TCH + tl] - pos[(1 * n + j) * AUX_TCH + tl],
+                              pos[(2 * n + i) * AUX_TCH + tl] - pos[(2 * n + j) * AUX_TCH + tl], a.lat, a.vert, 1.0,
+                              CUDART_INF, &az, &pol, &rad, nullptr, nullptr, nullptr);
+                const size_t o = (size_t)b * P * S + (size_t)term * S + t;
+                paz[o] = az;
+                ppol[o] = pol;
+                prad[o] = rad;
+            } else {
+                const int i = term - P;
+                ref_spherical(pos[(0 * n + i) * AUX_TCH + tl] - a.cx, pos[(1 * n + i) * AUX_TCH + tl] - a.cy,
+                              pos[(2 * n + i) * AUX_TCH + tl] - a.cz, a.ws_lat, a.ws_vert, 0.0, 1.0, &az, &pol,
+                              &rad, nullptr, nullptr, nullptr);
+                const size_t o = (size_t)b * n * S + (size_t)i * S + t;
+                waz[o] = az;
+                wpol[o] = pol;
+                wrad[o] = rad;
+            }
         }
     }
 }
@@ -243,29 +253,37 @@ __global__ void apply_FT_kernel(AuxParams a, int batch, const double* __restrict
     extern __shared__ __align__(16) unsigned char sm[];
     const int n = a.n, S = a.S, m1 = a.m1, P = a.P, dim = 3 * n * m1;
     const int axis_rows = (P + n) * S;
-    double* comb = (double*)sm;   // 3 x n x S
+    double* comb = (double*)sm;            // 3 x n x AUX_TCH (a window of time steps)
+    double* acc = comb + 3 * n * AUX_TCH;  // dim: the sums over the windows so far (ascending t)
     const int b = blockIdx.x;
     if (b >= batch) return;
     const double* vb = v + (size_t)b * 3 * axis_rows;
-    for (int e = threadIdx.x; e < 3 * n * S; e += blockDim.x) {
-        const int row = e / S, t = e - row * S, ax = row / n, i = row - ax * n;
-        const double* va = vb + (size_t)ax * axis_rows;
-        double s = 0.0;
-        int p = 0;
-        for (int r = 0; r < n; ++r)
-            for (int c = r + 1; c < n; ++c, ++p) {
-                if (r == i) s += va[p * S + t];
-                else if (c == i) s -= va[p * S + t];
-            }
-        comb[e] = s + va[P * S + i * S + t];
+    for (int e = threadIdx.x; e < dim; e += blockDim.x) acc[e] = 0.0;
+    for (int t0 = 0; t0 < S; t0 += AUX_TCH) {
+        const int tc = min(AUX_TCH, S - t0);
+        __syncthreads();
+        for (int e = threadIdx.x; e < 3 * n * tc; e += blockDim.x) {
+            const int row = e / tc, t = t0 + (e - row * tc), ax = row / n, i = row - ax * n;
+            const double* va = vb + (size_t)ax * axis_rows;
+            double s = 0.0;
+            int p = 0;
+            for (int r = 0; r < n; ++r)
+                for (int c = r + 1; c < n; ++c, ++p) {
+                    if (r == i) s += va[p * S + t];
+                    else if (c == i) s -= va[p * S + t];
+                }
+            comb[row * AUX_TCH + (t - t0)] = s + va[P * S + i * S + t];
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < dim; e += blockDim.x) {
+            const int row = e / m1, q = e - row * m1;
+            double s = acc[e];
+            for (int t = 0; t < tc; ++t) s = fma(comb[row * AUX_TCH + t], a.W[(t0 + t) * m1 + q], s);
+            acc[e] = s;
+        }
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < dim; e += blockDim.x) {
-        const int row = e / m1, q = e - row * m1;
-        double s = 0.0;
-        for (int t = 0; t < S; ++t) s = fma(comb[row * S + t], a.W[t * m1 + q], s);
-        out[(size_t)b * dim + e] = s;
-    }
+    for (int e = threadIdx.x; e < dim; e += blockDim.x) out[(size_t)b * dim + e] = acc[e];
 }
 
 // literal coefficient step from eta: C_i = Km11 eta_bar + Kd11 (eta_i - eta_bar) + cconst_i

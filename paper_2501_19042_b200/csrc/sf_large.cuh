@@ -1,0 +1,534 @@
+// sf_large.cuh -- K1L: the safety filter for 32 < n <= 64 robots (BASELINE config 4).
+//
+// Same alternating minimisation and the same per-term arithmetic as K1
+// (sf_persistent.cuh), organised for swarms whose state does not fit K1's
+// one-thread-per-time-step layout: a 64-robot step has 2016 pair terms, so
+// K1's per-step term bitmasks (66 words) and its two [S][3n] position
+// buffers (237 KB at H=150) do not fit registers / shared memory.
+//
+// One CTA of 8 warps per sample (persistent over the ordered sample queue).
+// Term pass: warp w takes time steps w, w+8, ...; per step the positions of
+// the new and of the previous iterate are evaluated into a per-warp scratch,
+// and lane l owns robots l and l+32: it visits every partner, so its
+// scattered residual R_i accumulates in registers in a fixed order
+// (deterministic; each pair is evaluated by both of its robots, its exit
+// residual counted once).  Terms are evaluated exactly every iteration
+// (interior test, trig-free target for non-interior terms, FP64 reference
+// trig for terms with an exactly-zero component); no motion bounds.
+// g = R W accumulates per lane for the active robot rows and is combined
+// across warps in warp order (ticket), so the FP sum order is fixed.
+// The FP64 xi-step, equality check and commit are K1's DMMA formulation,
+// one warp per axis with 8 robot tiles.
+#pragma once
+
+#include "sf_persistent.cuh"
+
+namespace sgsf {
+
+constexpr int kLargeWarps = 8;
+
+struct LargeShared {
+    int sample;
+    int active[2];   // by iteration parity (cleared for the other parity at the top of an iteration)
+    int g_ticket;    // fixed-order g accumulation: warp w adds when g_ticket == k * kLargeWarps + w
+};
+
+struct LargeLayout {
+    size_t W, KMm, KMd, cconst, B6, rhs, PBt;
+    size_t C, Cp, lam, U, xb, g, Cf, Cfo, scr, winf, wsq, eqerr, sh;
+    size_t total;
+};
+
+template <typename T, int NB>
+__host__ __device__ inline LargeLayout make_large_layout(int n, int S, int MP, int want_prev) {
+    LargeLayout L;
+    size_t o = 0;
+    const size_t d = sizeof(double), ts = sizeof(T);
+    const size_t dimp = (size_t)3 * n * MP;
+    L.W = o;      o = align16(o + (size_t)S * MP * ts);
+    L.KMm = o;    o = align16(o + (size_t)MP * 2 * MP * d);
+    L.KMd = o;    o = align16(o + (size_t)MP * 2 * MP * d);
+    L.cconst = o; o = align16(o + dimp * d);
+    L.B6 = o;     o = align16(o + (size_t)6 * MP * d);
+    L.rhs = o;    o = align16(o + (size_t)3 * n * 6 * d);
+    L.PBt = o;    o = align16(o + (size_t)MP * 6 * d);
+    L.C = o;      o = align16(o + dimp * d);
+    L.Cp = o;     o = align16(o + (want_prev ? dimp * d : 0));
+    L.lam = o;    o = align16(o + dimp * d);
+    L.U = o;      o = align16(o + dimp * d);
+    L.xb = o;     o = align16(o + dimp * d);
+    L.g = o;      o = align16(o + dimp * d);
+    L.Cf = o;     o = align16(o + (size_t)3 * MP * NB * ts);   // C of the current iterate, robot-minor
+    L.Cfo = o;    o = align16(o + (size_t)3 * MP * NB * ts);   // ... of the previous iterate
+    L.scr = o;    o = align16(o + (size_t)kLargeWarps * 2 * 3 * NB * ts);
+    L.winf = o;   o = align16(o + (size_t)kLargeWarps * ts);
+    L.wsq = o;    o = align16(o + (size_t)kLargeWarps * d);
+    L.eqerr = o;  o = align16(o + (size_t)4 * d);
+    L.sh = o;     o = align16(o + sizeof(LargeShared));
+    L.total = o;
+    return L;
+}
+
+// One term, evaluated exactly: r = d_new - e(d_new) (the lam' residual; 0 for interior terms) and
+// x = d_new - e(d_old) (the exit residual against the previous targets).  Terms with an exactly-zero
+// component use the FP64 reference formula (sf_device.cuh).
+template <typename T, bool PAIR>
+__device__ __forceinline__ void exact_term(const T (&dn)[3], const T (&dd)[3], const Family<T>& f, T (&r)[3],
+                                           T (&x)[3]) {
+    if (dn[0] == T(0) || dn[1] == T(0) || dn[2] == T(0)) {
+        T t[3];
+        target<T, PAIR>(dn[0], dn[1], dn[2], f, t[0], t[1], t[2]);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) r[a] = dn[a] - t[a];
+    } else {
+        const T q = fma_t<T>(dn[2] * f.beta, dn[2], fma_t<T>(dn[1], dn[1], dn[0] * dn[0]));
+        const bool in = PAIR ? (q >= f.lim) : (q <= f.lim);
+        const T s = in ? T(1) : f.lat * rsq<T>(q);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) r[a] = in ? T(0) : fma_t<T>(-s, dn[a], dn[a]);
+    }
+    if (dd[0] == T(0) || dd[1] == T(0) || dd[2] == T(0)) {
+        T e[3];
+        target<T, PAIR>(dd[0], dd[1], dd[2], f, e[0], e[1], e[2]);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) x[a] = dn[a] - e[a];
+    } else {
+        const T q = fma_t<T>(dd[2] * f.beta, dd[2], fma_t<T>(dd[1], dd[1], dd[0] * dd[0]));
+        const bool in = PAIR ? (q >= f.lim) : (q <= f.lim);
+        const T s = in ? T(1) : f.lat * rsq<T>(q);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) x[a] = in ? dn[a] - dd[a] : fma_t<T>(-s, dd[a], dn[a]);
+    }
+}
+
+template <typename T, int NB, int MP>
+__global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const SolveParams p) {
+    static_assert(NB == 64, "K1L is laid out for 64 robots (lane l owns robots l and l + 32)");
+    extern __shared__ __align__(16) unsigned char smem[];
+    const LargeLayout L = make_large_layout<T, NB>(p.n, p.S, MP, p.want_prev);
+    constexpr int M2P = 2 * MP;
+    constexpr int MT = NB / 8;   // 8-robot DMMA tiles
+    constexpr int KT = MP / 2;   // 4-column k-steps over [C | u]
+    constexpr int KC = MP / 4;
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+    const int n = p.n, S = p.S, m1 = p.m1;
+    const int R3 = 3 * n, dim = R3 * m1, dimp = R3 * MP;
+
+    T* Wt = (T*)(smem + L.W);
+    double* KMm = (double*)(smem + L.KMm);
+    double* KMd = (double*)(smem + L.KMd);
+    double* cconst = (double*)(smem + L.cconst);
+    double* B6 = (double*)(smem + L.B6);
+    double* rhs = (double*)(smem + L.rhs);
+    double* PBt = (double*)(smem + L.PBt);
+    double* C = (double*)(smem + L.C);
+    double* Cp = (double*)(smem + L.Cp);
+    double* lam = (double*)(smem + L.lam);
+    double* U = (double*)(smem + L.U);
+    double* xb = (double*)(smem + L.xb);
+    double* g = (double*)(smem + L.g);
+    T* Cf = (T*)(smem + L.Cf);
+    T* Cfo = (T*)(smem + L.Cfo);
+    T* winf = (T*)(smem + L.winf);
+    double* wsq = (double*)(smem + L.wsq);
+    double* eqerr = (double*)(smem + L.eqerr);
+    LargeShared* sh = (LargeShared*)(smem + L.sh);
+
+    // shared constants (as K1), zero-padded to MP columns
+    for (int i = tid; i < S * MP; i += nt) {
+        const int t = i / MP, q = i % MP;
+        Wt[i] = (q < m1) ? (T)p.W[t * m1 + q] : T(0);
+    }
+    for (int i = tid; i < MP * M2P; i += nt) {
+        const int q = i / M2P, c = i % M2P, half = c / MP, q2 = c % MP;
+        const bool in = q < m1 && q2 < m1;
+        KMm[i] = in ? p.KMm[q * 2 * m1 + half * m1 + q2] - p.KMd[q * 2 * m1 + half * m1 + q2] : 0.0;
+        KMd[i] = in ? p.KMd[q * 2 * m1 + half * m1 + q2] : 0.0;
+    }
+    for (int i = tid; i < dimp; i += nt) {
+        const int r = i / MP, q = i % MP;
+        cconst[i] = (q < m1) ? p.cconst[r * m1 + q] : 0.0;
+    }
+    for (int i = tid; i < 6 * MP; i += nt) {
+        const int c = i / MP, q = i % MP;
+        B6[i] = (q < m1) ? p.B6[c * m1 + q] : 0.0;
+    }
+    for (int i = tid; i < R3 * 6; i += nt) rhs[i] = p.rhs[i];
+    for (int i = tid; i < MP * 6; i += nt) PBt[i] = (i / 6 < m1) ? p.PBt[i] : 0.0;
+    if (tid == 0) {
+        sh->sample = next_sample(p);
+        sh->active[0] = sh->active[1] = 0;
+    }
+    __syncthreads();
+
+    const Family<T> fp = make_family<T>(p.lat, p.vert);
+    const Family<T> fw = make_family<T>(p.ws_lat, p.ws_vert);
+    const T cen[3] = {(T)p.cx, (T)p.cy, (T)p.cz};
+    const double inv_n = 1.0 / n;
+    T* sn = (T*)(smem + L.scr) + warp * 2 * 3 * NB;   // this warp's positions at the step: new [3][NB] ...
+    T* so = sn + 3 * NB;                              // ... and old [3][NB]
+    int sample = sh->sample;
+    bool prev_active = false;
+
+    while (sample < p.batch) {
+        // ---------------- load the sample (default start = boundary projection), g = 0
+        for (int r = tid; r < R3; r += nt) {
+            const double* xr = p.xi_bar + (size_t)sample * dim + r * m1;
+            double x[MP], c[MP], l[MP];
+#pragma unroll
+            for (int q = 0; q < MP; ++q) x[q] = (q < m1) ? xr[q] : 0.0;
+            const int mode = p.init_mode ? p.init_mode[sample] : 0;
+            if (mode) {
+                const double* cr = p.xi0 + (size_t)sample * dim + r * m1;
+                const double* lr = p.lam0 + (size_t)sample * dim + r * m1;
+#pragma unroll
+                for (int q = 0; q < MP; ++q) {
+                    c[q] = (q < m1) ? cr[q] : 0.0;
+                    l[q] = (q < m1) ? lr[q] : 0.0;
+                }
+            } else {
+                double res[6];
+#pragma unroll
+                for (int cnd = 0; cnd < 6; ++cnd) {
+                    double e = 0.0;
+#pragma unroll
+                    for (int q = 0; q < MP; ++q) e = fma(B6[cnd * MP + q], x[q], e);
+                    res[cnd] = e - rhs[r * 6 + cnd];
+                }
+#pragma unroll
+                for (int q = 0; q < MP; ++q) {
+                    double corr = 0.0;
+#pragma unroll
+                    for (int cnd = 0; cnd < 6; ++cnd) corr = fma(PBt[q * 6 + cnd], res[cnd], corr);
+                    c[q] = x[q] - corr;
+                    l[q] = 0.0;
+                }
+            }
+            const int ax = r / n, i = r - ax * n;
+#pragma unroll
+            for (int q = 0; q < MP; ++q) {
+                const int idx = r * MP + q;
+                xb[idx] = x[q];
+                C[idx] = c[q];
+                lam[idx] = l[q];
+                g[idx] = 0.0;
+                if (p.want_prev) Cp[idx] = c[q];
+                Cf[(ax * MP + q) * NB + i] = (T)c[q];
+                Cfo[(ax * MP + q) * NB + i] = (T)c[q];   // no previous iterate: "old" := "new"
+            }
+        }
+        if (tid == 0) sh->g_ticket = 0;
+        __syncthreads();
+
+        for (int k = 0;; ++k) {
+            const int par = k & 1;
+            if (tid == 0) sh->active[par ^ 1] = 0;   // last read before the previous closing barrier
+            // ---------------- term pass
+            T gacc[2][3][MP];
+#pragma unroll
+            for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+                for (int a = 0; a < 3; ++a)
+#pragma unroll
+                    for (int q = 0; q < MP; ++q) gacc[rr][a][q] = T(0);
+            T linf = T(0);
+            double lsq = 0.0;
+            bool lact = false;
+            for (int t = warp; t < S; t += kLargeWarps) {
+                T w[MP];
+                load_row16<T, MP>(Wt + t * MP, w);
+#pragma unroll
+                for (int rr = 0; rr < 2; ++rr) {
+                    const int i = lane + 32 * rr;
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) {
+                        T pn = T(0), po = T(0);
+#pragma unroll
+                        for (int q = 0; q < MP; ++q) {
+                            pn = fma_t<T>(Cf[(a * MP + q) * NB + i], w[q], pn);
+                            po = fma_t<T>(Cfo[(a * MP + q) * NB + i], w[q], po);
+                        }
+                        sn[a * NB + i] = pn;
+                        so[a * NB + i] = po;
+                    }
+                }
+                __syncwarp();
+#pragma unroll
+                for (int rr = 0; rr < 2; ++rr) {
+                    const int i = lane + 32 * rr;
+                    if (i >= n) continue;
+                    T Ri[3] = {T(0), T(0), T(0)};
+                    const T ni[3] = {sn[i], sn[NB + i], sn[2 * NB + i]};
+                    const T oi[3] = {so[i], so[NB + i], so[2 * NB + i]};
+                    for (int j = 0; j < n; ++j) {
+                        if (j == i) continue;
+                        const bool fwd = i < j;   // the pair is (min, max): d = p_min - p_max
+                        T dn[3], dd[3], r[3], x[3];
+#pragma unroll
+                        for (int a = 0; a < 3; ++a) {
+                            const T nj = sn[a * NB + j], oj = so[a * NB + j];
+                            dn[a] = fwd ? ni[a] - nj : nj - ni[a];
+                            dd[a] = fwd ? oi[a] - oj : oj - oi[a];
+                        }
+                        exact_term<T, true>(dn, dd, fp, r, x);
+#pragma unroll
+                        for (int a = 0; a < 3; ++a) Ri[a] += fwd ? r[a] : -r[a];
+                        if (fwd) {
+#pragma unroll
+                            for (int a = 0; a < 3; ++a) {
+                                linf = fmax(linf, fabs(x[a]));
+                                lsq = fma((double)x[a], (double)x[a], lsq);
+                            }
+                        }
+                    }
+                    {   // workspace term of robot i
+                        T dn[3], dd[3], r[3], x[3];
+#pragma unroll
+                        for (int a = 0; a < 3; ++a) {
+                            dn[a] = ni[a] - cen[a];
+                            dd[a] = oi[a] - cen[a];
+                        }
+                        exact_term<T, false>(dn, dd, fw, r, x);
+#pragma unroll
+                        for (int a = 0; a < 3; ++a) {
+                            Ri[a] += r[a];
+                            linf = fmax(linf, fabs(x[a]));
+                            lsq = fma((double)x[a], (double)x[a], lsq);
+                        }
+                    }
+                    if (Ri[0] != T(0) || Ri[1] != T(0) || Ri[2] != T(0)) {
+                        lact = true;
+#pragma unroll
+                        for (int a = 0; a < 3; ++a)
+#pragma unroll
+                            for (int q = 0; q < MP; ++q) gacc[rr][a][q] = fma_t<T>(Ri[a], w[q], gacc[rr][a][q]);
+                    }
+                }
+                __syncwarp();   // the scratch is rewritten for the next step
+            }
+            // per-warp partials of the exit norm, fixed order
+            {
+                const T wi = warp_max_nonneg(linf);
+                double wq = lsq;
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) wq += __shfl_xor_sync(0xffffffffu, wq, off);
+                if (lane == 0) {
+                    winf[warp] = wi;
+                    wsq[warp] = wq;
+                }
+            }
+            // g = sum over the warps of their partial R W, in warp order
+            {
+                const bool wact = __any_sync(0xffffffffu, lact);
+                const int ticket = k * kLargeWarps + warp;
+                if (lane == 0)
+                    while (*(volatile int*)&sh->g_ticket != ticket) __nanosleep(32);
+                __syncwarp();
+                __threadfence_block();
+                if (wact) {
+#pragma unroll
+                    for (int rr = 0; rr < 2; ++rr) {
+                        const int i = lane + 32 * rr;
+                        if (i < n) {
+#pragma unroll
+                            for (int a = 0; a < 3; ++a)
+#pragma unroll
+                                for (int q = 0; q < MP; ++q) g[((a * n) + i) * MP + q] += (double)gacc[rr][a][q];
+                        }
+                    }
+                    if (lane == 0) sh->active[par] = 1;
+                }
+                __threadfence_block();
+                __syncwarp();
+                if (lane == 0) *(volatile int*)&sh->g_ticket = ticket + 1;
+            }
+            __syncthreads();
+
+            // ---------------- decision (every thread): exit residual of iteration k-1, early stop, SingularKKT
+            double emax = 0.0, sqs = 0.0;
+            T inf = T(0);
+            if (k >= 1) {
+                emax = fmax(fmax(eqerr[0], eqerr[1]), eqerr[2]);
+                for (int w = 0; w < kLargeWarps; ++w) {
+                    inf = fmax(inf, winf[w]);
+                    sqs += wsq[w];
+                }
+            }
+            const bool failed = (k >= 1) && (emax > p.tol_eq);
+            bool done = failed;
+            if (k >= 1) {
+                done = done || (p.early_stop && (double)inf <= p.tol_res) || (k >= p.max_iters);
+                if (tid == 0) {
+                    const size_t hix = (size_t)sample * p.max_iters + (k - 1);
+                    p.res_inf[hix] = (double)inf;
+                    p.res_l2[hix] = sqrt(sqs);
+                }
+            }
+            if (done) {
+                // ---------------- finalize: outputs of the returned iterate, claim the next sample
+                if (!failed) {
+                    for (int e = tid; e < dim; e += nt) {
+                        const int r = e / m1, q = e - r * m1;
+                        const size_t o = (size_t)sample * dim + e;
+                        p.coeffs[o] = C[r * MP + q];
+                        p.mult[o] = lam[r * MP + q];
+                        if (p.want_prev && p.coeffs_prev) p.coeffs_prev[o] = Cp[r * MP + q];
+                    }
+                }
+                if (warp == 0) {
+                    double acc = 0.0;
+                    for (int e = lane; e < dimp; e += 32) {
+                        const double dd = C[e] - xb[e];
+                        acc = fma(dd, dd, acc);
+                    }
+#pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+                    if (lane == 0) {
+                        p.iterations[sample] = failed ? 0 : k;
+                        p.converged[sample] = (!failed && (double)inf <= p.tol_res) ? 1 : 0;
+                        p.displacement[sample] = failed ? CUDART_NAN : sqrt(acc);
+                        p.status[sample] = failed ? SAMPLE_SINGULAR_KKT : SAMPLE_OK;
+                        p.eq_err[sample] = emax;
+                        sh->sample = next_sample(p);
+                        sh->active[0] = sh->active[1] = 0;
+                    }
+                }
+                __syncthreads();
+                sample = sh->sample;
+                break;
+            }
+            const bool any_active = sh->active[par] != 0;
+
+            // ---------------- U = 2 lam' - lam + xi_bar (lam' = lam - rho g), element-wise
+            if (any_active || prev_active || k == 0) {
+                for (int e = tid; e < dimp; e += nt) {
+                    const double l = lam[e];
+                    const double lp = any_active ? l - p.rho * g[e] : l;
+                    U[e] = 2.0 * lp - l + xb[e];
+                }
+            }
+            __syncthreads();
+
+            // ---------------- xi-step per axis (K1's DMMA formulation), equality check, commit
+            const int fr = lane >> 2, fc = lane & 3;
+            for (int ax = warp; ax < 3; ax += kLargeWarps) {
+                const int rb = ax * n;
+                double dacc[MT][2][2];
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) {
+                    const int rob = 8 * mt + fr;
+#pragma unroll
+                    for (int nt2 = 0; nt2 < 2; ++nt2)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int q = 8 * nt2 + 2 * fc + e;
+                            dacc[mt][nt2][e] = (rob < n && q < MP) ? cconst[(rb + rob) * MP + q] : 0.0;
+                        }
+                }
+                double csum[KT];
+#pragma unroll
+                for (int kk = 0; kk < KT; ++kk) {
+                    const int c = 4 * kk + fc;
+                    double bf[2];
+#pragma unroll
+                    for (int nt2 = 0; nt2 < 2; ++nt2) {
+                        const int qb = 8 * nt2 + fr;
+                        bf[nt2] = qb < MP ? KMd[qb * M2P + c] : 0.0;
+                    }
+                    csum[kk] = 0.0;
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt) {
+                        const int rob = 8 * mt + fr;
+                        const double a = rob < n ? (kk < KC ? C[(rb + rob) * MP + c] : U[(rb + rob) * MP + c - MP]) : 0.0;
+                        csum[kk] += a;
+#pragma unroll
+                        for (int nt2 = 0; nt2 < 2; ++nt2) dmma884(dacc[mt][nt2][0], dacc[mt][nt2][1], a, bf[nt2]);
+                    }
+                }
+                {   // mean part: every row gets (column sums / n) . [Mm - Md | Km11 - Kd11]^T
+                    double dm[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+                    for (int kk = 0; kk < KT; ++kk) {
+                        double cs = csum[kk];
+                        cs += __shfl_xor_sync(0xffffffffu, cs, 4);
+                        cs += __shfl_xor_sync(0xffffffffu, cs, 8);
+                        cs += __shfl_xor_sync(0xffffffffu, cs, 16);
+                        const int c = 4 * kk + fc;
+                        const double a = cs * inv_n;
+#pragma unroll
+                        for (int nt2 = 0; nt2 < 2; ++nt2) {
+                            const int qb = 8 * nt2 + fr;
+                            dmma884(dm[nt2][0], dm[nt2][1], a, qb < MP ? KMm[qb * M2P + c] : 0.0);
+                        }
+                    }
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                        for (int nt2 = 0; nt2 < 2; ++nt2) {
+                            dacc[mt][nt2][0] += dm[nt2][0];
+                            dacc[mt][nt2][1] += dm[nt2][1];
+                        }
+                }
+                if (p.want_prev) {
+                    for (int e = lane; e < n * MP; e += 32) Cp[rb * MP + e] = C[rb * MP + e];
+                }
+                for (int e = lane; e < MP * NB; e += 32) Cfo[ax * MP * NB + e] = Cf[ax * MP * NB + e];
+                __syncwarp();   // every lane has read the rows before any lane writes them
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) {
+                    const int rob = 8 * mt + fr;
+#pragma unroll
+                    for (int nt2 = 0; nt2 < 2; ++nt2) {
+                        const int q = 8 * nt2 + 2 * fc;
+                        if (rob < n && q < MP) {
+                            const int idx = (rb + rob) * MP + q;
+                            *reinterpret_cast<double2*>(C + idx) = make_double2(dacc[mt][nt2][0], dacc[mt][nt2][1]);
+                            Cf[(ax * MP + q) * NB + rob] = (T)dacc[mt][nt2][0];
+                            Cf[(ax * MP + q + 1) * NB + rob] = (T)dacc[mt][nt2][1];
+                        }
+                    }
+                }
+                if (any_active) {   // commit lam', clear g
+                    for (int e = lane; e < n * MP; e += 32) {
+                        const int idx = rb * MP + e;
+                        lam[idx] = lam[idx] - p.rho * g[idx];
+                        g[idx] = 0.0;
+                    }
+                }
+                __syncwarp();
+                {   // ||A xi - b||_inf over this axis' new rows
+                    double eacc[MT][2];
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt) {
+                        const int rob = 8 * mt + fr;
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int c6 = 2 * fc + e;
+                            eacc[mt][e] = (rob < n && c6 < 6) ? -rhs[(rb + rob) * 6 + c6] : 0.0;
+                        }
+                    }
+#pragma unroll
+                    for (int kk = 0; kk < MP / 4; ++kk) {
+                        const int q = 4 * kk + fc;
+                        const double bv = fr < 6 ? B6[fr * MP + q] : 0.0;
+#pragma unroll
+                        for (int mt = 0; mt < MT; ++mt) {
+                            const int rob = 8 * mt + fr;
+                            const double a = rob < n ? C[(rb + rob) * MP + q] : 0.0;
+                            dmma884(eacc[mt][0], eacc[mt][1], a, bv);
+                        }
+                    }
+                    double em = 0.0;
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt) em = fmax(em, fmax(fabs(eacc[mt][0]), fabs(eacc[mt][1])));
+                    em = warp_max_nonneg(em);
+                    if (lane == 0) eqerr[ax] = em;
+                }
+            }
+            prev_active = any_active;
+            __syncthreads();
+        }
+    }
+}
+
+}  // namespace sgsf

@@ -21,6 +21,9 @@ int internal_fail(int code, const std::string& msg);
 void internal_count_launch(int n);
 // longest-first queue order (kernels_order.cu)
 int launch_order(const SolveParams& p, float* score, int* order, cudaStream_t stream);
+// K1L for 32 < n <= 64 (kernels_large.cu)
+int launch_large(const LaunchInfo& li, SolveParams& p, const sgsf_config_t* cfg, const sgsf_timing_t* timing,
+                 cudaStream_t stream, bool strict);
 
 template <typename T, int NB, int MP, int MAXT, int TPS>
 int launch_persistent(const LaunchInfo& li, SolveParams& p, const sgsf_config_t* cfg, const sgsf_timing_t* timing,

@@ -39,7 +39,7 @@ int fail(int code, const std::string& msg) {
             return fail(SGSF_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
     } while (0)
 
-constexpr int kMaxRobots = 32;
+constexpr int kMaxRobots = 64;
 
 }  // namespace
 
@@ -212,7 +212,7 @@ int sgsf_solve(sgsf_handle_t* h, int batch, const double* xi_bar, const double* 
     p.coeffs_prev = out->coeffs_prev;
     p.queue = (int*)workspace;
     CUDA_TRY(cudaMemsetAsync(workspace, 0, sizeof(int), stream));
-    if (batch > 1) {   // longest-first queue order (sf_order.cuh)
+    if (batch > 1 && h->n <= 32) {   // longest-first queue order (sf_order.cuh)
         float* score = (float*)((char*)workspace + 256);
         int* order = (int*)((char*)workspace + 256 + align256((size_t)batch * 4));
         const int rc = launch_order(p, score, order, stream);
@@ -224,6 +224,7 @@ int sgsf_solve(sgsf_handle_t* h, int batch, const double* xi_bar, const double* 
     const int n = h->n;
     const bool wide = h->m1 > 12;
     LaunchInfo li{h->device, h->sm_count};
+    if (n > 32) return launch_large(li, p, cfg, timing, stream, strict);
 #define SGSF_PICK(T, NB, MAXT, TPS)                                                       \
     return wide ? launch_persistent<T, NB, 16, MAXT, TPS>(li, p, cfg, timing, stream) \
                 : launch_persistent<T, NB, 12, MAXT, TPS>(li, p, cfg, timing, stream)
@@ -245,7 +246,7 @@ int sgsf_verdict(sgsf_handle_t* h, int batch, const double* coeffs, const uint8_
     if (!h || !out || (batch > 0 && !coeffs)) return fail(SGSF_ERR_INVALID, "null argument");
     if (batch == 0) return SGSF_OK;
     const int threads = 256;
-    const size_t smem = (size_t)(3 * h->n * h->m1 + 3 * h->n * h->S) * sizeof(double) +
+    const size_t smem = (size_t)(3 * h->n * h->m1 + 3 * h->n * AUX_TCH) * sizeof(double) +
                         threads * (2 * sizeof(double) + 2 * sizeof(int));
     CUDA_TRY(cudaFuncSetAttribute(verdict_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     verdict_kernel<<<batch, threads, smem, (cudaStream_t)stream>>>(aux_params(h), batch, coeffs, converged, tol,
@@ -275,7 +276,7 @@ int sgsf_svars(sgsf_handle_t* h, int batch, const double* coeffs, double* paz, d
     if (!h || (batch > 0 && (!coeffs || !waz || !wpol || !wrad))) return fail(SGSF_ERR_INVALID, "null argument");
     if (h->P > 0 && batch > 0 && (!paz || !ppol || !prad)) return fail(SGSF_ERR_INVALID, "null pair output");
     if (batch == 0) return SGSF_OK;
-    const size_t smem = (size_t)(3 * h->n * h->m1 + 3 * h->n * h->S) * sizeof(double);
+    const size_t smem = (size_t)(3 * h->n * h->m1 + 3 * h->n * AUX_TCH) * sizeof(double);
     CUDA_TRY(cudaFuncSetAttribute(svars_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     svars_kernel<<<batch, 256, smem, (cudaStream_t)stream>>>(aux_params(h), batch, coeffs, paz, ppol, prad, waz,
                                                               wpol, wrad);
@@ -315,7 +316,7 @@ int sgsf_apply_F(sgsf_handle_t* h, int batch, const double* xi, double* out, voi
 int sgsf_apply_FT(sgsf_handle_t* h, int batch, const double* v, double* out, void* stream) {
     if (!h || (batch > 0 && (!v || !out))) return fail(SGSF_ERR_INVALID, "null argument");
     if (batch == 0) return SGSF_OK;
-    const size_t smem = (size_t)3 * h->n * h->S * sizeof(double);
+    const size_t smem = (size_t)(3 * h->n * AUX_TCH + 3 * h->n * h->m1) * sizeof(double);
     CUDA_TRY(cudaFuncSetAttribute(apply_FT_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     apply_FT_kernel<<<batch, 256, smem, (cudaStream_t)stream>>>(aux_params(h), batch, v, out);
     g_launches.fetch_add(1);
