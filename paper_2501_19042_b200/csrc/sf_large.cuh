@@ -12,9 +12,12 @@
 // and lane l owns robots l and l+32: it visits every partner, so its
 // scattered residual R_i accumulates in registers in a fixed order
 // (deterministic; each pair is evaluated by both of its robots, its exit
-// residual counted once).  Terms are evaluated exactly every iteration
-// (interior test, trig-free target for non-interior terms, FP64 reference
-// trig for terms with an exactly-zero component); no motion bounds.
+// residual counted once).  Terms are evaluated exactly (interior test,
+// trig-free target for non-interior terms, FP64 reference trig for terms with
+// an exactly-zero component), except that a step whose pairs were all
+// interior at its last exact pass and provably still are (motion bound
+// rmin - cum > 1 + margin, as K1) skips the O(n^2) pair loop: its pair exit
+// residuals are then the O(n) statistics of the position change.
 // g = R W accumulates per lane for the active robot rows and is combined
 // across warps in warp order (ticket), so the FP sum order is fixed.
 // The FP64 xi-step, equality check and commit are K1's DMMA formulation,
@@ -35,7 +38,7 @@ struct LargeShared {
 
 struct LargeLayout {
     size_t W, KMm, KMd, cconst, B6, rhs, PBt;
-    size_t C, Cp, lam, U, xb, g, Cf, Cfo, scr, winf, wsq, eqerr, sh;
+    size_t C, Cp, lam, U, xb, g, Cf, Cfo, scr, winf, wsq, eqerr, srmin, scum, sflag, sh;
     size_t total;
 };
 
@@ -64,6 +67,9 @@ __host__ __device__ inline LargeLayout make_large_layout(int n, int S, int MP, i
     L.winf = o;   o = align16(o + (size_t)kLargeWarps * ts);
     L.wsq = o;    o = align16(o + (size_t)kLargeWarps * d);
     L.eqerr = o;  o = align16(o + (size_t)4 * d);
+    L.srmin = o;  o = align16(o + (size_t)S * ts);   // per step: min normalised pair distance at the last exact pass
+    L.scum = o;   o = align16(o + (size_t)S * ts);   // ... pair motion bound accumulated since
+    L.sflag = o;  o = align16(o + (size_t)S * 4);    // ... 1: every pair interior, no zero component there
     L.sh = o;     o = align16(o + sizeof(LargeShared));
     L.total = o;
     return L;
@@ -132,6 +138,9 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
     T* winf = (T*)(smem + L.winf);
     double* wsq = (double*)(smem + L.wsq);
     double* eqerr = (double*)(smem + L.eqerr);
+    T* srmin = (T*)(smem + L.srmin);
+    T* scum = (T*)(smem + L.scum);
+    int* sflag = (int*)(smem + L.sflag);
     LargeShared* sh = (LargeShared*)(smem + L.sh);
 
     // shared constants (as K1), zero-padded to MP columns
@@ -165,6 +174,7 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
     const Family<T> fw = make_family<T>(p.ws_lat, p.ws_vert);
     const T cen[3] = {(T)p.cx, (T)p.cy, (T)p.cz};
     const double inv_n = 1.0 / n;
+    const T inv_lat = T(1) / fp.lat;
     T* sn = (T*)(smem + L.scr) + warp * 2 * 3 * NB;   // this warp's positions at the step: new [3][NB] ...
     T* so = sn + 3 * NB;                              // ... and old [3][NB]
     int sample = sh->sample;
@@ -217,6 +227,7 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
                 Cfo[(ax * MP + q) * NB + i] = (T)c[q];   // no previous iterate: "old" := "new"
             }
         }
+        for (int t = tid; t < S; t += nt) sflag[t] = 0;   // the first iterate takes the exact pass everywhere
         if (tid == 0) sh->g_ticket = 0;
         __syncthreads();
 
@@ -253,6 +264,59 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
                     }
                 }
                 __syncwarp();
+                // O(n) statistics of the position change (lane: robots lane, lane + 32) and the pair
+                // motion bound: while rmin - cum > 1 + margin, every pair of this step is provably
+                // interior now, and if it was interior (and free of zero components) at the last exact
+                // pass, the pair exit residuals are the changes Dp_i - Dp_j: inf = per-axis range,
+                // sum of squares = n sum Dp^2 - (sum Dp)^2 per axis.  No R contribution.
+                T lo[3], hi[3], s1[3], s2[3], dmv = T(0);
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    lo[a] = T(1e30);
+                    hi[a] = T(-1e30);
+                    s1[a] = T(0);
+                    s2[a] = T(0);
+                }
+#pragma unroll
+                for (int rr = 0; rr < 2; ++rr) {
+                    const int i = lane + 32 * rr;
+                    if (i < n) {
+                        T dq = T(0);
+#pragma unroll
+                        for (int a = 0; a < 3; ++a) {
+                            const T dp = sn[a * NB + i] - so[a * NB + i];
+                            lo[a] = fmin(lo[a], dp);
+                            hi[a] = fmax(hi[a], dp);
+                            s1[a] += dp;
+                            s2[a] = fma_t<T>(dp, dp, s2[a]);
+                            dq = fma_t<T>(a == 2 ? dp * fp.beta : dp, dp, dq);
+                        }
+                        dmv = fmax(dmv, dq);
+                    }
+                }
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) {
+                    dmv = fmax(dmv, __shfl_xor_sync(0xffffffffu, dmv, off));
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) {
+                        lo[a] = fmin(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], off));
+                        hi[a] = fmax(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], off));
+                        s1[a] += __shfl_xor_sync(0xffffffffu, s1[a], off);
+                        s2[a] += __shfl_xor_sync(0xffffffffu, s2[a], off);
+                    }
+                }
+                const T cum_t = scum[t] + T(2) * sqrt(dmv) * inv_lat;
+                const bool quiet = k > 0 && sflag[t] != 0 && srmin[t] - cum_t > T(1) + T(1e-3);
+                if (quiet && lane == 0) {
+                    scum[t] = cum_t;
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) {
+                        linf = fmax(linf, hi[a] - lo[a]);
+                        lsq += (double)fmax(fma_t<T>((T)n, s2[a], -s1[a] * s1[a]), T(0));
+                    }
+                }
+                T qmin = T(1e30);   // exact pass: min q over this lane's pairs, non-interior / zero seen
+                bool nonint = false;
 #pragma unroll
                 for (int rr = 0; rr < 2; ++rr) {
                     const int i = lane + 32 * rr;
@@ -260,7 +324,7 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
                     T Ri[3] = {T(0), T(0), T(0)};
                     const T ni[3] = {sn[i], sn[NB + i], sn[2 * NB + i]};
                     const T oi[3] = {so[i], so[NB + i], so[2 * NB + i]};
-                    for (int j = 0; j < n; ++j) {
+                    for (int j = 0; j < (quiet ? 0 : n); ++j) {
                         if (j == i) continue;
                         const bool fwd = i < j;   // the pair is (min, max): d = p_min - p_max
                         T dn[3], dd[3], r[3], x[3];
@@ -271,6 +335,9 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
                             dd[a] = fwd ? oi[a] - oj : oj - oi[a];
                         }
                         exact_term<T, true>(dn, dd, fp, r, x);
+                        const T qn = fma_t<T>(dn[2] * fp.beta, dn[2], fma_t<T>(dn[1], dn[1], dn[0] * dn[0]));
+                        qmin = fmin(qmin, qn);
+                        nonint = nonint || !(qn >= fp.lim) || dn[0] == T(0) || dn[1] == T(0) || dn[2] == T(0);
 #pragma unroll
                         for (int a = 0; a < 3; ++a) Ri[a] += fwd ? r[a] : -r[a];
                         if (fwd) {
@@ -302,6 +369,15 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
                         for (int a = 0; a < 3; ++a)
 #pragma unroll
                             for (int q = 0; q < MP; ++q) gacc[rr][a][q] = fma_t<T>(Ri[a], w[q], gacc[rr][a][q]);
+                    }
+                }
+                if (!quiet) {   // refresh the step's motion-bound state from the exact pass
+                    const T qm = warp_min_nonneg(qmin);
+                    const bool ni = __any_sync(0xffffffffu, nonint);
+                    if (lane == 0) {
+                        srmin[t] = sqrt(qm) * inv_lat;
+                        scum[t] = T(0);
+                        sflag[t] = ni ? 0 : 1;
                     }
                 }
                 __syncwarp();   // the scratch is rewritten for the next step
