@@ -1,0 +1,90 @@
+"""Kernel-variant coverage on the GPU, against the oracle.
+
+* wide degree (m1 > 12 -> the 16-column variants) in every kernel family: K1 (n <= 16), K1 with two
+  lanes per step (n <= 32), K1L (n <= 64);
+* phantom robots inside a variant (n = 20 on the 32-robot layout, n = 48 on the 64-robot one);
+* warm starts and `want_prev` on K1L (a warm start continues the iteration exactly);
+* the windowed verdict and svars kernels at 40 robots.
+Parity is checked at a fixed iteration count (no early stop), so both sides take the same steps.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import sf_oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def _setup(n, horizon, seed, count, max_iters, precision, degree=10):
+    from paper_2501_19042_b200 import SafetyFilter, SolverConfig, sample_proposals
+    from paper_2501_19042_b200.problem import load_problem
+    from paper_2501_19042_b200.scenarios import random_swarm_doc
+    doc = random_swarm_doc(n, horizon, seed)
+    prob = load_problem(doc)
+    cfg = SolverConfig(max_iters=max_iters, early_stop=False, svars=False, precision=precision)
+    sf = SafetyFilter(prob, degree=degree, config=cfg)
+    props = sample_proposals(prob, sf.basis, count, seed=seed).proposals
+    return doc, sf, cfg, props
+
+
+@pytest.mark.parametrize("n,degree,precision,rtol", [
+    (16, 14, "lean", 1e-5), (16, 14, "strict", 1e-9),      # K1, wide
+    (20, 10, "lean", 1e-5), (24, 13, "lean", 1e-5),        # K1 two lanes per step: phantoms, wide
+    (48, 15, "lean", 1e-5), (48, 13, "strict", 1e-9),      # K1L: phantoms, wide
+])
+def test_variant_parity_fixed_iterations(n, degree, precision, rtol):
+    horizon = 30 if n <= 24 else 20
+    doc, sf, cfg, props = _setup(n, horizon, 5, 2, 10, precision, degree)
+    out = sf.solve_batched(torch.from_numpy(props).cuda(), config=cfg)
+    op = sf_oracle.make_problem(doc, degree=degree)
+    coeffs = out.coeffs.cpu().numpy()
+    lam = out.multipliers.cpu().numpy()
+    rinf = out.residual_inf.cpu().numpy()
+    for b, x in enumerate(props):
+        r = sf_oracle.solve(op, x, max_iters=10, early_stop=False)
+        assert np.abs(coeffs[b] - r.coeffs).max() <= rtol * np.abs(r.coeffs).max(), b
+        lscale = max(np.abs(r.multipliers).max(), 1e-12)
+        assert np.abs(lam[b] - r.multipliers).max() <= (1e-4 if precision == "lean" else 1e-8) * lscale, b
+        np.testing.assert_allclose(rinf[b], r.residual_inf, rtol=1e-3 if precision == "lean" else 1e-7, atol=1e-9)
+    assert out.eq_err.max().item() <= 1e-8
+
+
+def test_large_n_warm_start_continues_the_iteration():
+    """K1L: 5 iterations, then a warm start from (coeffs, multipliers) for 5 more, equals 10 straight
+    iterations; `want_prev` returns the 9-iteration coefficients."""
+    doc, sf, cfg, props = _setup(40, 20, 6, 3, 10, "lean")
+    xb = torch.from_numpy(props).cuda()
+    from dataclasses import replace
+    full = sf.solve_batched(xb, config=cfg, want_prev=True)
+    five = sf.solve_batched(xb, config=replace(cfg, max_iters=5))
+    cont = sf.solve_batched(xb, xi0=five.coeffs, lam0=five.multipliers, config=replace(cfg, max_iters=5))
+    nine = sf.solve_batched(xb, config=replace(cfg, max_iters=9))
+    scale = full.coeffs.abs().max().item()
+    assert (cont.coeffs - full.coeffs).abs().max().item() <= 1e-12 * scale
+    assert (cont.multipliers - full.multipliers).abs().max().item() <= 1e-12 * max(full.multipliers.abs().max().item(), 1e-12)
+    assert torch.equal(full.coeffs_prev, nine.coeffs)
+
+
+def test_large_n_verdict_and_svars_match_oracle():
+    """Windowed verdict (K2) and svars (K2b) at 40 robots, H=50: margins and counts as the oracle's
+    check, spherical variables as the reference formula on the same positions."""
+    from paper_2501_19042_b200.verdict import verdict_batched
+    doc, sf, cfg, props = _setup(40, 50, 7, 2, 15, "lean")
+    out = sf.solve_batched(torch.from_numpy(props).cuda(), config=cfg)
+    op = sf_oracle.make_problem(doc, degree=10)
+    v = {k: t.cpu().numpy() for k, t in verdict_batched(sf.operator, out.coeffs, None, 1e-3).items()}
+    svs = sf.svars_of(out.coeffs)
+    C = out.coeffs.cpu().numpy()
+    for b in range(C.shape[0]):
+        ref = sf_oracle.check_constraints(op, C[b], 1e-3)
+        assert bool(v["ok"][b]) == ref.ok
+        assert v["pair_viol"][b] == ref.pair_violation_count and v["ws_viol"][b] == ref.workspace_violation_count
+        assert abs(v["pair_margin_min"][b] - ref.pair_margin_min) <= 1e-12 * max(1.0, abs(ref.pair_margin_min))
+        assert abs(v["ws_margin_max"][b] - ref.workspace_margin_max) <= 1e-12 * max(1.0, abs(ref.workspace_margin_max))
+        pos = sf_oracle.positions(op, C[b].reshape(3, op.n, op.m1))
+        d = sf_oracle.pair_diffs(op, pos)
+        pa, pp, pr, *_ = sf_oracle.spherical_project(d[0].ravel(), d[1].ravel(), d[2].ravel(), op.lat, op.vert,
+                                                     1.0, np.inf)
+        np.testing.assert_allclose(svs[b].pair_radial.ravel(), pr, rtol=1e-12, atol=1e-14)
+        np.testing.assert_allclose(np.cos(svs[b].pair_polar.ravel()), np.cos(pp), rtol=0, atol=1e-12)
