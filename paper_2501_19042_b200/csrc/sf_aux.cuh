@@ -59,11 +59,18 @@ __global__ void verdict_kernel(AuxParams a, int batch, const double* __restrict_
     double* red_max = red_min + blockDim.x;
     int* red_pc = (int*)(red_max + blockDim.x);
     int* red_wc = red_pc + blockDim.x;
+    int* ptab = red_wc + blockDim.x;             // pair -> i | j << 8 (lexicographic)
     const int b = blockIdx.x;
     if (b >= batch) return;
     for (int e = threadIdx.x; e < dim; e += blockDim.x) C[e] = coeffs[(size_t)b * dim + e];
+    for (int q = threadIdx.x; q < P; q += blockDim.x) {
+        int i, j;
+        pair_of(q, n, i, j);
+        ptab[q] = i | (j << 8);
+    }
     const double ia2 = a.lat * a.lat, ib2 = a.vert * a.vert;
     const double wa2 = a.ws_lat * a.ws_lat, wb2 = a.ws_vert * a.ws_vert;
+    const double inv_ia2 = 1.0 / ia2, inv_ib2 = 1.0 / ib2, inv_wa2 = 1.0 / wa2, inv_wb2 = 1.0 / wb2;
     double pmin = CUDART_INF, wmax = -CUDART_INF;
     int pc = 0, wc = 0;
     for (int t0 = 0; t0 < S; t0 += AUX_TCH) {
@@ -74,12 +81,12 @@ __global__ void verdict_kernel(AuxParams a, int batch, const double* __restrict_
             pos[row * AUX_TCH + t] = eval_pos(C + row * m1, a.W + (t0 + t) * m1, m1);
         }
         __syncthreads();
-        for (int e = threadIdx.x; e < (P + n) * tc; e += blockDim.x) {
-            const int term = e / tc, t = e - term * tc;
+        for (int e = threadIdx.x; e < (P + n) * AUX_TCH; e += blockDim.x) {
+            const int term = e / AUX_TCH, t = e - term * AUX_TCH;   // t = lane: a warp takes one term
+            if (t >= tc) continue;
             double dx, dy, dz, a2, b2;
             if (term < P) {
-                int i, j;
-                pair_of(term, n, i, j);
+                const int ij = ptab[term], i = ij & 0xff, j = ij >> 8;
                 dx = pos[(0 * n + i) * AUX_TCH + t] - pos[(0 * n + j) * AUX_TCH + t];
                 dy = pos[(1 * n + i) * AUX_TCH + t] - pos[(1 * n + j) * AUX_TCH + t];
                 dz = pos[(2 * n + i) * AUX_TCH + t] - pos[(2 * n + j) * AUX_TCH + t];
@@ -93,14 +100,22 @@ __global__ void verdict_kernel(AuxParams a, int batch, const double* __restrict_
                 a2 = wa2;
                 b2 = wb2;
             }
-            const double m = __dadd_rn(__dadd_rn(__ddiv_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), a2),
-                                                 __ddiv_rn(__dmul_rn(dz, dz), b2)), -1.0);
+            // the reference margin, with its divisions (exact), is needed only near a decision: the
+            // reciprocal form differs from it by a few ulps of |q|, far below the slack
+            auto exact = [&]() {
+                return __dadd_rn(__dadd_rn(__ddiv_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), a2),
+                                           __ddiv_rn(__dmul_rn(dz, dz), b2)), -1.0);
+            };
+            const double ma = fma(dz * dz, term < P ? inv_ib2 : inv_wb2, (dx * dx + dy * dy) * (term < P ? inv_ia2 : inv_wa2)) - 1.0;
+            const double slack = 1e-12 * (1.0 + fabs(ma));
             if (term < P) {
-                pmin = fmin(pmin, m);
-                pc += (m < -tol);
+                if (ma < pmin + slack) pmin = fmin(pmin, exact());
+                if (ma < -tol - slack) ++pc;
+                else if (ma <= -tol + slack) pc += (exact() < -tol);
             } else {
-                wmax = fmax(wmax, m);
-                wc += (m > tol);
+                if (ma > wmax - slack) wmax = fmax(wmax, exact());
+                if (ma > tol + slack) ++wc;
+                else if (ma >= tol - slack) wc += (exact() > tol);
             }
         }
     }
