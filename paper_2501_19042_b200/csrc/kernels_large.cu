@@ -29,6 +29,16 @@ static int launch_large_t(const LaunchInfo& li, SolveParams& p, const sgsf_confi
     e = cudaGetLastError();
     if (e != cudaSuccess) return internal_fail(SGSF_ERR_CUDA, std::string("sf_large launch: ") + cudaGetErrorString(e));
     if (timing && timing->stop) cudaEventRecord((cudaEvent_t)timing->stop, stream);
+#ifdef SGSF_COUNTERS
+    {
+        unsigned long long c[8];
+        cudaStreamSynchronize(stream);
+        cudaMemcpyFromSymbol(c, g_sgsf_counts, sizeof(c));
+        printf("COUNTS(K1L) exact_steps %llu quiet_steps %llu\n", c[5], c[6]);
+        const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        cudaMemcpyToSymbol(g_sgsf_counts, z, sizeof(z));
+    }
+#endif
     return SGSF_OK;
 }
 

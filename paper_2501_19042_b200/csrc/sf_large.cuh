@@ -14,10 +14,14 @@
 // (deterministic; each pair is evaluated by both of its robots, its exit
 // residual counted once).  Terms are evaluated exactly (interior test,
 // trig-free target for non-interior terms, FP64 reference trig for terms with
-// an exactly-zero component), except that a step whose pairs were all
-// interior at its last exact pass and provably still are (motion bound
-// rmin - cum > 1 + margin, as K1) skips the O(n^2) pair loop: its pair exit
-// residuals are then the O(n) statistics of the position change.
+// an exactly-zero component) on a step's "exact pass", which also records the
+// step's near pairs (distance < 1.5, up to kNearCap, in a fixed ballot order)
+// and the min distance rmin of the others.  While rmin - cum > 1 + margin
+// (cum: accumulated pair motion, as K1) the far pairs are provably interior,
+// so the step is "quiet": only its near pairs are evaluated exactly, by the
+// lanes owning their robots, and the far pairs' exit residuals come from the
+// O(n) statistics of the position change minus the near pairs' share (the
+// far max is recomputed exactly if a near pair attains the statistic's max).
 // g = R W accumulates per lane for the active robot rows and is combined
 // across warps in warp order (ticket), so the FP sum order is fixed.
 // The FP64 xi-step, equality check and commit are K1's DMMA formulation,
@@ -29,6 +33,8 @@
 namespace sgsf {
 
 constexpr int kLargeWarps = 8;
+constexpr int kNearCap = 48;         // near pairs remembered per time step (more: the step stays exact)
+constexpr float kLargeSkin = 1.5f;   // near: normalised distance < kLargeSkin at the last exact pass
 
 struct LargeShared {
     int sample;
@@ -38,7 +44,7 @@ struct LargeShared {
 
 struct LargeLayout {
     size_t W, KMm, KMd, cconst, B6, rhs, PBt;
-    size_t C, Cp, lam, U, xb, g, Cf, Cfo, scr, winf, wsq, eqerr, srmin, scum, sflag, sh;
+    size_t C, Cp, lam, U, xb, g, Cf, Cfo, scr, winf, wsq, eqerr, srmin, scum, sflag, snear, sncnt, sh;
     size_t total;
 };
 
@@ -69,7 +75,9 @@ __host__ __device__ inline LargeLayout make_large_layout(int n, int S, int MP, i
     L.eqerr = o;  o = align16(o + (size_t)4 * d);
     L.srmin = o;  o = align16(o + (size_t)S * ts);   // per step: min normalised pair distance at the last exact pass
     L.scum = o;   o = align16(o + (size_t)S * ts);   // ... pair motion bound accumulated since
-    L.sflag = o;  o = align16(o + (size_t)S * 4);    // ... 1: every pair interior, no zero component there
+    L.sflag = o;  o = align16(o + (size_t)S * 4);    // ... 1: no far pair had a zero component
+    L.snear = o;  o = align16(o + (size_t)S * kNearCap * 2);   // ... the near pairs (i | j << 8), i < j
+    L.sncnt = o;  o = align16(o + (size_t)S * 4);    // ... how many (-1: none recorded / overflow)
     L.sh = o;     o = align16(o + sizeof(LargeShared));
     L.total = o;
     return L;
@@ -141,6 +149,8 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
     T* srmin = (T*)(smem + L.srmin);
     T* scum = (T*)(smem + L.scum);
     int* sflag = (int*)(smem + L.sflag);
+    uint16_t* snear = (uint16_t*)(smem + L.snear);
+    int* sncnt = (int*)(smem + L.sncnt);
     LargeShared* sh = (LargeShared*)(smem + L.sh);
 
     // shared constants (as K1), zero-padded to MP columns
@@ -175,6 +185,8 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
     const T cen[3] = {(T)p.cx, (T)p.cy, (T)p.cz};
     const double inv_n = 1.0 / n;
     const T inv_lat = T(1) / fp.lat;
+    const T skin_lim = T(kLargeSkin * kLargeSkin) * fp.lim;
+    const unsigned lanemask_lt = (1u << lane) - 1u;
     T* sn = (T*)(smem + L.scr) + warp * 2 * 3 * NB;   // this warp's positions at the step: new [3][NB] ...
     T* so = sn + 3 * NB;                              // ... and old [3][NB]
     int sample = sh->sample;
@@ -227,7 +239,10 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
                 Cfo[(ax * MP + q) * NB + i] = (T)c[q];   // no previous iterate: "old" := "new"
             }
         }
-        for (int t = tid; t < S; t += nt) sflag[t] = 0;   // the first iterate takes the exact pass everywhere
+        for (int t = tid; t < S; t += nt) {   // the first iterate takes the exact pass everywhere
+            sflag[t] = 0;
+            sncnt[t] = -1;
+        }
         if (tid == 0) sh->g_ticket = 0;
         __syncthreads();
 
@@ -306,26 +321,29 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
                     }
                 }
                 const T cum_t = scum[t] + T(2) * sqrt(dmv) * inv_lat;
-                const bool quiet = k > 0 && sflag[t] != 0 && srmin[t] - cum_t > T(1) + T(1e-3);
-                if (quiet && lane == 0) {
-                    scum[t] = cum_t;
-#pragma unroll
-                    for (int a = 0; a < 3; ++a) {
-                        linf = fmax(linf, hi[a] - lo[a]);
-                        lsq += (double)fmax(fma_t<T>((T)n, s2[a], -s1[a] * s1[a]), T(0));
-                    }
-                }
-                T qmin = T(1e30);   // exact pass: min q over this lane's pairs, non-interior / zero seen
-                bool nonint = false;
+                const int ncnt = sncnt[t];
+                // quiet: the far pairs (distance >= rmin >= skin at the last exact pass, no zero component
+                // there) are provably interior now and were before; the near pairs are evaluated exactly
+                const bool quiet = k > 0 && ncnt >= 0 && sflag[t] != 0 && srmin[t] - cum_t > T(1) + T(1e-3);
+                if (lane == 0) SGSF_COUNT(quiet ? 6 : 5, 1);   // diagnostics: quiet / exact steps
+                const uint16_t* nl = snear + (size_t)t * kNearCap;
+                T farmin = T(1e30);    // exact pass: min q over the far pairs of this lane's robots
+                bool zfar = false;     // ... a zero component in a far pair
+                int nbase = 0;         // ... near pairs recorded so far (warp-uniform)
+                T nq_sq = T(0), nq_max = T(0);   // quiet: near pairs' share of the O(n) statistics
+                uint64_t nmask[2] = {0ull, 0ull};  // quiet: near partners of this lane's robots
 #pragma unroll
                 for (int rr = 0; rr < 2; ++rr) {
                     const int i = lane + 32 * rr;
-                    if (i >= n) continue;
+                    const bool iv = i < n;
                     T Ri[3] = {T(0), T(0), T(0)};
-                    const T ni[3] = {sn[i], sn[NB + i], sn[2 * NB + i]};
-                    const T oi[3] = {so[i], so[NB + i], so[2 * NB + i]};
-                    for (int j = 0; j < (quiet ? 0 : n); ++j) {
-                        if (j == i) continue;
+                    T ni[3], oi[3];
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) {
+                        ni[a] = sn[a * NB + i];
+                        oi[a] = so[a * NB + i];
+                    }
+                    auto pair_exact = [&](int j, bool count_exit) {   // the pair (i, j), exactly
                         const bool fwd = i < j;   // the pair is (min, max): d = p_min - p_max
                         T dn[3], dd[3], r[3], x[3];
 #pragma unroll
@@ -335,20 +353,58 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
                             dd[a] = fwd ? oi[a] - oj : oj - oi[a];
                         }
                         exact_term<T, true>(dn, dd, fp, r, x);
-                        const T qn = fma_t<T>(dn[2] * fp.beta, dn[2], fma_t<T>(dn[1], dn[1], dn[0] * dn[0]));
-                        qmin = fmin(qmin, qn);
-                        nonint = nonint || !(qn >= fp.lim) || dn[0] == T(0) || dn[1] == T(0) || dn[2] == T(0);
 #pragma unroll
                         for (int a = 0; a < 3; ++a) Ri[a] += fwd ? r[a] : -r[a];
-                        if (fwd) {
+                        if (fwd && count_exit) {
 #pragma unroll
                             for (int a = 0; a < 3; ++a) {
                                 linf = fmax(linf, fabs(x[a]));
                                 lsq = fma((double)x[a], (double)x[a], lsq);
                             }
                         }
+                        return fma_t<T>(dn[2] * fp.beta, dn[2], fma_t<T>(dn[1], dn[1], dn[0] * dn[0]));
+                    };
+                    if (quiet) {
+                        for (int e = 0; e < ncnt; ++e) {
+                            const int code = nl[e], pa = code & 0xff, pb = code >> 8;
+                            if (!iv || (pa != i && pb != i)) continue;
+                            const int j = pa == i ? pb : pa;
+                            nmask[rr] |= 1ull << j;
+                            pair_exact(j, true);
+                            if (i < j) {
+                                T m = T(0), q2 = T(0);
+#pragma unroll
+                                for (int a = 0; a < 3; ++a) {
+                                    const T xq = (ni[a] - oi[a]) - (sn[a * NB + j] - so[a * NB + j]);
+                                    m = fmax(m, fabs(xq));
+                                    q2 = fma_t<T>(xq, xq, q2);
+                                }
+                                nq_max = fmax(nq_max, m);
+                                nq_sq += q2;
+                            }
+                        }
+                    } else {
+                        for (int j = 0; j < n; ++j) {   // warp-uniform: the near list is built with ballots
+                            bool is_near = false;
+                            if (iv && j != i) {
+                                const T qn = pair_exact(j, true);
+                                const bool zero = (sn[j] == ni[0]) || (sn[NB + j] == ni[1]) || (sn[2 * NB + j] == ni[2]);
+                                if (qn < skin_lim) {
+                                    is_near = i < j;
+                                } else {
+                                    farmin = fmin(farmin, qn);
+                                    zfar = zfar || zero;
+                                }
+                            }
+                            const uint32_t bm = __ballot_sync(0xffffffffu, is_near);
+                            if (bm) {
+                                const int pos = nbase + __popc(bm & lanemask_lt);
+                                if (is_near && pos < kNearCap) snear[(size_t)t * kNearCap + pos] = (uint16_t)(i | (j << 8));
+                                nbase += __popc(bm);
+                            }
+                        }
                     }
-                    {   // workspace term of robot i
+                    if (iv) {   // workspace term of robot i
                         T dn[3], dd[3], r[3], x[3];
 #pragma unroll
                         for (int a = 0; a < 3; ++a) {
@@ -371,13 +427,46 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
                             for (int q = 0; q < MP; ++q) gacc[rr][a][q] = fma_t<T>(Ri[a], w[q], gacc[rr][a][q]);
                     }
                 }
-                if (!quiet) {   // refresh the step's motion-bound state from the exact pass
-                    const T qm = warp_min_nonneg(qmin);
-                    const bool ni = __any_sync(0xffffffffu, nonint);
+                if (quiet) {   // far pairs: the O(n) statistics without the near pairs' share
+                    T qinf_p = T(0), qsq_p = T(0);
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) {
+                        qinf_p = fmax(qinf_p, hi[a] - lo[a]);
+                        qsq_p += fmax(fma_t<T>((T)n, s2[a], -s1[a] * s1[a]), T(0));
+                    }
+                    const T nmax = warp_max_nonneg(nq_max);
+                    T nsq = nq_sq;
+#pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) nsq += __shfl_xor_sync(0xffffffffu, nsq, off);
+                    T far_max = qinf_p;
+                    if (nmax >= qinf_p) {   // a near pair attains the quiet max: the far max, exactly
+                        T fm = T(0);
+#pragma unroll
+                        for (int rr = 0; rr < 2; ++rr) {
+                            const int i = lane + 32 * rr;
+                            if (i >= n) continue;
+                            for (int j = i + 1; j < n; ++j) {
+                                if ((nmask[rr] >> j) & 1ull) continue;
+#pragma unroll
+                                for (int a = 0; a < 3; ++a)
+                                    fm = fmax(fm, fabs((sn[a * NB + i] - so[a * NB + i]) - (sn[a * NB + j] - so[a * NB + j])));
+                            }
+                        }
+                        far_max = warp_max_nonneg(fm);
+                    }
+                    if (lane == 0) {
+                        scum[t] = cum_t;
+                        linf = fmax(linf, far_max);
+                        lsq += (double)fmax(qsq_p - nsq, T(0));
+                    }
+                } else {   // refresh the step's state from the exact pass
+                    const T qm = warp_min_nonneg(farmin);
+                    const bool zf = __any_sync(0xffffffffu, zfar);
                     if (lane == 0) {
                         srmin[t] = sqrt(qm) * inv_lat;
                         scum[t] = T(0);
-                        sflag[t] = ni ? 0 : 1;
+                        sflag[t] = zf ? 0 : 1;
+                        sncnt[t] = nbase <= kNearCap ? nbase : -1;
                     }
                 }
                 __syncwarp();   // the scratch is rewritten for the next step

@@ -66,3 +66,19 @@ def test_config4_properties():
     assert np.all((last <= 1e-3) == conv)
     alt = sf.solve_batched(xb[:64], config=cfg, grid=7)
     assert torch.equal(alt.coeffs, out.coeffs[:64]) and torch.equal(alt.iterations, out.iterations[:64])
+
+
+def test_large_n_long_run_matches_oracle():
+    """60 iterations at 40 robots: long enough for K1L's quiet steps (near list + motion bound) to carry
+    most of the pass, against the oracle's plain every-term evaluation."""
+    doc, sf, cfg, props = _setup(40, 30, 9, 2, 60, "lean")
+    out = sf.solve_batched(torch.from_numpy(props).cuda(), config=cfg)
+    op = sf_oracle.make_problem(doc, degree=10)
+    coeffs = out.coeffs.cpu().numpy()
+    rinf = out.residual_inf.cpu().numpy()
+    rl2 = out.residual_l2.cpu().numpy()
+    for b, x in enumerate(props):
+        r = sf_oracle.solve(op, x, max_iters=60, early_stop=False)
+        assert np.abs(coeffs[b] - r.coeffs).max() <= 1e-5 * np.abs(r.coeffs).max(), b
+        np.testing.assert_allclose(rinf[b], r.residual_inf, rtol=1e-3, atol=1e-9)
+        np.testing.assert_allclose(rl2[b], r.residual_l2, rtol=1e-3, atol=1e-9)
