@@ -165,6 +165,15 @@ int sgsf_apply_FT(sgsf_handle_t* h, int batch, const double* v, double* out, voi
 /* literal coefficient step from eta (3 x n x m1 per sample): C_i = Km11 eta_bar + Kd11 (eta_i - eta_bar) + cconst_i */
 int sgsf_kkt_step(sgsf_handle_t* h, int batch, const double* eta, double* out, double* eq_err, void* stream);
 
+/*
+ * Mean pairwise cosine of `count` vectors of length `dim` (device, row-major), optionally centred by the
+ * column mean (metrics.mean_pairwise_cosine / diversity_cosine, metrics.py:83-115).  NaN if a (centred)
+ * vector is zero.  work: sgsf_cosine_work_doubles(count, dim) doubles (device); result: 1 double (device).
+ */
+size_t sgsf_cosine_work_doubles(int count, int dim);
+int sgsf_pairwise_cosine(int count, int dim, const double* vectors, int center, double* work, double* result,
+                         void* stream);
+
 /* FP32 FFMA throughput microbenchmark (roofline denominator); returns TFLOP/s in *tflops */
 int sgsf_fp32_peak(double* tflops, double* ms, void* stream);
 

@@ -368,3 +368,25 @@ def check_constraints(prob: OracleProblem, coeffs, tol: float = 1e-3) -> OracleV
 def feasible(prob: OracleProblem, res: OracleResult, tol: float = 1e-3) -> bool:
     """converged and passes the original constraints (metrics.py:57-69)."""
     return bool(res.converged and res.coeffs is not None and check_constraints(prob, res.coeffs, tol).ok)
+
+
+def mean_pairwise_cosine(vectors) -> float:
+    """Mean cosine over all unordered pairs, the reference's Gram-matrix formula (metrics.py:83-99)."""
+    V = np.asarray(vectors, dtype=float)
+    if V.ndim != 2:
+        V = V.reshape(len(V), -1)
+    norms = np.linalg.norm(V, axis=1)
+    if np.any(norms == 0.0):
+        return float("nan")
+    U = V / norms[:, None]
+    G = U @ U.T
+    idx = np.triu_indices(V.shape[0], k=1)
+    return float(G[idx].mean())
+
+
+def diversity_cosine(position_sets, center: bool = True) -> float:
+    """metrics.py:102-115 on a list of (n, S, 3) position arrays."""
+    V = np.stack([np.asarray(p, dtype=float).ravel() for p in position_sets])
+    if center:
+        V = V - V.mean(axis=0)
+    return mean_pairwise_cosine(V)

@@ -60,6 +60,18 @@ from .solver import (
     spherical_step,
     write_residuals_csv,
 )
+from .metrics import (
+    DIVERSITY_DEFINITION,
+    BatchReport,
+    build_batch_report,
+    build_spherical_rhs,
+    diversity_cosine,
+    mean_pairwise_cosine,
+    primal_residual,
+    save_report_json,
+    spherical_targets,
+    write_csv,
+)
 from .verdict import (
     ViolationReport,
     check_coefficients,

@@ -363,3 +363,78 @@ __global__ void ffma_peak_kernel(float* out, int iters, float seed) {
 }
 
 }  // namespace sgsf
+
+namespace sgsf {
+
+// ---------------------------------------------------------------- pairwise cosine / diversity (metrics.py:83-115)
+// mean over i < j of cos(v_i, v_j) with v optionally centred by the column mean.  With u_i = v_i / |v_i|:
+//   sum_{i<j} u_i . u_j = (|sum_i u_i|^2 - sum_i |u_i|^2) / 2,
+// so the mean is an O(count * dim) reduction instead of a count x count Gram matrix.  All sums run in a
+// fixed order (deterministic).
+constexpr int COS_THREADS = 256;
+
+__device__ __forceinline__ double block_sum_fixed(double v, double* red) {
+    red[threadIdx.x] = v;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    const double r = red[0];
+    __syncthreads();
+    return r;
+}
+
+__global__ void cos_colmean_kernel(int count, int dim, const double* __restrict__ V, double* mean) {
+    const int d = blockIdx.x * blockDim.x + threadIdx.x;
+    if (d >= dim) return;
+    double s = 0.0;
+    for (int b = 0; b < count; ++b) s += V[(size_t)b * dim + d];
+    mean[d] = s / count;
+}
+
+__global__ void cos_rownorm_kernel(int count, int dim, const double* __restrict__ V, const double* __restrict__ mean,
+                                   double* inv, double* u2, int* zero) {
+    __shared__ double red[COS_THREADS];
+    const int b = blockIdx.x;
+    double s = 0.0;
+    for (int d = threadIdx.x; d < dim; d += blockDim.x) {
+        const double x = V[(size_t)b * dim + d] - (mean ? mean[d] : 0.0);
+        s = fma(x, x, s);
+    }
+    const double n2 = block_sum_fixed(s, red);
+    if (threadIdx.x == 0) {
+        if (n2 == 0.0) {
+            atomicOr(zero, 1);
+            inv[b] = 0.0;
+            u2[b] = 0.0;
+        } else {
+            const double iv = 1.0 / sqrt(n2);
+            inv[b] = iv;
+            u2[b] = n2 * iv * iv;
+        }
+    }
+}
+
+__global__ void cos_colsum_kernel(int count, int dim, const double* __restrict__ V, const double* __restrict__ mean,
+                                  const double* __restrict__ inv, double* ssum) {
+    const int d = blockIdx.x * blockDim.x + threadIdx.x;
+    if (d >= dim) return;
+    const double m = mean ? mean[d] : 0.0;
+    double s = 0.0;
+    for (int b = 0; b < count; ++b) s = fma(V[(size_t)b * dim + d] - m, inv[b], s);
+    ssum[d] = s;
+}
+
+__global__ void cos_final_kernel(int count, int dim, const double* __restrict__ ssum, const double* __restrict__ u2,
+                                 const int* __restrict__ zero, double* out) {
+    __shared__ double red[COS_THREADS];
+    double a = 0.0, c = 0.0;
+    for (int d = threadIdx.x; d < dim; d += blockDim.x) a = fma(ssum[d], ssum[d], a);
+    for (int b = threadIdx.x; b < count; b += blockDim.x) c += u2[b];
+    const double s2 = block_sum_fixed(a, red);
+    const double uu = block_sum_fixed(c, red);
+    if (threadIdx.x == 0) out[0] = *zero ? CUDART_NAN : (s2 - uu) / ((double)count * (count - 1));
+}
+
+}  // namespace sgsf

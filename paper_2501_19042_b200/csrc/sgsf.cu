@@ -407,6 +407,34 @@ int sgsf_solve_host(sgsf_handle_t* h, int batch, const double* xi_bar, const dou
     return rc;
 }
 
+size_t sgsf_cosine_work_doubles(int count, int dim) {
+    return 2 * (size_t)(dim > 0 ? dim : 0) + 2 * (size_t)(count > 0 ? count : 0) + 2;
+}
+
+int sgsf_pairwise_cosine(int count, int dim, const double* vectors, int center, double* work, double* result,
+                         void* stream_) {
+    if (count < 2 || dim < 1 || !vectors || !work || !result)
+        return fail(SGSF_ERR_INVALID, "pairwise cosine needs >= 2 vectors of length >= 1 and buffers");
+    cudaStream_t stream = (cudaStream_t)stream_;
+    double* mean = work;
+    double* ssum = mean + dim;
+    double* inv = ssum + dim;
+    double* u2 = inv + count;
+    int* zero = (int*)(u2 + count);
+    CUDA_TRY(cudaMemsetAsync(zero, 0, sizeof(int), stream));
+    const int blocks = (dim + COS_THREADS - 1) / COS_THREADS;
+    if (center) {
+        cos_colmean_kernel<<<blocks, COS_THREADS, 0, stream>>>(count, dim, vectors, mean);
+        internal_count_launch(1);
+    }
+    cos_rownorm_kernel<<<count, COS_THREADS, 0, stream>>>(count, dim, vectors, center ? mean : nullptr, inv, u2, zero);
+    cos_colsum_kernel<<<blocks, COS_THREADS, 0, stream>>>(count, dim, vectors, center ? mean : nullptr, inv, ssum);
+    cos_final_kernel<<<1, COS_THREADS, 0, stream>>>(count, dim, ssum, u2, zero, result);
+    internal_count_launch(3);
+    CUDA_TRY(cudaGetLastError());
+    return SGSF_OK;
+}
+
 int sgsf_fp32_peak(double* tflops, double* ms, void* stream_) {
     cudaStream_t stream = (cudaStream_t)stream_;
     int dev = 0, sms = 0;
