@@ -63,6 +63,8 @@ from .solver import (
 from .metrics import (
     DIVERSITY_DEFINITION,
     BatchReport,
+    BenchmarkGrid,
+    benchmark,
     build_batch_report,
     build_spherical_rhs,
     diversity_cosine,

@@ -14,6 +14,7 @@ from __future__ import annotations
 import csv
 import json
 from dataclasses import dataclass, field
+from pathlib import Path
 
 import numpy as np
 import torch
@@ -167,3 +168,120 @@ def save_report_json(report: BatchReport, path, metadata: dict | None = None) ->
     with open(path, "w") as fh:
         json.dump(doc, fh, indent=2)
         fh.write("\n")
+
+
+# ------------------------------------------------------------------ benchmark sweeps (metrics.py:188-395)
+@dataclass(frozen=True)
+class BenchmarkGrid:
+    """Axes of the benchmark sweeps (fig5a/5b: batch sizes; fig6: batch sizes and iteration counts;
+    fig7: init strategies)."""
+
+    batch_sizes: tuple = (1, 10, 50)
+    iteration_counts: tuple = (50, 100, 200, 400)
+    strategies: tuple = ("zero", "projected", "warmstart")
+    timing_batch: int = 10
+    trace_iters: int = 200
+    seed: int = 0
+    spread: float = 0.25
+
+    def __post_init__(self):
+        unknown = sorted(set(self.strategies) - {"zero", "projected", "warmstart"})
+        if unknown:
+            raise ValueError(f"unknown init strategies {unknown}; choose from ['projected', 'warmstart', 'zero']")
+        if not self.batch_sizes or min(self.batch_sizes) < 1:
+            raise ValueError(f"batch sizes must be >= 1, got {self.batch_sizes}")
+        if not self.iteration_counts or min(self.iteration_counts) < 1:
+            raise ValueError(f"iteration counts must be >= 1, got {self.iteration_counts}")
+
+
+_PLOTS = {
+    "fig5a": ("feasible fraction vs batch size",
+              "set xlabel 'batch size'\nset ylabel 'feasible fraction'\nset yrange [0:1.05]\n"
+              "plot 'fig5a.csv' using 2:3 with linespoints title 'feasible fraction'\n"),
+    "fig5b": ("mean pairwise cosine of feasible solutions",
+              "set xlabel 'row'\nset ylabel 'mean pairwise cosine'\n"
+              "plot 'fig5b.csv' using 0:2 with linespoints title 'cosine'\n"),
+    "fig6": ("wall-clock time scaling",
+             "set xlabel 'iterations'\nset ylabel 'seconds'\n"
+             "plot 'fig6.csv' using 2:3 with linespoints title 'batch time'\n"),
+    "fig7": ("residual vs iteration per init strategy",
+             "set xlabel 'iteration'\nset ylabel 'inf-norm residual'\nset logscale y\n"
+             "plot for [s in strategies] 'fig7.csv' using (strcol(1) eq s ? $2 : 1/0):3 with lines title s\n"),
+}
+
+
+def _fmt(x) -> str:
+    return "nan" if x is None else repr(float(x))
+
+
+def _gnuplot(out_dir: Path, name: str, strategies=None) -> Path:
+    title, body = _PLOTS[name]
+    head = ["#!/usr/bin/env gnuplot", "set datafile separator ','", "set datafile commentschars '#'",
+            "set key autotitle columnhead", f"set title '{title}'", "set terminal pngcairo size 800,600",
+            f"set output '{name}.png'"]
+    if name == "fig7" and strategies is not None:
+        head.append(f"strategies = '{' '.join(strategies)}'")
+    path = out_dir / f"{name}.gp"
+    path.write_text("\n".join(head + [body]))
+    return path
+
+
+def benchmark(problem, grid: BenchmarkGrid, out_dir, config=None, degree: int = 10, threads: int = 1,
+              metadata: dict | None = None, tol_check: float = 1e-3) -> dict:
+    """The reference's three sweeps (metrics.py:266-389), on the device solver: feasibility and diversity
+    vs batch size (fig5a, fig5b), wall clock vs batch size and iteration count with early stop off (fig6),
+    and the residual trace of one proposal per init strategy (fig7).  Returns the output paths."""
+    import time
+    from dataclasses import replace
+
+    from .proposals import WarmStart, sample_proposals
+    from .solver import SafetyFilter, SolverConfig
+
+    out_dir = Path(out_dir)
+    out_dir.mkdir(parents=True, exist_ok=True)
+    cfg = config if config is not None else SolverConfig()
+    sf = SafetyFilter(problem, degree=degree, config=cfg)
+    meta = dict(metadata or {})
+    meta.setdefault("seed", grid.seed)
+    meta.setdefault("diversity_definition", DIVERSITY_DEFINITION)
+    props_of = lambda count: sample_proposals(problem, sf.basis, count, seed=grid.seed, spread=grid.spread).proposals
+    paths = {}
+
+    rows_a, rows_b = [], []
+    for batch_size in grid.batch_sizes:
+        report = build_batch_report(sf.batch_solve(props_of(batch_size), threads=threads), problem, tol=tol_check)
+        rows_a.append([problem.n, batch_size, _fmt(report.feasible_fraction)])
+        rows_b.append([problem.n, _fmt(report.mean_pairwise_cosine)])
+    paths["fig5a"], paths["fig5b"] = out_dir / "fig5a.csv", out_dir / "fig5b.csv"
+    write_csv(paths["fig5a"], meta, ["n", "batch", "feasible_fraction"], rows_a)
+    write_csv(paths["fig5b"], meta, ["n", "mean_pairwise_cosine"], rows_b)
+
+    fixed = replace(cfg, early_stop=False)
+    rows_6 = []
+    timed = [(b, props_of(b), fixed) for b in grid.batch_sizes]
+    timed += [(grid.timing_batch, props_of(grid.timing_batch), replace(fixed, max_iters=it))
+              for it in grid.iteration_counts]
+    for batch_size, props, c in timed:
+        t0 = time.perf_counter()
+        sf.batch_solve(props, threads=threads, config=c)
+        dt = time.perf_counter() - t0
+        rows_6.append([batch_size, c.max_iters, _fmt(dt), _fmt(dt / batch_size)])
+    paths["fig6"] = out_dir / "fig6.csv"
+    write_csv(paths["fig6"], meta, ["batch", "iters", "seconds", "seconds_per_proposal"], rows_6)
+
+    proposal = props_of(1)[0]
+    trace = replace(fixed, max_iters=grid.trace_iters)
+    inits = {"zero": (np.zeros(proposal.size), np.zeros(proposal.size)), "projected": None}
+    if "warmstart" in grid.strategies:
+        prior = sf.solve(proposal, config=trace)
+        inits["warmstart"] = WarmStart(xi0=prior.coeffs, lambda0=prior.multipliers)
+    rows_7 = []
+    for strategy in grid.strategies:
+        res = sf.solve(proposal, init=inits[strategy], config=trace)
+        rows_7 += [[strategy, k + 1, _fmt(float(res.residual_inf[k]))] for k in range(res.iterations)]
+    paths["fig7"] = out_dir / "fig7.csv"
+    write_csv(paths["fig7"], meta, ["strategy", "iter", "res_inf"], rows_7)
+
+    for name in ("fig5a", "fig5b", "fig6", "fig7"):
+        paths[f"{name}_plot"] = _gnuplot(out_dir, name, grid.strategies if name == "fig7" else None)
+    return paths

@@ -105,3 +105,23 @@ def test_batch_report_and_writers(tmp_path):
     assert doc["metadata"] == {"seed": 2} and doc["report"]["diversity_definition"].startswith("centered")
     write_csv(tmp_path / "x.csv", {"k": 1}, ["a", "b"], [[1, 2], [3, 4]])
     assert (tmp_path / "x.csv").read_text().splitlines() == ["# k=1", "a,b", "1,2", "3,4"]
+
+
+def test_benchmark_sweep_outputs(tmp_path):
+    """metrics.benchmark (test_metrics.py:230-): the four CSVs and plot scripts, deterministic fig5 rows,
+    one fig7 trace per strategy."""
+    import csv as _csv
+    from paper_2501_19042_b200 import BenchmarkGrid, SolverConfig, benchmark
+    from paper_2501_19042_b200.scenarios import config_problem
+    prob = config_problem(1)
+    grid = BenchmarkGrid(batch_sizes=(2, 4), iteration_counts=(5, 10), timing_batch=2, trace_iters=20)
+    paths = benchmark(prob, grid, tmp_path, config=SolverConfig(max_iters=100))
+    for name in ("fig5a", "fig5b", "fig6", "fig7"):
+        assert paths[name].exists() and paths[f"{name}_plot"].exists()
+    rows = [r for r in _csv.reader(open(paths["fig7"])) if r and not r[0].startswith("#")]
+    assert rows[0] == ["strategy", "iter", "res_inf"]
+    assert {r[0] for r in rows[1:]} == {"zero", "projected", "warmstart"}
+    again = benchmark(prob, grid, tmp_path / "b", config=SolverConfig(max_iters=100))
+    assert open(paths["fig5a"]).read() == open(again["fig5a"]).read()
+    with pytest.raises(ValueError):
+        BenchmarkGrid(strategies=("bogus",))
