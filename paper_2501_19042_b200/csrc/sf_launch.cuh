@@ -82,8 +82,8 @@ int launch_persistent(const LaunchInfo& li, SolveParams& p, const sgsf_config_t*
         unsigned long long c[8];
         cudaStreamSynchronize(stream);
         cudaMemcpyFromSymbol(c, g_sgsf_counts, sizeof(c));
-        printf("COUNTS finish %llu flagged %llu exact %llu careful %llu flagged_terms %llu near_checks %llu scans %llu\n",
-               c[0], c[1], c[2], c[3], c[4], c[5], c[6]);
+        printf("COUNTS finish %llu flagged %llu exact %llu careful %llu flagged_terms %llu near_checks %llu scans %llu exact_f1 %llu\n",
+               c[0], c[1], c[2], c[3], c[4], c[5], c[6], c[7]);
         const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         cudaMemcpyToSymbol(g_sgsf_counts, z, sizeof(z));
     }

@@ -557,6 +557,28 @@ template <int NB> __device__ __forceinline__ void term_robots(const int* __restr
     }
 }
 
+// insertion of (v, i) into a descending three-deep selection (registers: compile-time indices only)
+template <typename T> __device__ __forceinline__ void top3_insert(T (&t)[3], int (&ti)[3], T v, int i) {
+    if (v > t[2]) {
+        if (v > t[1]) {
+            t[2] = t[1];
+            ti[2] = ti[1];
+            if (v > t[0]) {
+                t[1] = t[0];
+                ti[1] = ti[0];
+                t[0] = v;
+                ti[0] = i;
+            } else {
+                t[1] = v;
+                ti[1] = i;
+            }
+        } else {
+            t[2] = v;
+            ti[2] = i;
+        }
+    }
+}
+
 template <typename T, int NB>
 __device__ __forceinline__ StepOut<T> flagged_path(const T* __restrict__ Pnew, T* __restrict__ Pold, int n,
                                                    const int* __restrict__ ptab, const Family<T>& fp,
@@ -619,30 +641,88 @@ __device__ __forceinline__ StepOut<T> flagged_path(const T* __restrict__ Pnew, T
     // the unflagged max is <= qinf; it matters only when the flagged terms' true max stays below qinf
     if (need_exact && flmax < qinf) {   // exact max of |x| over the unflagged terms (needs the old row)
         SGSF_COUNT(2, 1);
-        base = T(0);
-        int b = 0;
-#pragma unroll 1
-        for (int i = 0; i < NB; ++i) {
-#pragma unroll 1
-            for (int j = i + 1; j < NB; ++j, ++b) {
-                if (j < n && bit_of(nm.w, b) && bit_of(om.w, b)) {
-                    T m = T(0);
+        // F <= 2 flagged terms: on each axis the max over the unflagged pairs of dp_a - dp_b is attained with
+        // a among the F+1 largest and b among the F+1 smallest dp (were a outside them, the F+1 pairs
+        // (top_k, b) hold an unflagged one at least as large; then the same for b), and the workspace max
+        // among the F+1 largest |dp|: three-deep selections and a 3 x 3 candidate set.
+        int fb0 = -1, fb1 = -1, fcnt = 0;
 #pragma unroll
-                    for (int ax = 0; ax < 3; ++ax)
-                        m = fmax(m, fabs((Pnew[ax * NB + i] - Pold[ax * NB + i]) - (Pnew[ax * NB + j] - Pold[ax * NB + j])));
-                    base = fmax(base, m);
+        for (int w = 0; w < NWD; ++w) {
+            const uint32_t fl = ~(nm.w[w] & om.w[w]);
+            fcnt += __popc(fl);
+            if (fl) {
+                fb1 = fb0;
+                fb0 = w * 32 + __ffs(fl) - 1;
+                const uint32_t r = fl & (fl - 1);
+                if (r) fb1 = w * 32 + __ffs(r) - 1;
+            }
+        }
+        base = T(0);
+        if (fcnt <= 2) {
+            SGSF_COUNT(7, 1);
+#pragma unroll 1
+            for (int ax = 0; ax < 3; ++ax) {
+                T tv[3], bv[3], av[3];
+                int ti[3], bi[3], ai[3];
+#pragma unroll
+                for (int u = 0; u < 3; ++u) {
+                    tv[u] = T(-1e38);
+                    bv[u] = T(-1e38);   // negated values: the smallest dp as the largest -dp
+                    av[u] = T(-1);
+                    ti[u] = bi[u] = ai[u] = -1;
+                }
+#pragma unroll 1
+                for (int i = 0; i < n; ++i) {
+                    const T v = Pnew[ax * NB + i] - Pold[ax * NB + i];
+                    top3_insert(tv, ti, v, i);
+                    top3_insert(bv, bi, -v, i);
+                    top3_insert(av, ai, fabs(v), i);
+                }
+#pragma unroll
+                for (int u = 0; u < 3; ++u) {
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) {
+                        const int ia = ti[u], ib = bi[k];
+                        if (ia >= 0 && ib >= 0 && ia != ib) {
+                            const int pb = pair_bit<NB>(min(ia, ib), max(ia, ib));
+                            if (pb != fb0 && pb != fb1) base = fmax(base, tv[u] + bv[k]);
+                        }
+                    }
+                    if (ai[u] >= 0 && ws_bit<NB>(ai[u]) != fb0 && ws_bit<NB>(ai[u]) != fb1) base = fmax(base, av[u]);
                 }
             }
         }
+        auto full_max = [&]() {   // every unflagged term
+            T mx = T(0);
+            int b = 0;
 #pragma unroll 1
-        for (int i = 0; i < n; ++i) {
-            if (bit_of(nm.w, NP + i) && bit_of(om.w, NP + i)) {
-                T m = T(0);
+            for (int i = 0; i < NB; ++i) {
+#pragma unroll 1
+                for (int j = i + 1; j < NB; ++j, ++b) {
+                    if (j < n && bit_of(nm.w, b) && bit_of(om.w, b)) {
+                        T m = T(0);
 #pragma unroll
-                for (int ax = 0; ax < 3; ++ax) m = fmax(m, fabs(Pnew[ax * NB + i] - Pold[ax * NB + i]));
-                base = fmax(base, m);
+                        for (int ax = 0; ax < 3; ++ax)
+                            m = fmax(m, fabs((Pnew[ax * NB + i] - Pold[ax * NB + i]) - (Pnew[ax * NB + j] - Pold[ax * NB + j])));
+                        mx = fmax(mx, m);
+                    }
+                }
             }
-        }
+#pragma unroll 1
+            for (int i = 0; i < n; ++i) {
+                if (bit_of(nm.w, NP + i) && bit_of(om.w, NP + i)) {
+                    T m = T(0);
+#pragma unroll
+                    for (int ax = 0; ax < 3; ++ax) m = fmax(m, fabs(Pnew[ax * NB + i] - Pold[ax * NB + i]));
+                    mx = fmax(mx, m);
+                }
+            }
+            return mx;
+        };
+        if (fcnt > 2) base = full_max();
+#ifdef SGSF_CHECK_EXACT
+        else if (full_max() != base) printf("SGSF_CHECK_EXACT mismatch: F=%d fast %g full %g\n", fcnt, (double)base, (double)full_max());
+#endif
     }
     if (act_new) {
         // pass 2: the old row is dead now -- it becomes this thread's R row (d - e of the active terms)
