@@ -18,6 +18,9 @@
  *                                                                                  _speedups.pyx:18-73
  *   sgsf_apply_F / sgsf_apply_FT PairwiseOperator.apply / apply_transpose          assembly.py:285-310
  *   sgsf_kkt_step                KktFactorization.solve                            assembly.py:186-219
+ *   sgsf_unroll / _backward      K unrolled fixed-point steps and their reverse sweep: the differentiable
+ *                                SF of PAPER.md "Learned Initialization for SF" (eq. NN_loss); the step is
+ *                                the solve loop body solver.py:314-328 (the reference has no autodiff)
  */
 #ifndef SGSF_H
 #define SGSF_H
@@ -164,6 +167,19 @@ int sgsf_apply_F(sgsf_handle_t* h, int batch, const double* xi, double* out, voi
 int sgsf_apply_FT(sgsf_handle_t* h, int batch, const double* v, double* out, void* stream);
 /* literal coefficient step from eta (3 x n x m1 per sample): C_i = Km11 eta_bar + Kd11 (eta_i - eta_bar) + cconst_i */
 int sgsf_kkt_step(sgsf_handle_t* h, int batch, const double* eta, double* out, double* eq_err, void* stream);
+
+/*
+ * Differentiable SF (FP64).  sgsf_unroll runs `iters` fixed-point steps z_{k+1} = f(z_k), z = (xi, lambda),
+ * from (xi0, lam0) with no early stop, and writes every iterate: xs, ls are B x (iters + 1) x dim (device),
+ * row 0 = (xi0, lam0).  sgsf_unroll_backward is its vector-Jacobian product: given dL/dxs and dL/dls
+ * (either may be NULL = zero; same shape), it writes dL/dxi_bar, dL/dxi0, dL/dlam0 (B x dim) using the
+ * iterates xs of the forward.  Active terms use the Jacobian of the target d / r; interior terms the
+ * identity; a zero pair difference (target locally constant) a zero Jacobian.
+ */
+int sgsf_unroll(sgsf_handle_t* h, int batch, int iters, const double* xi_bar, const double* xi0,
+                const double* lam0, double* xs, double* ls, void* stream);
+int sgsf_unroll_backward(sgsf_handle_t* h, int batch, int iters, const double* xs, const double* gxs,
+                         const double* gls, double* g_xi_bar, double* g_xi0, double* g_lam0, void* stream);
 
 /*
  * Mean pairwise cosine of `count` vectors of length `dim` (device, row-major), optionally centred by the

@@ -74,6 +74,7 @@ from .metrics import (
     spherical_targets,
     write_csv,
 )
+from .unrolled import UnrolledIterates, boundary_projection, fixed_point_loss, unrolled_solve
 from .verdict import (
     ViolationReport,
     check_coefficients,

@@ -16,6 +16,7 @@
 
 #include "../../include/sgsf.h"
 #include "sf_aux.cuh"
+#include "sf_unroll.cuh"
 #include "sf_device.cuh"
 #include "sf_launch.cuh"
 #include "sf_persistent.cuh"
@@ -47,6 +48,7 @@ struct sgsf_handle_s {
     int n, S, m1, P;
     double rho, lat, vert, ws_lat, ws_vert, center[3];
     double *W, *Wd, *Wdd, *KMm, *KMd, *Km11, *Kd11, *cconst, *B6, *rhs, *PBt;
+    double *Mm, *Md, *G;   // plain m1 x m1 (unrolled solver)
     int device, sm_count;
 };
 
@@ -96,7 +98,8 @@ static int upload(double** dst, const double* src, size_t count) {
 
 void sgsf_destroy(sgsf_handle_t* h) {
     if (!h) return;
-    double* ptrs[] = {h->W, h->Wd, h->Wdd, h->KMm, h->KMd, h->Km11, h->Kd11, h->cconst, h->B6, h->rhs, h->PBt};
+    double* ptrs[] = {h->W,  h->Wd,  h->Wdd, h->KMm, h->KMd, h->Km11, h->Kd11,
+                      h->cconst, h->B6, h->rhs, h->PBt, h->Mm,  h->Md,  h->G};
     for (double* q : ptrs)
         if (q) cudaFree(q);
     delete h;
@@ -128,13 +131,19 @@ int sgsf_create(const sgsf_problem_t* pr, sgsf_handle_t** out) {
             kmd[q * 2 * m1 + q2] = pr->Md[q * m1 + q2];
             kmd[q * 2 * m1 + m1 + q2] = pr->Kd11[q * m1 + q2];
         }
+    std::vector<double> gram((size_t)m1 * m1, 0.0);   // G = W^T W
+    for (int q = 0; q < m1; ++q)
+        for (int q2 = 0; q2 < m1; ++q2)
+            for (int t = 0; t < S; ++t) gram[q * m1 + q2] += pr->W[t * m1 + q] * pr->W[t * m1 + q2];
     int rc = SGSF_OK;
     if ((rc = upload(&h->W, pr->W, (size_t)S * m1)) || (rc = upload(&h->Wd, pr->Wd, (size_t)S * m1)) ||
         (rc = upload(&h->Wdd, pr->Wdd, (size_t)S * m1)) || (rc = upload(&h->KMm, kmm.data(), kmm.size())) ||
         (rc = upload(&h->KMd, kmd.data(), kmd.size())) || (rc = upload(&h->Km11, pr->Km11, (size_t)m1 * m1)) ||
         (rc = upload(&h->Kd11, pr->Kd11, (size_t)m1 * m1)) ||
         (rc = upload(&h->cconst, pr->cconst, (size_t)3 * n * m1)) || (rc = upload(&h->B6, pr->B, (size_t)6 * m1)) ||
-        (rc = upload(&h->rhs, pr->rhs, (size_t)3 * n * 6)) || (rc = upload(&h->PBt, pr->PBt, (size_t)m1 * 6))) {
+        (rc = upload(&h->rhs, pr->rhs, (size_t)3 * n * 6)) || (rc = upload(&h->PBt, pr->PBt, (size_t)m1 * 6)) ||
+        (rc = upload(&h->Mm, pr->Mm, (size_t)m1 * m1)) || (rc = upload(&h->Md, pr->Md, (size_t)m1 * m1)) ||
+        (rc = upload(&h->G, gram.data(), gram.size()))) {
         sgsf_destroy(h);
         return rc;
     }
@@ -461,6 +470,70 @@ int sgsf_fp32_peak(double* tflops, double* ms, void* stream_) {
     if (ms) *ms = t;
     if (tflops) *tflops = flops / (t * 1e-3) / 1e12;
     return SGSF_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- differentiable SF (sf_unroll.cuh)
+static sgsf::UnrollParams unroll_params(const sgsf_handle_t* h, int batch, int iters) {
+    sgsf::UnrollParams p;
+    std::memset(&p, 0, sizeof(p));
+    p.n = h->n;
+    p.S = h->S;
+    p.m1 = h->m1;
+    p.batch = batch;
+    p.iters = iters;
+    p.rho = h->rho;
+    p.lat = h->lat;
+    p.vert = h->vert;
+    p.ws_lat = h->ws_lat;
+    p.ws_vert = h->ws_vert;
+    p.cx = h->center[0];
+    p.cy = h->center[1];
+    p.cz = h->center[2];
+    p.W = h->W;
+    p.Km11 = h->Km11;
+    p.Kd11 = h->Kd11;
+    p.Mm = h->Mm;
+    p.Md = h->Md;
+    p.G = h->G;
+    p.cconst = h->cconst;
+    return p;
+}
+
+extern "C" {
+
+int sgsf_unroll(sgsf_handle_t* h, int batch, int iters, const double* xi_bar, const double* xi0,
+                const double* lam0, double* xs, double* ls, void* stream) {
+    if (!h) return fail(SGSF_ERR_INVALID, "null handle");
+    if (batch < 0 || iters < 0) return fail(SGSF_ERR_INVALID, "negative batch or iteration count");
+    if (h->n > kMaxRobots) return fail(SGSF_ERR_UNSUPPORTED, "n above sgsf_max_robots() is not supported yet");
+    if (batch == 0) return SGSF_OK;
+    if (!xi_bar || !xi0 || !lam0 || !xs || !ls) return fail(SGSF_ERR_INVALID, "null input/output buffer");
+    sgsf::UnrollParams p = unroll_params(h, batch, iters);
+    p.xi_bar = xi_bar;
+    p.xi0 = xi0;
+    p.lam0 = lam0;
+    p.xs = xs;
+    p.ls = ls;
+    return sgsf::launch_unroll_forward(p, (cudaStream_t)stream);
+}
+
+int sgsf_unroll_backward(sgsf_handle_t* h, int batch, int iters, const double* xs, const double* gxs,
+                         const double* gls, double* g_xi_bar, double* g_xi0, double* g_lam0, void* stream) {
+    if (!h) return fail(SGSF_ERR_INVALID, "null handle");
+    if (batch < 0 || iters < 0) return fail(SGSF_ERR_INVALID, "negative batch or iteration count");
+    if (h->n > kMaxRobots) return fail(SGSF_ERR_UNSUPPORTED, "n above sgsf_max_robots() is not supported yet");
+    if (batch == 0) return SGSF_OK;
+    if (!xs || !g_xi_bar || !g_xi0 || !g_lam0) return fail(SGSF_ERR_INVALID, "null input/output buffer");
+    sgsf::UnrollParams p = unroll_params(h, batch, iters);
+    p.xs = const_cast<double*>(xs);
+    p.gxs = gxs;
+    p.gls = gls;
+    p.g_xi_bar = g_xi_bar;
+    p.g_xi0 = g_xi0;
+    p.g_lam0 = g_lam0;
+    return sgsf::launch_unroll_backward(p, (cudaStream_t)stream);
 }
 
 }  // extern "C"
