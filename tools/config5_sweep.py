@@ -7,7 +7,7 @@ K unrolled SF steps (CUDA forward + reverse kernels).  Every strategy is then ev
 Also times the unrolled SF alone: forward + backward of K steps for a 1000-sample batch (CUDA events).
 Writes gpurun_out/config5.json.
 
-    python tools/config5_sweep.py [--steps 300] [--iters 10] [--batch 256]
+    python tools/config5_sweep.py [--steps 1500] [--iters 20] [--batch 256]
 """
 import argparse
 import json
@@ -49,8 +49,8 @@ def time_unrolled(sf, xb, iters, reps=5):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--steps", type=int, default=300)
-    ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=1500)
+    ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--pool", type=int, default=8192)
     ap.add_argument("--lr", type=float, default=1e-3)
