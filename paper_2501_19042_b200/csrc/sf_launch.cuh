@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include "../../include/sgsf.h"
@@ -28,7 +29,7 @@ int launch_large(const LaunchInfo& li, SolveParams& p, const sgsf_config_t* cfg,
 template <typename T, int NB, int MP, int MAXT, int TPS>
 int launch_persistent(const LaunchInfo& li, SolveParams& p, const sgsf_config_t* cfg, const sgsf_timing_t* timing,
                       cudaStream_t stream) {
-    auto kern = sf_persistent_kernel<T, NB, MP, MAXT, TPS>;
+    void (*kern)(const SolveParams) = sf_persistent_kernel<T, NB, MP, MAXT, TPS>;
     int dev_smem = 0;
     cudaError_t e = cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, li.device);
     if (e != cudaSuccess) return internal_fail(SGSF_ERR_CUDA, cudaGetErrorString(e));
@@ -36,11 +37,21 @@ int launch_persistent(const LaunchInfo& li, SolveParams& p, const sgsf_config_t*
     // thread per time step, ceil(S/16) warps with two (TPS = 2: 16 steps per warp)
     const int wps = TPS == 2 ? (p.S + 15) / 16 : (p.S + 31) / 32;
     const int slot_threads = 32 * wps;
+    // positions on the tensor cores (3xTF32 tcgen05 GEMM, sf_tc.cuh) when a slot is exactly one
+    // 128-lane TMEM tile: float, 16 robots, 97..128 steps.  SGSF_NO_TC=1 keeps the FFMA path.
+    bool tc = false;
+    if constexpr (sizeof(T) == 4 && NB == 16 && TPS == 1 && MP <= 16) {
+        const char* off = std::getenv("SGSF_NO_TC");
+        if (wps == 4 && !(off && off[0] == '1')) {
+            tc = true;
+            kern = sf_persistent_kernel<T, NB, MP, MAXT, TPS, true>;
+        }
+    }
     int spb = cfg->slots_per_block;
     if (spb <= 0) {
         spb = 0;
         for (int s = 1; s * slot_threads <= MAXT && s <= 15; ++s) {
-            if (make_layout<T, NB>(p.n, p.S, MP, s, p.want_prev).total > (size_t)dev_smem) break;
+            if (make_layout<T, NB>(p.n, p.S, MP, s, p.want_prev, tc).total > (size_t)dev_smem) break;
             spb = s;
         }
         // small batches: spread samples over the SMs instead of packing few CTAs
@@ -48,7 +59,7 @@ int launch_persistent(const LaunchInfo& li, SolveParams& p, const sgsf_config_t*
         if (spb > spread) spb = spread > 0 ? spread : 1;
     }
     if (spb <= 0) {
-        const size_t need = make_layout<T, NB>(p.n, p.S, MP, 1, p.want_prev).total;
+        const size_t need = make_layout<T, NB>(p.n, p.S, MP, 1, p.want_prev, tc).total;
         return internal_fail(SGSF_ERR_UNSUPPORTED,
                              "problem too large for one CTA: one sample slot needs " + std::to_string(need / 1024) +
                                  " KB of shared memory, the device allows " + std::to_string(dev_smem / 1024) +
@@ -60,7 +71,7 @@ int launch_persistent(const LaunchInfo& li, SolveParams& p, const sgsf_config_t*
     p.spb = spb;
     p.wps = wps;
     p.MP = MP;
-    const SmemLayout L = make_layout<T, NB>(p.n, p.S, MP, spb, p.want_prev);
+    const SmemLayout L = make_layout<T, NB>(p.n, p.S, MP, spb, p.want_prev, tc);
     if (L.total > (size_t)dev_smem) return internal_fail(SGSF_ERR_UNSUPPORTED, "shared memory budget exceeded");
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
     if (e != cudaSuccess) return internal_fail(SGSF_ERR_CUDA, cudaGetErrorString(e));

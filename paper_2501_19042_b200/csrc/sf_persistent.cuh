@@ -43,6 +43,7 @@
 #pragma once
 
 #include "sf_device.cuh"
+#include "sf_tc.cuh"
 
 namespace sgsf {
 
@@ -90,6 +91,7 @@ __device__ __forceinline__ int next_sample(const SolveParams& p) {
 // term pass with no extra barrier.
 constexpr int MAX_SLOT_WORDS = 16;   // time-step bit words (slot size <= 512 threads)
 struct SlotShared {
+    uint64_t mbar;   // TC: completion of the position MMAs of the next iterate (3 arrivals, one per axis)
     int sample;
     int active[2];   // some term had an active constraint in the term pass
     uint32_t amask[2][MAX_SLOT_WORDS];   // time steps with an active term (their R row is valid)
@@ -120,14 +122,18 @@ template <typename T, int NB> struct RowStride {
 // the dead old row is reused for the thread's scattered residual R, valid
 // where bit t of the slot's active-step mask is set.
 struct SmemLayout {
-    size_t W, KMm, KMd, cconst, B6, rhs, PBt, ptab;
+    size_t W, KMm, KMd, cconst, B6, rhs, PBt, ptab, tmem;
     size_t slot0, slot_stride;
     size_t C, Cp, lam, U, xb, eqerr, psq, P0, P1, Cf, pinf, sh;
     size_t total;
 };
 
+// TC: the FP32 copy of C becomes the 3xTF32 B operand of the position GEMM, [axis][hi, lo] blocks of
+// 16 robots x 16 k in the UMMA K-major layout (tc::kmajor16_offset)
+constexpr int kTcBopBytes = 3 * 2 * 1024;
+
 template <typename T, int NB>
-__host__ __device__ inline SmemLayout make_layout(int n, int S, int MP, int spb, int want_prev) {
+__host__ __device__ inline SmemLayout make_layout(int n, int S, int MP, int spb, int want_prev, bool tc = false) {
     const int RS = RowStride<T, NB>::value;
     SmemLayout L;
     size_t o = 0;
@@ -141,6 +147,7 @@ __host__ __device__ inline SmemLayout make_layout(int n, int S, int MP, int spb,
     L.rhs = o;    o = align16(o + (size_t)R3 * 6 * d);
     L.PBt = o;    o = align16(o + (size_t)MP * 6 * d);
     L.ptab = o;   o = align16(o + (size_t)NB * (NB - 1) / 2 * sizeof(int));
+    L.tmem = o;   o = align16(o + 2 * sizeof(uint32_t));               // TC: TMEM base, finished-slot count
     L.slot0 = o;
     size_t q = 0;
     L.C = q;      q = align16(q + (size_t)dimp * d);
@@ -152,7 +159,7 @@ __host__ __device__ inline SmemLayout make_layout(int n, int S, int MP, int spb,
     L.psq = q;    q = align16(q + (size_t)MAX_SLOT_WORDS * d);        // per warp sum of the l2 partials
     L.P0 = q;     q = align16(q + (size_t)RS * S * ts);
     L.P1 = q;     q = align16(q + (size_t)RS * S * ts);
-    L.Cf = q;     q = align16(q + (size_t)3 * MP * NB * ts);
+    L.Cf = q;     q = align16(q + (tc ? (size_t)kTcBopBytes : (size_t)3 * MP * NB * ts));
     L.pinf = q;   q = align16(q + (size_t)MAX_SLOT_WORDS * ts);       // per warp max of the inf partials
     L.sh = q;     q = align16(q + sizeof(SlotShared));
     L.slot_stride = q;
@@ -917,7 +924,7 @@ __device__ __forceinline__ Partials<T> finish_step(const SlotPtrs& sp, const int
 }
 
 // ---------------------------------------------------------------- load a sample (one coefficient row)
-template <typename T, int NB, int MP>
+template <typename T, int NB, int MP, bool TC>
 __device__ __forceinline__ void load_row(const SolveParams& p, const SlotPtrs& sp, int sample, int r,
                                          const double* __restrict__ B6, const double* __restrict__ rhs,
                                          const double* __restrict__ PBt) {
@@ -962,15 +969,44 @@ __device__ __forceinline__ void load_row(const SolveParams& p, const SlotPtrs& s
         if (p.want_prev) sp.Cp[idx] = c[q];
     }
     const int ax = r / p.n, i = r - ax * p.n;
+    if constexpr (TC) {
+        unsigned char* b = (unsigned char*)sp.Cf + ax * 2048;
 #pragma unroll
-    for (int q = 0; q < MP; ++q) ((T*)sp.Cf)[(ax * MP + q) * NB + i] = (T)c[q];
+        for (int q = 0; q < MP; ++q) {
+            const float v = (float)c[q], hi = tc::tf32_rna(v);
+            *reinterpret_cast<float*>(b + tc::kmajor16_offset(i, q)) = hi;
+            *reinterpret_cast<float*>(b + 1024 + tc::kmajor16_offset(i, q)) = tc::tf32_rna(v - hi);
+        }
+        tc::fence_proxy_async();   // visible to the tensor core after the next slot barrier
+    } else {
+#pragma unroll
+        for (int q = 0; q < MP; ++q) ((T*)sp.Cf)[(ax * MP + q) * NB + i] = (T)c[q];
+    }
+}
+
+// TC: the 3xTF32 position GEMM of one axis, D[step][robot] = W[step] . C[robot], issued by one thread.
+// A (W rows of the slot's steps, tf32 hi at TMEM columns 0..15, lo at 16..31) is shared by the slots;
+// B = this axis' C hi / lo blocks; the small products go first (FP32-level accuracy).
+__device__ __forceinline__ void tc_issue_axis(uint32_t tbase, int slot, int ax, const void* cf) {
+    const uint32_t idesc = tc::idesc_tf32(128, 16);
+    const uint32_t d = tbase + 64 + 64 * slot + 16 * ax;
+    const uint32_t b0 = tc::smem_u32(cf) + ax * 2048;
+    const uint32_t acol[3] = {0, 16, 0}, bofs[3] = {1024, 0, 0};   // W_hi C_lo, W_lo C_hi, W_hi C_hi
+#pragma unroll
+    for (int pr = 0; pr < 3; ++pr)
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks)
+            tc::mma_tf32_ts(d, tbase + acol[pr] + 8 * ks, tc::smem_desc(b0 + bofs[pr] + 256 * ks, 128, 512), idesc,
+                            (pr | ks) ? 1u : 0u);
 }
 
 // ---------------------------------------------------------------- the kernel
-template <typename T, int NB, int MP, int MAXT, int TPS>
+// TC = positions by the 3xTF32 tcgen05 GEMM (float, 16 robots, one thread per step, 4 warps per slot)
+template <typename T, int NB, int MP, int MAXT, int TPS, bool TC = false>
 __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParams p) {
+    static_assert(!TC || (sizeof(T) == 4 && NB == 16 && TPS == 1 && MP <= 16), "TC positions: float, 16 robots");
     extern __shared__ __align__(16) unsigned char smem[];
-    const SmemLayout L = make_layout<T, NB>(p.n, p.S, MP, p.spb, p.want_prev);
+    const SmemLayout L = make_layout<T, NB>(p.n, p.S, MP, p.spb, p.want_prev, TC);
     constexpr int RS = RowStride<T, NB>::value;
     constexpr int M2P = 2 * MP;
     constexpr int NW = TermBits<NB>::words;
@@ -1017,7 +1053,42 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
         for (int i = 0; i < NB; ++i)
             for (int j = i + 1; j < NB; ++j) ptab[b++] = i | (j << 8);
     }
+    uint32_t* tmem_info = (uint32_t*)(smem + L.tmem);   // [0] TMEM base, [1] finished slots
+    if constexpr (TC) {
+        // TMEM: columns 0..31 = A operand (W rows, tf32 hi / lo), 64 + 64 s = slot s's 16 x 3 positions
+        if (tid < 32) tc::tmem_alloc(tmem_info, 256);
+        if (tid == 0) {
+            tmem_info[1] = 0u;
+            for (int s = 0; s < p.spb; ++s) tc::mbar_init(&slot_ptrs(smem, L, s).sh->mbar, 3);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        for (int s = 0; s < p.spb; ++s) {   // B operands start at zero (k >= m1 and robots >= n stay zero)
+            uint32_t* b = (uint32_t*)slot_ptrs(smem, L, s).Cf;
+            for (int e = tid; e < kTcBopBytes / 4; e += nt) b[e] = 0u;
+        }
+    }
     __syncthreads();
+    if constexpr (TC) {
+        const uint32_t tb = tmem_info[0];
+        if (tid < 128) {   // A rows: TMEM lane 32 w + l holds the step of lane l of warp w (4 warps per slot)
+            const int w = tid >> 5, l = tid & 31, t = 8 * (w + 4 * (l >> 3)) + (l & 7);
+            float hi[16], lo[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const float v = (t < S && q < m1) ? (float)p.W[t * m1 + q] : 0.f;
+                hi[q] = tc::tf32_rna(v);
+                lo[q] = tc::tf32_rna(v - hi[q]);
+            }
+            const uint32_t la = tb + ((uint32_t)(32 * w) << 16);
+            tc::tmem_st16(la, hi);
+            tc::tmem_st16(la + 16, lo);
+            tc::tmem_wait_st();
+        }
+        tc::fence_proxy_async();
+        tc::fence_before_sync();
+        __syncthreads();
+        tc::fence_after_sync();
+    }
 
     // ---- this thread's slot (an independent warp group)
     const int gsize = 32 * p.wps;
@@ -1087,10 +1158,22 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
     slot_barrier(bar_id, gsize);
     int sample = sp.sh->sample;
 
+    uint32_t mph = 0;   // TC: parity of the slot's next position-MMA completion
+    const uint32_t tbase = TC ? tmem_info[0] : 0u;
     while (sample < p.batch) {
         // ---------------- load the sample, default start = boundary projection
-        for (int r = lt; r < R3; r += gsize) load_row<T, NB, MP>(p, sp, sample, r, B6, rhs, PBt);
+        for (int r = lt; r < R3; r += gsize) load_row<T, NB, MP, TC>(p, sp, sample, r, B6, rhs, PBt);
         slot_barrier(bar_id, gsize);
+        if constexpr (TC) {
+            if (lt == 0) {   // positions of the first iterate
+                tc::fence_after_sync();
+#pragma unroll 1
+                for (int ax = 0; ax < 3; ++ax) {
+                    tc_issue_axis(tbase, slot, ax, sp.Cf);
+                    tc::mma_commit(&sp.sh->mbar);
+                }
+            }
+        }
 
         for (int k = 0;; ++k) {
             SGSF_PT(0);
@@ -1104,9 +1187,23 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
             bool need_scan = false;
             uint32_t nm[NW];
             T zmin_ws = T(1), qinf = T(0), qsq = T(0);   // quiet statistics, kept for T3
+            T pos[3 * RH];
+            if constexpr (TC) {   // warp-collective TMEM loads, before the per-step branch
+                tc::mbar_wait(&sp.sh->mbar, mph);
+                mph ^= 1u;
+                tc::fence_after_sync();
+                const uint32_t ta = tbase + ((uint32_t)(32 * lwarp) << 16) + 64 + 64 * slot;
+                tc::tmem_ld16(ta, *reinterpret_cast<float(*)[16]>(&pos[0]));
+                tc::tmem_ld16(ta + 16, *reinterpret_cast<float(*)[16]>(&pos[16]));
+                tc::tmem_ld16(ta + 32, *reinterpret_cast<float(*)[16]>(&pos[32]));
+                tc::tmem_wait_ld();
+                tc::fence_before_sync();
+#pragma unroll
+                for (int q = 0; q < 3 * RH; ++q)
+                    if ((q % RH) >= n) pos[q] = phantom_pos<T>(q % RH);
+            }
             if (ts < S) {
-                T pos[3 * RH];
-                positions_part<T, NB, RH, MP>(Wt, (const T*)sp.Cf, ts, r0, n, pos);
+                if constexpr (!TC) positions_part<T, NB, RH, MP>(Wt, (const T*)sp.Cf, ts, r0, n, pos);
                 store_part<T, NB, RH>(Prow_new, r0, pos);
                 if (k == 0) {
                     store_part<T, NB, RH>(Prow_old, r0, pos);   // no previous iterate: "old" := "new"
@@ -1421,14 +1518,34 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                             if (rob < n && q < MP) {
                                 const int idx = (rb + rob) * MP + q;
                                 *reinterpret_cast<double2*>(sp.C + idx) = make_double2(dacc[mt][nt][0], dacc[mt][nt][1]);
-                                ((T*)sp.Cf)[(ax * MP + q) * NB + rob] = (T)dacc[mt][nt][0];
-                                ((T*)sp.Cf)[(ax * MP + q + 1) * NB + rob] = (T)dacc[mt][nt][1];
+                                if constexpr (TC) {
+                                    unsigned char* bo = (unsigned char*)sp.Cf + ax * 2048;
+#pragma unroll
+                                    for (int e = 0; e < 2; ++e) {
+                                        const float v = (float)dacc[mt][nt][e], hi = tc::tf32_rna(v);
+                                        *reinterpret_cast<float*>(bo + tc::kmajor16_offset(rob, q + e)) = hi;
+                                        *reinterpret_cast<float*>(bo + 1024 + tc::kmajor16_offset(rob, q + e)) =
+                                            tc::tf32_rna(v - hi);
+                                    }
+                                } else {
+                                    ((T*)sp.Cf)[(ax * MP + q) * NB + rob] = (T)dacc[mt][nt][0];
+                                    ((T*)sp.Cf)[(ax * MP + q + 1) * NB + rob] = (T)dacc[mt][nt][1];
+                                }
                                 if (any_active) {   // commit lam'
                                     const double2 l = *reinterpret_cast<const double2*>(sp.lam + idx);
                                     *reinterpret_cast<double2*>(sp.lam + idx) =
                                         make_double2(l.x - p.rho * gq[mt][nt][0], l.y - p.rho * gq[mt][nt][1]);
                                 }
                             }
+                        }
+                    }
+                    if constexpr (TC) {   // this axis' positions of the next iterate, overlapping the check below
+                        tc::fence_proxy_async();
+                        __syncwarp();
+                        if (lane == 0) {
+                            tc::fence_after_sync();
+                            tc_issue_axis(tbase, slot, ax, sp.Cf);
+                            tc::mma_commit(&sp.sh->mbar);
                         }
                     }
                     __syncwarp();
@@ -1468,6 +1585,17 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
             }
             slot_barrier(bar_id, gsize);
             SGSF_PT(4);
+        }
+    }
+    if constexpr (TC) {   // the last slot to finish frees the TMEM
+        tc::fence_before_sync();
+        if (lwarp == 0) {
+            uint32_t last = 0;
+            if (lane == 0) last = atomicAdd(&tmem_info[1], 1u) == (uint32_t)(p.spb - 1);
+            if (__shfl_sync(0xffffffffu, last, 0)) {
+                tc::fence_after_sync();
+                tc::tmem_dealloc(tbase, 256);
+            }
         }
     }
 #ifdef SGSF_PHASE_TIMING
