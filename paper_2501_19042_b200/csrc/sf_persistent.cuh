@@ -988,16 +988,16 @@ __device__ __forceinline__ void load_row(const SolveParams& p, const SlotPtrs& s
 // A (W rows of the slot's steps, tf32 hi at TMEM columns 0..15, lo at 16..31) is shared by the slots;
 // B = this axis' C hi / lo blocks; the small products go first (FP32-level accuracy).
 __device__ __forceinline__ void tc_issue_axis(uint32_t tbase, int slot, int ax, const void* cf) {
-    const uint32_t idesc = tc::idesc_tf32(128, 16);
+    constexpr uint32_t idesc = tc::idesc_tf32(128, 16);
     const uint32_t d = tbase + 64 + 64 * slot + 16 * ax;
-    const uint32_t b0 = tc::smem_u32(cf) + ax * 2048;
-    const uint32_t acol[3] = {0, 16, 0}, bofs[3] = {1024, 0, 0};   // W_hi C_lo, W_lo C_hi, W_hi C_hi
+    // descriptor of the axis' B block; the start-address field (16-byte units) takes the offsets directly
+    const uint64_t bd = tc::smem_desc(tc::smem_u32(cf) + ax * 2048, 128, 512);
+    constexpr uint32_t acol[3] = {0, 16, 0}, bofs[3] = {1024, 0, 0};   // W_hi C_lo, W_lo C_hi, W_hi C_hi
 #pragma unroll
     for (int pr = 0; pr < 3; ++pr)
 #pragma unroll
         for (int ks = 0; ks < 2; ++ks)
-            tc::mma_tf32_ts(d, tbase + acol[pr] + 8 * ks, tc::smem_desc(b0 + bofs[pr] + 256 * ks, 128, 512), idesc,
-                            (pr | ks) ? 1u : 0u);
+            tc::mma_tf32_ts(d, tbase + acol[pr] + 8 * ks, bd + ((bofs[pr] + 256 * ks) >> 4), idesc, (pr | ks) ? 1u : 0u);
 }
 
 // ---------------------------------------------------------------- the kernel
@@ -1540,7 +1540,9 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                         }
                     }
                     if constexpr (TC) {   // this axis' positions of the next iterate, overlapping the check below
+#ifndef SGSF_TC_NOFENCE_EXPERIMENT
                         tc::fence_proxy_async();
+#endif
                         __syncwarp();
                         if (lane == 0) {
                             tc::fence_after_sync();

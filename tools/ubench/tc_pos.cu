@@ -15,7 +15,19 @@ using namespace sgsf::tc;
 
 constexpr int S = 101, MP = 12, NB = 16;
 
-template <int NPROD, int NAX>
+// TRUNC: hi = the raw FP32 value (the tensor core reads its top 19 bits), lo = x - (x & ~0x1fff)
+template <bool TRUNC>
+__device__ __forceinline__ void split(float x, float& hi, float& lo) {
+    if (TRUNC) {
+        hi = x;
+        lo = x - __uint_as_float(__float_as_uint(x) & 0xffffe000u);
+    } else {
+        hi = tf32_rna(x);
+        lo = tf32_rna(x - hi);
+    }
+}
+
+template <int NPROD, int NAX, bool TRUNC = false>
 __global__ void tc_pos_kernel(const float* W, const float* C, float* out, long long* cycles) {
     __shared__ __align__(1024) unsigned char bop[3][2][1024];   // [axis][hi, lo] K-major 16 x 16 tf32
     __shared__ __align__(8) uint64_t mbar;
@@ -27,7 +39,8 @@ __global__ void tc_pos_kernel(const float* W, const float* C, float* out, long l
     for (int e = tid; e < 3 * 16 * 16; e += blockDim.x) {
         const int ax = e / 256, i = (e / 16) % 16, k = e % 16;
         const float c = k < MP ? C[(ax * MP + k) * NB + i] : 0.f;
-        const float hi = tf32_rna(c), lo = tf32_rna(c - hi);
+        float hi, lo;
+        split<TRUNC>(c, hi, lo);
         *reinterpret_cast<float*>(&bop[ax][0][kmajor16_offset(i, k)]) = hi;
         *reinterpret_cast<float*>(&bop[ax][1][kmajor16_offset(i, k)]) = lo;
     }
@@ -40,8 +53,7 @@ __global__ void tc_pos_kernel(const float* W, const float* C, float* out, long l
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
             const float w = (ts < S && k < MP) ? W[ts * MP + k] : 0.f;
-            hi[k] = tf32_rna(w);
-            lo[k] = tf32_rna(w - hi[k]);
+            split<TRUNC>(w, hi[k], lo[k]);
         }
         const uint32_t lane_addr = base + ((uint32_t)(32 * warp) << 16);
         tmem_st16(lane_addr + 0, hi);
@@ -109,7 +121,8 @@ int main(int argc, char** argv) {
     cudaMemcpy(&cy1, dcy, 8, cudaMemcpyDeviceToHost);
     printf("one axis, 4 products: %lld cycles\n", cy1);
     const int nprod = argc > 1 ? atoi(argv[1]) : 3;
-    if (nprod == 4) tc_pos_kernel<4, 3><<<1, 128>>>(dW, dC, dO, dcy);
+    if (nprod == 5) tc_pos_kernel<3, 3, true><<<1, 128>>>(dW, dC, dO, dcy);   // 3 products, truncation split
+    else if (nprod == 4) tc_pos_kernel<4, 3><<<1, 128>>>(dW, dC, dO, dcy);
     else tc_pos_kernel<3, 3><<<1, 128>>>(dW, dC, dO, dcy);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
