@@ -1540,9 +1540,7 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                         }
                     }
                     if constexpr (TC) {   // this axis' positions of the next iterate, overlapping the check below
-#ifndef SGSF_TC_NOFENCE_EXPERIMENT
                         tc::fence_proxy_async();
-#endif
                         __syncwarp();
                         if (lane == 0) {
                             tc::fence_after_sync();
