@@ -88,3 +88,51 @@ def test_large_n_verdict_and_svars_match_oracle():
                                                      1.0, np.inf)
         np.testing.assert_allclose(svs[b].pair_radial.ravel(), pr, rtol=1e-12, atol=1e-14)
         np.testing.assert_allclose(np.cos(svs[b].pair_polar.ravel()), np.cos(pp), rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("n,degree", [(12, 10), (16, 14), (9, 13)])
+def test_tensor_core_positions_variants(n, degree):
+    """The 3xTF32 tcgen05 position GEMM (K1 with 97..128 steps, <= 16 robots, lean): phantom robots
+    (n < 16) and the 16-column variant (degree > 11) against the oracle at a fixed iteration count."""
+    doc, sf, cfg, props = _setup(n, 100, 8, 2, 10, "lean", degree)
+    out = sf.solve_batched(torch.from_numpy(props).cuda(), config=cfg)
+    op = sf_oracle.make_problem(doc, degree=degree)
+    coeffs = out.coeffs.cpu().numpy()
+    rinf = out.residual_inf.cpu().numpy()
+    for b, x in enumerate(props):
+        r = sf_oracle.solve(op, x, max_iters=10, early_stop=False)
+        assert np.abs(coeffs[b] - r.coeffs).max() <= 1e-5 * np.abs(r.coeffs).max(), b
+        np.testing.assert_allclose(rinf[b], r.residual_inf, rtol=1e-3, atol=1e-9)
+    assert out.eq_err.max().item() <= 1e-8
+
+
+def test_tensor_core_and_ffma_positions_agree():
+    """Config 2 with the tcgen05 positions (default) and with SGSF_NO_TC=1 (packed FFMA): the same
+    iterations and verdicts up to borderline flips, coefficients within the lean tolerance."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import torch, numpy as np, sys\n"
+        "sys.path.insert(0, '.')\n"
+        "import bench\n"
+        "from paper_2501_19042_b200 import SafetyFilter\n"
+        "prob, shard, cfg = bench.workload(0, 1, 300)\n"
+        "sf = SafetyFilter(prob, degree=10, config=cfg)\n"
+        "out = sf.solve_batched(torch.from_numpy(shard).cuda(), config=cfg)\n"
+        "np.savez(sys.argv[1], c=out.coeffs.cpu().numpy(), it=out.iterations.cpu().numpy(), "
+        "f=out.feasible.cpu().numpy())\n")
+    import tempfile
+    with tempfile.TemporaryDirectory() as d:
+        res = {}
+        for tag, env in (("tc", {}), ("ffma", {"SGSF_NO_TC": "1"})):
+            path = os.path.join(d, tag + ".npz")
+            subprocess.run([sys.executable, "-c", code, path], check=True, env={**os.environ, **env},
+                           cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+            res[tag] = np.load(path)
+    it_tc, it_f = res["tc"]["it"], res["ffma"]["it"]
+    same = it_tc == it_f
+    assert same.mean() >= 0.95
+    c_tc, c_f = res["tc"]["c"][same], res["ffma"]["c"][same]
+    assert np.abs(c_tc - c_f).max() <= 1e-5 * np.abs(c_f).max()
+    assert (res["tc"]["f"] == res["ffma"]["f"]).mean() >= 0.97
