@@ -331,9 +331,11 @@ __device__ __forceinline__ void positions_part(const T* __restrict__ Wt, const T
             }
         }
     }
+    if (n < NB) {   // uniform: phantom robots only in the smaller swarms
 #pragma unroll
-    for (int q = 0; q < 3 * RH; ++q)
-        if (r0 + (q % RH) >= n) pos[q] = phantom_pos<T>(r0 + (q % RH));
+        for (int q = 0; q < 3 * RH; ++q)
+            if (r0 + (q % RH) >= n) pos[q] = phantom_pos<T>(r0 + (q % RH));
+    }
 }
 
 // 16-byte vector copies of this thread's part of a position row
@@ -1198,9 +1200,11 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                 tc::tmem_ld16(ta + 32, *reinterpret_cast<float(*)[16]>(&pos[32]));
                 tc::tmem_wait_ld();
                 tc::fence_before_sync();
+                if (n < NB) {   // uniform: phantom robots only in the smaller swarms
 #pragma unroll
-                for (int q = 0; q < 3 * RH; ++q)
-                    if ((q % RH) >= n) pos[q] = phantom_pos<T>(q % RH);
+                    for (int q = 0; q < 3 * RH; ++q)
+                        if ((q % RH) >= n) pos[q] = phantom_pos<T>(q % RH);
+                }
             }
             if (ts < S) {
                 if constexpr (!TC) positions_part<T, NB, RH, MP>(Wt, (const T*)sp.Cf, ts, r0, n, pos);
