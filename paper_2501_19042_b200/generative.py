@@ -1,0 +1,150 @@
+"""Generative proposal decoders (CVAE / VQ-VAE) feeding the safety filter on the device.
+
+BASELINE configs 1-3 sample their SF inputs from a CVAE or VQ-VAE decoder. The reference package
+has no network. These modules follow the paper's descriptions
+(PAPER.md "VQ-VAE Network Details", "CVAE Network Details", :302-307):
+
+* CVAE decoder:
+  * a Gaussian latent Z of L x 3;
+  * a state network of two convolution layers (ReLU, batch norm) over the per-robot start/goal
+    states, concatenated with the latent;
+  * 4 transposed-convolution layers with 128 channels, LeakyReLU, batch norm and dropout.
+* VQ-VAE decoder:
+  * a codebook of 512 three-dimensional vectors and L latent positions;
+  * 4 transposed-convolution layers with 128 channels, ReLU, batch norm and dropout.
+  * Without a trained PixelCNN prior, the code indices are sampled uniformly.
+
+Both decoders emit a correction xi' to the straight-line coefficients. The differentiable QP layer
+of the paper (the boundary projection, ``projection.py:11-25``) turns it into xi_bar, which
+:func:`generate_and_filter` hands to the SF kernel without leaving the device.
+
+The weights are random-init (BASELINE config 1: "random-init decoder"); :func:`calibrate_batchnorm`
+sets their batch-norm statistics from sampled latents so that the samples differ. The parity target
+is the same module on the CPU with the same weights (``tests/test_gpu_generative.py``).
+"""
+from __future__ import annotations
+
+import torch
+from torch import nn
+
+from .initnet import context_features
+from .proposals import straight_line_coeffs
+from .unrolled import boundary_projection
+
+
+def latent_length(n: int) -> int:
+    """L = 25 latent vectors for the 4- and 8-agent models, 100 for 16 agents and more."""
+    return 25 if n <= 8 else 100
+
+
+class StateNet(nn.Module):
+    """Two convolution layers (ReLU, batch norm) over the 18 start/goal channels of each robot, max-pooled
+    over the robots and broadcast along the latent positions."""
+
+    def __init__(self, width: int = 64):
+        super().__init__()
+        self.net = nn.Sequential(nn.Conv1d(18, width, 1), nn.BatchNorm1d(width), nn.ReLU(),
+                                 nn.Conv1d(width, width, 1), nn.BatchNorm1d(width), nn.ReLU())
+
+    def forward(self, state: torch.Tensor, length: int) -> torch.Tensor:
+        return self.net(state).amax(dim=2, keepdim=True).expand(-1, -1, length)
+
+
+def _deconv_stack(c_in: int, act, dropout: float) -> nn.Sequential:
+    layers = []
+    for i in range(4):
+        layers += [nn.ConvTranspose1d(c_in if i == 0 else 128, 128, kernel_size=3, padding=1), nn.BatchNorm1d(128),
+                   act(), nn.Dropout(dropout)]
+    return nn.Sequential(*layers)
+
+
+class _Decoder(nn.Module):
+    def __init__(self, n: int, m1: int, c_in: int, act, dropout: float, scale: float):
+        super().__init__()
+        self.n, self.m1, self.L, self.scale = n, m1, latent_length(n), scale
+        self.body = _deconv_stack(c_in, act, dropout)
+        self.head = nn.Conv1d(128, 3, 1)                         # 3 axes per latent position
+        self.expand = nn.Linear(self.L, n * m1)                 # latent positions -> robot x coefficient
+
+    def _coeffs(self, h: torch.Tensor) -> torch.Tensor:
+        out = self.expand(self.head(self.body(h)))              # (B, 3, n m1)
+        return self.scale * out.reshape(out.shape[0], -1)
+
+
+class CVAEDecoder(_Decoder):
+    """Gaussian latent (B, 3, L) + state features -> coefficient correction (B, 3 n m1)."""
+
+    def __init__(self, n: int, m1: int = 11, state_width: int = 64, dropout: float = 0.1, scale: float = 0.5):
+        super().__init__(n, m1, 3 + state_width, lambda: nn.LeakyReLU(0.01), dropout, scale)
+        self.state = StateNet(state_width)
+
+    def sample_latent(self, batch: int, generator: torch.Generator | None = None, device=None) -> torch.Tensor:
+        return torch.randn((batch, 3, self.L), generator=generator, device=device)
+
+    def forward(self, z: torch.Tensor, state: torch.Tensor) -> torch.Tensor:
+        return self._coeffs(torch.cat([z, self.state(state, self.L)], dim=1))
+
+
+class VQVAEDecoder(_Decoder):
+    """Code indices (B, L) into a 512 x 3 codebook -> coefficient correction (B, 3 n m1)."""
+
+    def __init__(self, n: int, m1: int = 11, codes: int = 512, dropout: float = 0.1, scale: float = 0.5):
+        super().__init__(n, m1, 3, nn.ReLU, dropout, scale)
+        self.codebook = nn.Embedding(codes, 3)
+
+    def sample_latent(self, batch: int, generator: torch.Generator | None = None, device=None) -> torch.Tensor:
+        return torch.randint(0, self.codebook.num_embeddings, (batch, self.L), generator=generator, device=device)
+
+    def forward(self, idx: torch.Tensor, state: torch.Tensor | None = None) -> torch.Tensor:
+        return self._coeffs(self.codebook(idx).transpose(1, 2))
+
+
+@torch.no_grad()
+def calibrate_batchnorm(sf, decoder: nn.Module, batches: int = 4, batch: int = 256, seed: int = 0) -> nn.Module:
+    """Set the batch-norm running statistics of a random-init decoder from its own sampled latents
+    (train-mode passes with a cumulative average), so the eval-mode decoder normalises its activations
+    and the latent keeps its influence through the four layers."""
+    dev = next(decoder.parameters()).device
+    for m in decoder.modules():
+        if isinstance(m, nn.modules.batchnorm._BatchNorm):
+            m.reset_running_stats()
+            m.momentum = None
+    decoder.train()
+    gen = torch.Generator(device=dev).manual_seed(seed)
+    state = torch.as_tensor(context_features(sf.problem), dtype=torch.float32, device=dev)
+    for _ in range(batches):
+        decoder(decoder.sample_latent(batch, gen, dev), state.expand(batch, -1, -1))
+    return decoder.eval()
+
+
+def make_decoder(kind: str, n: int, m1: int = 11, **kw) -> nn.Module:
+    if kind == "cvae":
+        return CVAEDecoder(n, m1, **kw)
+    if kind == "vqvae":
+        return VQVAEDecoder(n, m1, **kw)
+    raise ValueError(f"decoder kind must be 'cvae' or 'vqvae', got {kind!r}")
+
+
+def decode_proposals(sf, decoder: nn.Module, latent: torch.Tensor) -> torch.Tensor:
+    """xi_bar (B, dim) float64 on the decoder's device: the straight line plus the decoder's correction,
+    through the boundary QP layer (projection.py:11-25)."""
+    dev = latent.device
+    state = torch.as_tensor(context_features(sf.problem), dtype=torch.float32, device=dev)
+    base = torch.as_tensor(straight_line_coeffs(sf.problem, sf.basis), dtype=torch.float64, device=dev)
+    corr = decoder(latent, state.expand(latent.shape[0], -1, -1)).to(torch.float64)
+    return boundary_projection(sf, base + corr)
+
+
+@torch.no_grad()
+def generate_and_filter(sf, decoder: nn.Module, batch: int, seed: int = 0, init_net=None, config=None):
+    """Sample ``batch`` proposals from the decoder and filter them, all on the current CUDA device (no host
+    round trip): latent -> decoder -> QP layer -> (init network) -> SF kernel.  Returns (xi_bar, DeviceBatch)."""
+    dev = torch.device("cuda", torch.cuda.current_device())
+    decoder.to(dev).eval()
+    gen = torch.Generator(device=dev).manual_seed(seed)
+    xb = decode_proposals(sf, decoder, decoder.sample_latent(batch, gen, dev))
+    xi0 = lam0 = None
+    if init_net is not None:
+        from .initnet import initial_states
+        xi0, lam0 = initial_states(sf, xb, "initnet", init_net)
+    return xb, sf.solve_batched(xb, xi0=xi0, lam0=lam0, config=config)

@@ -151,6 +151,7 @@ class Operator:
         self.equality = equality
         self.pair_i, self.pair_j = np.triu_indices(problem.n, k=1)
         self._handles: dict = {}
+        self._consts: dict = {}
 
     n_pairs = property(lambda self: int(self.pair_i.size))
     samples = property(lambda self: self.basis.samples)
@@ -161,7 +162,11 @@ class Operator:
     coeff_dim = property(lambda self: 3 * self.n * (self.basis.degree + 1))
 
     def constants(self, rho: float) -> DeviceConstants:
-        return device_constants(self.problem, self.basis, self.equality, rho)
+        key = float(rho)
+        k = self._consts.get(key)
+        if k is None:   # immutable per (problem, degree, rho), like the reference's rho-keyed KKT cache
+            k = self._consts[key] = device_constants(self.problem, self.basis, self.equality, rho)
+        return k
 
     def handle(self, rho: float, device: torch.device | None = None):
         if not torch.cuda.is_available():

@@ -1,0 +1,34 @@
+"""Decoder -> QP layer -> SF on the device (configs 1-3 pipeline).  The GPU decoder matches the same
+random-init module on the CPU to 1e-4 of its output scale (FP32 convolutions; cuDNN's default TF32 is
+turned off for the comparison, the pipeline keeps it), and the device pipeline's SF result equals
+solve_batched on the same proposals."""
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("kind,config", [("cvae", 2), ("vqvae", 1)])
+def test_decoder_gpu_matches_cpu_and_pipeline(kind, config):
+    from paper_2501_19042_b200 import SafetyFilter, SolverConfig
+    from paper_2501_19042_b200.generative import decode_proposals, generate_and_filter, make_decoder
+    from paper_2501_19042_b200.scenarios import config_problem
+    prob = config_problem(config)
+    sf = SafetyFilter(prob, config=SolverConfig(max_iters=100, svars=False))
+    from paper_2501_19042_b200.generative import calibrate_batchnorm
+    from paper_2501_19042_b200.initnet import context_features
+    torch.manual_seed(1)
+    dec = calibrate_batchnorm(sf, make_decoder(kind, prob.n))
+    lat = dec.sample_latent(16, torch.Generator().manual_seed(5))
+    state = torch.as_tensor(context_features(prob), dtype=torch.float32).expand(16, -1, -1)
+    with torch.no_grad(), torch.backends.cudnn.flags(enabled=True, allow_tf32=False):
+        cpu = dec(lat, state)
+        gpu = dec.cuda()(lat.cuda(), state.cuda()).cpu()
+    scale = float(cpu.abs().max())
+    assert float((gpu - cpu).abs().max()) <= 1e-4 * scale
+    assert float(cpu.std(dim=0).mean()) > 0.05 * float(cpu.abs().mean())   # the latent matters
+    xb, out = generate_and_filter(sf, dec, 64, seed=2)
+    assert xb.is_cuda and out.coeffs.shape == (64, sf.coeff_dim)
+    assert (out.status == 0).all() and out.eq_err.max().item() <= 1e-8
+    ref = sf.solve_batched(xb)
+    assert torch.equal(ref.coeffs, out.coeffs) and torch.equal(ref.iterations, out.iterations)
