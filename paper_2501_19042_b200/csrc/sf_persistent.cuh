@@ -1314,9 +1314,21 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
             T inf = T(0);
             if (k >= 1) {   // partials: per axis (MX of iteration k-1), per warp (T3 above)
                 emax = fmax(fmax(sp.eqerr[0], sp.eqerr[1]), sp.eqerr[2]);
-                for (int w = 0; w < p.wps; ++w) {
-                    inf = fmax(inf, ((const T*)sp.pinf)[w]);
-                    sqs += sp.psq[w];
+                if (TC) {   // 4 warps per slot: independent loads, fixed summation order
+                    T pi[4];
+                    double ps[4];
+#pragma unroll
+                    for (int w = 0; w < 4; ++w) {
+                        pi[w] = ((const T*)sp.pinf)[w];
+                        ps[w] = sp.psq[w];
+                    }
+                    inf = fmax(fmax(pi[0], pi[1]), fmax(pi[2], pi[3]));
+                    sqs = ((ps[0] + ps[1]) + ps[2]) + ps[3];
+                } else {
+                    for (int w = 0; w < p.wps; ++w) {
+                        inf = fmax(inf, ((const T*)sp.pinf)[w]);
+                        sqs += sp.psq[w];
+                    }
                 }
             }
             // (a sample can only finish at k >= 1, so `inf` is always the last exit residual there)
