@@ -1408,20 +1408,33 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                         for (int nt = 0; nt < 2; ++nt) gq[mt][nt][0] = gq[mt][nt][1] = 0.0;
                     if (any_active) {   // G
                         const uint32_t* am = sp.sh->amask[par];
-                        int na = 0;
-                        for (int w = 0; w < SWT; ++w) na += __popc(am[w]);
+                        int na = 0, c0 = 0, c1 = 0, c2 = 0;   // TC (4 mask words): prefix counts of the words
+                        if constexpr (TC) {
+                            c0 = __popc(am[0]);
+                            c1 = c0 + __popc(am[1]);
+                            c2 = c1 + __popc(am[2]);
+                            na = c2 + __popc(am[3]);
+                        } else {
+                            for (int w = 0; w < SWT; ++w) na += __popc(am[w]);
+                        }
                         const T* Rb = (const T*)(par ? sp.P1 : sp.P0) + ax * NB;   // the old rows hold R
                         for (int kk = 0; 4 * kk < na; ++kk) {
                             int rem = 4 * kk + fc, t = -1;   // this lane's k = active step number
                             if (rem < na) {
-                                for (int w = 0;; ++w) {
-                                    const uint32_t bits = am[w];
-                                    const int c = __popc(bits);
-                                    if (rem < c) {
-                                        t = w * 32 + (int)__fns(bits, 0, rem + 1);
-                                        break;
+                                if constexpr (TC) {   // one load: the word from the prefix counts
+                                    const int w = (rem >= c0) + (rem >= c1) + (rem >= c2);
+                                    const int before = w == 0 ? 0 : (w == 1 ? c0 : (w == 2 ? c1 : c2));
+                                    t = w * 32 + (int)__fns(am[w], 0, rem - before + 1);
+                                } else {
+                                    for (int w = 0;; ++w) {
+                                        const uint32_t bits = am[w];
+                                        const int c = __popc(bits);
+                                        if (rem < c) {
+                                            t = w * 32 + (int)__fns(bits, 0, rem + 1);
+                                            break;
+                                        }
+                                        rem -= c;
                                     }
-                                    rem -= c;
                                 }
                             }
                             double bw[2];
