@@ -72,6 +72,8 @@ int launch_persistent(const LaunchInfo& li, SolveParams& p, const sgsf_config_t*
     p.wps = wps;
     p.MP = MP;
     const SmemLayout L = make_layout<T, NB>(p.n, p.S, MP, spb, p.want_prev, tc);
+    p.L = L;
+    set_family_constants(p);
     if (L.total > (size_t)dev_smem) return internal_fail(SGSF_ERR_UNSUPPORTED, "shared memory budget exceeded");
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
     if (e != cudaSuccess) return internal_fail(SGSF_ERR_CUDA, cudaGetErrorString(e));

@@ -49,6 +49,14 @@ namespace sgsf {
 
 enum { SAMPLE_OK = 0, SAMPLE_SINGULAR_KKT = 1 };
 
+// shared-memory offsets of one launch (make_layout below)
+struct SmemLayout {
+    size_t W, KMm, KMd, cconst, B6, rhs, PBt, ptab, tmem;
+    size_t slot0, slot_stride;
+    size_t C, Cp, lam, U, xb, eqerr, psq, P0, P1, Cf, pinf, sh;
+    size_t total;
+};
+
 struct SolveParams {
     int n, S, m1, MP, batch, max_iters, early_stop, want_prev, spb, wps;
     double rho, tol_res, tol_eq;
@@ -76,7 +84,26 @@ struct SolveParams {
     double* coeffs_prev;
     int* queue;
     const int* order;   // queue position -> sample (longest-first), or null for index order
+    // K1: the launch's shared-memory map and the spheroid constants, computed on the host so the
+    // kernel reads them from the parameter bank instead of recomputing them
+    SmemLayout L;
+    float fp_lat_f, fp_lim_f, fp_beta_f, fw_lat_f, fw_lim_f, fw_beta_f;
+    double fp_lim_d, fp_beta_d, fw_lim_d, fw_beta_d;
 };
+
+// the host-side precomputation of SolveParams' constants (make_family's expressions)
+inline void set_family_constants(SolveParams& p) {
+    p.fp_lat_f = (float)p.lat;
+    p.fp_lim_f = (float)(p.lat * p.lat);
+    p.fp_beta_f = (float)((p.lat * p.lat) / (p.vert * p.vert));
+    p.fw_lat_f = (float)p.ws_lat;
+    p.fw_lim_f = (float)(p.ws_lat * p.ws_lat);
+    p.fw_beta_f = (float)((p.ws_lat * p.ws_lat) / (p.ws_vert * p.ws_vert));
+    p.fp_lim_d = p.lat * p.lat;
+    p.fp_beta_d = (p.lat * p.lat) / (p.vert * p.vert);
+    p.fw_lim_d = p.ws_lat * p.ws_lat;
+    p.fw_beta_d = (p.ws_lat * p.ws_lat) / (p.ws_vert * p.ws_vert);
+}
 
 // next sample for a slot: queue position -> sample index
 __device__ __forceinline__ int next_sample(const SolveParams& p) {
@@ -121,12 +148,6 @@ template <typename T, int NB> struct RowStride {
 // (thread t owns row t; odd stride -> distinct banks); after the term pass
 // the dead old row is reused for the thread's scattered residual R, valid
 // where bit t of the slot's active-step mask is set.
-struct SmemLayout {
-    size_t W, KMm, KMd, cconst, B6, rhs, PBt, ptab, tmem;
-    size_t slot0, slot_stride;
-    size_t C, Cp, lam, U, xb, eqerr, psq, P0, P1, Cf, pinf, sh;
-    size_t total;
-};
 
 // TC: the FP32 copy of C becomes the 3xTF32 B operand of the position GEMM, [axis][hi, lo] blocks of
 // 16 robots x 16 k in the UMMA K-major layout (tc::kmajor16_offset)
@@ -1008,7 +1029,7 @@ template <typename T, int NB, int MP, int MAXT, int TPS, bool TC = false>
 __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParams p) {
     static_assert(!TC || (sizeof(T) == 4 && NB == 16 && TPS == 1 && MP <= 16), "TC positions: float, 16 robots");
     extern __shared__ __align__(16) unsigned char smem[];
-    const SmemLayout L = make_layout<T, NB>(p.n, p.S, MP, p.spb, p.want_prev, TC);
+    const SmemLayout& L = p.L;   // = make_layout<T, NB>(p.n, p.S, MP, p.spb, p.want_prev, TC), host-computed
     constexpr int RS = RowStride<T, NB>::value;
     constexpr int M2P = 2 * MP;
     constexpr int NW = TermBits<NB>::words;
@@ -1098,8 +1119,15 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
     if (slot >= p.spb) return;
     const int bar_id = 1 + slot;
     const SlotPtrs sp = slot_ptrs(smem, L, slot);
-    const Family<T> fp = make_family<T>(p.lat, p.vert);
-    const Family<T> fw = make_family<T>(p.ws_lat, p.ws_vert);
+    Family<T> fp, fw;   // = make_family<T>(lat, vert), from the parameter bank
+    if constexpr (sizeof(T) == 4) {
+        fp.lat = p.fp_lat_f, fp.lim = p.fp_lim_f, fp.beta = p.fp_beta_f;
+        fw.lat = p.fw_lat_f, fw.lim = p.fw_lim_f, fw.beta = p.fw_beta_f;
+    } else {
+        fp.lat = p.lat, fp.lim = p.fp_lim_d, fp.beta = p.fp_beta_d;
+        fw.lat = p.ws_lat, fw.lim = p.fw_lim_d, fw.beta = p.fw_beta_d;
+    }
+    fp.lat64 = p.lat, fp.vert64 = p.vert, fw.lat64 = p.ws_lat, fw.vert64 = p.ws_vert;
     const T cx = (T)p.cx, cy = (T)p.cy, cz = (T)p.cz;
     const int SWT = (S + 31) >> 5;   // words of the active-step mask
     const double inv_n = 1.0 / n;
@@ -1112,7 +1140,8 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
     // TPS = 1: steps are dealt to the warps in chunks of 8 (warp w gets chunks w, w + wps, ...), so
     // every warp covers the whole horizon -- the exact-path work clusters in time (collisions) and
     // would otherwise load one warp -- while 8 consecutive rows keep 16-byte row access conflict-free
-    const int ts = TPS == 2 ? lwarp * 16 + (lane & 15) : 8 * (lwarp + p.wps * (lane >> 3)) + (lane & 7);
+    const int wpsx = TC ? 4 : p.wps;   // TC: four warps per slot
+    const int ts = TPS == 2 ? lwarp * 16 + (lane & 15) : 8 * (lwarp + wpsx * (lane >> 3)) + (lane & 7);
     const int h = TPS == 2 ? lane >> 4 : 0;
     const int r0 = h * RH;
     const bool owner = h == 0;
@@ -1253,7 +1282,7 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                 const int src = __ffs(qmask) - 1;
                 qmask &= qmask - 1;
                 if (lane == 0) SGSF_COUNT(6, 1);
-                const int tsrc = TPS == 2 ? lwarp * 16 + src : 8 * (lwarp + p.wps * (src >> 3)) + (src & 7);
+                const int tsrc = TPS == 2 ? lwarp * 16 + src : 8 * (lwarp + wpsx * (src >> 3)) + (src & 7);
                 const T* row = Pbase_new + tsrc * RS;
                 T qm = T(1e30), zm = T(1);   // min q over the far pairs, min |component| over all pairs
                 uint32_t words[NPW], nwords[NPW];
