@@ -69,9 +69,14 @@ def random_swarm(n: int, horizon: int, seed: int, **kw):
     return load_problem(random_swarm_doc(n, horizon, seed, **kw))
 
 
+def config_doc(config: int) -> dict:
+    """Reference-schema problem dict of BASELINE config 1..4 (1 = crossing4; 2..4 seeded random swarms)."""
+    if config == 1:
+        return CROSSING4
+    n, H = {2: (16, 100), 3: (32, 100), 4: (64, 150)}[config]
+    return random_swarm_doc(n, H, seed=config)
+
+
 def config_problem(config: int):
     """Problem for BASELINE config 1..4 (1 = crossing4; 2..4 seeded random swarms)."""
-    if config == 1:
-        return load_problem(CROSSING4)
-    n, H = {2: (16, 100), 3: (32, 100), 4: (64, 150)}[config]
-    return random_swarm(n, H, seed=config)
+    return load_problem(config_doc(config))
