@@ -1600,9 +1600,13 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                     if constexpr (TC) {   // this axis' positions of the next iterate, overlapping the check below
                         tc::fence_proxy_async();
                         __syncwarp();
-                        if (lane == 0) {
+                        // warp-uniform operands (broadcast from lane 0) let the MMA take them as uniform
+                        // registers directly instead of a per-lane loop
+                        const uint32_t tb_u = __shfl_sync(0xffffffffu, tbase, 0);
+                        const int slot_u = __shfl_sync(0xffffffffu, slot, 0), ax_u = __shfl_sync(0xffffffffu, ax, 0);
+                        if (tc::elect_one()) {
                             tc::fence_after_sync();
-                            tc_issue_axis(tbase, slot, ax, sp.Cf);
+                            tc_issue_axis(tb_u, slot_u, ax_u, sp.Cf);
                             tc::mma_commit(&sp.sh->mbar);
                         }
                     }
