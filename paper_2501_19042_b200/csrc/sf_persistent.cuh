@@ -1196,12 +1196,16 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
         for (int r = lt; r < R3; r += gsize) load_row<T, NB, MP, TC>(p, sp, sample, r, B6, rhs, PBt);
         slot_barrier(bar_id, gsize);
         if constexpr (TC) {
-            if (lt == 0) {   // positions of the first iterate
-                tc::fence_after_sync();
+            if (lwarp == 0) {   // positions of the first iterate (warp-uniform operands, one elected lane)
+                const uint32_t tb_u = __shfl_sync(0xffffffffu, tbase, 0);
+                const int slot_u = __shfl_sync(0xffffffffu, slot, 0);
+                if (tc::elect_one()) {
+                    tc::fence_after_sync();
 #pragma unroll 1
-                for (int ax = 0; ax < 3; ++ax) {
-                    tc_issue_axis(tbase, slot, ax, sp.Cf);
-                    tc::mma_commit(&sp.sh->mbar);
+                    for (int ax = 0; ax < 3; ++ax) {
+                        tc_issue_axis(tb_u, slot_u, ax, sp.Cf);
+                        tc::mma_commit(&sp.sh->mbar);
+                    }
                 }
             }
         }
