@@ -136,3 +136,17 @@ def test_tensor_core_and_ffma_positions_agree():
     c_tc, c_f = res["tc"]["c"][same], res["ffma"]["c"][same]
     assert np.abs(c_tc - c_f).max() <= 1e-5 * np.abs(c_f).max()
     assert (res["tc"]["f"] == res["ffma"]["f"]).mean() >= 0.97
+
+
+@pytest.mark.parametrize("horizon,count", [(96, 3), (127, 2), (100, 1)])
+def test_tensor_core_positions_horizon_edges(horizon, count):
+    """The tcgen05 position path at the ends of its range: S = 97 (one valid step in the last 8-step
+    chunk), S = 128 (every TMEM lane a real step), and a batch of one sample."""
+    doc, sf, cfg, props = _setup(16, horizon, 9, count, 8, "lean", 10)
+    out = sf.solve_batched(torch.from_numpy(props).cuda(), config=cfg)
+    op = sf_oracle.make_problem(doc, degree=10)
+    coeffs = out.coeffs.cpu().numpy()
+    for b, x in enumerate(props):
+        r = sf_oracle.solve(op, x, max_iters=8, early_stop=False)
+        assert np.abs(coeffs[b] - r.coeffs).max() <= 1e-5 * np.abs(r.coeffs).max(), b
+    assert out.eq_err.max().item() <= 1e-8
