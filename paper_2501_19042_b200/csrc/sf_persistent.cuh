@@ -1233,6 +1233,7 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                 tc::tmem_ld16(ta + 32, *reinterpret_cast<float(*)[16]>(&pos[32]));
                 tc::tmem_wait_ld();
                 tc::fence_before_sync();
+                SGSF_PT(15);   // phase timing: the wait for the position MMAs + TMEM loads
                 if (n < NB) {   // uniform: phantom robots only in the smaller swarms
 #pragma unroll
                     for (int q = 0; q < 3 * RH; ++q)
@@ -1667,16 +1668,16 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
 #ifdef SGSF_PHASE_TIMING
     if (tid == 0)
         printf("PT block %d iters %d total %.0f T1 %.0f T2 %.0f T3bar %.0f dec %.0f G %.0f MX %.0f "
-               "mxG %.0f mxU %.0f mxM %.0f mxP %.0f mxX %.0f mxC %.0f mxE %.0f\n", blockIdx.x, pt_iters,
+               "mxG %.0f mxU %.0f mxM %.0f mxP %.0f mxX %.0f mxC %.0f mxE %.0f t1tc %.0f\n", blockIdx.x, pt_iters,
                (double)(pt_acc[0] + pt_acc[1] + pt_acc[2] + pt_acc[3] + pt_acc[4] + pt_acc[5] + pt_acc[6] + pt_acc[8] +
-                        pt_acc[9] + pt_acc[10] + pt_acc[11] + pt_acc[12] + pt_acc[13] + pt_acc[14]),
-               (double)pt_acc[5] / pt_iters, (double)pt_acc[6] / pt_iters, (double)pt_acc[1] / pt_iters,
+                        pt_acc[9] + pt_acc[10] + pt_acc[11] + pt_acc[12] + pt_acc[13] + pt_acc[14] + pt_acc[15]),
+               (double)(pt_acc[5] + pt_acc[15]) / pt_iters, (double)pt_acc[6] / pt_iters, (double)pt_acc[1] / pt_iters,
                (double)pt_acc[2] / pt_iters, (double)pt_acc[3] / pt_iters,
                (double)(pt_acc[4] + pt_acc[0] + pt_acc[8] + pt_acc[9] + pt_acc[10] + pt_acc[11] + pt_acc[12] + pt_acc[13] +
                         pt_acc[14]) / pt_iters,
                (double)pt_acc[8] / pt_iters, (double)pt_acc[9] / pt_iters, (double)pt_acc[10] / pt_iters,
                (double)pt_acc[11] / pt_iters, (double)pt_acc[12] / pt_iters, (double)pt_acc[13] / pt_iters,
-               (double)pt_acc[14] / pt_iters);
+               (double)pt_acc[14] / pt_iters, (double)pt_acc[15] / pt_iters);
 #endif
 }
 

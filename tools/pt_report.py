@@ -15,6 +15,6 @@ for tag in sys.argv[1:] or ["fixed1", "fixed3", "full"]:
     o = np.argsort(-tot)
     print(tag, "CTAs", len(rows), "slot-0 cycles: max %.3g median %.3g" % (tot.max(), np.median(tot)),
           "| cycles/iter median %.0f max %.0f" % (np.median(per), per.max()))
-    keys = [k for k in ["T1", "T2", "T3bar", "dec", "G", "MX", "mxG", "mxU", "mxM", "mxP", "mxX", "mxC", "mxE", "t1pos", "t1quiet", "t1ws"] if k in rows[0]]
+    keys = [k for k in ["T1", "T2", "T3bar", "dec", "G", "MX", "mxG", "mxU", "mxM", "mxP", "mxX", "mxC", "mxE", "t1tc", "t1pos", "t1quiet", "t1ws"] if k in rows[0]]
     for lab, idx in [("slowest", o[:3]), ("median", o[len(o) // 2 - 1:len(o) // 2 + 2])]:
         print("   ", lab, {k: int(np.mean([rows[i][k] for i in idx])) for k in keys}, "iters", [int(its[i]) for i in idx])
