@@ -1023,6 +1023,17 @@ __device__ __forceinline__ void tc_issue_axis(uint32_t tbase, int slot, int ax, 
             tc::mma_tf32_ts(d, tbase + acol[pr] + 8 * ks, bd + ((bofs[pr] + 256 * ks) >> 4), idesc, (pr | ks) ? 1u : 0u);
 }
 
+// Time step of lane `lane` of warp `lwarp` in a slot of `wps` warps, one thread per step.  Steps go to the
+// warps in 8-step chunks (warp w takes chunks w, w + wps, ...): every warp covers the whole horizon (the
+// exact-path work clusters in time) and 8 consecutive rows keep the 16-byte row accesses conflict-free.
+// The 8 wps-step group that holds the end of the horizon is dealt step by step instead, so the warps get
+// equal step counts (S = 101: 26/25/25/25 instead of 29/24/24/24).
+__host__ __device__ __forceinline__ int step_of(int lwarp, int lane, int wps, int S) {
+    const int g = lane >> 3, base = 8 * wps * g;
+    if (base + 8 * wps <= S) return base + 8 * lwarp + (lane & 7);
+    return base + wps * (lane & 7) + lwarp;
+}
+
 // ---------------------------------------------------------------- the kernel
 // TC = positions by the 3xTF32 tcgen05 GEMM (float, 16 robots, one thread per step, 4 warps per slot)
 template <typename T, int NB, int MP, int MAXT, int TPS, bool TC = false>
@@ -1094,7 +1105,7 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
     if constexpr (TC) {
         const uint32_t tb = tmem_info[0];
         if (tid < 128) {   // A rows: TMEM lane 32 w + l holds the step of lane l of warp w (4 warps per slot)
-            const int w = tid >> 5, l = tid & 31, t = 8 * (w + 4 * (l >> 3)) + (l & 7);
+            const int w = tid >> 5, l = tid & 31, t = step_of(w, l, 4, S);
             float hi[16], lo[16];
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
@@ -1137,11 +1148,9 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
     // time step of this thread and the part of the robots it owns: TPS = 2 puts the two halves
     // of a step in lanes l and l ^ 16 (16 steps per warp); the h = 0 lane owns the step's state
     constexpr int RH = NB / TPS;
-    // TPS = 1: steps are dealt to the warps in chunks of 8 (warp w gets chunks w, w + wps, ...), so
-    // every warp covers the whole horizon -- the exact-path work clusters in time (collisions) and
-    // would otherwise load one warp -- while 8 consecutive rows keep 16-byte row access conflict-free
+    // TPS = 1: steps are dealt to the warps by step_of (8-step chunks over the whole horizon, equal counts)
     const int wpsx = TC ? 4 : p.wps;   // TC: four warps per slot
-    const int ts = TPS == 2 ? lwarp * 16 + (lane & 15) : 8 * (lwarp + wpsx * (lane >> 3)) + (lane & 7);
+    const int ts = TPS == 2 ? lwarp * 16 + (lane & 15) : step_of(lwarp, lane, wpsx, S);
     const int h = TPS == 2 ? lane >> 4 : 0;
     const int r0 = h * RH;
     const bool owner = h == 0;
@@ -1153,6 +1162,9 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
     // clock64 stamps of slot 0 / thread 0 of CTA 0: [0] loop top (after MX barrier), [5] T1 end,
     // [6] T2 end, [1] after the term-pass barrier, [2] after decision, [3] after G, [4] after MX barrier
     long long pt_last = 0, pt_acc[16] = {0};
+    __shared__ long long pt_arrive[4];
+    long long pt_spread = 0;
+    int pt_lastw[4] = {0, 0, 0, 0};
     int pt_prev = -1, pt_iters = 0;
 #define SGSF_PT(ID)                                                                          \
     do {                                                                                      \
@@ -1287,7 +1299,7 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                 const int src = __ffs(qmask) - 1;
                 qmask &= qmask - 1;
                 if (lane == 0) SGSF_COUNT(6, 1);
-                const int tsrc = TPS == 2 ? lwarp * 16 + src : 8 * (lwarp + wpsx * (src >> 3)) + (src & 7);
+                const int tsrc = TPS == 2 ? lwarp * 16 + src : step_of(lwarp, src, wpsx, S);
                 const T* row = Pbase_new + tsrc * RS;
                 T qm = T(1e30), zm = T(1);   // min q over the far pairs, min |component| over all pairs
                 uint32_t words[NPW], nwords[NPW];
@@ -1340,8 +1352,23 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                     sp.psq[lwarp] = wq;
                 }
             }
+#ifdef SGSF_PHASE_TIMING
+            if (slot == 0 && lane == 0 && lwarp < 4) pt_arrive[lwarp] = clock64();   // term-pass barrier arrivals
+#endif
             slot_barrier(bar_id, gsize);
             SGSF_PT(1);
+#ifdef SGSF_PHASE_TIMING
+            if (tid == 0) {   // spread of the four warps' arrivals and which one came last
+                long long lo = pt_arrive[0], hi = pt_arrive[0];
+                int last = 0;
+                for (int w = 1; w < 4; ++w) {
+                    lo = min(lo, pt_arrive[w]);
+                    if (pt_arrive[w] > hi) hi = pt_arrive[w], last = w;
+                }
+                pt_spread += hi - lo;
+                ++pt_lastw[last];
+            }
+#endif
 
             // ---------------- decision (every warp, redundantly): exit residual of iteration k-1, early stop, SingularKKT
             double emax = 0.0, sqs = 0.0;
@@ -1678,6 +1705,9 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                (double)pt_acc[8] / pt_iters, (double)pt_acc[9] / pt_iters, (double)pt_acc[10] / pt_iters,
                (double)pt_acc[11] / pt_iters, (double)pt_acc[12] / pt_iters, (double)pt_acc[13] / pt_iters,
                (double)pt_acc[14] / pt_iters, (double)pt_acc[15] / pt_iters);
+    if (tid == 0)
+        printf("PTW block %d spread %.0f last %d %d %d %d\n", blockIdx.x, (double)pt_spread / pt_iters, pt_lastw[0],
+               pt_lastw[1], pt_lastw[2], pt_lastw[3]);
 #endif
 }
 
