@@ -44,7 +44,8 @@ int launch_persistent(const LaunchInfo& li, SolveParams& p, const sgsf_config_t*
         const char* off = std::getenv("SGSF_NO_TC");
         if (wps == 4 && !(off && off[0] == '1')) {
             tc = true;
-            kern = sf_persistent_kernel<T, NB, MP, MAXT, TPS, true>;
+            kern = p.n == NB ? sf_persistent_kernel<T, NB, MP, MAXT, TPS, true, 1>
+                             : sf_persistent_kernel<T, NB, MP, MAXT, TPS, true, 2>;
         }
     }
     int spb = cfg->slots_per_block;

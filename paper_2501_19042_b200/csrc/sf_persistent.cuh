@@ -1036,7 +1036,9 @@ __host__ __device__ __forceinline__ int step_of(int lwarp, int lane, int wps, in
 
 // ---------------------------------------------------------------- the kernel
 // TC = positions by the 3xTF32 tcgen05 GEMM (float, 16 robots, one thread per step, 4 warps per slot)
-template <typename T, int NB, int MP, int MAXT, int TPS, bool TC = false>
+// FULLN: 0 = both term-pass variants, chosen at run time by n == NB; 1 = only the phantom-free one
+// (n == NB); 2 = only the one with phantoms (n < NB).  A single variant keeps the hot loop's code small.
+template <typename T, int NB, int MP, int MAXT, int TPS, bool TC = false, int FULLN = 0>
 __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParams p) {
     static_assert(!TC || (sizeof(T) == 4 && NB == 16 && TPS == 1 && MP <= 16), "TC positions: float, 16 robots");
     extern __shared__ __align__(16) unsigned char smem[];
@@ -1261,15 +1263,20 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                     for (int w = 0; w < NW; ++w) imask[w] = 0xffffffffu;
                     zprev = false;
                 }
-                const bool full = n == NB;   // uniform: no phantom robots -> guard-free tree reductions
-                const PartStats<T> st = full ? quiet_part<T, NB, RH, TPS, true>(pos, Prow_old, r0, n, fp.beta, smask)
-                                             : quiet_part<T, NB, RH, TPS, false>(pos, Prow_old, r0, n, fp.beta, smask);
+                const bool full = FULLN == 1 || (FULLN == 0 && n == NB);   // no phantom robots: guard-free trees
+                PartStats<T> st;
+                if (FULLN == 1 || (FULLN == 0 && full))
+                    st = quiet_part<T, NB, RH, TPS, FULLN != 2>(pos, Prow_old, r0, n, fp.beta, smask);
+                else
+                    st = quiet_part<T, NB, RH, TPS, false>(pos, Prow_old, r0, n, fp.beta, smask);
                 qinf = st.inf;
                 qsq = st.sq;
                 cum += T(2) * sqrt(st.dmax2) * inv_lat;
                 need_scan = (k == 0) || zprev || !(rmin - cum > T(1) + T(1e-3));
-                zmin_ws = full ? ws_part<T, NB, RH, TPS, true>(pos, r0, h, n, fw, cx, cy, cz, nm, smask)
-                               : ws_part<T, NB, RH, TPS, false>(pos, r0, h, n, fw, cx, cy, cz, nm, smask);
+                if (FULLN == 1 || (FULLN == 0 && full))
+                    zmin_ws = ws_part<T, NB, RH, TPS, FULLN != 2>(pos, r0, h, n, fw, cx, cy, cz, nm, smask);
+                else
+                    zmin_ws = ws_part<T, NB, RH, TPS, false>(pos, r0, h, n, fw, cx, cy, cz, nm, smask);
             }
             __syncwarp();   // both halves of every row written before the owners and the scans read them
             if (ts < S && owner && !need_scan) {   // near pairs of the last scan, exactly (a pair active before is near)
