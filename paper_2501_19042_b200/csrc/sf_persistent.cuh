@@ -14,7 +14,8 @@
 // Term pass: thread t of a slot owns time step t of its sample for ALL
 // robots; the positions of every robot at t live in its registers.  Per
 // iteration k it
-//   T1 evaluates p_k(t) = C_k W[t]^T, the O(n) statistics of the position
+//   T1 evaluates p_k(t) = C_k W[t]^T (TC variant: read from TMEM, where the
+//      3xTF32 tcgen05 GEMM issued at the previous MX commit left it), the O(n) statistics of the position
 //      change and the workspace terms, and decides whether the O(n^2) pair
 //      scan is needed: a motion bound (every pair had normalised distance >=
 //      rmin at the last scan and moved by at most cum since) proves all pairs
@@ -31,13 +32,13 @@
 //      terms with an exactly-zero component rerun on the careful path, which
 //      uses the FP64 reference trig formula.
 // Then every warp takes the stop decision from the per-step partials (no
-// barrier), G forms lam' = lam - rho R W over the active steps only (skipped
-// with its barrier when nothing is active), and MX -- one warp per axis --
+// barrier), and MX -- one warp per axis, FP64 tensor-core (DMMA) tiles -- forms
+// G: lam' = lam - rho R W over the active steps only, then
 // forms the swarm means and the decoupled FP64 xi-step
 //   C_i = Mm Cb + Km11 ub + Md (C_i - Cb) + Kd11 (u_i - ub) + cconst_i,
 //   u = 2 lam' - lam + xi_bar,
-// with the ||A xi - b||_inf check (assembly.py:198-217).  Two slot barriers
-// per quiet iteration.
+// with the ||A xi - b||_inf check (assembly.py:198-217), and (TC) issues the
+// position MMAs of the next iterate.  Two slot barriers per iteration.
 // T is float ("lean") or double ("strict") for positions and term math;
 // state and xi-step are FP64.
 #pragma once
