@@ -44,8 +44,9 @@ int launch_persistent(const LaunchInfo& li, SolveParams& p, const sgsf_config_t*
         const char* off = std::getenv("SGSF_NO_TC");
         if (wps == 4 && !(off && off[0] == '1')) {
             tc = true;
-            kern = p.n == NB ? sf_persistent_kernel<T, NB, MP, MAXT, TPS, true, 1>
-                             : sf_persistent_kernel<T, NB, MP, MAXT, TPS, true, 2>;
+            // (one term-pass variant per instantiation, FULLN = 1 / 2, is 832 instructions smaller but
+            // measured 1% slower)
+            kern = sf_persistent_kernel<T, NB, MP, MAXT, TPS, true>;
         }
     }
     int spb = cfg->slots_per_block;
