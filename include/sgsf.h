@@ -80,7 +80,18 @@ typedef struct {
     int want_prev;        /* also write coefficients of iteration K-1 (for svars) */
     int slots_per_block;  /* 0 = auto (smem/thread budget) */
     int grid;             /* 0 = auto (persistent: #SM x CTAs/SM) */
+    double verdict_tol;   /* tolerance of outputs->verdict (check_original_constraints, metrics.py:57-69) */
 } sgsf_config_t;
+
+/* Verdict outputs (check_original_constraints at tol), device pointers. */
+typedef struct {
+    uint8_t* ok;              /* B: no violation */
+    uint8_t* feasible;        /* B: ok && converged[b] (converged may be NULL -> ok) */
+    double* pair_margin_min;  /* B (+inf when n == 1) */
+    double* ws_margin_max;    /* B */
+    int32_t* pair_viol;       /* B */
+    int32_t* ws_viol;         /* B */
+} sgsf_verdict_t;
 
 /* Per-sample outputs, device pointers, caller-owned. dim = 3 n m1. */
 typedef struct {
@@ -94,17 +105,11 @@ typedef struct {
     int32_t* status;        /* B: SGSF_SAMPLE_* */
     double* eq_err;         /* B: ||A xi - b||_inf of the returned iterate */
     double* coeffs_prev;    /* B x dim, nullable (needs cfg.want_prev) */
+    /* nullable: the feasible verdict of the returned iterates at cfg->verdict_tol (sgsf_verdict, launched
+       right behind the solve kernel on the same stream); NULL fields are skipped */
+    const sgsf_verdict_t* verdict;
 } sgsf_outputs_t;
 
-/* Verdict outputs (check_original_constraints at tol), device pointers. */
-typedef struct {
-    uint8_t* ok;              /* B: no violation */
-    uint8_t* feasible;        /* B: ok && converged[b] (converged may be NULL -> ok) */
-    double* pair_margin_min;  /* B (+inf when n == 1) */
-    double* ws_margin_max;    /* B */
-    int32_t* pair_viol;       /* B */
-    int32_t* ws_viol;         /* B */
-} sgsf_verdict_t;
 
 typedef struct {
     void* start;   /* cudaEvent_t recorded just before the main solve kernel (nullable) */

@@ -100,23 +100,8 @@ __global__ void verdict_kernel(AuxParams a, int batch, const double* __restrict_
                 a2 = wa2;
                 b2 = wb2;
             }
-            // the reference margin, with its divisions (exact), is needed only near a decision: the
-            // reciprocal form differs from it by a few ulps of |q|, far below the slack
-            auto exact = [&]() {
-                return __dadd_rn(__dadd_rn(__ddiv_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), a2),
-                                           __ddiv_rn(__dmul_rn(dz, dz), b2)), -1.0);
-            };
-            const double ma = fma(dz * dz, term < P ? inv_ib2 : inv_wb2, (dx * dx + dy * dy) * (term < P ? inv_ia2 : inv_wa2)) - 1.0;
-            const double slack = 1e-12 * (1.0 + fabs(ma));
-            if (term < P) {
-                if (ma < pmin + slack) pmin = fmin(pmin, exact());
-                if (ma < -tol - slack) ++pc;
-                else if (ma <= -tol + slack) pc += (exact() < -tol);
-            } else {
-                if (ma > wmax - slack) wmax = fmax(wmax, exact());
-                if (ma > tol + slack) ++wc;
-                else if (ma >= tol - slack) wc += (exact() > tol);
-            }
+            verdict_term(term < P, dx, dy, dz, a2, b2, term < P ? inv_ia2 : inv_wa2, term < P ? inv_ib2 : inv_wb2, tol,
+                         pmin, wmax, pc, wc);
         }
     }
     red_min[threadIdx.x] = pmin;

@@ -204,3 +204,32 @@ __device__ __forceinline__ void target_generic(T dx, T dy, T dz, const Family<T>
 }
 
 }  // namespace sgsf
+
+namespace sgsf {
+
+// One term of the feasible verdict (check_original_constraints, assembly.py:437-487; margins as
+// problem.py:113-137: ((dx^2 + dy^2) / a^2 + dz^2 / b^2) - 1).  Pairs must keep margin >= -tol, workspace
+// terms margin <= tol.  The reciprocal form screens; the reference's divisions (exact) decide the terms
+// within a few ulps of a threshold and the extremes.  Shared by the standalone verdict kernel and K1's
+// fused epilogue, so both give the same bits.
+__device__ __forceinline__ void verdict_term(bool pair, double dx, double dy, double dz, double a2, double b2,
+                                             double inv_a2, double inv_b2, double tol, double& pmin, double& wmax,
+                                             int& pc, int& wc) {
+    auto exact = [&]() {
+        return __dadd_rn(__dadd_rn(__ddiv_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), a2),
+                                   __ddiv_rn(__dmul_rn(dz, dz), b2)), -1.0);
+    };
+    const double ma = fma(dz * dz, inv_b2, (dx * dx + dy * dy) * inv_a2) - 1.0;
+    const double slack = 1e-12 * (1.0 + fabs(ma));
+    if (pair) {
+        if (ma < pmin + slack) pmin = fmin(pmin, exact());
+        if (ma < -tol - slack) ++pc;
+        else if (ma <= -tol + slack) pc += (exact() < -tol);
+    } else {
+        if (ma > wmax - slack) wmax = fmax(wmax, exact());
+        if (ma > tol + slack) ++wc;
+        else if (ma >= tol - slack) wc += (exact() > tol);
+    }
+}
+
+}  // namespace sgsf

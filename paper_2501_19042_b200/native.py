@@ -32,14 +32,14 @@ class Problem(C.Structure):
 class Config(C.Structure):
     _fields_ = [("max_iters", C.c_int), ("tol_residual", C.c_double), ("tol_eq", C.c_double),
                 ("early_stop", C.c_int), ("precision", C.c_int), ("want_prev", C.c_int),
-                ("slots_per_block", C.c_int), ("grid", C.c_int)]
+                ("slots_per_block", C.c_int), ("grid", C.c_int), ("verdict_tol", C.c_double)]
 
 
 class Outputs(C.Structure):
     _fields_ = [("coeffs", C.c_void_p), ("multipliers", C.c_void_p), ("res_inf", C.c_void_p),
                 ("res_l2", C.c_void_p), ("iterations", C.c_void_p), ("converged", C.c_void_p),
                 ("displacement", C.c_void_p), ("status", C.c_void_p), ("eq_err", C.c_void_p),
-                ("coeffs_prev", C.c_void_p)]
+                ("coeffs_prev", C.c_void_p), ("verdict", C.c_void_p)]
 
 
 class Verdict(C.Structure):

@@ -8,7 +8,7 @@ the step functions ``spherical_step`` / ``multiplier_update`` /
 keeps working.
 
 Underneath, one ``batch_solve`` is ONE launch of the persistent kernel over
-the whole batch (``sgsf_solve``) plus one verdict launch; ``threads`` is
+the whole batch (``sgsf_solve``, with the verdict in its epilogue); ``threads`` is
 accepted and recorded but has no effect.  ``SafetyFilter.solve_batched`` is
 the tensor-native fast path (device tensors in and out, no per-sample Python).
 
@@ -327,11 +327,15 @@ class SafetyFilter:
         lib = native.load()
         handle = self.operator.handle(cfg.rho, dev)
         ccfg = native.Config(int(mi), float(cfg.tol_residual), float(cfg.tol_eq), int(bool(cfg.early_stop)),
-                             _PRECISIONS[cfg.precision], int(bool(want_prev)), int(slots_per_block), int(grid))
+                             _PRECISIONS[cfg.precision], int(bool(want_prev)), int(slots_per_block), int(grid),
+                             float(verdict_tol))
+        # the feasible verdict rides in the solve: K1's per-sample epilogue (n <= 32), else a verdict launch
+        v = native.Verdict(None, out.feasible.data_ptr(), None, None, None, None) if verdict else None
         o = native.Outputs(out.coeffs.data_ptr(), out.multipliers.data_ptr(), out.residual_inf.data_ptr(),
                            out.residual_l2.data_ptr(), out.iterations.data_ptr(), out.converged.data_ptr(),
                            out.displacement.data_ptr(), out.status.data_ptr(), out.eq_err.data_ptr(),
-                           out.coeffs_prev.data_ptr() if want_prev else None)
+                           out.coeffs_prev.data_ptr() if want_prev else None,
+                           native.C.addressof(v) if v is not None else None)
         ws = torch.empty(int(lib.sgsf_workspace_bytes(B)), dtype=torch.uint8, device=dev)
         tm = None
         if timing is not None:
@@ -345,10 +349,6 @@ class SafetyFilter:
                                 native.ptr(init_mode), native.C.byref(ccfg), native.C.byref(o), ws.data_ptr(),
                                 native.C.byref(tm) if tm is not None else None, stream)
             native.check(rc, "sgsf_solve")
-            if verdict:
-                v = native.Verdict(None, out.feasible.data_ptr(), None, None, None, None)
-                native.check(lib.sgsf_verdict(handle, B, out.coeffs.data_ptr(), out.converged.data_ptr(),
-                                              float(verdict_tol), native.C.byref(v), stream), "sgsf_verdict")
         return out
 
     def svars_of(self, coeffs: torch.Tensor) -> list:
