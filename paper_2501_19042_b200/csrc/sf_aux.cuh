@@ -55,7 +55,8 @@ __global__ void verdict_kernel(AuxParams a, int batch, const double* __restrict_
     const int n = a.n, S = a.S, m1 = a.m1, P = a.P, dim = 3 * n * m1;
     double* C = (double*)sm;
     double* pos = C + dim;                       // 3 x n x AUX_TCH (a window of time steps)
-    double* red_min = pos + 3 * n * AUX_TCH;     // blockDim
+    double* Ww = pos + 3 * n * AUX_TCH;          // the window's W rows, AUX_TCH x m1
+    double* red_min = Ww + AUX_TCH * m1;         // per warp
     double* red_max = red_min + blockDim.x;
     int* red_pc = (int*)(red_max + blockDim.x);
     int* red_wc = red_pc + blockDim.x;
@@ -76,9 +77,11 @@ __global__ void verdict_kernel(AuxParams a, int batch, const double* __restrict_
     for (int t0 = 0; t0 < S; t0 += AUX_TCH) {
         const int tc = min(AUX_TCH, S - t0);
         __syncthreads();
+        for (int e = threadIdx.x; e < tc * m1; e += blockDim.x) Ww[e] = a.W[t0 * m1 + e];
+        __syncthreads();
         for (int e = threadIdx.x; e < 3 * n * tc; e += blockDim.x) {
             const int row = e / tc, t = e - row * tc;
-            pos[row * AUX_TCH + t] = eval_pos(C + row * m1, a.W + (t0 + t) * m1, m1);
+            pos[row * AUX_TCH + t] = eval_pos(C + row * m1, Ww + t * m1, m1);
         }
         __syncthreads();
         for (int e = threadIdx.x; e < (P + n) * AUX_TCH; e += blockDim.x) {
@@ -104,13 +107,24 @@ __global__ void verdict_kernel(AuxParams a, int batch, const double* __restrict_
                          pmin, wmax, pc, wc);
         }
     }
-    red_min[threadIdx.x] = pmin;
-    red_max[threadIdx.x] = wmax;
-    red_pc[threadIdx.x] = pc;
-    red_wc[threadIdx.x] = wc;
+    // warp reductions, then one combine over the warps (min / max exact, integer counts: any order)
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        pmin = fmin(pmin, __shfl_xor_sync(0xffffffffu, pmin, off));
+        wmax = fmax(wmax, __shfl_xor_sync(0xffffffffu, wmax, off));
+    }
+    pc = __reduce_add_sync(0xffffffffu, pc);
+    wc = __reduce_add_sync(0xffffffffu, wc);
+    const int warp = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        red_min[warp] = pmin;
+        red_max[warp] = wmax;
+        red_pc[warp] = pc;
+        red_wc[warp] = wc;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
-        for (int q = 1; q < blockDim.x; ++q) {
+        for (int q = 1; q < (int)(blockDim.x >> 5); ++q) {
             pmin = fmin(pmin, red_min[q]);
             wmax = fmax(wmax, red_max[q]);
             pc += red_pc[q];

@@ -265,7 +265,7 @@ int sgsf_verdict(sgsf_handle_t* h, int batch, const double* coeffs, const uint8_
     if (!h || !out || (batch > 0 && !coeffs)) return fail(SGSF_ERR_INVALID, "null argument");
     if (batch == 0) return SGSF_OK;
     const int threads = 256;
-    const size_t smem = (size_t)(3 * h->n * h->m1 + 3 * h->n * AUX_TCH) * sizeof(double) +
+    const size_t smem = (size_t)(3 * h->n * h->m1 + 3 * h->n * AUX_TCH + AUX_TCH * h->m1) * sizeof(double) +
                         threads * (2 * sizeof(double) + 2 * sizeof(int)) + (size_t)h->P * sizeof(int);
     CUDA_TRY(cudaFuncSetAttribute(verdict_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     verdict_kernel<<<batch, threads, smem, (cudaStream_t)stream>>>(aux_params(h), batch, coeffs, converged, tol,
