@@ -129,13 +129,32 @@ __global__ void __launch_bounds__(kOrderThreads) lpt_order_kernel(const float* _
     };
     for (int b = threadIdx.x; b < batch; b += blockDim.x) atomicAdd(&cnt[bucket(score[b])], 1u);
     __syncthreads();
-    if (threadIdx.x == 0) {   // exclusive scan (2048 entries, once per solve)
-        unsigned int run = 0;
-        for (int k = 0; k < kOrderBuckets; ++k) {
-            const unsigned int c = cnt[k];
-            cnt[k] = run;
-            run += c;
+    {   // exclusive scan of the 2048 counts: two per thread, warp scans, then the warp totals
+        static_assert(kOrderBuckets == 2 * kOrderThreads, "two buckets per thread");
+        __shared__ unsigned int wsum[kOrderThreads / 32];
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        const unsigned int c0 = cnt[2 * threadIdx.x], c1 = cnt[2 * threadIdx.x + 1];
+        unsigned int incl = c0 + c1;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const unsigned int y = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += y;
         }
+        if (lane == 31) wsum[warp] = incl;
+        __syncthreads();
+        if (warp == 0) {   // scan of the 32 warp totals
+            unsigned int w = wsum[lane];
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const unsigned int y = __shfl_up_sync(0xffffffffu, w, off);
+                if (lane >= off) w += y;
+            }
+            wsum[lane] = w;   // inclusive
+        }
+        __syncthreads();
+        const unsigned int base = (warp ? wsum[warp - 1] : 0u) + incl - (c0 + c1);
+        cnt[2 * threadIdx.x] = base;
+        cnt[2 * threadIdx.x + 1] = base + c0;
     }
     __syncthreads();
     for (int b = threadIdx.x; b < batch; b += blockDim.x) order[atomicAdd(&cnt[bucket(score[b])], 1u)] = b;
