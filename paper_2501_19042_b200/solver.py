@@ -329,7 +329,7 @@ class SafetyFilter:
         ccfg = native.Config(int(mi), float(cfg.tol_residual), float(cfg.tol_eq), int(bool(cfg.early_stop)),
                              _PRECISIONS[cfg.precision], int(bool(want_prev)), int(slots_per_block), int(grid),
                              float(verdict_tol))
-        # the feasible verdict rides in the solve: K1's per-sample epilogue (n <= 32), else a verdict launch
+        # the feasible verdict rides in the solve call: sgsf_solve launches it right behind the solve kernel
         v = native.Verdict(None, out.feasible.data_ptr(), None, None, None, None) if verdict else None
         o = native.Outputs(out.coeffs.data_ptr(), out.multipliers.data_ptr(), out.residual_inf.data_ptr(),
                            out.residual_l2.data_ptr(), out.iterations.data_ptr(), out.converged.data_ptr(),
