@@ -1,0 +1,61 @@
+"""(box) Randomised parity sweep of the solve kernels against the CPU oracle at a fixed iteration count.
+
+Random (n, H, degree, precision, seed) cases; each solves a few proposals for 10 iterations with early
+stop off and compares coefficients and residual histories with oracle/sf_oracle.py (lean 1e-5 / 1e-3,
+strict 1e-9 / 1e-7 relative; histories with the tests' 1e-9 absolute floor).  Prints one line per case and a summary; exit code 1 on any failure.
+
+    python tools/fuzz_parity.py [cases] [seed]
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from oracle import sf_oracle  # noqa: E402
+from paper_2501_19042_b200 import SafetyFilter, SolverConfig, sample_proposals  # noqa: E402
+from paper_2501_19042_b200.problem import load_problem  # noqa: E402
+from paper_2501_19042_b200.scenarios import random_swarm_doc  # noqa: E402
+
+
+def main():
+    cases = int(sys.argv[1]) if len(sys.argv) > 1 else 40
+    rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 0)
+    fails = 0
+    for c in range(cases):
+        n = int(rng.integers(2, 17))
+        H = int(rng.choice([20, 50, 96, 100, 127]))
+        degree = int(rng.integers(7, 16))
+        precision = "strict" if rng.random() < 0.3 else "lean"
+        if precision == "strict" and H > 100:
+            H = 100
+        seed = int(rng.integers(0, 1000))
+        spread = float(rng.choice([0.25, 0.6, 1.2]))
+        doc = random_swarm_doc(n, H, seed)
+        prob = load_problem(doc)
+        cfg = SolverConfig(max_iters=10, early_stop=False, svars=False, precision=precision)
+        sf = SafetyFilter(prob, degree=degree, config=cfg)
+        props = sample_proposals(prob, sf.basis, 2, seed=seed, spread=spread).proposals
+        out = sf.solve_batched(torch.from_numpy(props).cuda(), config=cfg)
+        op = sf_oracle.make_problem(doc, degree=degree)
+        ctol, htol = (1e-5, 1e-3) if precision == "lean" else (1e-9, 1e-7)
+        worst_c = worst_h = 0.0
+        for b, x in enumerate(props):
+            r = sf_oracle.solve(op, x, max_iters=10, early_stop=False)
+            worst_c = max(worst_c, float(np.abs(out.coeffs[b].cpu().numpy() - r.coeffs).max() / np.abs(r.coeffs).max()))
+            # the tests' criterion: |h - r| <= atol + rtol |r| with atol = 1e-9 (a proposal already at a fixed
+            # point has residuals of ~1e-14, where only the absolute bound is meaningful)
+            h = out.residual_inf[b].cpu().numpy()
+            worst_h = max(worst_h, float(np.max(np.abs(h - r.residual_inf) / (1e-9 / htol + np.abs(r.residual_inf)))))
+        ok = worst_c <= ctol and worst_h <= htol and out.eq_err.max().item() <= 1e-8
+        fails += not ok
+        print(f"case {c:2d} n={n:2d} H={H:3d} deg={degree:2d} {precision:6s} spread={spread:4.2f}: coeff {worst_c:.2e} "
+              f"hist {worst_h:.2e} {'ok' if ok else 'FAIL'}", flush=True)
+    print(f"{cases - fails}/{cases} cases within tolerance")
+    sys.exit(1 if fails else 0)
+
+
+if __name__ == "__main__":
+    main()
