@@ -4,7 +4,7 @@ Random (n, H, degree, precision, seed) cases; each solves a few proposals for 10
 stop off and compares coefficients and residual histories with oracle/sf_oracle.py (lean 1e-5 / 1e-3,
 strict 1e-9 / 1e-7 relative; histories with the tests' 1e-9 absolute floor).  Prints one line per case and a summary; exit code 1 on any failure.
 
-    python tools/fuzz_parity.py [cases] [seed]
+    python tools/fuzz_parity.py [cases] [seed] [large]
 """
 import os
 import sys
@@ -23,10 +23,11 @@ from paper_2501_19042_b200.scenarios import random_swarm_doc  # noqa: E402
 def main():
     cases = int(sys.argv[1]) if len(sys.argv) > 1 else 40
     rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 0)
+    large = len(sys.argv) > 3 and sys.argv[3] == "large"   # 17..64 robots: the two-lane and K1L families
     fails = 0
     for c in range(cases):
-        n = int(rng.integers(2, 17))
-        H = int(rng.choice([20, 50, 96, 100, 127]))
+        n = int(rng.integers(17, 65)) if large else int(rng.integers(2, 17))
+        H = int(rng.choice([20, 40])) if large else int(rng.choice([20, 50, 96, 100, 127]))
         degree = int(rng.integers(7, 16))
         precision = "strict" if rng.random() < 0.3 else "lean"
         if precision == "strict" and H > 100:
