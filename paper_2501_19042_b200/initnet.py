@@ -107,6 +107,51 @@ def train_init_net(sf, net: InitNet, proposals: torch.Tensor, iters: int = 10, s
     return log
 
 
+def train_init_net_multi(scenarios, net: InitNet, iters: int = 10, steps: int = 200, batch: int = 256,
+                         per_step: int = 4, lr: float = 1e-3, seed: int = 0) -> TrainLog:
+    """Training over several problems of the same shape (n, degree, horizon): ``scenarios`` is a list of
+    (SafetyFilter, (N, dim) proposal pool) pairs.  Every step mixes ``per_step`` scenarios (round-robin)
+    in one network batch, so the batch-norm statistics see several contexts, as they will at evaluation;
+    each scenario's slice then runs through its own unrolled SF.  The network learns a start/goal-
+    context-specific initialisation (PAPER.md "Learned Initialization for SF")."""
+    dev = scenarios[0][1].device
+    net.to(dev).train()
+    ctxs = [torch.as_tensor(context_features(sf.problem), device=dev) for sf, _ in scenarios]
+    opt = torch.optim.Adam(net.parameters(), lr=lr)
+    gen = torch.Generator(device="cpu").manual_seed(seed)
+    log = TrainLog()
+    t0 = time.perf_counter()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sub = max(1, batch // per_step)
+    for k in range(steps):
+        picks = [(k * per_step + u) % len(scenarios) for u in range(per_step)]
+        xbs, cs = [], []
+        for s_i in picks:
+            pool = scenarios[s_i][1]
+            idx = torch.randint(0, pool.shape[0], (min(sub, pool.shape[0]),), generator=gen).to(dev)
+            xbs.append(pool[idx])
+            cs.append(ctxs[s_i].expand(xbs[-1].shape[0], -1, -1))
+        xi0, lam0 = net(torch.cat(cs), torch.cat(xbs))
+        start.record()
+        loss, o = 0.0, 0
+        for s_i, xb in zip(picks, xbs):
+            m = xb.shape[0]
+            it = unrolled_solve(scenarios[s_i][0], xb, xi0[o:o + m], lam0[o:o + m], iters=iters)
+            loss = loss + fixed_point_loss(it, xb, reduction="sum")
+            o += m
+        loss = loss / o
+        opt.zero_grad(set_to_none=True)
+        loss.backward()
+        stop.record()
+        opt.step()
+        stop.synchronize()
+        log.sf_seconds += start.elapsed_time(stop) / 1e3
+        log.losses.append(float(loss.detach()))
+        log.steps += 1
+    log.seconds = time.perf_counter() - t0
+    return log
+
+
 def initial_states(sf, proposals: torch.Tensor, strategy: str, net: InitNet | None = None):
     """(xi_0, lambda_0) of one strategy: zero vectors, the raw proposal, its boundary projection (the
     reference default, solver.py:264-284), or the init net's prediction."""

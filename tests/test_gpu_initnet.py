@@ -27,3 +27,18 @@ def test_training_lowers_the_loss_and_sweep_runs():
     for s, r in res.items():
         assert 1 <= r["mean_iterations"] <= 300 and 0 <= r["converged"] <= 1
         assert len(r["residual_trace"]) == 20
+
+
+def test_multi_scenario_training_runs():
+    """train_init_net_multi: mixed-context batches through several problems' unrolled SFs."""
+    from paper_2501_19042_b200 import SafetyFilter, SolverConfig, sample_proposals
+    from paper_2501_19042_b200.initnet import InitNet, train_init_net_multi
+    from paper_2501_19042_b200.scenarios import random_swarm
+    torch.manual_seed(0)
+    scen = []
+    for s in range(3):
+        sf = SafetyFilter(random_swarm(8, 20, seed=10 + s), config=SolverConfig())
+        scen.append((sf, torch.from_numpy(sample_proposals(sf.problem, sf.basis, 128, seed=1).proposals).cuda()))
+    net = InitNet(8, scen[0][0].coeff_dim)
+    log = train_init_net_multi(scen, net, iters=3, steps=12, batch=96, per_step=3)
+    assert log.steps == 12 and np.isfinite(log.losses).all() and log.sf_seconds > 0
