@@ -28,8 +28,7 @@ import torch
 from torch import nn
 
 from .initnet import context_features
-from .proposals import straight_line_coeffs
-from .unrolled import boundary_projection
+from .unrolled import boundary_projection, device_constants_of
 
 
 def latent_length(n: int) -> int:
@@ -128,9 +127,8 @@ def make_decoder(kind: str, n: int, m1: int = 11, **kw) -> nn.Module:
 def decode_proposals(sf, decoder: nn.Module, latent: torch.Tensor) -> torch.Tensor:
     """xi_bar (B, dim) float64 on the decoder's device: the straight line plus the decoder's correction,
     through the boundary QP layer (projection.py:11-25)."""
-    dev = latent.device
-    state = torch.as_tensor(context_features(sf.problem), dtype=torch.float32, device=dev)
-    base = torch.as_tensor(straight_line_coeffs(sf.problem, sf.basis), dtype=torch.float64, device=dev)
+    k = device_constants_of(sf, latent.device)
+    state, base = k["context"].to(torch.float32), k["base"]
     corr = decoder(latent, state.expand(latent.shape[0], -1, -1)).to(torch.float64)
     return boundary_projection(sf, base + corr)
 

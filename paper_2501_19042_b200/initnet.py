@@ -167,7 +167,8 @@ def initial_states(sf, proposals: torch.Tensor, strategy: str, net: InitNet | No
             raise ValueError("strategy 'initnet' needs a network")
         net.eval()
         with torch.no_grad():
-            ctx = torch.as_tensor(context_features(sf.problem), device=proposals.device)
+            from .unrolled import device_constants_of
+            ctx = device_constants_of(sf, proposals.device)["context"]
             return net(ctx.expand(proposals.shape[0], -1, -1), proposals)
     raise ValueError(f"unknown strategy {strategy!r}; choose from {list(STRATEGIES)}")
 

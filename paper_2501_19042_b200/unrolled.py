@@ -62,15 +62,32 @@ class _Unrolled(torch.autograd.Function):
         return g_xb, g_x0, g_l0, None, None
 
 
+def device_constants_of(sf, device) -> dict:
+    """Per-(filter, device) cache of the small constants the torch-side layers need (boundary rows,
+    projector, endpoint rhs, straight-line coefficients, start/goal context), uploaded once so the
+    decoder -> QP layer -> SF pipeline makes no host transfers per call."""
+    cache = sf.__dict__.setdefault("_device_consts", {})
+    key = (str(torch.device(device)), float(sf.config.rho))
+    if key not in cache:
+        from .initnet import context_features
+        from .proposals import straight_line_coeffs
+        k = sf.operator.constants(sf.config.rho)
+        f64 = dict(dtype=torch.float64, device=device)
+        cache[key] = {
+            "B": torch.as_tensor(k.B, **f64), "PBt": torch.as_tensor(k.PBt, **f64),
+            "rhs": torch.as_tensor(k.rhs, **f64), "n": k.n, "m1": k.m1,
+            "base": torch.as_tensor(straight_line_coeffs(sf.problem, sf.basis), **f64),
+            "context": torch.as_tensor(context_features(sf.problem), **f64),
+        }
+    return cache[key]
+
+
 def boundary_projection(sf, xi_bar: torch.Tensor) -> torch.Tensor:
     """The default start xi_0 = xi_bar - B^T (B B^T)^-1 (B xi_bar - b) per robot and axis
     (``projection.py:11-25``) as torch ops, so gradients reach the proposal through it."""
-    k = sf.operator.constants(sf.config.rho)
-    dev = xi_bar.device
-    Bm = torch.as_tensor(k.B, dtype=torch.float64, device=dev)          # (6, m1)
-    PBt = torch.as_tensor(k.PBt, dtype=torch.float64, device=dev)       # (m1, 6)
-    rhs = torch.as_tensor(k.rhs, dtype=torch.float64, device=dev)       # (3, n, 6)
-    C = xi_bar.reshape(xi_bar.shape[0], 3, k.n, k.m1)
+    k = device_constants_of(sf, xi_bar.device)
+    Bm, PBt, rhs = k["B"], k["PBt"], k["rhs"]   # (6, m1), (m1, 6), (3, n, 6)
+    C = xi_bar.reshape(xi_bar.shape[0], 3, k["n"], k["m1"])
     res = C @ Bm.T - rhs
     return (C - res @ PBt.T).reshape(xi_bar.shape)
 
