@@ -74,7 +74,15 @@ from .metrics import (
     spherical_targets,
     write_csv,
 )
-from .generative import CVAEDecoder, VQVAEDecoder, calibrate_batchnorm, decode_proposals, generate_and_filter, make_decoder
+from .generative import (
+    CVAEDecoder,
+    PipelineGraph,
+    VQVAEDecoder,
+    calibrate_batchnorm,
+    decode_proposals,
+    generate_and_filter,
+    make_decoder,
+)
 from .unrolled import UnrolledIterates, boundary_projection, fixed_point_loss, unrolled_solve
 from .verdict import (
     ViolationReport,

@@ -32,3 +32,26 @@ def test_decoder_gpu_matches_cpu_and_pipeline(kind, config):
     assert (out.status == 0).all() and out.eq_err.max().item() <= 1e-8
     ref = sf.solve_batched(xb)
     assert torch.equal(ref.coeffs, out.coeffs) and torch.equal(ref.iterations, out.iterations)
+
+
+def test_pipeline_graph_replays_the_eager_pipeline():
+    """The CUDA-graph pipeline (config 1 size) gives the eager pipeline's results bit for bit, for the
+    captured latent and for a new one copied in."""
+    from paper_2501_19042_b200 import SafetyFilter, SolverConfig
+    from paper_2501_19042_b200.generative import PipelineGraph, calibrate_batchnorm, decode_proposals, make_decoder
+    from paper_2501_19042_b200.scenarios import config_problem
+    prob = config_problem(1)
+    cfg = SolverConfig(max_iters=100, svars=False)
+    sf = SafetyFilter(prob, config=cfg)
+    torch.manual_seed(3)
+    dec = calibrate_batchnorm(sf, make_decoder("cvae", prob.n).cuda())
+    g = PipelineGraph(sf, dec, 8, config=cfg, seed=1)
+    for latent in (g.latent.clone(), dec.sample_latent(8, torch.Generator(device="cuda").manual_seed(9), "cuda")):
+        xb, out = g.replay(latent)
+        with torch.no_grad():
+            xe = decode_proposals(sf, dec, latent)
+        ref = sf.solve_batched(xe, config=cfg)
+        torch.cuda.synchronize()
+        assert torch.equal(xb, xe)
+        assert torch.equal(out.coeffs, ref.coeffs) and torch.equal(out.iterations, ref.iterations)
+        assert torch.equal(out.feasible, ref.feasible)

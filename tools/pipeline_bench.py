@@ -53,14 +53,47 @@ def run(config, kind, batch, max_iters, reps=3):
 
 def main():
     rows = [run(*c) for c in CASES]
+    graph = graph_vs_eager()
     os.makedirs("gpurun_out", exist_ok=True)
     with open("gpurun_out/pipeline.json", "w") as fh:
         json.dump({"note": "random-init decoders (no trained weights exist offline); all stages on one B200",
-                   "rows": rows}, fh, indent=1)
+                   "rows": rows, "config1_graph": graph}, fh, indent=1)
     for r in rows:
         print(f"config {r['config']} {r['decoder']:5s} B={r['batch']:5d}: decode+QP {r['decode_qp_ms']:.2f} ms, "
               f"SF+verdict {r['sf_verdict_ms']:.2f} ms, iterations {r['mean_iterations']:.1f}, "
               f"converged {r['converged']:.3f}, feasible {r['feasible']:.3f}")
+
+
+
+def graph_vs_eager(reps=20):
+    """Config 1 (8 samples, launch-bound): the eager pipeline against its CUDA-graph replay."""
+    from paper_2501_19042_b200.generative import PipelineGraph
+    prob = config_problem(1)
+    cfg = SolverConfig(max_iters=100, svars=False)
+    sf = SafetyFilter(prob, config=cfg)
+    torch.manual_seed(0)
+    dec = calibrate_batchnorm(sf, make_decoder("cvae", prob.n).cuda())
+    g = PipelineGraph(sf, dec, 8, config=cfg)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(3):
+        g.replay()
+    s.record()
+    for _ in range(reps):
+        g.replay()
+    e.record()
+    e.synchronize()
+    graph_ms = s.elapsed_time(e) / reps
+    with torch.no_grad():
+        for _ in range(3):
+            sf.solve_batched(decode_proposals(sf, dec, g.latent), config=cfg)
+        s.record()
+        for _ in range(reps):
+            sf.solve_batched(decode_proposals(sf, dec, g.latent), config=cfg)
+        e.record()
+        e.synchronize()
+    eager_ms = s.elapsed_time(e) / reps
+    print(f"config 1 pipeline (decode + QP + SF + verdict, 8 samples): eager {eager_ms:.2f} ms, CUDA graph {graph_ms:.2f} ms")
+    return {"eager_ms": eager_ms, "graph_ms": graph_ms}
 
 
 if __name__ == "__main__":
