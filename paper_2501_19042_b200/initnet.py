@@ -80,31 +80,8 @@ class TrainLog:
 def train_init_net(sf, net: InitNet, proposals: torch.Tensor, iters: int = 10, steps: int = 200,
                    batch: int = 256, lr: float = 1e-3, seed: int = 0) -> TrainLog:
     """Self-supervised training on a (N, dim) float64 CUDA pool of proposals of one problem."""
-    dev = proposals.device
-    net.to(dev).train()
-    ctx = torch.as_tensor(context_features(sf.problem), device=dev)
-    opt = torch.optim.Adam(net.parameters(), lr=lr)
-    gen = torch.Generator(device="cpu").manual_seed(seed)
-    log = TrainLog()
-    t0 = time.perf_counter()
-    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    for _ in range(steps):
-        idx = torch.randint(0, proposals.shape[0], (min(batch, proposals.shape[0]),), generator=gen).to(dev)
-        xb = proposals[idx]
-        xi0, lam0 = net(ctx.expand(xb.shape[0], -1, -1), xb)
-        start.record()
-        it = unrolled_solve(sf, xb, xi0, lam0, iters=iters)
-        loss = fixed_point_loss(it, xb)
-        opt.zero_grad(set_to_none=True)
-        loss.backward()
-        stop.record()
-        opt.step()
-        stop.synchronize()
-        log.sf_seconds += start.elapsed_time(stop) / 1e3
-        log.losses.append(float(loss.detach()))
-        log.steps += 1
-    log.seconds = time.perf_counter() - t0
-    return log
+    return train_init_net_multi([(sf, proposals)], net, iters=iters, steps=steps, batch=batch, per_step=1, lr=lr,
+                                seed=seed)
 
 
 def train_init_net_multi(scenarios, net: InitNet, iters: int = 10, steps: int = 200, batch: int = 256,
