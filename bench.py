@@ -175,11 +175,14 @@ def run_reference(args, rank: int, world: int) -> None:
     doc = prob.to_doc()
     steps = []
     total_feas = total_samples = 0
+    # per-step CPU budget: --ref-budget, or ~150 s over the timed steps (1.5-12 s each: at least one
+    # round of proposals per core), so the whole --steps K --warmup W run stays within a few minutes
+    budget = args.ref_budget if args.ref_budget is not None else min(12.0, max(1.5, 150.0 / max(1, args.steps)))
     for _ in range(args.warmup):
         cpu_sample(doc, shard, budget_s=0.0, max_samples=os.cpu_count() or 1)
     for k in range(args.steps):
         off = (k * (os.cpu_count() or 1)) % len(shard)
-        r = cpu_sample(doc, list(shard[off:]) + list(shard[:off]), budget_s=args.ref_budget)
+        r = cpu_sample(doc, list(shard[off:]) + list(shard[:off]), budget_s=budget)
         steps.append(r)
         total_feas += r["feasible"]
         total_samples += r["samples"]
@@ -359,7 +362,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         "clocks": clocks.summary(local_rank) if clocks else None,
     }
     if args.cpu_baseline and world == 1:
-        cb = cpu_sample(prob.to_doc(), shard, budget_s=args.ref_budget)
+        cb = cpu_sample(prob.to_doc(), shard, budget_s=args.ref_budget if args.ref_budget is not None else 12.0)
         v = cb["feasible"] / cb["wall_s"]
         line["cpu_baseline"] = {"value": v, "unit": "feasible samples/s", "cores": cb["cores"], "kind": "port",
                                 "sample": f"{cb['samples']} proposals of this batch, all iterations "
@@ -386,7 +389,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=BATCH_PER_GPU)
     ap.add_argument("--precision", default="lean", choices=["lean", "strict"])
-    ap.add_argument("--ref-budget", type=float, default=12.0, help="seconds of CPU work per reference step")
+    ap.add_argument("--ref-budget", type=float, default=None,
+                    help="seconds of CPU work per reference step (default: 12 s for the cpu_baseline leg; "
+                         "150 s / steps, within 1.5-12 s, for --impl reference)")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
