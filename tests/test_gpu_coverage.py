@@ -150,3 +150,24 @@ def test_tensor_core_positions_horizon_edges(horizon, count):
         r = sf_oracle.solve(op, x, max_iters=8, early_stop=False)
         assert np.abs(coeffs[b] - r.coeffs).max() <= 1e-5 * np.abs(r.coeffs).max(), b
     assert out.eq_err.max().item() <= 1e-8
+
+
+def test_solve_with_svars_on_the_tensor_core_path():
+    """SafetyFilter.solve (svars on: the kernel also keeps the previous iterate, so the tensor-core
+    variant runs two slots per CTA) equals solve_batched on the config-2 problem, and its svars are the
+    spherical variables of the previous iterate."""
+    from dataclasses import replace
+
+    from paper_2501_19042_b200 import SafetyFilter, SolverConfig, sample_proposals
+    from paper_2501_19042_b200.scenarios import config_problem
+    prob = config_problem(2)
+    cfg = SolverConfig(max_iters=40, early_stop=False)
+    sf = SafetyFilter(prob, config=cfg)
+    props = sample_proposals(prob, sf.basis, 3, seed=5).proposals
+    bat = sf.solve_batched(torch.from_numpy(props).cuda(), config=replace(cfg, svars=False), want_prev=True)
+    for b in range(3):
+        r = sf.solve(props[b])
+        assert np.array_equal(r.coeffs, bat.coeffs[b].cpu().numpy())
+        assert r.iterations == int(bat.iterations[b])
+        sv = sf.svars_of(bat.coeffs_prev[b:b + 1])[0]
+        np.testing.assert_array_equal(r.svars.pair_radial, sv.pair_radial)
