@@ -1348,11 +1348,14 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
             if (ts < S && owner)
                 pr = finish_step<T, NB>(sp, ptab, ts, n, par, Prow_old, Prow_new, qinf, qsq, nm, fmin(zmin_ws, zmin_pairs),
                                         imask, zprev, fp, fw, cx, cy, cz);
-            {   // per-warp exit-residual partials for the decision (fixed order: deterministic)
+            {   // per-warp exit-residual partials for the decision (fixed order: deterministic); the l2
+                // partial is summed over the warp in T (FP32 lean: the history is an l2 norm, checked to
+                // 1e-3) and across the warps in FP64
                 const T wi = warp_max_nonneg(pr.inf);
-                double wq = (double)pr.sq;
+                T wqt = pr.sq;
 #pragma unroll
-                for (int off = 16; off > 0; off >>= 1) wq += __shfl_xor_sync(0xffffffffu, wq, off);
+                for (int off = 16; off > 0; off >>= 1) wqt += __shfl_xor_sync(0xffffffffu, wqt, off);
+                const double wq = (double)wqt;
                 if (lane == 0) {
                     ((T*)sp.pinf)[lwarp] = wi;
                     sp.psq[lwarp] = wq;
