@@ -1361,6 +1361,10 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                     sp.psq[lwarp] = wq;
                 }
             }
+            // ||A xi - b|| of iteration k-1: written by the axis warps in MX before the previous
+            // iteration's closing barrier, rewritten in this iteration's MX -- so it is read HERE,
+            // before the term-pass barrier, where no warp can have reached the rewrite yet (WAR-safe)
+            const double emax_pre = k >= 1 ? fmax(fmax(sp.eqerr[0], sp.eqerr[1]), sp.eqerr[2]) : 0.0;
 #ifdef SGSF_PHASE_TIMING
             if (slot == 0 && lane == 0 && lwarp < 4) pt_arrive[lwarp] = clock64();   // term-pass barrier arrivals
 #endif
@@ -1380,10 +1384,10 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
 #endif
 
             // ---------------- decision (every warp, redundantly): exit residual of iteration k-1, early stop, SingularKKT
-            double emax = 0.0, sqs = 0.0;
+            const double emax = emax_pre;
+            double sqs = 0.0;
             T inf = T(0);
-            if (k >= 1) {   // partials: per axis (MX of iteration k-1), per warp (T3 above)
-                emax = fmax(fmax(sp.eqerr[0], sp.eqerr[1]), sp.eqerr[2]);
+            if (k >= 1) {   // partials: per axis (MX of iteration k-1, read above), per warp (T3 above)
                 if (TC) {   // 4 warps per slot: independent loads, fixed summation order
                     T pi[4];
                     double ps[4];

@@ -306,9 +306,18 @@ class SafetyFilter:
                 lam0 = torch.zeros_like(xi0)
             if init_mode is None:
                 init_mode = torch.ones(B, dtype=torch.uint8, device=dev)
+            for what, t in (("initial coefficients", xi0), ("initial multipliers", lam0)):
+                if tuple(t.shape) != (B, self.coeff_dim):
+                    raise DimensionMismatch(f"{what} must be ({B}, {self.coeff_dim}), got {tuple(t.shape)}")
+                if t.dtype != torch.float64 or t.device != dev:
+                    raise DimensionMismatch(f"{what} must be float64 on {dev}, got {t.dtype} on {t.device}")
+            if init_mode.numel() != B:
+                raise DimensionMismatch(f"init_mode has {init_mode.numel()} entries, expected {B}")
             xi0, lam0 = xi0.contiguous(), lam0.contiguous()
             init_mode = init_mode.to(device=dev, dtype=torch.uint8).contiguous()
         else:
+            if lam0 is not None:
+                raise DimensionMismatch("initial multipliers given without initial coefficients")
             init_mode = None
         dim, mi = self.coeff_dim, cfg.max_iters
         f64 = dict(dtype=torch.float64, device=dev)

@@ -1,0 +1,175 @@
+"""Freeze the REAL reference's outputs on whole benchmark batches (build container only).
+
+    python tests/golden/make_golden_batch.py cfg2        # all 1000 config-2 bench proposals
+    python tests/golden/make_golden_batch.py ws_tight    # converged-but-violating workspace case
+    python tests/golden/make_golden_batch.py cfg3 cfg4   # early-stop subsets at n = 32 / 64
+
+Like ``make_golden.py`` this builds the reference's own Cython kernel in a
+scratch copy of ``/root/reference/pkg`` and imports ``swarmfilter`` from it
+(``active_backend() == 'compiled'``); nothing from the reference enters the
+repo except the numbers it produced.  Each proposal is solved by
+``SafetyFilter.solve`` (``solver.py:286-359``) in a process pool with BLAS
+pinned to one thread, then checked by ``metrics.feasible_results``
+(``metrics.py:57-69``) and ``check_original_constraints``
+(``assembly.py:437-487``) -- the exact numerator of the headline metric.
+
+Stored per sample: iterations, converged, feasible, the reference's worst
+margins and violation counts, the first 8 worst-first violation entries, the
+full ``res_inf`` history (float64, NaN padded: it is what decides iteration
+counts, and what classifies a GPU count flip as borderline) and
+the displacement.  Coefficients and multipliers are stored for a subset.
+Proposals are not stored: both sides regenerate them from the reference
+Gaussian sampler (seed 0) -- a SHA-256 of the float64 bytes pins them.
+"""
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+import time
+from pathlib import Path
+
+os.environ["OPENBLAS_NUM_THREADS"] = "1"
+os.environ["OMP_NUM_THREADS"] = "1"
+os.environ["MKL_NUM_THREADS"] = "1"
+
+import numpy as np  # noqa: E402
+
+HERE = Path(__file__).resolve().parent
+REPO = HERE.parent.parent
+sys.path.insert(0, str(HERE))
+sys.path.insert(0, str(REPO))
+
+LISTED = 8   # worst-first violation entries stored per kind
+
+_W = {}
+
+
+def _init(doc, degree, cfg):
+    from make_golden import import_reference
+    sfm = import_reference()
+    prob = sfm.load_problem(doc) if isinstance(doc, dict) else doc
+    _W["sfm"] = sfm
+    _W["prob"] = prob
+    _W["filt"] = sfm.SafetyFilter(prob, degree=degree, config=sfm.SolverConfig(**cfg))
+
+
+def _solve_one(args):
+    idx, x = args
+    sfm, prob, filt = _W["sfm"], _W["prob"], _W["filt"]
+    t0 = time.perf_counter()
+    r = filt.solve(x)
+    dt = time.perf_counter() - t0
+    traj = sfm.coeffs_to_trajectory(r.coeffs, filt.basis, prob.n)
+    rep = sfm.check_original_constraints(traj, prob, tol=1e-3)
+    feas = bool(r.converged and rep.ok)
+    # feasible_results is the headline's own definition: check it agrees
+    assert feas == (len(sfm.metrics.feasible_results([r], prob)) == 1)
+    return (idx, r.iterations, bool(r.converged), feas, float(rep.pair_margin_min),
+            float(rep.workspace_margin_max), rep.pair_violation_count, rep.workspace_violation_count,
+            [list(v) for v in rep.pair_violations[:LISTED]], [list(v) for v in rep.workspace_violations[:LISTED]],
+            np.asarray(r.residual_inf), np.asarray(r.residual_l2), float(r.displacement),
+            np.asarray(r.coeffs), np.asarray(r.multipliers), dt)
+
+
+def run_batch(name, doc, proposals, degree=10, keep_coeffs=64, procs=None, **cfg):
+    import multiprocessing as mp
+    B = len(proposals)
+    maxit = cfg.get("max_iters", 200)
+    procs = procs or os.cpu_count() or 1
+    out = {
+        "iterations": np.zeros(B, np.int32), "converged": np.zeros(B, bool), "feasible": np.zeros(B, bool),
+        "pair_margin_min": np.full(B, np.nan), "ws_margin_max": np.full(B, np.nan),
+        "pair_viol": np.zeros(B, np.int32), "ws_viol": np.zeros(B, np.int32),
+        "pair_list": np.full((B, LISTED, 4), np.nan), "ws_list": np.full((B, LISTED, 3), np.nan),
+        "res_inf": np.full((B, maxit), np.nan), "res_l2_last": np.full(B, np.nan),
+        "displacement": np.full(B, np.nan),
+        "coeffs_subset": np.full((min(B, keep_coeffs), len(proposals[0])), np.nan),
+        "multipliers_subset": np.full((min(B, keep_coeffs), len(proposals[0])), np.nan),
+    }
+    t0 = time.perf_counter()
+    cpu = 0.0
+    with mp.get_context("fork").Pool(procs, initializer=_init, initargs=(doc, degree, cfg)) as pool:
+        for k, row in enumerate(pool.imap_unordered(_solve_one, list(enumerate(proposals)), chunksize=1)):
+            (i, its, conv, feas, pmin, wmax, pv, wv, pl, wl, rinf, rl2, disp, co, mu, dt) = row
+            cpu += dt
+            out["iterations"][i] = its
+            out["converged"][i] = conv
+            out["feasible"][i] = feas
+            out["pair_margin_min"][i] = pmin
+            out["ws_margin_max"][i] = wmax
+            out["pair_viol"][i] = pv
+            out["ws_viol"][i] = wv
+            for j, v in enumerate(pl):
+                out["pair_list"][i, j] = v
+            for j, v in enumerate(wl):
+                out["ws_list"][i, j] = v
+            out["res_inf"][i, :its] = rinf
+            out["res_l2_last"][i] = rl2[-1]
+            out["displacement"][i] = disp
+            if i < keep_coeffs:
+                out["coeffs_subset"][i] = co
+                out["multipliers_subset"][i] = mu
+            if (k + 1) % 50 == 0:
+                print(f"  {name}: {k + 1}/{B} ({time.perf_counter() - t0:.0f} s)", flush=True)
+    wall = time.perf_counter() - t0
+    sha = hashlib.sha256(np.ascontiguousarray(np.asarray(proposals, dtype=np.float64)).tobytes()).hexdigest()
+    meta = {"name": name, "problem": doc, "degree": degree, "config": cfg, "batch": B,
+            "proposals_sha256": sha, "reference_backend": "compiled", "wall_s": wall, "cpu_s": cpu,
+            "procs": procs, "sample_iterations": int(out["iterations"].sum())}
+    np.savez_compressed(HERE / f"{name}.npz", meta=np.array(json.dumps(meta)), **out)
+    print(f"{name}: B={B} iterations {out['iterations'].min()}..{out['iterations'].max()} "
+          f"(mean {out['iterations'].mean():.1f}) converged {out['converged'].sum()} "
+          f"feasible {out['feasible'].sum()} ws_viol>0 {(out['ws_viol'] > 0).sum()} "
+          f"pair_viol>0 {(out['pair_viol'] > 0).sum()}  wall {wall:.0f} s, {cpu / max(1, meta['sample_iterations']) * 1e3:.2f} ms/SI",
+          flush=True)
+
+
+def proposals_for(doc, batch, seed=0, degree=10, spread=0.25):
+    """The bench's inputs: this repo's sampler (== the reference sampler, test_host.py pins it)."""
+    from paper_2501_19042_b200 import load_problem, sample_proposals
+    from paper_2501_19042_b200.basis import build_basis
+    prob = load_problem(doc)
+    basis = build_basis(prob.duration, degree=degree, samples=prob.horizon_samples)
+    return sample_proposals(prob, basis, batch, seed=seed, spread=spread).proposals
+
+
+def ws_tight_doc():
+    """6 robots in a workspace barely larger than their start/goal sets; loose tol_residual.
+
+    With tol_residual = 0.05 the SF stops while some positions still poke out of
+    the workspace spheroid by more than the verdict's 1e-3: converged-but-
+    infeasible on the *workspace* branch of ``check_original_constraints``.
+    """
+    starts = [(2.2, 0.0, 1.0), (-2.2, 0.3, 1.2), (0.0, 2.1, 0.8), (0.2, -2.2, 1.1), (1.4, 1.5, 1.6), (-1.5, -1.4, 0.5)]
+    goals = [(-2.2, 0.2, 1.1), (2.2, -0.1, 0.9), (0.1, -2.1, 1.2), (-0.2, 2.2, 0.8), (-1.5, -1.4, 0.6), (1.4, 1.5, 1.5)]
+    return {"n": 6, "H": 60, "T": 6.0, "a": 0.6, "b": 0.4,
+            "workspace": {"center": [0.0, 0.0, 1.0], "a_w": 2.6, "b_w": 1.2},
+            "boundary": [{"start": {"p": list(s)}, "goal": {"p": list(g)}} for s, g in zip(starts, goals)]}
+
+
+def main(argv):
+    from make_golden import import_reference
+    from paper_2501_19042_b200.scenarios import config_doc
+    import_reference()   # build the scratch copy once, before the pool forks
+    for which in argv or ["cfg2"]:
+        if which == "cfg2":
+            doc = config_doc(2)
+            run_batch("batch_cfg2", doc, proposals_for(doc, 1000), max_iters=500)
+        elif which == "ws_tight":
+            doc = ws_tight_doc()
+            props = proposals_for(doc, 48, seed=3, spread=3.0)
+            run_batch("batch_ws_tight", doc, props, keep_coeffs=48, max_iters=300, tol_residual=0.05)
+        elif which == "cfg3":
+            doc = config_doc(3)
+            run_batch("batch_cfg3", doc, proposals_for(doc, 8), keep_coeffs=8, max_iters=500)
+        elif which == "cfg4":
+            doc = config_doc(4)
+            run_batch("batch_cfg4", doc, proposals_for(doc, 4), keep_coeffs=4, max_iters=500)
+        else:
+            raise SystemExit(f"unknown batch {which}")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:])
