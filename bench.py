@@ -340,7 +340,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         "metric": METRIC, "value": value, "unit": "feasible samples/s", "n_gpus": world,
         "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": total_ms_max / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32 terms + f64 state" if args.precision == "lean" else "f64",
+        "dtype": {"lean": "f32 terms + f64 state", "hybrid": "f32 screening + f64 values", "strict": "f64"}[args.precision],
         "data": "synthetic (seeded 16-robot scenario, reference Gaussian sampler proposals)",
         "config": {"workload": "BASELINE config 2: 16 drones, H=100, batch 1000 per GPU, SF to 1e-3 "
                                "(max_iters 500), boundary-projected start",
@@ -388,7 +388,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=BATCH_PER_GPU)
-    ap.add_argument("--precision", default="lean", choices=["lean", "strict"])
+    ap.add_argument("--precision", default="lean", choices=["lean", "strict", "hybrid"])
     ap.add_argument("--ref-budget", type=float, default=None,
                     help="seconds of CPU work per reference step (default: 12 s for the cpu_baseline leg; "
                          "150 s / steps, within 1.5-12 s, for --impl reference)")

@@ -29,7 +29,12 @@ int launch_large(const LaunchInfo& li, SolveParams& p, const sgsf_config_t* cfg,
 template <typename T, int NB, int MP, int MAXT, int TPS>
 int launch_persistent(const LaunchInfo& li, SolveParams& p, const sgsf_config_t* cfg, const sgsf_timing_t* timing,
                       cudaStream_t stream) {
+    // hybrid precision: the FP32 kernels with guard bands and FP64 values (sf_persistent.cuh, HY)
+    const bool hy = sizeof(T) == 4 && cfg->precision == SGSF_PRECISION_HYBRID;
     void (*kern)(const SolveParams) = sf_persistent_kernel<T, NB, MP, MAXT, TPS>;
+    if constexpr (sizeof(T) == 4) {
+        if (hy) kern = sf_persistent_kernel<T, NB, MP, MAXT, TPS, false, 0, true>;
+    }
     int dev_smem = 0;
     cudaError_t e = cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, li.device);
     if (e != cudaSuccess) return internal_fail(SGSF_ERR_CUDA, cudaGetErrorString(e));
@@ -46,14 +51,15 @@ int launch_persistent(const LaunchInfo& li, SolveParams& p, const sgsf_config_t*
             tc = true;
             // (one term-pass variant per instantiation, FULLN = 1 / 2, is 832 instructions smaller but
             // measured 1% slower)
-            kern = sf_persistent_kernel<T, NB, MP, MAXT, TPS, true>;
+            kern = hy ? sf_persistent_kernel<T, NB, MP, MAXT, TPS, true, 0, true>
+                      : sf_persistent_kernel<T, NB, MP, MAXT, TPS, true>;
         }
     }
     int spb = cfg->slots_per_block;
     if (spb <= 0) {
         spb = 0;
         for (int s = 1; s * slot_threads <= MAXT && s <= 15; ++s) {
-            if (make_layout<T, NB>(p.n, p.S, MP, s, p.want_prev, tc).total > (size_t)dev_smem) break;
+            if (make_layout<T, NB>(p.n, p.S, MP, s, p.want_prev, tc, hy).total > (size_t)dev_smem) break;
             spb = s;
         }
         // small batches: spread samples over the SMs instead of packing few CTAs
@@ -61,7 +67,7 @@ int launch_persistent(const LaunchInfo& li, SolveParams& p, const sgsf_config_t*
         if (spb > spread) spb = spread > 0 ? spread : 1;
     }
     if (spb <= 0) {
-        const size_t need = make_layout<T, NB>(p.n, p.S, MP, 1, p.want_prev, tc).total;
+        const size_t need = make_layout<T, NB>(p.n, p.S, MP, 1, p.want_prev, tc, hy).total;
         return internal_fail(SGSF_ERR_UNSUPPORTED,
                              "problem too large for one CTA: one sample slot needs " + std::to_string(need / 1024) +
                                  " KB of shared memory, the device allows " + std::to_string(dev_smem / 1024) +
@@ -73,7 +79,7 @@ int launch_persistent(const LaunchInfo& li, SolveParams& p, const sgsf_config_t*
     p.spb = spb;
     p.wps = wps;
     p.MP = MP;
-    const SmemLayout L = make_layout<T, NB>(p.n, p.S, MP, spb, p.want_prev, tc);
+    const SmemLayout L = make_layout<T, NB>(p.n, p.S, MP, spb, p.want_prev, tc, hy);
     p.L = L;
     set_family_constants(p);
     if (L.total > (size_t)dev_smem) return internal_fail(SGSF_ERR_UNSUPPORTED, "shared memory budget exceeded");
@@ -94,12 +100,12 @@ int launch_persistent(const LaunchInfo& li, SolveParams& p, const sgsf_config_t*
     if (timing && timing->stop) cudaEventRecord((cudaEvent_t)timing->stop, stream);
 #ifdef SGSF_COUNTERS
     {
-        unsigned long long c[8];
+        unsigned long long c[10];
         cudaStreamSynchronize(stream);
         cudaMemcpyFromSymbol(c, g_sgsf_counts, sizeof(c));
-        printf("COUNTS finish %llu flagged %llu exact %llu careful %llu flagged_terms %llu near_checks %llu scans %llu exact_f1 %llu\n",
-               c[0], c[1], c[2], c[3], c[4], c[5], c[6], c[7]);
-        const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        printf("COUNTS finish %llu flagged %llu exact %llu careful %llu flagged_terms %llu near_checks %llu scans %llu exact_f1 %llu hy_recompute %llu\n",
+               c[0], c[1], c[2], c[3], c[4], c[5], c[6], c[7], c[8]);
+        const unsigned long long z[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
         cudaMemcpyToSymbol(g_sgsf_counts, z, sizeof(z));
     }
 #endif

@@ -43,6 +43,8 @@
 // state and xi-step are FP64.
 #pragma once
 
+#include <cmath>
+
 #include "sf_device.cuh"
 #include "sf_tc.cuh"
 
@@ -52,15 +54,18 @@ enum { SAMPLE_OK = 0, SAMPLE_SINGULAR_KKT = 1 };
 
 // shared-memory offsets of one launch (make_layout below)
 struct SmemLayout {
-    size_t W, KMm, KMd, cconst, B6, rhs, PBt, ptab, tmem;
+    size_t W, KMm, KMd, cconst, B6, rhs, ptab, tmem;
     size_t slot0, slot_stride;
-    size_t C, Cp, lam, U, xb, eqerr, psq, P0, P1, Cf, pinf, sh;
+    size_t C, Cp, lam, U, xb, eqerr, psq, pex, P0, P1, Cf, pinf, sh;
     size_t total;
 };
 
 struct SolveParams {
     int n, S, m1, MP, batch, max_iters, early_stop, want_prev, spb, wps;
     double rho, tol_res, tol_eq;
+    // hybrid precision (HY kernels): FP32 screening with guard bands, FP64 values.  hy_delta = half-width of
+    // the band around tol_res in which the FP32-measured exit residual is re-evaluated in FP64
+    double hy_delta;
     double lat, vert, ws_lat, ws_vert, cx, cy, cz;
     const double* W;       // S x m1
     const double* KMm;     // m1 x 2m1  [Mm | Km11]
@@ -68,7 +73,7 @@ struct SolveParams {
     const double* cconst;  // 3n x m1
     const double* B6;      // 6 x m1
     const double* rhs;     // 3n x 6
-    const double* PBt;     // m1 x 6
+    const double* PBt;     // m1 x 6 (read from global memory: the per-sample prologue only)
     const double* xi_bar;
     const double* xi0;
     const double* lam0;
@@ -89,11 +94,24 @@ struct SolveParams {
     // kernel reads them from the parameter bank instead of recomputing them
     SmemLayout L;
     float fp_lat_f, fp_lim_f, fp_beta_f, fw_lat_f, fw_lim_f, fw_beta_f;
+    float hy_fp_lim_f, hy_fw_lim_f;   // HY: interior limits narrowed by the FP32 guard band
     double fp_lim_d, fp_beta_d, fw_lim_d, fw_beta_d;
 };
 
 // the host-side precomputation of SolveParams' constants (make_family's expressions)
 inline void set_family_constants(SolveParams& p) {
+    // hybrid guard bands.  e_pos bounds the FP32 position error (3xTF32 keeps ~21 bits per product) over the
+    // workspace; the interior tests are narrowed by 4 e_pos (x4: positions outside the workspace early on)
+    // relative to the smallest semiaxis, and the stop decision re-evaluates in FP64 within
+    // max(1% of tol_res, 2 e_pos) of tol_res
+    {
+        const double c = fmax(fabs(p.cx), fmax(fabs(p.cy), fabs(p.cz)));
+        const double e_pos = std::ldexp(1.0, -20) * (fmax(p.ws_lat, p.ws_vert) + c);
+        const double ep = 4.0 * 4.0 * e_pos / fmin(p.lat, p.vert), ew = 4.0 * 4.0 * e_pos / fmin(p.ws_lat, p.ws_vert);
+        p.hy_fp_lim_f = (float)(p.lat * p.lat * (1.0 + ep));
+        p.hy_fw_lim_f = (float)(p.ws_lat * p.ws_lat * (1.0 - ew));
+        p.hy_delta = fmax(0.01 * p.tol_res, 2.0 * e_pos);
+    }
     p.fp_lat_f = (float)p.lat;
     p.fp_lim_f = (float)(p.lat * p.lat);
     p.fp_beta_f = (float)((p.lat * p.lat) / (p.vert * p.vert));
@@ -154,8 +172,11 @@ template <typename T, int NB> struct RowStride {
 // 16 robots x 16 k in the UMMA K-major layout (tc::kmajor16_offset)
 constexpr int kTcBopBytes = 3 * 2 * 1024;
 
+// hy: hybrid precision keeps the previous iterate's FP64 coefficients (Cp) and FP64 exit-residual partials
+// (pex).  The per-warp partial arrays are sized for the slot's warps: 4 on the tensor-core path.
 template <typename T, int NB>
-__host__ __device__ inline SmemLayout make_layout(int n, int S, int MP, int spb, int want_prev, bool tc = false) {
+__host__ __device__ inline SmemLayout make_layout(int n, int S, int MP, int spb, int want_prev, bool tc = false,
+                                                  bool hy = false) {
     const int RS = RowStride<T, NB>::value;
     SmemLayout L;
     size_t o = 0;
@@ -167,22 +188,23 @@ __host__ __device__ inline SmemLayout make_layout(int n, int S, int MP, int spb,
     L.cconst = o; o = align16(o + (size_t)dimp * d);
     L.B6 = o;     o = align16(o + (size_t)6 * MP * d);
     L.rhs = o;    o = align16(o + (size_t)R3 * 6 * d);
-    L.PBt = o;    o = align16(o + (size_t)MP * 6 * d);
     L.ptab = o;   o = align16(o + (size_t)NB * (NB - 1) / 2 * sizeof(int));
     L.tmem = o;   o = align16(o + 2 * sizeof(uint32_t));               // TC: TMEM base, finished-slot count
     L.slot0 = o;
     size_t q = 0;
     L.C = q;      q = align16(q + (size_t)dimp * d);
-    L.Cp = q;     q = align16(q + (want_prev ? (size_t)dimp * d : 0));
+    L.Cp = q;     q = align16(q + ((want_prev || hy) ? (size_t)dimp * d : 0));
     L.lam = q;    q = align16(q + (size_t)dimp * d);
     L.U = q;      q = align16(q + (size_t)dimp * d);                // u = 2 lam' - lam + xi_bar
     L.xb = q;     q = align16(q + (size_t)dimp * d);
     L.eqerr = q;  q = align16(q + (size_t)4 * d);                     // per axis max ||A xi - b|| over its rows
-    L.psq = q;    q = align16(q + (size_t)MAX_SLOT_WORDS * d);        // per warp sum of the l2 partials
+    const size_t pw = tc ? 4 : MAX_SLOT_WORDS;                        // partial-array entries (warps)
+    L.psq = q;    q = align16(q + pw * d);                             // per warp sum of the l2 partials
+    L.pex = q;    q = align16(q + (hy ? 2 * pw * d : 0));              // hy: FP64 exit-residual partials (inf, l2)
     L.P0 = q;     q = align16(q + (size_t)RS * S * ts);
     L.P1 = q;     q = align16(q + (size_t)RS * S * ts);
     L.Cf = q;     q = align16(q + (tc ? (size_t)kTcBopBytes : (size_t)3 * MP * NB * ts));
-    L.pinf = q;   q = align16(q + (size_t)MAX_SLOT_WORDS * ts);       // per warp max of the inf partials
+    L.pinf = q;   q = align16(q + pw * ts);                            // per warp max of the inf partials
     L.sh = q;     q = align16(q + sizeof(SlotShared));
     L.slot_stride = q;
     L.total = o + (size_t)spb * q;
@@ -190,7 +212,7 @@ __host__ __device__ inline SmemLayout make_layout(int n, int S, int MP, int spb,
 }
 
 struct SlotPtrs {
-    double *C, *Cp, *lam, *U, *xb, *eqerr, *psq;
+    double *C, *Cp, *lam, *U, *xb, *eqerr, *psq, *pex;
     void *P0, *P1, *Cf, *pinf;
     SlotShared* sh;
 };
@@ -205,6 +227,7 @@ __device__ __forceinline__ SlotPtrs slot_ptrs(unsigned char* smem, const SmemLay
     P.xb = (double*)(b + L.xb);
     P.eqerr = (double*)(b + L.eqerr);
     P.psq = (double*)(b + L.psq);
+    P.pex = (double*)(b + L.pex);
     P.P0 = (void*)(b + L.P0);
     P.P1 = (void*)(b + L.P1);
     P.Cf = (void*)(b + L.Cf);
@@ -222,8 +245,9 @@ __device__ __forceinline__ void slot_barrier(int id, int nthreads) {
 
 #ifdef SGSF_COUNTERS
 // event counters of the instrumented build: [0] finish calls, [1] flagged path, [2] exact recompute,
-// [3] careful path, [4] flagged terms, [5] near checks, [6] pair scans, [7] G items with work
-__device__ unsigned long long g_sgsf_counts[8];
+// [3] careful path, [4] flagged terms, [5] near checks, [6] pair scans, [7] fast exact far max, [8] HY FP64
+// exit-residual re-evaluations
+__device__ unsigned long long g_sgsf_counts[10];
 #define SGSF_COUNT(I, V) atomicAdd(&g_sgsf_counts[I], (unsigned long long)(V))
 #else
 #define SGSF_COUNT(I, V) ((void)0)
@@ -560,6 +584,170 @@ template <int NB> struct MaskPack {
     uint32_t w[TermBits<NB>::words];
 };
 
+// ---------------------------------------------------------------- hybrid precision (HY): FP64 values
+// The HY kernels screen in FP32 exactly like the lean ones, with the interior tests narrowed by a guard band
+// (fp.lim, fw.lim scaled on the host side of the kernel): a term the FP32 test calls interior is interior in
+// FP64.  Every value that reaches the state or a stop decision is FP64: the targets and residuals of the
+// flagged (non-interior now or before) terms come from FP64 positions of the FP64 coefficients of both
+// iterates (C = C_k, Cp = C_{k-1}), in strict's exact operation order; the quiet (all-interior) terms have
+// zero scattered residual, so they never touch the state.  The FP32-measured exit residual decides the stop
+// unless it lies within hy_delta of tol_res; then the whole exit residual is re-evaluated in FP64
+// (hy_step_full over every time step).
+struct D3 {
+    double x, y, z;
+};
+
+template <int MP>
+__device__ __forceinline__ void w64_row(const double* __restrict__ W, int t, int m1, double (&w)[MP]) {
+#pragma unroll
+    for (int q = 0; q < MP; ++q) w[q] = q < m1 ? __ldg(W + t * m1 + q) : 0.0;
+}
+// FP64 position of coefficient row `row` (strict's order: fma over q ascending from 0)
+template <int MP>
+__device__ __forceinline__ double pos64(const double* __restrict__ C, const double (&w)[MP], int row) {
+    const double* c = C + row * MP;
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < MP; ++q) s = fma(c[q], w[q], s);
+    return s;
+}
+
+__device__ __forceinline__ Family<double> family64(const SolveParams& p, bool pair) {
+    Family<double> f;
+    f.lat = pair ? p.lat : p.ws_lat;
+    f.lim = pair ? p.fp_lim_d : p.fw_lim_d;
+    f.beta = pair ? p.fp_beta_d : p.fw_beta_d;
+    f.lat64 = pair ? p.lat : p.ws_lat;
+    f.vert64 = pair ? p.vert : p.ws_vert;
+    return f;
+}
+
+// difference vector of term (i, j) (j < 0: workspace term of robot i, relative to the centre) at step t of C
+template <int MP>
+__device__ __forceinline__ D3 term_diff64(const SolveParams& p, const double* __restrict__ C, const double (&w)[MP],
+                                          int i, int j) {
+    const int n = p.n;
+    D3 d;
+    if (j >= 0) {
+        d.x = pos64<MP>(C, w, i) - pos64<MP>(C, w, j);
+        d.y = pos64<MP>(C, w, n + i) - pos64<MP>(C, w, n + j);
+        d.z = pos64<MP>(C, w, 2 * n + i) - pos64<MP>(C, w, 2 * n + j);
+    } else {
+        d.x = pos64<MP>(C, w, i) - p.cx;
+        d.y = pos64<MP>(C, w, n + i) - p.cy;
+        d.z = pos64<MP>(C, w, 2 * n + i) - p.cz;
+    }
+    return d;
+}
+
+// FP64 b - target(d) of one term (zero components: the reference trig formula)
+__device__ __forceinline__ D3 resid64(bool pair, const D3& d, const D3& b, const Family<double>& f) {
+    double zu = 1.0;
+    D3 r;
+    if (pair) resid<double, true, true>(d.x, d.y, d.z, b.x, b.y, b.z, f, zu, r.x, r.y, r.z);
+    else resid<double, false, true>(d.x, d.y, d.z, b.x, b.y, b.z, f, zu, r.x, r.y, r.z);
+    return r;
+}
+
+// exit residual d(C_k) - e(C_{k-1}) of term (i, j) at step t
+template <int MP>
+__device__ __noinline__ D3 hy_term_exit(const SolveParams& p, const double* Cn, const double* Co, int t, int i, int j) {
+    double w[MP];
+    w64_row<MP>(p.W, t, p.m1, w);
+    const D3 dn = term_diff64<MP>(p, Cn, w, i, j), dol = term_diff64<MP>(p, Co, w, i, j);
+    return resid64(j >= 0, dol, dn, family64(p, j >= 0));
+}
+
+// scattered residual d(C_k) - e(C_k) of term (i, j) at step t (0 for an FP64-interior term)
+template <int MP>
+__device__ __noinline__ D3 hy_term_resid(const SolveParams& p, const double* Cn, int t, int i, int j) {
+    double w[MP];
+    w64_row<MP>(p.W, t, p.m1, w);
+    const D3 dn = term_diff64<MP>(p, Cn, w, i, j);
+    return resid64(j >= 0, dn, dn, family64(p, j >= 0));
+}
+
+// Every term of time step t in FP64: exit residual statistics (max |x|, sum x^2) and, when Rrow != null, the
+// careful path -- R row (written over the dead old row), interior bits (zero-component terms count as active)
+template <typename T, int NB, int MP> struct HyStepOut {
+    double inf, sq;
+    bool zero, active;
+};
+template <typename T, int NB, int MP>
+__device__ __noinline__ HyStepOut<T, NB, MP> hy_step_full(const SolveParams& p, const double* Cn, const double* Co,
+                                                         int t, T* Rrow, MaskPack<NB>* nmo) {
+    const int n = p.n;
+    double w[MP];
+    w64_row<MP>(p.W, t, p.m1, w);
+    double pn[3 * NB], po[3 * NB], R[3 * NB];
+    for (int q = 0; q < 3 * NB; ++q) {
+        const int ax = q / NB, i = q % NB;
+        pn[q] = i < n ? pos64<MP>(Cn, w, ax * n + i) : 0.0;
+        po[q] = i < n ? pos64<MP>(Co, w, ax * n + i) : 0.0;
+        R[q] = 0.0;
+    }
+    const Family<double> fp = family64(p, true), fw = family64(p, false);
+    MaskPack<NB> nmw;
+    for (int u = 0; u < TermBits<NB>::words; ++u) nmw.w[u] = 0xffffffffu;
+    double mx = 0.0, s2 = 0.0;
+    bool znow = false, act = false;
+    int b = 0;
+    for (int i = 0; i < NB; ++i) {
+        for (int j = i + 1; j < NB; ++j, ++b) {
+            if (j >= n) continue;
+            const D3 d{pn[i] - pn[j], pn[NB + i] - pn[NB + j], pn[2 * NB + i] - pn[2 * NB + j]};
+            const D3 o{po[i] - po[j], po[NB + i] - po[NB + j], po[2 * NB + i] - po[2 * NB + j]};
+            const D3 x = resid64(true, o, d, fp);
+            mx = fmax(mx, fmax(fabs(x.x), fmax(fabs(x.y), fabs(x.z))));
+            s2 = fma(x.x, x.x, fma(x.y, x.y, fma(x.z, x.z, s2)));
+            if (Rrow) {
+                const D3 r = resid64(true, d, d, fp);
+                R[i] += r.x, R[NB + i] += r.y, R[2 * NB + i] += r.z;
+                R[j] -= r.x, R[NB + j] -= r.y, R[2 * NB + j] -= r.z;
+                const double q = fma(d.z * fp.beta, d.z, fma(d.y, d.y, d.x * d.x));
+                const bool zero = d.x == 0.0 || d.y == 0.0 || d.z == 0.0;
+                znow = znow || zero;
+                if (!(q >= fp.lim) || zero) {
+                    nmw.w[b >> 5] &= ~(1u << (b & 31));
+                    act = true;
+                }
+            }
+        }
+    }
+    b = NB * (NB - 1) / 2;
+    for (int i = 0; i < NB; ++i, ++b) {
+        if (i >= n) continue;
+        const D3 d{pn[i] - p.cx, pn[NB + i] - p.cy, pn[2 * NB + i] - p.cz};
+        const D3 o{po[i] - p.cx, po[NB + i] - p.cy, po[2 * NB + i] - p.cz};
+        const D3 x = resid64(false, o, d, fw);
+        mx = fmax(mx, fmax(fabs(x.x), fmax(fabs(x.y), fabs(x.z))));
+        s2 = fma(x.x, x.x, fma(x.y, x.y, fma(x.z, x.z, s2)));
+        if (Rrow) {
+            const D3 r = resid64(false, d, d, fw);
+            R[i] += r.x, R[NB + i] += r.y, R[2 * NB + i] += r.z;
+            const double q = fma(d.z * fw.beta, d.z, fma(d.y, d.y, d.x * d.x));
+            const bool zero = d.x == 0.0 || d.y == 0.0 || d.z == 0.0;
+            znow = znow || zero;
+            if (!(q <= fw.lim) || zero) {
+                nmw.w[b >> 5] &= ~(1u << (b & 31));
+                act = true;
+            }
+        }
+    }
+    if (Rrow) {
+        for (int q = 0; q < 3 * NB; ++q)
+            if ((q % NB) < n) Rrow[q] = (T)R[q];
+        *nmo = nmw;
+    }
+    HyStepOut<T, NB, MP> r;
+    r.inf = mx;
+    r.sq = s2;
+    r.zero = znow;
+    r.active = act;
+    return r;
+}
+
+
 // Flagged terms (active now or at the previous iterate) of one time step,
 // O(#flagged): true exit residual, scatter of d - e for terms active now,
 // and the corrections of the quiet statistics (qinf, qsq).  The quiet
@@ -610,16 +798,17 @@ template <typename T> __device__ __forceinline__ void top3_insert(T (&t)[3], int
     }
 }
 
-template <typename T, int NB>
+template <typename T, int NB, int MP, bool HY>
 __device__ __forceinline__ StepOut<T> flagged_path(const T* __restrict__ Pnew, T* __restrict__ Pold, int n,
                                                    const int* __restrict__ ptab, const Family<T>& fp,
                                                    const Family<T>& fw, T cx, T cy, T cz, const MaskPack<NB>& nm,
-                                                   const MaskPack<NB>& om, T qinf, T qsq) {
+                                                   const MaskPack<NB>& om, T qinf, T qsq, const SolveParams& p,
+                                                   const double* Cn, const double* Co, int t) {
     constexpr int NP = NB * (NB - 1) / 2;
     constexpr int NWD = TermBits<NB>::words;
     const T c3[3] = {cx, cy, cz};
     T flmax = T(0), dsq = T(0);
-    bool need_exact = false, act_new = false;
+    bool need_exact = false, act_new = false, act64 = false;
     // pass 1: exit residual of the flagged terms (needs the old row)
 #pragma unroll 1
     for (int w = 0; w < NWD; ++w) {
@@ -655,7 +844,7 @@ __device__ __forceinline__ StepOut<T> flagged_path(const T* __restrict__ Pnew, T
                 dsq -= x[ax] * x[ax];
             }
             need_exact = need_exact || (xq >= qinf);
-            if (!in_old) {
+            if (!in_old) {   // (HY: an FP32 measurement like the rest; the stop decision re-evaluates in FP64)
                 const T qo = fma_t<T>(o[2] * fm.beta, o[2], fma_t<T>(o[1], o[1], o[0] * o[0]));
                 const T so = qo > T(0) ? fm.lat * rsq<T>(qo) : T(0);
 #pragma unroll
@@ -775,6 +964,17 @@ __device__ __forceinline__ StepOut<T> flagged_path(const T* __restrict__ Pnew, T
                 int i, j;
                 term_robots<NB>(ptab, b, i, j);
                 const bool pair = j >= 0;
+                if constexpr (HY) {   // FP64 scattered residual (0 for a term interior in FP64), rounded once
+                    const D3 r = hy_term_resid<MP>(p, Cn, t, i, j);
+                    act64 = act64 || r.x != 0.0 || r.y != 0.0 || r.z != 0.0;
+                    const T rr[3] = {(T)r.x, (T)r.y, (T)r.z};
+#pragma unroll
+                    for (int ax = 0; ax < 3; ++ax) {
+                        Pold[ax * NB + i] += rr[ax];
+                        if (pair) Pold[ax * NB + j] -= rr[ax];
+                    }
+                    continue;
+                }
                 const Family<T>& fm = pair ? fp : fw;
                 T d[3];
 #pragma unroll
@@ -793,7 +993,7 @@ __device__ __forceinline__ StepOut<T> flagged_path(const T* __restrict__ Pnew, T
     StepOut<T> r;
     r.inf = fmax(base, flmax);
     r.sq = fmax(qsq + dsq, T(0));
-    r.active = act_new;
+    r.active = HY ? act64 : act_new;   // HY: a step whose flagged terms are all interior in FP64 has R = 0
     return r;
 }
 
@@ -884,6 +1084,78 @@ __device__ __noinline__ CarefulOut<T> careful_pass(const PosPack<T, NB> pk, T* _
     return r;
 }
 
+// FP64 exit residual (max |x|, sum x^2) of time step t for the stop decision near tol_res.  A term interior
+// at the old iterate (bit set in om -- the guarded FP32 test, so interior in FP64 too) has exit residual
+// Dd = D(p_i) - D(p_j) (workspace: D(p_i)), with D p = (C_k - C_{k-1}) W[t]^T: the per-axis range / max |D p|
+// of the robots, O(n).  The few terms non-interior at the old iterate take the FP64 target formula and, only
+// then, the max over the other terms is taken term by term.
+template <int NB, int MP>
+__device__ __noinline__ double2 hy_exit64(const SolveParams& p, const double* Cn, const double* Co, int t,
+                                          const MaskPack<NB> om) {
+    const int n = p.n;
+    double w[MP];
+    w64_row<MP>(p.W, t, p.m1, w);
+    double dp[3 * NB];
+    double mx = 0.0, s2 = 0.0;
+    for (int ax = 0; ax < 3; ++ax) {
+        double lo = 0.0, hi = 0.0, s1 = 0.0, sq = 0.0;
+        for (int i = 0; i < n; ++i) {
+            const double* cn = Cn + (ax * n + i) * MP;
+            const double* co = Co + (ax * n + i) * MP;
+            double v = 0.0;
+#pragma unroll
+            for (int q = 0; q < MP; ++q) v = fma(cn[q] - co[q], w[q], v);
+            dp[ax * NB + i] = v;
+            lo = i ? fmin(lo, v) : v;
+            hi = i ? fmax(hi, v) : v;
+            s1 += v;
+            sq = fma(v, v, sq);
+        }
+        mx = fmax(mx, fmax(hi - lo, fmax(hi, -lo)));
+        s2 += fmax(fma((double)(n + 1), sq, -s1 * s1), sq);
+    }
+    constexpr int NP = NB * (NB - 1) / 2;
+    bool any = false;   // (phantom robots' terms are always interior: their bits are set)
+    for (int b = 0; b < TermBits<NB>::count; ++b) any = any || !bit_of(om.w, b);
+    if (any) {   // terms non-interior at the old iterate: exact targets, then the max over the rest
+        double base = 0.0, flmax = 0.0, adj = 0.0;
+        int b = 0;
+        for (int i = 0; i < NB; ++i) {
+            for (int j = i + 1; j < NB; ++j, ++b) {
+                if (j >= n) continue;
+                const double ex = dp[i] - dp[j], ey = dp[NB + i] - dp[NB + j], ez = dp[2 * NB + i] - dp[2 * NB + j];
+                if (bit_of(om.w, b)) {
+                    base = fmax(base, fmax(fabs(ex), fmax(fabs(ey), fabs(ez))));
+                } else {
+                    double wr[MP];
+                    w64_row<MP>(p.W, t, p.m1, wr);
+                    const D3 dn = term_diff64<MP>(p, Cn, wr, i, j), dol = term_diff64<MP>(p, Co, wr, i, j);
+                    const D3 x = resid64(true, dol, dn, family64(p, true));
+                    flmax = fmax(flmax, fmax(fabs(x.x), fmax(fabs(x.y), fabs(x.z))));
+                    adj += (x.x * x.x + x.y * x.y + x.z * x.z) - (ex * ex + ey * ey + ez * ez);
+                }
+            }
+        }
+        b = NP;
+        for (int i = 0; i < n; ++i, ++b) {
+            const double ex = dp[i], ey = dp[NB + i], ez = dp[2 * NB + i];
+            if (bit_of(om.w, b)) {
+                base = fmax(base, fmax(fabs(ex), fmax(fabs(ey), fabs(ez))));
+            } else {
+                double wr[MP];
+                w64_row<MP>(p.W, t, p.m1, wr);
+                const D3 dn = term_diff64<MP>(p, Cn, wr, i, -1), dol = term_diff64<MP>(p, Co, wr, i, -1);
+                const D3 x = resid64(false, dol, dn, family64(p, false));
+                flmax = fmax(flmax, fmax(fabs(x.x), fmax(fabs(x.y), fabs(x.z))));
+                adj += (x.x * x.x + x.y * x.y + x.z * x.z) - (ex * ex + ey * ey + ez * ez);
+            }
+        }
+        mx = fmax(base, flmax);
+        s2 = fmax(s2 + adj, 0.0);
+    }
+    return make_double2(mx, s2);
+}
+
 // ---------------------------------------------------------------- finishing a time step
 // Given the interior bits of every term (nm) and min |component| (zmin), run
 // the careful / quiet / flagged path of time step `lt` and write its outputs:
@@ -893,8 +1165,9 @@ template <typename T> struct Partials {
     T inf, sq;
 };
 
-template <typename T, int NB>
-__device__ __forceinline__ Partials<T> finish_step(const SlotPtrs& sp, const int* __restrict__ ptab, int lt, int n,
+template <typename T, int NB, int MP, bool HY>
+__device__ __forceinline__ Partials<T> finish_step(const SolveParams& p, const SlotPtrs& sp, const double* Ck,
+                                                   const double* Ckm1, const int* __restrict__ ptab, int lt, int n,
                                                    int par, T* __restrict__ Prow_old,
                                             const T* __restrict__ Prow_new, T qinf, T qsq,
                                             uint32_t (&nm)[TermBits<NB>::words],
@@ -906,17 +1179,28 @@ __device__ __forceinline__ Partials<T> finish_step(const SlotPtrs& sp, const int
     SGSF_COUNT(0, 1);
     if (__builtin_expect(zmin == T(0) || zprev, 0)) {
         SGSF_COUNT(3, 1);
-        PosPack<T, NB> pk;
+        if constexpr (HY) {   // careful path from FP64 positions of both iterates
+            MaskPack<NB> mo;
+            const HyStepOut<T, NB, MP> co = hy_step_full<T, NB, MP>(p, Ck, Ckm1, lt, Prow_old, &mo);
 #pragma unroll
-        for (int q = 0; q < 3 * NB; ++q) pk.v[q] = ((q % NB) < n) ? Prow_new[q] : phantom_pos<T>(q % NB);
-        MaskPack<NB> mo;
-        const CarefulOut<T> co = careful_pass<T, NB>(pk, Prow_old, n, fp, fw, cx, cy, cz, &mo);
+            for (int w = 0; w < NW; ++w) nm[w] = mo.w[w];
+            inf = (T)co.inf;
+            sq = (T)co.sq;
+            active = co.active;
+            zprev = co.zero;
+        } else {
+            PosPack<T, NB> pk;
 #pragma unroll
-        for (int w = 0; w < NW; ++w) nm[w] = mo.w[w];
-        inf = co.inf;
-        sq = co.sq;
-        active = co.active;
-        zprev = co.zero;
+            for (int q = 0; q < 3 * NB; ++q) pk.v[q] = ((q % NB) < n) ? Prow_new[q] : phantom_pos<T>(q % NB);
+            MaskPack<NB> mo;
+            const CarefulOut<T> co = careful_pass<T, NB>(pk, Prow_old, n, fp, fw, cx, cy, cz, &mo);
+#pragma unroll
+            for (int w = 0; w < NW; ++w) nm[w] = mo.w[w];
+            inf = co.inf;
+            sq = co.sq;
+            active = co.active;
+            zprev = co.zero;
+        }
     } else {
         uint32_t any = 0u;
 #pragma unroll
@@ -929,14 +1213,14 @@ __device__ __forceinline__ Partials<T> finish_step(const SlotPtrs& sp, const int
                 omp.w[w] = imask[w];
             }
             SGSF_COUNT(1, 1);
-            const StepOut<T> o = flagged_path<T, NB>(Prow_new, Prow_old, n, ptab, fp, fw, cx, cy, cz, nmp, omp, inf, sq);
+            const StepOut<T> o = flagged_path<T, NB, MP, HY>(Prow_new, Prow_old, n, ptab, fp, fw, cx, cy, cz, nmp, omp,
+                                                            inf, sq, p, Ck, Ckm1, lt);
             inf = o.inf;
             sq = o.sq;
             active = o.active;
         }
     }
-#pragma unroll
-    for (int w = 0; w < NW; ++w) imask[w] = nm[w];
+    // (imask, the interior bits of the previous iterate, becomes nm after the stop decision: HY reads it there)
     if (active) {
         atomicOr(&sp.sh->amask[par][lt >> 5], 1u << (lt & 31));
         sp.sh->active[par] = 1;
@@ -948,10 +1232,10 @@ __device__ __forceinline__ Partials<T> finish_step(const SlotPtrs& sp, const int
 }
 
 // ---------------------------------------------------------------- load a sample (one coefficient row)
-template <typename T, int NB, int MP, bool TC>
+template <typename T, int NB, int MP, bool TC, bool HY>
 __device__ __forceinline__ void load_row(const SolveParams& p, const SlotPtrs& sp, int sample, int r,
-                                         const double* __restrict__ B6, const double* __restrict__ rhs,
-                                         const double* __restrict__ PBt) {
+                                         const double* __restrict__ B6, const double* __restrict__ rhs) {
+    const double* __restrict__ PBt = p.PBt;   // m1 x 6, global
     const int m1 = p.m1, dim = 3 * p.n * m1;
     const double* xr = p.xi_bar + (size_t)sample * dim + r * m1;
     double x[MP], c[MP], l[MP];
@@ -979,7 +1263,7 @@ __device__ __forceinline__ void load_row(const SolveParams& p, const SlotPtrs& s
         for (int q = 0; q < MP; ++q) {
             double corr = 0.0;
 #pragma unroll
-            for (int cnd = 0; cnd < 6; ++cnd) corr = fma(PBt[q * 6 + cnd], res[cnd], corr);
+            for (int cnd = 0; cnd < 6; ++cnd) corr = q < m1 ? fma(PBt[q * 6 + cnd], res[cnd], corr) : corr;
             c[q] = x[q] - corr;
             l[q] = 0.0;
         }
@@ -990,7 +1274,7 @@ __device__ __forceinline__ void load_row(const SolveParams& p, const SlotPtrs& s
         sp.xb[idx] = x[q];
         sp.C[idx] = c[q];
         sp.lam[idx] = l[q];
-        if (p.want_prev) sp.Cp[idx] = c[q];
+        if (p.want_prev || HY) sp.Cp[idx] = c[q];
     }
     const int ax = r / p.n, i = r - ax * p.n;
     if constexpr (TC) {
@@ -1037,9 +1321,10 @@ __host__ __device__ __forceinline__ int step_of(int lwarp, int lane, int wps, in
 // TC = positions by the 3xTF32 tcgen05 GEMM (float, 16 robots, one thread per step, 4 warps per slot)
 // FULLN: 0 = both term-pass variants, chosen at run time by n == NB; 1 = only the phantom-free one
 // (n == NB); 2 = only the one with phantoms (n < NB).  A single variant keeps the hot loop's code small.
-template <typename T, int NB, int MP, int MAXT, int TPS, bool TC = false, int FULLN = 0>
+template <typename T, int NB, int MP, int MAXT, int TPS, bool TC = false, int FULLN = 0, bool HY = false>
 __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParams p) {
     static_assert(!TC || (sizeof(T) == 4 && NB == 16 && TPS == 1 && MP <= 16), "TC positions: float, 16 robots");
+    static_assert(!HY || sizeof(T) == 4, "hybrid precision screens in FP32");
     extern __shared__ __align__(16) unsigned char smem[];
     const SmemLayout& L = p.L;   // = make_layout<T, NB>(p.n, p.S, MP, p.spb, p.want_prev, TC), host-computed
     constexpr int RS = RowStride<T, NB>::value;
@@ -1055,7 +1340,6 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
     double* cconst = (double*)(smem + L.cconst);
     double* B6 = (double*)(smem + L.B6);
     double* rhs = (double*)(smem + L.rhs);
-    double* PBt = (double*)(smem + L.PBt);
 
     // shared constants, zero-padded to MP columns
     for (int i = tid; i < S * MP; i += nt) {
@@ -1078,10 +1362,6 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
         B6[i] = (q < m1) ? p.B6[c * m1 + q] : 0.0;
     }
     for (int i = tid; i < R3 * 6; i += nt) rhs[i] = p.rhs[i];
-    for (int i = tid; i < MP * 6; i += nt) {
-        const int q = i / 6;
-        PBt[i] = (q < m1) ? p.PBt[i] : 0.0;
-    }
     int* ptab = (int*)(smem + L.ptab);   // pair index -> (i | j << 8), lexicographic i < j
     if (tid == 0) {
         int b = 0;
@@ -1133,8 +1413,8 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
     const SlotPtrs sp = slot_ptrs(smem, L, slot);
     Family<T> fp, fw;   // = make_family<T>(lat, vert), from the parameter bank
     if constexpr (sizeof(T) == 4) {
-        fp.lat = p.fp_lat_f, fp.lim = p.fp_lim_f, fp.beta = p.fp_beta_f;
-        fw.lat = p.fw_lat_f, fw.lim = p.fw_lim_f, fw.beta = p.fw_beta_f;
+        fp.lat = p.fp_lat_f, fp.lim = HY ? p.hy_fp_lim_f : p.fp_lim_f, fp.beta = p.fp_beta_f;
+        fw.lat = p.fw_lat_f, fw.lim = HY ? p.hy_fw_lim_f : p.fw_lim_f, fw.beta = p.fw_beta_f;
     } else {
         fp.lat = p.lat, fp.lim = p.fp_lim_d, fp.beta = p.fp_beta_d;
         fw.lat = p.ws_lat, fw.lim = p.fw_lim_d, fw.beta = p.fw_beta_d;
@@ -1206,7 +1486,7 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
     const uint32_t tbase = TC ? tmem_info[0] : 0u;
     while (sample < p.batch) {
         // ---------------- load the sample, default start = boundary projection
-        for (int r = lt; r < R3; r += gsize) load_row<T, NB, MP, TC>(p, sp, sample, r, B6, rhs, PBt);
+        for (int r = lt; r < R3; r += gsize) load_row<T, NB, MP, TC, HY>(p, sp, sample, r, B6, rhs);
         slot_barrier(bar_id, gsize);
         if constexpr (TC) {
             if (lwarp == 0) {   // positions of the first iterate (warp-uniform operands, one elected lane)
@@ -1226,6 +1506,11 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
         for (int k = 0;; ++k) {
             SGSF_PT(0);
             const int par = k & 1;
+            // HY: C_k and C_{k-1} alternate between the C and Cp buffers (the xi-step writes C_{k+1} over C_{k-1});
+            // otherwise C is updated in place and Cp is a copy (want_prev)
+            double* const Ccur = (HY && par) ? sp.Cp : sp.C;
+            double* const Cprv = (HY && par) ? sp.C : sp.Cp;
+            double* const Cnext = HY ? Cprv : Ccur;   // where the xi-step writes C_{k+1}
             if (lt == 0) clear_flags(sp.sh, par ^ 1, SWT);   // last read before the previous closing barrier
             // position rows: old = iterate k, new = iterate k+1's input positions; R -> old row
             T* const Pbase_new = (T*)((k & 1) ? sp.P0 : sp.P1);
@@ -1346,7 +1631,7 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
             // ---------------- T3: every time step finishes (quiet / flagged / careful path), by its owner lane
             Partials<T> pr{T(0), T(0)};
             if (ts < S && owner)
-                pr = finish_step<T, NB>(sp, ptab, ts, n, par, Prow_old, Prow_new, qinf, qsq, nm, fmin(zmin_ws, zmin_pairs),
+                pr = finish_step<T, NB, MP, HY>(p, sp, Ccur, Cprv, ptab, ts, n, par, Prow_old, Prow_new, qinf, qsq, nm, fmin(zmin_ws, zmin_pairs),
                                         imask, zprev, fp, fw, cx, cy, cz);
             {   // per-warp exit-residual partials for the decision (fixed order: deterministic); the l2
                 // partial is summed over the warp in T (FP32 lean: the history is an l2 norm, checked to
@@ -1405,14 +1690,51 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                     }
                 }
             }
-            // (a sample can only finish at k >= 1, so `inf` is always the last exit residual there)
+            double infd = (double)inf;
+            if constexpr (HY) {
+                // the FP32-measured exit residual sits within hy_delta of tol_res (slot-uniform: every warp
+                // read the same partials): re-evaluate it in FP64 over every time step, so the stop decision
+                // is the one the FP64 iterates give
+                if (k >= 1 && p.early_stop && fabs(infd - p.tol_res) <= p.hy_delta) {
+                    if (lt == 0) SGSF_COUNT(8, 1);
+                    double xi = 0.0, xs = 0.0;
+                    if (ts < S && owner) {
+                        MaskPack<NB> om;
+#pragma unroll
+                        for (int w = 0; w < NW; ++w) om.w[w] = imask[w];
+                        const double2 e = hy_exit64<NB, MP>(p, Ccur, Cprv, ts, om);
+                        xi = e.x;
+                        xs = e.y;
+                    }
+                    xi = warp_max_nonneg(xi);
+#pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) xs += __shfl_xor_sync(0xffffffffu, xs, off);
+                    const int pw = TC ? 4 : MAX_SLOT_WORDS;
+                    if (lane == 0) {
+                        sp.pex[lwarp] = xi;
+                        sp.pex[pw + lwarp] = xs;
+                    }
+                    slot_barrier(bar_id, gsize);
+                    infd = 0.0;
+                    sqs = 0.0;
+                    for (int w = 0; w < p.wps; ++w) {
+                        infd = fmax(infd, sp.pex[w]);
+                        sqs += sp.pex[pw + w];
+                    }
+                }
+            }
+            if (ts < S && owner) {   // interior bits of this iterate: the "old" ones of the next
+#pragma unroll
+                for (int w = 0; w < NW; ++w) imask[w] = nm[w];
+            }
+            // (a sample can only finish at k >= 1, so `infd` is always the last exit residual there)
             const bool failed = (k >= 1) && (emax > p.tol_eq);
             bool done = failed;
             if (k >= 1) {
-                done = done || (p.early_stop && (double)inf <= p.tol_res) || (k >= p.max_iters);
+                done = done || (p.early_stop && infd <= p.tol_res) || (k >= p.max_iters);
                 if (lt == hist_lt) {
                     const size_t hix = (size_t)sample * p.max_iters + (k - 1);
-                    p.res_inf[hix] = (double)inf;
+                    p.res_inf[hix] = infd;
                     p.res_l2[hix] = sqrt(sqs);
                 }
             }
@@ -1423,22 +1745,22 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                     for (int e = lt; e < dim; e += gsize) {
                         const int r = e / m1, q = e - r * m1;
                         const size_t o = (size_t)sample * dim + e;
-                        p.coeffs[o] = sp.C[r * MP + q];
+                        p.coeffs[o] = Ccur[r * MP + q];
                         p.mult[o] = sp.lam[r * MP + q];
-                        if (p.want_prev && p.coeffs_prev) p.coeffs_prev[o] = sp.Cp[r * MP + q];
+                        if (p.want_prev && p.coeffs_prev) p.coeffs_prev[o] = Cprv[r * MP + q];
                     }
                 }
                 if (lwarp == 0) {
                     double acc = 0.0;
                     for (int e = lane; e < dimp; e += 32) {
-                        const double dd = sp.C[e] - sp.xb[e];
+                        const double dd = Ccur[e] - sp.xb[e];
                         acc = fma(dd, dd, acc);
                     }
 #pragma unroll
                     for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
                     if (lane == 0) {
                         p.iterations[sample] = failed ? 0 : k;
-                        p.converged[sample] = (!failed && (double)inf <= p.tol_res) ? 1 : 0;
+                        p.converged[sample] = (!failed && infd <= p.tol_res) ? 1 : 0;
                         p.displacement[sample] = failed ? CUDART_NAN : sqrt(acc);
                         p.status[sample] = failed ? SAMPLE_SINGULAR_KKT : SAMPLE_OK;
                         p.eq_err[sample] = emax;
@@ -1574,7 +1896,7 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
 #pragma unroll
                         for (int mt = 0; mt < MT; ++mt) {
                             const int rob = 8 * mt + fr;
-                            const double a = rob < n ? (kk < KC ? sp.C[(rb + rob) * MP + c] : sp.U[(rb + rob) * MP + c - MP])
+                            const double a = rob < n ? (kk < KC ? Ccur[(rb + rob) * MP + c] : sp.U[(rb + rob) * MP + c - MP])
                                                      : 0.0;
                             csum[kk] += a;
 #pragma unroll
@@ -1608,7 +1930,7 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                     }
                     SGSF_PT(11);
                     SGSF_PT(12);
-                    if (p.want_prev) {
+                    if (p.want_prev && !HY) {
                         for (int e = lane; e < n * MP; e += 32) sp.Cp[rb * MP + e] = sp.C[rb * MP + e];
                     }
                     __syncwarp();   // every lane has read the rows before any lane writes them
@@ -1620,7 +1942,7 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                             const int q = 8 * nt + 2 * fc;
                             if (rob < n && q < MP) {
                                 const int idx = (rb + rob) * MP + q;
-                                *reinterpret_cast<double2*>(sp.C + idx) = make_double2(dacc[mt][nt][0], dacc[mt][nt][1]);
+                                *reinterpret_cast<double2*>(Cnext + idx) = make_double2(dacc[mt][nt][0], dacc[mt][nt][1]);
                                 if constexpr (TC) {
                                     unsigned char* bo = (unsigned char*)sp.Cf + ax * 2048;
 #pragma unroll
@@ -1675,7 +1997,7 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
 #pragma unroll
                             for (int mt = 0; mt < MT; ++mt) {
                                 const int rob = 8 * mt + fr;
-                                const double a = rob < n ? sp.C[(rb + rob) * MP + q] : 0.0;
+                                const double a = rob < n ? Cnext[(rb + rob) * MP + q] : 0.0;
                                 dmma884(eacc[mt][0], eacc[mt][1], a, bv);
                             }
                         }

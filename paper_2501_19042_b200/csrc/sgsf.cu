@@ -229,13 +229,16 @@ int sgsf_solve(sgsf_handle_t* h, int batch, const double* xi_bar, const double* 
         p.order = order;
     }
 
+    if (cfg->precision < SGSF_PRECISION_LEAN || cfg->precision > SGSF_PRECISION_HYBRID)
+        return fail(SGSF_ERR_INVALID, "precision must be SGSF_PRECISION_LEAN, _STRICT or _HYBRID");
     const bool strict = cfg->precision == SGSF_PRECISION_STRICT;
     const int n = h->n;
     const bool wide = h->m1 > 12;
     LaunchInfo li{h->device, h->sm_count};
     int rc = SGSF_OK;
     if (n > 32) {
-        rc = launch_large(li, p, cfg, timing, stream, strict);
+        // (K1L has no hybrid variant: hybrid runs it in FP64)
+        rc = launch_large(li, p, cfg, timing, stream, cfg->precision != SGSF_PRECISION_LEAN);
     } else {
 #define SGSF_PICK(T, NB, MAXT, TPS)                                                      \
     rc = wide ? launch_persistent<T, NB, 16, MAXT, TPS>(li, p, cfg, timing, stream) \

@@ -16,7 +16,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libsgsf.so"
 
 SGSF_OK, SGSF_ERR_INVALID, SGSF_ERR_CUDA, SGSF_ERR_UNSUPPORTED, SGSF_ERR_SINGULAR = 0, 1, 2, 3, 4
 SAMPLE_OK, SAMPLE_SINGULAR_KKT = 0, 1
-PRECISION_LEAN, PRECISION_STRICT = 0, 1
+PRECISION_LEAN, PRECISION_STRICT, PRECISION_HYBRID = 0, 1, 2
 
 _dp = C.POINTER(C.c_double)
 

@@ -32,7 +32,7 @@ from .errors import DimensionMismatch, SingularKKT, SwarmFilterError
 from .precompute import DeviceConstants, EqualitySystem, build_equality, device_constants
 from .problem import validate_problem
 
-_PRECISIONS = {"lean": native.PRECISION_LEAN, "strict": native.PRECISION_STRICT}
+_PRECISIONS = {"lean": native.PRECISION_LEAN, "strict": native.PRECISION_STRICT, "hybrid": native.PRECISION_HYBRID}
 
 
 @dataclass(frozen=True)

@@ -51,7 +51,7 @@ def swap_proposal(two_robot_filter):
     return straight_line_coeffs(two_robot_filter.problem, two_robot_filter.basis)
 
 
-@pytest.mark.parametrize("precision", ["lean", "strict"])
+@pytest.mark.parametrize("precision", ["lean", "strict", "hybrid"])
 def test_feasible_proposal_converges_immediately(parallel_filter, feasible_proposal, precision):
     from paper_2501_19042_b200 import SolverConfig
     res = parallel_filter.solve(feasible_proposal, config=SolverConfig(precision=precision))

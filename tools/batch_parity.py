@@ -20,7 +20,7 @@ from tests.batch_parity import compare, run  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("names", nargs="*", default=["batch_cfg2", "batch_ws_tight"])
-    ap.add_argument("--precision", nargs="*", default=["strict", "lean"])
+    ap.add_argument("--precision", nargs="*", default=["strict", "hybrid", "lean"])
     ap.add_argument("--band", type=float, default=1e-6)
     a = ap.parse_args()
     (ROOT / "gpurun_out").mkdir(exist_ok=True)

@@ -27,6 +27,7 @@ if os.environ.get("PT_CONFIG", "2") != "2":
     run("full", xb, cfg)
     raise SystemExit
 prob, shard, cfg = bench.workload(0, 1, bench.BATCH_PER_GPU)
+cfg = replace(cfg, precision=os.environ.get("PT_PRECISION", cfg.precision))
 sf = SafetyFilter(prob, degree=10, config=cfg)
 xb = torch.from_numpy(shard).cuda()
 sms = torch.cuda.get_device_properties(0).multi_processor_count

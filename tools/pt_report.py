@@ -7,7 +7,7 @@ import numpy as np
 for tag in sys.argv[1:] or ["fixed1", "fixed3", "full"]:
     rows = []
     for ln in open(f"gpurun_out/pt_{tag}.log"):
-        if ln.startswith("PT"):
+        if ln.startswith("PT block"):
             rows.append({k: float(v) for k, v in re.findall(r"([A-Za-z0-9]+) ([0-9.]+)", ln)})
     tot = np.array([r["total"] for r in rows])
     its = np.array([r["iters"] for r in rows])
