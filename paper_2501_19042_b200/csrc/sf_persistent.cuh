@@ -584,6 +584,20 @@ template <int NB> struct MaskPack {
     uint32_t w[TermBits<NB>::words];
 };
 
+// robots of term bit b: pair (i, j) from the lexicographic pair table, or workspace term i (j = -1)
+template <int NB> __device__ __forceinline__ void term_robots(const int* __restrict__ ptab, int b, int& i, int& j) {
+    constexpr int NP = NB * (NB - 1) / 2;
+    if (b < NP) {
+        const int ij = ptab[b];
+        i = ij & 0xff;
+        j = ij >> 8;
+    } else {
+        i = b - NP;
+        j = -1;
+    }
+}
+
+
 // ---------------------------------------------------------------- hybrid precision (HY): FP64 values
 // The HY kernels screen in FP32 exactly like the lean ones, with the interior tests narrowed by a guard band
 // (fp.lim, fw.lim scaled on the host side of the kernel): a term the FP32 test calls interior is interior in
@@ -649,22 +663,38 @@ __device__ __forceinline__ D3 resid64(bool pair, const D3& d, const D3& b, const
     return r;
 }
 
-// exit residual d(C_k) - e(C_{k-1}) of term (i, j) at step t
-template <int MP>
-__device__ __noinline__ D3 hy_term_exit(const SolveParams& p, const double* Cn, const double* Co, int t, int i, int j) {
+// Scattered residual R of every term non-interior (guarded FP32 test) in the new iterate at step t, in
+// FP64 from C_k: W row loaded once, R accumulated into the thread's (dead) old row.  Returns whether some term
+// has a non-zero residual (is active in FP64).
+template <typename T, int NB, int MP>
+__device__ __noinline__ bool hy_scatter_step(const SolveParams& p, const double* Cn, int t, const MaskPack<NB> nm,
+                                             const int* __restrict__ ptab, T* Pold) {
     double w[MP];
     w64_row<MP>(p.W, t, p.m1, w);
-    const D3 dn = term_diff64<MP>(p, Cn, w, i, j), dol = term_diff64<MP>(p, Co, w, i, j);
-    return resid64(j >= 0, dol, dn, family64(p, j >= 0));
-}
-
-// scattered residual d(C_k) - e(C_k) of term (i, j) at step t (0 for an FP64-interior term)
-template <int MP>
-__device__ __noinline__ D3 hy_term_resid(const SolveParams& p, const double* Cn, int t, int i, int j) {
-    double w[MP];
-    w64_row<MP>(p.W, t, p.m1, w);
-    const D3 dn = term_diff64<MP>(p, Cn, w, i, j);
-    return resid64(j >= 0, dn, dn, family64(p, j >= 0));
+    bool act = false;
+    for (int wd = 0; wd < TermBits<NB>::words; ++wd) {
+        uint32_t ac = ~nm.w[wd];
+        while (ac) {
+            const int bit = __ffs(ac) - 1;
+            ac &= ac - 1;
+            const int b = wd * 32 + bit;
+            if (b >= TermBits<NB>::count) break;
+            int i, j;
+            term_robots<NB>(ptab, b, i, j);
+            const D3 dn = term_diff64<MP>(p, Cn, w, i, j);
+            const D3 r = resid64(j >= 0, dn, dn, family64(p, j >= 0));
+            act = act || r.x != 0.0 || r.y != 0.0 || r.z != 0.0;
+            Pold[i] += (T)r.x;
+            Pold[NB + i] += (T)r.y;
+            Pold[2 * NB + i] += (T)r.z;
+            if (j >= 0) {
+                Pold[j] -= (T)r.x;
+                Pold[NB + j] -= (T)r.y;
+                Pold[2 * NB + j] -= (T)r.z;
+            }
+        }
+    }
+    return act;
 }
 
 // Every term of time step t in FP64: exit residual statistics (max |x|, sum x^2) and, when Rrow != null, the
@@ -762,19 +792,6 @@ template <typename T> struct StepOut {
     T inf, sq;
     bool active;
 };
-
-// robots of term bit b: pair (i, j) from the lexicographic pair table, or workspace term i (j = -1)
-template <int NB> __device__ __forceinline__ void term_robots(const int* __restrict__ ptab, int b, int& i, int& j) {
-    constexpr int NP = NB * (NB - 1) / 2;
-    if (b < NP) {
-        const int ij = ptab[b];
-        i = ij & 0xff;
-        j = ij >> 8;
-    } else {
-        i = b - NP;
-        j = -1;
-    }
-}
 
 // insertion of (v, i) into a descending three-deep selection (registers: compile-time indices only)
 template <typename T> __device__ __forceinline__ void top3_insert(T (&t)[3], int (&ti)[3], T v, int i) {
@@ -953,6 +970,9 @@ __device__ __forceinline__ StepOut<T> flagged_path(const T* __restrict__ Pnew, T
         for (int u = 0; u < L; ++u) reinterpret_cast<T*>(&z)[u] = T(0);
 #pragma unroll
         for (int c = 0; c < 3 * NB / L; ++c) reinterpret_cast<V*>(Pold)[c] = z;
+        if constexpr (HY) {   // FP64 scattered residuals (0 for terms interior in FP64), rounded once
+            act64 = hy_scatter_step<T, NB, MP>(p, Cn, t, nm, ptab, Pold);
+        } else {
 #pragma unroll 1
         for (int w = 0; w < NWD; ++w) {
             uint32_t ac = ~nm.w[w];
@@ -964,17 +984,6 @@ __device__ __forceinline__ StepOut<T> flagged_path(const T* __restrict__ Pnew, T
                 int i, j;
                 term_robots<NB>(ptab, b, i, j);
                 const bool pair = j >= 0;
-                if constexpr (HY) {   // FP64 scattered residual (0 for a term interior in FP64), rounded once
-                    const D3 r = hy_term_resid<MP>(p, Cn, t, i, j);
-                    act64 = act64 || r.x != 0.0 || r.y != 0.0 || r.z != 0.0;
-                    const T rr[3] = {(T)r.x, (T)r.y, (T)r.z};
-#pragma unroll
-                    for (int ax = 0; ax < 3; ++ax) {
-                        Pold[ax * NB + i] += rr[ax];
-                        if (pair) Pold[ax * NB + j] -= rr[ax];
-                    }
-                    continue;
-                }
                 const Family<T>& fm = pair ? fp : fw;
                 T d[3];
 #pragma unroll
@@ -988,6 +997,7 @@ __device__ __forceinline__ StepOut<T> flagged_path(const T* __restrict__ Pnew, T
                     if (pair) Pold[ax * NB + j] -= r;
                 }
             }
+        }
         }
     }
     StepOut<T> r;
