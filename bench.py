@@ -1,30 +1,40 @@
 """Benchmark: SF-projected feasible swarm samples/s (16 drones, H=100) on B200.
 
-    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config 2|3|4]
+                    [--precision hybrid|lean|strict]
 
-One "step" = one pass of the hot path over one batch: the persistent SF kernel
-solves every sample of the batch to tol 1e-3 (or max_iters), then the fused
-feasibility verdict (and, for N > 1, the NCCL gather of the projected
-trajectories, iterations and verdicts).  Workload = BASELINE config 2: seeded
-16-robot H=100 scenario (paper_2501_19042_b200.scenarios, seed 2), 1000
-proposals per GPU from the reference's Gaussian sampler (seed 0), boundary-
-projected start, degree 10, rho 1, max_iters 500 (this scenario needs
-~290-380 iterations; none converge within 200).  Weak scaling: each rank
-solves its own contiguous 1000-sample shard of one global seeded batch.
+One "step" = one pass of the hot path over one batch: the persistent SF kernel solves every sample of the
+batch to tol 1e-3 (or max_iters), the feasible verdict runs behind it, and for N > 1 the per-sample outputs
+(coefficients, multipliers, residual histories, iterations, verdicts, displacement, status) are all-gathered
+over NCCL.  The headline is BASELINE config 2 (`--config 2`, default): a seeded 16-robot H=100 scenario,
+1000 proposals per GPU from the reference's Gaussian sampler (seed 0), boundary-projected start, degree 10,
+rho 1, max_iters 500 -- weak scaling over N GPUs.  `--config 3` (32 robots, H=100, 4096 samples) and
+`--config 4` (64 robots, H=150, 8192 samples) strong-scale one batch over the N GPUs, as BASELINE states them.
 
-`value` is device-timed (CUDA events, inputs resident in HBM, L2 flushed
-between steps, max over ranks); `e2e` is the same metric through the public
-API with pinned host buffers, H2D and D2H inside the timed region.
-`--impl reference` times the CPU oracle port of the reference algorithm
-(oracle/sf_oracle.py: trig projection + dense LU, the reference's own
-arithmetic) on the host cores with a process pool, on a bounded sample.
+Precision (default "hybrid"): FP32 screening with guard bands, FP64 targets/residuals/state and an FP64
+re-evaluation of the stop decision near tol -- the precision whose iteration counts and verdicts equal the
+reference's on all 1000 headline samples (tests/test_gpu_batch_parity.py).  At N = 1 the line also carries
+device-timed numbers of "lean" (FP32 terms) and "strict" (FP64 everywhere) from the same run.
+
+`value` is device-timed (CUDA events, inputs resident in HBM, a 256 MB write flushes L2 between steps, max
+over ranks); `e2e` is the same metric through the public API with pinned host buffers, the H2D copy of the
+proposals and the D2H copy of every per-sample output inside the timed region.  At N = 1 two more end-to-end
+numbers: `e2e_dropin` (the reference-compatible `SafetyFilter.batch_solve` on a list of numpy proposals at its
+defaults, plus `feasible_results`) and `pipeline` (config 2 as BASELINE states it: CVAE samples -> boundary QP
+-> init-network warm start -> SF -> verdict, all on the device).
+
+`--impl reference` (and the `cpu_baseline` leg) time the reference's own CPU solver on the host cores: the
+compiled reference built into oracle/_ref by oracle/build_ref.sh (`kind: "reference"`), or, where that is
+missing, the numpy port oracle/sf_oracle.py (`kind: "port"`).  One persistent process pool (BLAS pinned to 1
+thread per process) streams the batch's proposals; each timed step counts the samples the pool completes in
+its time slice, so the rate is the pool's steady-state throughput.
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -35,8 +45,10 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "SF-projected feasible swarm samples/sec (16 drones, H=100); ms per 1k batch"
-BATCH_PER_GPU = 1000
 MAX_ITERS = 500
+# per BASELINE config: (robots, horizon, batch, scaling); config 2's batch is per GPU (weak scaling)
+CONFIGS = {2: (16, 100, 1000, "weak"), 3: (32, 100, 4096, "strong"), 4: (64, 150, 8192, "strong")}
+REF_DIR = ROOT / "oracle" / "_ref"
 
 
 def flop_per_si(n: int, S: int, m1: int) -> int:
@@ -45,51 +57,117 @@ def flop_per_si(n: int, S: int, m1: int) -> int:
     return 33 * P * S + 30 * n * S + 12 * n * S * m1 + 12 * n * m1 * m1 + 42 * n * m1
 
 
-def workload(rank: int, world: int, batch: int):
-    from paper_2501_19042_b200 import SolverConfig, sample_proposals
+def global_batch(config: int, world: int, batch: int | None) -> int:
+    n, H, b, scaling = CONFIGS[config]
+    b = batch or b
+    return b * world if scaling == "weak" else b
+
+
+def workload(config: int, rank: int, world: int, batch: int | None = None):
+    """(problem, this rank's proposal shard, global batch): one global seeded batch, contiguous shards."""
+    from paper_2501_19042_b200 import sample_proposals
     from paper_2501_19042_b200.basis import build_basis
+    from paper_2501_19042_b200.distributed import shard_range
     from paper_2501_19042_b200.scenarios import config_problem
-    prob = config_problem(2)
+    prob = config_problem(config)
     basis = build_basis(prob.duration, degree=10, samples=prob.horizon_samples)
-    props = sample_proposals(prob, basis, batch * world, seed=0).proposals
-    shard = props[rank * batch:(rank + 1) * batch]
-    return prob, shard, SolverConfig(max_iters=MAX_ITERS, svars=False)
+    B = global_batch(config, world, batch)
+    props = sample_proposals(prob, basis, B, seed=0).proposals
+    lo, hi = shard_range(B, world, rank)
+    return prob, props[lo:hi], B
 
 
-# ----------------------------------------------------------------------------- CPU legs
-def _oracle_worker(args):
-    from threadpoolctl import threadpool_limits
-    doc, xb, max_iters = args
-    with threadpool_limits(limits=1):
+def config2_case(batch: int = 1000, precision: str = "lean"):
+    """(problem, proposals, SolverConfig) of the headline workload on one GPU (tools and tests)."""
+    from paper_2501_19042_b200 import SolverConfig
+    prob, shard, _ = workload(2, 0, 1, batch)
+    return prob, shard, SolverConfig(max_iters=MAX_ITERS, svars=False, precision=precision)
+
+
+def config_label(config: int, B: int, world: int) -> str:
+    n, H, _, scaling = CONFIGS[config]
+    what = {2: "CVAE-shaped Gaussian proposals", 3: "VQ-VAE-shaped Gaussian proposals", 4: "Gaussian proposals"}
+    per = f"{B // world} per GPU" if scaling == "weak" else f"{B} strong-scaled over {world} GPU(s)"
+    return (f"BASELINE config {config}: {n} drones, H={H}, batch {per}, SF to 1e-3 (max_iters {MAX_ITERS}), "
+            f"boundary-projected start; {what[config]}")
+
+
+# ----------------------------------------------------------------------------- CPU legs (reference solver)
+_W = {}
+
+
+def _pool_init(doc, use_ref):
+    os.environ["OPENBLAS_NUM_THREADS"] = os.environ["OMP_NUM_THREADS"] = os.environ["MKL_NUM_THREADS"] = "1"
+    if use_ref:
+        sys.path.insert(0, str(REF_DIR))
+        import swarmfilter as sfm
+        prob = sfm.load_problem(doc)
+        _W.update(kind="reference", sfm=sfm, prob=prob,
+                  filt=sfm.SafetyFilter(prob, degree=10, config=sfm.SolverConfig(max_iters=MAX_ITERS)))
+    else:
         from oracle import sf_oracle
-        prob = sf_oracle.make_problem(doc, degree=10)
+        _W.update(kind="port", mod=sf_oracle, prob=sf_oracle.make_problem(doc, degree=10))
+
+
+def _pool_solve(x):
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(limits=1):
         t0 = time.perf_counter()
-        r = sf_oracle.solve(prob, xb, max_iters=max_iters)
-        dt = time.perf_counter() - t0
-        return r.iterations, sf_oracle.feasible(prob, r), dt
+        if _W["kind"] == "reference":
+            sfm = _W["sfm"]
+            r = _W["filt"].solve(x)
+            feas = len(sfm.metrics.feasible_results([r], _W["prob"])) == 1   # the headline's own numerator
+            its = r.iterations
+        else:
+            r = _W["mod"].solve(_W["prob"], x, max_iters=MAX_ITERS)
+            feas, its = _W["mod"].feasible(_W["prob"], r), r.iterations
+        return its, bool(feas), time.perf_counter() - t0
 
 
-def cpu_sample(doc, props, budget_s: float, max_samples: int | None = None):
-    """Run the oracle port over as many proposals as fit ~budget_s on all host cores."""
-    import multiprocessing as mp
-    cores = os.cpu_count() or 1
-    ctx = mp.get_context("fork")
-    done, feas, its, t_start = 0, 0, 0, time.perf_counter()
-    with ctx.Pool(cores) as pool:
-        while True:
-            chunk = props[done:done + cores]
-            if max_samples is not None:
-                chunk = chunk[:max(0, max_samples - done)]
-            if len(chunk) == 0:
-                break
-            for it, fe, _ in pool.map(_oracle_worker, [(doc, x, MAX_ITERS) for x in chunk]):
-                its += it
-                feas += int(fe)
-            done += len(chunk)
-            if time.perf_counter() - t_start >= budget_s:
-                break
-    wall = time.perf_counter() - t_start
-    return {"samples": done, "feasible": feas, "sample_iterations": its, "wall_s": wall, "cores": cores}
+def reference_available() -> bool:
+    if not (REF_DIR / "swarmfilter").is_dir():
+        return False
+    code = ("import sys; sys.path.insert(0, %r); from swarmfilter import kernels; "
+            "assert kernels.active_backend() == 'compiled'" % str(REF_DIR))
+    return subprocess.run([sys.executable, "-c", code], capture_output=True).returncode == 0
+
+
+class CpuStream:
+    """One persistent fork pool streaming the proposals (cyclically) through the reference solver, 2 tasks per
+    core in flight; `take(s)` counts what completes in the next s seconds: the pool's steady-state throughput,
+    with no per-step pool start-up and no straggler wave at the end of a step."""
+
+    def __init__(self, doc, props, cores=None):
+        import itertools
+        import multiprocessing as mp
+        import queue
+        self.use_ref = reference_available()
+        self.kind = "reference" if self.use_ref else "port"
+        self.cores = cores or os.cpu_count() or 1
+        self.pool = mp.get_context("fork").Pool(self.cores, initializer=_pool_init, initargs=(doc, self.use_ref))
+        self.cyc = itertools.cycle(list(props))
+        self.done = queue.Queue()
+        for _ in range(2 * self.cores):
+            self._submit()
+
+    def _submit(self):
+        self.pool.apply_async(_pool_solve, (next(self.cyc),), callback=self.done.put, error_callback=self.done.put)
+
+    def take(self, seconds: float) -> dict:
+        n = feas = its = 0
+        t0 = time.perf_counter()
+        while time.perf_counter() - t0 < seconds:
+            r = self.done.get()
+            if isinstance(r, BaseException):
+                raise r
+            self._submit()
+            i, f, _ = r
+            n, feas, its = n + 1, feas + int(f), its + i
+        return {"samples": n, "feasible": feas, "sample_iterations": its, "wall_s": time.perf_counter() - t0}
+
+    def close(self):
+        self.pool.terminate()
+        self.pool.join()
 
 
 def cpu_model() -> str:
@@ -100,6 +178,14 @@ def cpu_model() -> str:
     except OSError:
         pass
     return "unknown"
+
+
+def cpu_desc(stream: CpuStream, r: dict, what: str) -> str:
+    src = ("compiled reference (oracle/_ref: swarmfilter with its Cython kernel, SafetyFilter.solve + "
+           "metrics.feasible_results)" if stream.kind == "reference" else "numpy port oracle/sf_oracle.py")
+    return (f"{what}: {r['samples']} proposals of this batch, all iterations ({r['sample_iterations']} sample-"
+            f"iterations) in {r['wall_s']:.1f} s, {src}, persistent process pool on {stream.cores} cores "
+            f"({cpu_model()}), BLAS 1 thread/process")
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -171,54 +257,143 @@ class ClockSampler:
 def run_reference(args, rank: int, world: int) -> None:
     if rank != 0:
         return
-    prob, shard, cfg = workload(0, 1, BATCH_PER_GPU)
-    doc = prob.to_doc()
-    steps = []
-    total_feas = total_samples = 0
-    # per-step CPU budget: --ref-budget, or ~150 s over the timed steps (1.5-12 s each: at least one
-    # round of proposals per core), so the whole --steps K --warmup W run stays within a few minutes
-    budget = args.ref_budget if args.ref_budget is not None else min(12.0, max(1.5, 150.0 / max(1, args.steps)))
-    for _ in range(args.warmup):
-        cpu_sample(doc, shard, budget_s=0.0, max_samples=os.cpu_count() or 1)
-    for k in range(args.steps):
-        off = (k * (os.cpu_count() or 1)) % len(shard)
-        r = cpu_sample(doc, list(shard[off:]) + list(shard[:off]), budget_s=budget)
-        steps.append(r)
-        total_feas += r["feasible"]
-        total_samples += r["samples"]
+    prob, shard, B = workload(args.config, 0, 1, args.batch)
+    stream = CpuStream(prob.to_doc(), shard)
+    # per-step CPU time slice: --ref-budget, or ~150 s over the timed steps (2-12 s each), so the whole
+    # --steps K --warmup W run stays within a few minutes
+    budget = args.ref_budget if args.ref_budget is not None else min(12.0, max(2.0, 150.0 / max(1, args.steps)))
+    try:
+        # warm-up: fill the pool's pipeline (workers import the solver and start their first samples)
+        for _ in range(max(1, args.warmup)):
+            stream.take(min(budget, 3.0))
+        steps = [stream.take(budget) for _ in range(args.steps)]
+    finally:
+        stream.close()
     wall = sum(s["wall_s"] for s in steps)
-    value = total_feas / wall if wall > 0 else 0.0
-    cores = steps[0]["cores"]
+    feas = sum(s["feasible"] for s in steps)
+    done = sum(s["samples"] for s in steps)
+    value = feas / wall if wall > 0 else 0.0
+    tot = {"samples": done, "sample_iterations": sum(s["sample_iterations"] for s in steps), "wall_s": wall}
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "feasible samples/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * wall / max(1, args.steps), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded scenario + reference Gaussian sampler)",
-        "config": {"workload": "BASELINE config 2: 16 drones, H=100, SF to 1e-3 (max_iters 500); "
-                               "each step a bounded sample of the 1000-proposal batch",
-                   "n": 16, "H": 100, "batch": BATCH_PER_GPU, "max_iters": MAX_ITERS},
+        "ms_per_step": 1e3 * wall / max(1, args.steps), "higher_is_better": True,
+        "scaling": CONFIGS[args.config][3], "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded scenario + reference Gaussian sampler)",
+        "config": {"workload": config_label(args.config, B, 1) + "; each step a time slice of the batch",
+                   "n": prob.n, "H": prob.horizon_samples - 1, "batch": B, "max_iters": MAX_ITERS},
         "ms_per_1k_batch": 1e3 * 1000 / value if value > 0 else None,
-        "cpu_baseline": {"value": value, "unit": "feasible samples/s", "cores": cores, "kind": "port",
-                         "sample": f"{total_samples} proposals over {args.steps} steps, all iterations, "
-                                   f"process pool on {cores} cores ({cpu_model()}), BLAS 1 thread/process"},
+        "feasible_fraction": feas / done if done else None,
+        "cpu_baseline": {"value": value, "unit": "feasible samples/s", "cores": stream.cores, "kind": stream.kind,
+                         "sample": cpu_desc(stream, tot, f"{args.steps} steps of {budget:.1f} s")},
         "e2e": {"value": value, "unit": "feasible samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
 # ----------------------------------------------------------------------------- our arm
+def _timed(fn, reps: int = 1):
+    import torch
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        r = fn()
+    b.record()
+    b.synchronize()
+    return r, a.elapsed_time(b) / reps
+
+
+def side_precisions(sf, xb, cfg, flush, steps: int = 3) -> dict:
+    """Device-timed step of the other precisions on the same batch (N = 1 only)."""
+    import torch
+    from dataclasses import replace
+    out = {}
+    for prec in ("hybrid", "lean", "strict"):
+        if prec == cfg.precision:
+            continue
+        c = replace(cfg, precision=prec)
+        sf.solve_batched(xb, config=c)
+        torch.cuda.synchronize()
+        step_ms, kern_ms, feas, its = [], [], 0, 0
+        for k in range(steps):
+            flush.fill_(float(k))
+            kev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            o, ms = _timed(lambda: sf.solve_batched(xb, config=c, timing=kev))
+            step_ms.append(ms)
+            kern_ms.append(kev[0].elapsed_time(kev[1]))
+            feas, its = int(o.feasible.sum().item()), int(o.iterations.sum().item())
+        ms = statistics.median(step_ms)
+        out[prec] = {"value": feas / (ms * 1e-3), "ms_per_step": ms, "ms_per_1k_batch": ms * 1000 / xb.shape[0],
+                     "kernel_ms": statistics.median(kern_ms), "step_ms_all": step_ms, "feasible": feas,
+                     "mean_iterations": its / xb.shape[0]}
+    return out
+
+
+def dropin_e2e(prob, shard, reps: int = 2) -> dict:
+    """The reference-compatible call: SafetyFilter.batch_solve(list of numpy proposals) at its defaults
+    (svars on) + metrics.feasible_results -- numpy in, SolveResults out (solver.py:368-407, metrics.py:57-69)."""
+    from paper_2501_19042_b200 import SafetyFilter, SolverConfig, feasible_results
+    sf = SafetyFilter(prob, degree=10, config=SolverConfig(max_iters=MAX_ITERS))
+    props = [x.copy() for x in shard]
+    sf.batch_solve(props[:8])
+    times, feas = [], 0
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        res = sf.batch_solve(props)
+        feas = len(feasible_results(res.results, prob))
+        times.append(time.perf_counter() - t0)
+    t = statistics.median(times)
+    return {"value": feas / t, "unit": "feasible samples/s", "ms_per_batch": 1e3 * t, "feasible": feas,
+            "precision": sf.config.precision, "svars": True,
+            "what": "SafetyFilter.batch_solve(list of numpy proposals) + feasible_results, host wall clock"}
+
+
+def pipeline_e2e(prob, batch: int, reps: int = 3) -> dict:
+    """BASELINE config 2 as stated: CVAE samples -> QP layer -> init-network warm start -> SF -> verdict."""
+    import torch
+
+    from paper_2501_19042_b200 import SafetyFilter, SolverConfig
+    from paper_2501_19042_b200.generative import calibrate_batchnorm, decode_proposals, make_decoder
+    from paper_2501_19042_b200.initnet import InitNet, initial_states
+    torch.manual_seed(0)
+    sf = SafetyFilter(prob, degree=10, config=SolverConfig(max_iters=MAX_ITERS, svars=False))
+    dec = calibrate_batchnorm(sf, make_decoder("cvae", prob.n).cuda()).eval()
+    net = InitNet(prob.n, sf.coeff_dim).cuda().eval()
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    acc = [0.0, 0.0, 0.0]
+    out = None
+    for r in range(reps + 1):
+        with torch.no_grad():
+            ev[0].record()
+            xb = decode_proposals(sf, dec, dec.sample_latent(batch, gen, "cuda"))
+            ev[1].record()
+            xi0, lam0 = initial_states(sf, xb, "initnet", net)
+            ev[2].record()
+            out = sf.solve_batched(xb, xi0=xi0, lam0=lam0)
+            ev[3].record()
+        ev[3].synchronize()
+        if r:
+            for i in range(3):
+                acc[i] += ev[i].elapsed_time(ev[i + 1]) / reps
+    total = sum(acc)
+    feas = int(out.feasible.sum().item())
+    return {"value": feas / (total * 1e-3), "unit": "feasible samples/s", "decode_qp_ms": acc[0],
+            "initnet_ms": acc[1], "sf_verdict_ms": acc[2], "total_ms": total, "feasible": feas,
+            "mean_iterations": float(out.iterations.double().mean()),
+            "note": "random-init CVAE decoder and init network (no trained weights offline), device-timed"}
+
+
 def run_ours(args, rank: int, world: int, local_rank: int) -> None:
-    import numpy as np
     import torch
     import torch.distributed as dist
 
-    from paper_2501_19042_b200 import SafetyFilter, native
+    from paper_2501_19042_b200 import SafetyFilter, SolverConfig, native
+    from paper_2501_19042_b200.distributed import GATHERED_FIELDS, gather_outputs
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    prob, shard, cfg = workload(rank, world, args.batch)
-    if args.precision != "lean":
-        from paper_2501_19042_b200 import SolverConfig
-        cfg = SolverConfig(max_iters=MAX_ITERS, svars=False, precision=args.precision)
+    prob, shard, B = workload(args.config, rank, world, args.batch)
+    cfg = SolverConfig(max_iters=MAX_ITERS, svars=False, precision=args.precision)
     sf = SafetyFilter(prob, degree=10, config=cfg)
     n, S, m1 = prob.n, prob.horizon_samples, 11
     xb_host = torch.from_numpy(shard).pin_memory()
@@ -227,24 +402,17 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # 256 MB > 126 MB L2
     peak_tflops = ctypes_peak(native)
 
-    def gather(out):
-        if world == 1:
-            return
-        for t in (out.coeffs, out.iterations, out.feasible, out.residual_inf):
-            buf = torch.empty((world * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype, device=dev)
-            dist.all_gather_into_tensor(buf, t.contiguous())
-
-    def step(timing=None):
-        out = sf.solve_batched(xb, config=cfg, timing=timing)
-        gather(out)
-        return out
+    def step(x, timing=None):
+        out = sf.solve_batched(x, config=cfg, timing=timing)
+        full = gather_outputs(out, B) if world > 1 else None
+        return out, full
 
     clocks = ClockSampler(ROOT / "gpurun_out" / f"clocks_rank{rank}.csv") if rank == 0 else None
     if clocks:
         (ROOT / "gpurun_out").mkdir(exist_ok=True)
         clocks.__enter__()
     for _ in range(max(3, args.warmup)):
-        step()
+        step(xb)
     torch.cuda.synchronize()
     if clocks:
         clocks.wait_first()
@@ -252,7 +420,6 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     # ---- device-timed region: inputs resident in HBM
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    feas_counts, its_total = [], []
     launches0 = native.launch_count()
     if world > 1:
         dist.barrier()
@@ -263,10 +430,10 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     for k in range(args.steps):
         flush.fill_(float(k))
         ev[k][0].record()
-        out = step(timing=kev[k])
+        out, full = step(xb, timing=kev[k])
         ev[k][1].record()
         outs.append((out.feasible, out.iterations))   # the rest is freed: the next step reuses its blocks
-        del out
+        del out, full
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -277,40 +444,43 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     launches = native.launch_count() - launches0
     step_ms = [a.elapsed_time(b) for a, b in ev]
     kern_ms = [a.elapsed_time(b) for a, b in kev]
-    for feas, its in outs:
-        feas_counts.append(int(feas.sum().item()))
-        its_total.append(int(its.sum().item()))
-    total_ms = sum(step_ms)
-    t = torch.tensor([total_ms, float(sum(feas_counts))], dtype=torch.float64, device=dev)
+    feas_counts = [int(f.sum().item()) for f, _ in outs]
+    its_total = [int(i.sum().item()) for _, i in outs]
+    t = torch.tensor([sum(step_ms), float(sum(feas_counts)), float(sum(its_total))], dtype=torch.float64, device=dev)
     if world > 1:
         tmax = t.clone()
         dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
         dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
-        total_ms_max, feas_all = float(tmax[0]), float(t[1])
+        total_ms_max = float(tmax[0])
     else:
-        total_ms_max, feas_all = total_ms, float(t[1])
+        total_ms_max = float(t[0])
+    feas_all, its_all = float(t[1]), float(t[2])
     value = feas_all / (total_ms_max * 1e-3)
 
-    # ---- end-to-end through the public API: pinned host in, host out
-    h_coeffs = torch.empty((xb.shape[0], dim), dtype=torch.float64).pin_memory()
-    h_its = torch.empty(xb.shape[0], dtype=torch.int32).pin_memory()
-    h_feas = torch.empty(xb.shape[0], dtype=torch.uint8).pin_memory()
+    # ---- end to end through the public API: pinned host proposals in, every per-sample output out
+    host = {}
+    probe, _ = step(xb)
+    for k in GATHERED_FIELDS + ("eq_err",):
+        v = getattr(probe, k, None)
+        if v is not None:
+            host[k] = torch.empty(tuple(v.shape), dtype=v.dtype).pin_memory()
+    del probe
     e2e_ms = []
     for k in range(args.steps + 1):
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         xd = xb_host.to(dev, non_blocking=True)
         out = sf.solve_batched(xd, config=cfg)
-        gather(out)
-        h_coeffs.copy_(out.coeffs, non_blocking=True)
-        h_its.copy_(out.iterations, non_blocking=True)
-        h_feas.copy_(out.feasible, non_blocking=True)
+        for key, h in host.items():
+            h.copy_(getattr(out, key), non_blocking=True)
         b.record()
         b.synchronize()
-        if k:   # first one is a warm-up
+        if k:   # the first one is a warm-up
             e2e_ms.append(a.elapsed_time(b))
-    e2e_feas = int(h_feas.numpy().sum())
+    e2e_feas = int(host["feasible"].numpy().sum())
     te = torch.tensor([sum(e2e_ms), float(e2e_feas * len(e2e_ms))], dtype=torch.float64, device=dev)
     if world > 1:
         temax = te.clone()
@@ -320,11 +490,11 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     else:
         e2e_value = float(te[1]) / (float(te[0]) * 1e-3)
     h2d = xb_host.numel() * 8
-    d2h = h_coeffs.numel() * 8 + h_its.numel() * 4 + h_feas.numel()
+    d2h = sum(h.numel() * h.element_size() for h in host.values())
 
     if rank != 0:
         return
-    # ---- roofline of the dominant kernel (persistent SF kernel)
+    # ---- roofline of the dominant kernel (persistent SF kernel, this rank)
     fps = flop_per_si(n, S, m1)
     flops_per_launch = statistics.mean(its_total) * fps
     kern_avg_ms = statistics.mean(kern_ms)
@@ -333,70 +503,102 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     tfile = ROOT / "profiles" / "ncu_traffic.json"
     if tfile.exists():
         try:
-            traffic = json.loads(tfile.read_text()).get("dram_bytes_per_launch")
-        except (ValueError, OSError):
+            tj = json.loads(tfile.read_text())
+            traffic = tj.get(f"config{args.config}_{args.precision}", {}).get("dram_bytes_per_launch")
+        except (ValueError, OSError, AttributeError):
             traffic = None
+    kname = {16: "sf_persistent_kernel<float,16> (tcgen05 positions)", 32: "sf_persistent_kernel<32, two lanes>",
+             64: "sf_large_kernel<64>"}.get(n, "sf_persistent_kernel")
     line = {
         "metric": METRIC, "value": value, "unit": "feasible samples/s", "n_gpus": world,
         "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": total_ms_max / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": {"lean": "f32 terms + f64 state", "hybrid": "f32 screening + f64 values", "strict": "f64"}[args.precision],
-        "data": "synthetic (seeded 16-robot scenario, reference Gaussian sampler proposals)",
-        "config": {"workload": "BASELINE config 2: 16 drones, H=100, batch 1000 per GPU, SF to 1e-3 "
-                               "(max_iters 500), boundary-projected start",
-                   "n": n, "H": S - 1, "degree": 10, "batch_per_gpu": int(xb.shape[0]), "max_iters": MAX_ITERS,
-                   "rho": 1.0, "precision": args.precision, "l2_flush": "256 MB write between steps",
-                   "parallelism": f"dp{world} (contiguous sample shards, NCCL all_gather of outputs)"},
-        "ms_per_1k_batch": (total_ms_max / args.steps) * 1000.0 / xb.shape[0],
-        "feasible_fraction": feas_all / (args.steps * xb.shape[0] * world),
-        "mean_iterations": statistics.mean(its_total) / xb.shape[0],
+        "higher_is_better": True, "scaling": CONFIGS[args.config][3], "vs_baseline": None,
+        "dtype": {"lean": "f32 terms + f64 state", "hybrid": "f32 screening + f64 values",
+                  "strict": "f64"}[args.precision],
+        "data": "synthetic (seeded scenario, reference Gaussian sampler proposals)",
+        "config": {"workload": config_label(args.config, B, world), "n": n, "H": S - 1, "degree": 10,
+                   "batch": B, "batch_per_gpu": int(xb.shape[0]), "max_iters": MAX_ITERS, "rho": 1.0,
+                   "precision": args.precision, "l2_flush": "256 MB write between steps",
+                   "parallelism": f"dp{world} (contiguous sample shards"
+                                  + (", NCCL all_gather of every per-sample output in the step)" if world > 1 else ")")},
+        "ms_per_1k_batch": (total_ms_max / args.steps) * 1000.0 / B,
+        "feasible_fraction": feas_all / (args.steps * B),
+        "mean_iterations": its_all / (args.steps * B),
         "gpu_launches": int(round(launches / args.steps)),
         "e2e": {"value": e2e_value, "unit": "feasible samples/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h},
+                "d2h_bytes_per_step": d2h, "outputs": sorted(host)},
         "roofline": {"bound": "fp32_cuda_core", "achieved": achieved, "peak": peak_tflops,
                      "unit": "TFLOP/s", "frac": achieved / peak_tflops if peak_tflops else None,
-                     "traffic": traffic, "kernel": "sf_persistent_kernel<float,16>",
-                     "kernel_ms": kern_avg_ms, "flop_per_si": fps,
+                     "traffic": traffic, "kernel": kname, "kernel_ms": kern_avg_ms, "flop_per_si": fps,
                      "peak_source": "FFMA microbenchmark (sgsf_fp32_peak) run live in this process; "
                                     "MEASURED_PEAKS.json has no FP32 figure"},
         "clocks": clocks.summary(local_rank) if clocks else None,
     }
+    if world == 1 and not args.quick:
+        line["precisions"] = side_precisions(sf, xb, cfg, flush)
+        if args.config == 2:
+            line["e2e_dropin"] = dropin_e2e(prob, shard)
+            line["pipeline"] = pipeline_e2e(prob, int(xb.shape[0]))
     if args.cpu_baseline and world == 1:
-        cb = cpu_sample(prob.to_doc(), shard, budget_s=args.ref_budget if args.ref_budget is not None else 12.0)
-        v = cb["feasible"] / cb["wall_s"]
-        line["cpu_baseline"] = {"value": v, "unit": "feasible samples/s", "cores": cb["cores"], "kind": "port",
-                                "sample": f"{cb['samples']} proposals of this batch, all iterations "
-                                          f"({cb['sample_iterations']} sample-iterations) in {cb['wall_s']:.1f} s, "
-                                          f"oracle/sf_oracle.py process pool on {cb['cores']} cores "
-                                          f"({cpu_model()})"}
+        stream = CpuStream(prob.to_doc(), shard)
+        try:
+            stream.take(3.0)   # pool start-up and the first wave
+            r = stream.take(args.ref_budget if args.ref_budget is not None else 12.0)
+        finally:
+            stream.close()
+        line["cpu_baseline"] = {"value": r["feasible"] / r["wall_s"], "unit": "feasible samples/s",
+                                "cores": stream.cores, "kind": stream.kind,
+                                "sample": cpu_desc(stream, r, "one 12 s time slice")}
     print(json.dumps(line), flush=True)
 
 
 def ctypes_peak(native) -> float:
     import ctypes
-    tf, ms = ctypes.c_double(), ctypes.c_double()
+
     import torch
+    tf, ms = ctypes.c_double(), ctypes.c_double()
     native.check(native.load().sgsf_fp32_peak(ctypes.byref(tf), ctypes.byref(ms),
                                               torch.cuda.current_stream().cuda_stream), "sgsf_fp32_peak")
     return float(tf.value)
 
 
-def main():
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def launch_ranks(n: int) -> int:
+    """`--gpus N` outside torchrun: re-run this command as N ranks (one process per GPU, NCCL)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
+def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--batch", type=int, default=BATCH_PER_GPU)
-    ap.add_argument("--precision", default="lean", choices=["lean", "strict", "hybrid"])
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--batch", type=int, default=None, help="batch (per GPU for config 2; global for 3/4)")
+    ap.add_argument("--precision", default="hybrid", choices=["hybrid", "lean", "strict"])
     ap.add_argument("--ref-budget", type=float, default=None,
-                    help="seconds of CPU work per reference step (default: 12 s for the cpu_baseline leg; "
-                         "150 s / steps, within 1.5-12 s, for --impl reference)")
+                    help="seconds of CPU time slice per reference step (default: 12 s for the cpu_baseline leg; "
+                         "150 s / steps, within 2-12 s, for --impl reference)")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
-    args = ap.parse_args()
+    ap.add_argument("--quick", action="store_true", help="skip the side precisions, drop-in and pipeline numbers")
+    return ap.parse_args(argv)
+
+
+def main():
+    args = parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(launch_ranks(args.gpus))
     if args.impl == "reference":
         run_reference(args, rank, world)
         return

@@ -87,6 +87,7 @@ from .unrolled import UnrolledIterates, boundary_projection, fixed_point_loss, u
 from .verdict import (
     ViolationReport,
     check_coefficients,
+    check_original_constraints,
     coeffs_to_trajectory,
     feasible_fraction,
     feasible_results,

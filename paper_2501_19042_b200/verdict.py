@@ -6,9 +6,14 @@ samples/s): converged AND every original constraint within ``tol``
 evaluated in FP64 on the sampled trajectory C W^T by ``sgsf_verdict``; the
 sampled trajectory itself (positions, velocities, accelerations,
 ``basis.py:149-160``) comes from ``sgsf_trajectory``.
+
+``check_original_constraints`` is the reference's full report (``assembly.py:437-487``): counts, worst
+margins and the worst-first violation lists, with the margins of ``problem.py:113-137`` evaluated on the
+device in the reference's operation order (FP64, no contraction) and ordered by a stable device sort.
 """
 from __future__ import annotations
 
+from collections import OrderedDict
 from dataclasses import dataclass
 
 import numpy as np
@@ -23,8 +28,8 @@ from .solver import Operator, _stream, _to_dev
 
 @dataclass(frozen=True)
 class ViolationReport:
-    """Counts and worst margins (the reference also lists the worst violations;
-    those lists are left empty here)."""
+    """Original-constraint check of a trajectory (``assembly.py:410-433``): counts, worst margins and the
+    worst-first lists (i, j, sample, margin) / (robot, sample, margin)."""
 
     ok: bool
     tol: float
@@ -44,18 +49,25 @@ class ViolationReport:
                 "workspace_violations": [list(v) for v in self.workspace_violations]}
 
 
-_OPS: dict = {}
+_CACHE_SIZE = 8   # operators (and their device constants) kept per cache: least recently used evicted
+_OPS: OrderedDict = OrderedDict()
+
+
+def _lru_get(cache: OrderedDict, key, make):
+    hit = cache.get(key)
+    if hit is None:
+        hit = cache[key] = make()
+        while len(cache) > _CACHE_SIZE:
+            cache.popitem(last=False)
+    cache.move_to_end(key)
+    return hit[0]
 
 
 def _operator(problem, degree: int) -> Operator:
-    key = (id(problem), degree)
-    op = _OPS.get(key)
-    if op is None:
+    def make():
         basis = build_basis(problem.duration, degree=degree, samples=problem.horizon_samples)
-        op = Operator(problem, basis, build_equality(problem, basis))
-        _OPS[key] = (op, problem)   # keep the problem alive so id() stays unique
-        return op
-    return op[0]
+        return Operator(problem, basis, build_equality(problem, basis)), problem   # (problem kept: id() unique)
+    return _lru_get(_OPS, (id(problem), degree), make)
 
 
 def verdict_batched(operator: Operator, coeffs: torch.Tensor, converged: torch.Tensor | None = None,
@@ -84,9 +96,71 @@ def check_coefficients(coeffs, problem, degree: int = 10, tol: float = 1e-3) -> 
     c = np.asarray(coeffs, dtype=float).ravel()
     if c.size != op.coeff_dim:
         raise DimensionMismatch(f"coefficient vector has length {c.size}, expected {op.coeff_dim}")
-    v = {k: t.cpu().numpy()[0] for k, t in verdict_batched(op, _to_dev(c.reshape(1, -1)), None, tol).items()}
+    cd = _to_dev(c.reshape(1, -1))
+    v = {k: t.cpu().numpy()[0] for k, t in verdict_batched(op, cd, None, tol).items()}
+    pl, wl = (), ()
+    if not v["ok"]:   # the worst-first lists, from the device trajectory
+        pos, _, _ = _trajectories(op.basis, problem.n, cd, host=False)
+        rep = _check_positions(pos[0], problem, tol, 100)
+        pl, wl = rep.pair_violations, rep.workspace_violations
     return ViolationReport(bool(v["ok"]), tol, float(v["pair_margin_min"]) if problem.n > 1 else np.inf,
-                           float(v["ws_margin_max"]), int(v["pair_viol"]), int(v["ws_viol"]))
+                           float(v["ws_margin_max"]), int(v["pair_viol"]), int(v["ws_viol"]), pl, wl)
+
+
+def _check_positions(pos: torch.Tensor, problem, tol: float, max_listed: int) -> ViolationReport:
+    """check_original_constraints on device positions (n, S, 3) FP64: the margins of problem.py:113-137 as
+    separate IEEE operations in the reference's order, counts, worst margins and worst-first lists."""
+    n = int(pos.shape[0])
+    if n != problem.n:
+        raise DimensionMismatch(f"trajectory has {n} robots, problem expects {problem.n}")
+    ws_ = problem.workspace
+    d = pos - torch.as_tensor(np.asarray(ws_.center, dtype=float), device=pos.device)
+    aw2, bw2 = float(ws_.lateral) ** 2, float(ws_.vertical) ** 2
+    ws_m = ((d[..., 0] * d[..., 0] + d[..., 1] * d[..., 1]) / aw2 + (d[..., 2] * d[..., 2]) / bw2) - 1.0
+    bad = torch.nonzero(ws_m > tol)                                   # row-major, like np.argwhere
+    vals = ws_m[bad[:, 0], bad[:, 1]]
+    order = torch.sort(-vals, stable=True).indices[:max_listed]
+    ws_list = [(int(r), int(t), float(m)) for (r, t), m in zip(bad[order].tolist(), vals[order].tolist())]
+    n_ws = int(bad.shape[0])
+    pair_list, pair_min, n_pair = [], np.inf, 0
+    if n > 1:
+        ii, jj = np.triu_indices(n, k=1)
+        it, jt = (torch.as_tensor(a, device=pos.device) for a in (ii, jj))
+        dl = pos[it] - pos[jt]
+        a2, b2 = float(problem.shape.lateral) ** 2, float(problem.shape.vertical) ** 2
+        pm = ((dl[..., 0] * dl[..., 0] + dl[..., 1] * dl[..., 1]) / a2 + (dl[..., 2] * dl[..., 2]) / b2) - 1.0
+        pair_min = float(pm.min())
+        bad = torch.nonzero(pm < -tol)
+        vals = pm[bad[:, 0], bad[:, 1]]
+        order = torch.sort(vals, stable=True).indices[:max_listed]
+        pair_list = [(int(ii[p]), int(jj[p]), int(t), float(m))
+                     for (p, t), m in zip(bad[order].tolist(), vals[order].tolist())]
+        n_pair = int(bad.shape[0])
+    return ViolationReport(n_pair == 0 and n_ws == 0, tol, pair_min if n > 1 else np.inf, float(ws_m.max()),
+                           n_pair, n_ws, tuple(pair_list), tuple(ws_list))
+
+
+def check_original_constraints(traj: Trajectory, problem, tol: float = 1e-3, max_listed: int = 100) -> ViolationReport:
+    """The reference's original-constraint check of a sampled trajectory (assembly.py:437-487), on the device."""
+    pos = np.asarray(traj.positions, dtype=float)
+    if pos.ndim != 3 or pos.shape[0] != problem.n:
+        raise DimensionMismatch(f"trajectory has {pos.shape[0] if pos.ndim else 0} robots, problem expects {problem.n}")
+    return _check_positions(_to_dev(pos), problem, tol, max_listed)
+
+
+def _trajectories(basis, n, cd: torch.Tensor, host: bool = True):
+    """Sampled positions / velocities / accelerations (B, n, S, 3) of (B, dim) device coefficients: one launch
+    (numpy when `host`, else the device tensors)."""
+    from .solver import _to_host
+    op = _trajectory_operator(basis, n)
+    B, S = int(cd.shape[0]), basis.samples
+    pos, vel, acc = (torch.empty((B, n, S, 3), dtype=torch.float64, device=cd.device) for _ in range(3))
+    native.check(native.load().sgsf_trajectory(op.handle(1.0, cd.device), B, cd.data_ptr(), pos.data_ptr(),
+                                               vel.data_ptr(), acc.data_ptr(), _stream()), "sgsf_trajectory")
+    if not host:
+        return pos, vel, acc
+    h = _to_host({"p": pos, "v": vel, "a": acc})
+    return h["p"], h["v"], h["a"]
 
 
 def coeffs_to_trajectory(coeffs, basis, n) -> Trajectory:
@@ -120,17 +194,14 @@ class _BasisOnlyProblem:
         self.boundary = tuple(RobotBoundary(z, z) for _ in range(n))
 
 
-_TRAJ: dict = {}
+_TRAJ: OrderedDict = OrderedDict()
 
 
 def _trajectory_operator(basis, n) -> Operator:
-    key = (id(basis), n)
-    hit = _TRAJ.get(key)
-    if hit is None:
+    def make():
         prob = _BasisOnlyProblem(n, basis)
-        hit = (Operator(prob, basis, build_equality(prob, basis)), basis)
-        _TRAJ[key] = hit
-    return hit[0]
+        return Operator(prob, basis, build_equality(prob, basis)), basis
+    return _lru_get(_TRAJ, (id(basis), n), make)
 
 
 def feasible_results(results, problem, tol: float = 1e-3) -> list:
@@ -138,11 +209,24 @@ def feasible_results(results, problem, tol: float = 1e-3) -> list:
     keep = [(i, r) for i, r in enumerate(results) if r.converged and r.coeffs is not None]
     if not keep:
         return []
-    degree = keep[0][1].coeffs.size // (3 * problem.n) - 1
-    op = _operator(problem, degree)
-    cd = _to_dev(np.stack([r.coeffs for _, r in keep]))
-    ok = verdict_batched(op, cd, None, tol)["ok"].cpu().numpy()
-    return [(i, coeffs_to_trajectory(r.coeffs, op.basis, problem.n)) for (i, r), good in zip(keep, ok) if good]
+    out = []
+    by_degree: dict = {}   # (the reference takes each result's degree from its own coefficient count)
+    for i, r in keep:
+        by_degree.setdefault(r.coeffs.size // (3 * problem.n) - 1, []).append((i, r))
+    for degree, group in by_degree.items():
+        op = _operator(problem, degree)
+        cd = _to_dev(np.stack([r.coeffs for _, r in group]))
+        ok = verdict_batched(op, cd, None, tol)["ok"].cpu().numpy().astype(bool)
+        if not ok.any():
+            continue
+        good = cd[torch.from_numpy(ok).to(cd.device)].contiguous()
+        pos, vel, acc = _trajectories(op.basis, problem.n, good)
+        k = 0
+        for (i, _), g in zip(group, ok):
+            if g:
+                out.append((i, Trajectory(pos[k], vel[k], acc[k], op.basis.time_grid)))
+                k += 1
+    return sorted(out, key=lambda t: t[0])
 
 
 def feasible_fraction(results, problem, tol: float = 1e-3):

@@ -45,3 +45,39 @@ def test_lean_whole_batch_flip_rate(name):
     assert rep["iter_flip_count"] <= 0.10 * rep["batch"]
     assert abs(rep["feasible_gpu"] - rep["feasible_ref"]) <= 0.05 * rep["batch"]
     assert rep["coeff_rel_err_max"] is None or rep["coeff_rel_err_max"] <= 1e-3
+
+
+def test_worst_first_violation_lists_match_reference():
+    """check_coefficients / check_original_constraints list the violations worst first like the reference
+    (assembly.py:437-487): the frozen first 8 entries of every violating headline sample, and both branches
+    (pairs: batch_cfg2; workspace: batch_ws_tight)."""
+    import numpy as np
+
+    from paper_2501_19042_b200 import check_coefficients, coeffs_to_trajectory, check_original_constraints, load_problem
+    from paper_2501_19042_b200.basis import build_basis
+    for name in ("batch_cfg2", "batch_ws_tight"):
+        g, o = run(name, "strict")
+        prob = load_problem(g["meta"]["problem"])
+        bad = np.nonzero((g["pair_viol"] > 0) | (g["ws_viol"] > 0))[0]
+        assert bad.size > 0
+        for s in bad[:60]:
+            rep = check_coefficients(o["coeffs"][s], prob, degree=g["meta"]["degree"])
+            assert rep.pair_violation_count == g["pair_viol"][s] and rep.workspace_violation_count == g["ws_viol"][s]
+            for got, ref, width in ((rep.pair_violations, g["pair_list"][s], 3), (rep.workspace_violations, g["ws_list"][s], 2)):
+                ref = [r for r in ref if np.isfinite(r).all()]
+                assert len(got) >= len(ref)
+                for k, r in enumerate(ref):
+                    gk = got[k]
+                    assert abs(gk[width] - r[width]) <= 1e-9, (name, s, k, gk, r)
+                    # identical entry, or a swap of two margins equal to within 1e-9
+                    assert tuple(gk[:width]) == tuple(int(v) for v in r[:width]) or \
+                        any(abs(gk[width] - rr[width]) <= 1e-9 and tuple(gk[:width]) == tuple(int(v) for v in rr[:width])
+                            for rr in ref), (name, s, k, gk, r)
+        # the trajectory-level entry point gives the same report
+        s = bad[0]
+        basis = build_basis(prob.duration, degree=g["meta"]["degree"], samples=prob.horizon_samples)
+        rep2 = check_original_constraints(coeffs_to_trajectory(o["coeffs"][s], basis, prob.n), prob)
+        rep1 = check_coefficients(o["coeffs"][s], prob, degree=g["meta"]["degree"])
+        assert rep2.pair_violation_count == rep1.pair_violation_count
+        assert rep2.workspace_violation_count == rep1.workspace_violation_count
+        assert [v[:-1] for v in rep2.pair_violations] == [v[:-1] for v in rep1.pair_violations]

@@ -121,7 +121,7 @@ def test_tensor_core_and_ffma_positions_agree():
         "sys.path.insert(0, '.')\n"
         "import bench\n"
         "from paper_2501_19042_b200 import SafetyFilter\n"
-        "prob, shard, cfg = bench.workload(0, 1, 300)\n"
+        "prob, shard, cfg = bench.config2_case(300)\n"
         "sf = SafetyFilter(prob, degree=10, config=cfg)\n"
         "out = sf.solve_batched(torch.from_numpy(shard).cuda(), config=cfg)\n"
         "np.savez(sys.argv[1], c=out.coeffs.cpu().numpy(), it=out.iterations.cpu().numpy(), "

@@ -9,7 +9,7 @@ import torch
 import bench
 from paper_2501_19042_b200 import SafetyFilter
 
-prob, shard, cfg = bench.workload(0, 1, bench.BATCH_PER_GPU)
+prob, shard, cfg = bench.config2_case()
 sf = SafetyFilter(prob, degree=10, config=cfg)
 out = sf.solve_batched(torch.from_numpy(shard).cuda(), config=cfg)
 torch.cuda.synchronize()

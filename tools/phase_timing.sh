@@ -26,7 +26,7 @@ if os.environ.get("PT_CONFIG", "2") != "2":
     xb = torch.from_numpy(sample_proposals(prob, sf.basis, {1: 8, 3: 4096, 4: 8192}[c], seed=0).proposals).cuda()
     run("full", xb, cfg)
     raise SystemExit
-prob, shard, cfg = bench.workload(0, 1, bench.BATCH_PER_GPU)
+prob, shard, cfg = bench.config2_case()
 cfg = replace(cfg, precision=os.environ.get("PT_PRECISION", cfg.precision))
 sf = SafetyFilter(prob, degree=10, config=cfg)
 xb = torch.from_numpy(shard).cuda()
