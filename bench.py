@@ -329,13 +329,13 @@ def side_precisions(sf, xb, cfg, flush, steps: int = 3) -> dict:
     return out
 
 
-def dropin_e2e(prob, shard, reps: int = 2) -> dict:
+def dropin_e2e(prob, shard, reps: int = 3) -> dict:
     """The reference-compatible call: SafetyFilter.batch_solve(list of numpy proposals) at its defaults
     (svars on) + metrics.feasible_results -- numpy in, SolveResults out (solver.py:368-407, metrics.py:57-69)."""
     from paper_2501_19042_b200 import SafetyFilter, SolverConfig, feasible_results
     sf = SafetyFilter(prob, degree=10, config=SolverConfig(max_iters=MAX_ITERS))
     props = [x.copy() for x in shard]
-    sf.batch_solve(props[:8])
+    feasible_results(sf.batch_solve(props).results, prob)   # warm-up: handles, pinned staging buffers
     times, feas = [], 0
     for _ in range(reps):
         t0 = time.perf_counter()

@@ -239,7 +239,7 @@ def _to_dev(a: np.ndarray) -> torch.Tensor:
 
 def _to_host(tensors: dict) -> dict:
     """Device tensors -> numpy through pinned staging buffers (one synchronisation for all of them)."""
-    pinned = {k: torch.empty(tuple(t.shape), dtype=t.dtype).pin_memory() for k, t in tensors.items()}
+    pinned = {k: torch.empty(tuple(t.shape), dtype=t.dtype, pin_memory=True) for k, t in tensors.items()}   # (cached)
     for k, t in tensors.items():
         pinned[k].copy_(t, non_blocking=True)
     torch.cuda.current_stream().synchronize()
