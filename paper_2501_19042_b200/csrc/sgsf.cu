@@ -396,35 +396,40 @@ int sgsf_solve_host(sgsf_handle_t* h, int batch, const double* xi_bar, const dou
     o.eq_err = (double*)take(sizes[12]);
     uint8_t* d_feas = (uint8_t*)take(sizes[13]);
     void* ws = take(sizes[14]);
-    CUDA_TRY(cudaMemcpyAsync(d_xb, xi_bar, B * dim * 8, cudaMemcpyHostToDevice, stream));
+    // every step after the arena allocation goes through one cleanup path: the arena is freed and the stream
+    // synchronised whatever fails, and the first error is the one reported
+    int rc = SGSF_OK;
+    auto step = [&](cudaError_t e, const char* what) {
+        if (rc == SGSF_OK && e != cudaSuccess) rc = fail(SGSF_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    };
+    step(cudaMemcpyAsync(d_xb, xi_bar, B * dim * 8, cudaMemcpyHostToDevice, stream), "H2D xi_bar");
     if (init_mode) {
-        CUDA_TRY(cudaMemcpyAsync(d_x0, xi0, B * dim * 8, cudaMemcpyHostToDevice, stream));
-        CUDA_TRY(cudaMemcpyAsync(d_l0, lam0, B * dim * 8, cudaMemcpyHostToDevice, stream));
-        CUDA_TRY(cudaMemcpyAsync(d_mode, init_mode, B, cudaMemcpyHostToDevice, stream));
+        step(cudaMemcpyAsync(d_x0, xi0, B * dim * 8, cudaMemcpyHostToDevice, stream), "H2D xi0");
+        step(cudaMemcpyAsync(d_l0, lam0, B * dim * 8, cudaMemcpyHostToDevice, stream), "H2D lam0");
+        step(cudaMemcpyAsync(d_mode, init_mode, B, cudaMemcpyHostToDevice, stream), "H2D init_mode");
     }
     sgsf_config_t c = *cfg;
     c.want_prev = 0;
-    c.verdict_tol = 1e-3;   // feasible = converged and the original constraints at 1e-3 (metrics.py:57-69)
+    if (!(c.verdict_tol > 0)) c.verdict_tol = 1e-3;   // feasible = converged and the constraints at 1e-3 (metrics.py:57-69)
     sgsf_verdict_t v;
     std::memset(&v, 0, sizeof(v));
     v.feasible = d_feas;
     o.verdict = &v;
-    int rc = sgsf_solve(h, batch, d_xb, d_x0, d_l0, d_mode, &c, &o, ws, nullptr, stream);
+    if (rc == SGSF_OK) rc = sgsf_solve(h, batch, d_xb, d_x0, d_l0, d_mode, &c, &o, ws, nullptr, stream);
     if (rc == SGSF_OK) {
-        if (coeffs) CUDA_TRY(cudaMemcpyAsync(coeffs, o.coeffs, B * dim * 8, cudaMemcpyDeviceToHost, stream));
-        if (multipliers)
-            CUDA_TRY(cudaMemcpyAsync(multipliers, o.multipliers, B * dim * 8, cudaMemcpyDeviceToHost, stream));
-        if (res_inf) CUDA_TRY(cudaMemcpyAsync(res_inf, o.res_inf, B * MI * 8, cudaMemcpyDeviceToHost, stream));
-        if (res_l2) CUDA_TRY(cudaMemcpyAsync(res_l2, o.res_l2, B * MI * 8, cudaMemcpyDeviceToHost, stream));
-        if (iterations) CUDA_TRY(cudaMemcpyAsync(iterations, o.iterations, B * 4, cudaMemcpyDeviceToHost, stream));
-        if (converged) CUDA_TRY(cudaMemcpyAsync(converged, o.converged, B, cudaMemcpyDeviceToHost, stream));
-        if (feasible) CUDA_TRY(cudaMemcpyAsync(feasible, d_feas, B, cudaMemcpyDeviceToHost, stream));
-        if (displacement)
-            CUDA_TRY(cudaMemcpyAsync(displacement, o.displacement, B * 8, cudaMemcpyDeviceToHost, stream));
-        if (status) CUDA_TRY(cudaMemcpyAsync(status, o.status, B * 4, cudaMemcpyDeviceToHost, stream));
+        struct {
+            void* dst;
+            const void* src;
+            size_t n;
+        } outs[] = {{coeffs, o.coeffs, B * dim * 8}, {multipliers, o.multipliers, B * dim * 8},
+                    {res_inf, o.res_inf, B * MI * 8}, {res_l2, o.res_l2, B * MI * 8},
+                    {iterations, o.iterations, B * 4}, {converged, o.converged, B}, {feasible, d_feas, B},
+                    {displacement, o.displacement, B * 8}, {status, o.status, B * 4}};
+        for (auto& c2 : outs)
+            if (c2.dst) step(cudaMemcpyAsync(c2.dst, c2.src, c2.n, cudaMemcpyDeviceToHost, stream), "D2H output");
     }
-    cudaFreeAsync(arena, stream);
-    CUDA_TRY(cudaStreamSynchronize(stream));
+    step(cudaFreeAsync(arena, stream), "free arena");
+    step(cudaStreamSynchronize(stream), "synchronize");
     return rc;
 }
 

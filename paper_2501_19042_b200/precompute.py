@@ -132,7 +132,19 @@ class DeviceConstants:
     cconst: np.ndarray        # (3, n, m1)
 
 
+def _projector(equality, B: np.ndarray) -> np.ndarray:
+    """B^T (B B^T)^-1 (m1 x 6).  This package's EqualitySystem carries it; the reference's
+    (``assembly.py:56-70``: block, rhs_axes and a Cholesky factor of B B^T) does not, so derive it."""
+    proj = getattr(equality, "projector", None)
+    if proj is not None:
+        return proj
+    return B.T @ np.linalg.inv(B @ B.T)
+
+
 def device_constants(problem, basis: BasisMatrices, equality: EqualitySystem, rho: float) -> DeviceConstants:
+    """FP64 constants of one (problem, degree, rho).  ``problem``, ``basis`` and ``equality`` may be this
+    package's objects or the reference's (``swarmfilter.SafetyFilter``'s problem / basis / equality: same
+    attribute names, ``problem.py:28-104``, ``basis.py:73-88``, ``assembly.py:56-70``)."""
     if not rho >= 0:
         raise ValueError(f"penalty weight must be nonnegative, got {rho}")
     n, m1 = problem.n, basis.degree + 1
@@ -156,7 +168,7 @@ def device_constants(problem, basis: BasisMatrices, equality: EqualitySystem, rh
         W=np.ascontiguousarray(W), Wd=np.ascontiguousarray(basis.velocity),
         Wdd=np.ascontiguousarray(basis.acceleration),
         B=np.ascontiguousarray(B), rhs=np.ascontiguousarray(rhs),
-        PBt=np.ascontiguousarray(equality.projector),
+        PBt=np.ascontiguousarray(_projector(equality, B)),
         Km11=np.ascontiguousarray(Km11), Kd11=np.ascontiguousarray(Kd11),
         Mm=np.ascontiguousarray(rho * Km11 @ G), Md=np.ascontiguousarray(rho * (n + 1) * Kd11 @ G),
         cconst=np.ascontiguousarray(cconst),
