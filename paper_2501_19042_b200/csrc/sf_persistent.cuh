@@ -1749,6 +1749,21 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                 }
             }
 
+#ifdef SGSF_SYNC_CHECK
+            {   // debug build: every warp of the slot must take the same decision (the slot's barriers depend on it)
+                __shared__ int sc_dec[16][MAX_SLOT_WORDS];
+                if (lane == 0) sc_dec[slot][lwarp] = (int)done | ((int)failed << 1) | ((k & 0xffff) << 2);
+                slot_barrier(bar_id, gsize);
+                if (lt == 0)
+                    for (int w = 1; w < p.wps; ++w)
+                        if (sc_dec[slot][w] != sc_dec[slot][0]) {
+                            printf("SGSF_SYNC_CHECK: slot %d warp %d decision %x != warp 0 %x (sample %d, k %d)\n", slot,
+                                   w, sc_dec[slot][w], sc_dec[slot][0], sample, k);
+                            __trap();
+                        }
+                slot_barrier(bar_id, gsize);
+            }
+#endif
             if (done) {
                 // ---------------- finalize: outputs of the returned iterate, claim the next sample
                 if (!failed) {
