@@ -56,7 +56,7 @@ enum { SAMPLE_OK = 0, SAMPLE_SINGULAR_KKT = 1 };
 struct SmemLayout {
     size_t W, KMm, KMd, cconst, B6, rhs, ptab, tmem;
     size_t slot0, slot_stride;
-    size_t C, Cp, lam, U, xb, eqerr, psq, pex, P0, P1, Cf, pinf, sh;
+    size_t C, Cp, lam, U, xb, eqerr, psq, pex, P0, P1, Cf, pinf, sh, sc;
     size_t total;
 };
 
@@ -206,6 +206,11 @@ __host__ __device__ inline SmemLayout make_layout(int n, int S, int MP, int spb,
     L.Cf = q;     q = align16(q + (tc ? (size_t)kTcBopBytes : (size_t)3 * MP * NB * ts));
     L.pinf = q;   q = align16(q + pw * ts);                            // per warp max of the inf partials
     L.sh = q;     q = align16(q + sizeof(SlotShared));
+#ifdef SGSF_SYNC_CHECK
+    L.sc = q;     q = align16(q + pw * sizeof(int));                   // debug: per-warp decisions
+#else
+    L.sc = q;
+#endif
     L.slot_stride = q;
     L.total = o + (size_t)spb * q;
     return L;
@@ -1751,14 +1756,14 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
 
 #ifdef SGSF_SYNC_CHECK
             {   // debug build: every warp of the slot must take the same decision (the slot's barriers depend on it)
-                __shared__ int sc_dec[16][MAX_SLOT_WORDS];
-                if (lane == 0) sc_dec[slot][lwarp] = (int)done | ((int)failed << 1) | ((k & 0xffff) << 2);
+                int* sc_dec = (int*)(smem + L.slot0 + (size_t)slot * L.slot_stride + L.sc);
+                if (lane == 0) sc_dec[lwarp] = (int)done | ((int)failed << 1) | ((k & 0xffff) << 2);
                 slot_barrier(bar_id, gsize);
                 if (lt == 0)
                     for (int w = 1; w < p.wps; ++w)
-                        if (sc_dec[slot][w] != sc_dec[slot][0]) {
+                        if (sc_dec[w] != sc_dec[0]) {
                             printf("SGSF_SYNC_CHECK: slot %d warp %d decision %x != warp 0 %x (sample %d, k %d)\n", slot,
-                                   w, sc_dec[slot][w], sc_dec[slot][0], sample, k);
+                                   w, sc_dec[w], sc_dec[0], sample, k);
                             __trap();
                         }
                 slot_barrier(bar_id, gsize);
