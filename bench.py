@@ -46,8 +46,9 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "SF-projected feasible swarm samples/sec (16 drones, H=100); ms per 1k batch"
 MAX_ITERS = 500
-# per BASELINE config: (robots, horizon, batch, scaling); config 2's batch is per GPU (weak scaling)
-CONFIGS = {2: (16, 100, 1000, "weak"), 3: (32, 100, 4096, "strong"), 4: (64, 150, 8192, "strong")}
+# per BASELINE config: (robots, horizon, batch, scaling, max_iters); config 2's batch is per GPU (weak scaling).
+# Config 4 states "SF to 1e-3 residual" with no cap; its 64-robot swarm needs ~1000 iterations
+CONFIGS = {2: (16, 100, 1000, "weak", 500), 3: (32, 100, 4096, "strong", 500), 4: (64, 150, 8192, "strong", 1000)}
 REF_DIR = ROOT / "oracle" / "_ref"
 
 
@@ -57,8 +58,12 @@ def flop_per_si(n: int, S: int, m1: int) -> int:
     return 33 * P * S + 30 * n * S + 12 * n * S * m1 + 12 * n * m1 * m1 + 42 * n * m1
 
 
+def max_iters_of(config: int) -> int:
+    return CONFIGS[config][4]
+
+
 def global_batch(config: int, world: int, batch: int | None) -> int:
-    n, H, b, scaling = CONFIGS[config]
+    n, H, b, scaling, _ = CONFIGS[config]
     b = batch or b
     return b * world if scaling == "weak" else b
 
@@ -85,10 +90,10 @@ def config2_case(batch: int = 1000, precision: str = "lean"):
 
 
 def config_label(config: int, B: int, world: int) -> str:
-    n, H, _, scaling = CONFIGS[config]
+    n, H, _, scaling, mi = CONFIGS[config]
     what = {2: "CVAE-shaped Gaussian proposals", 3: "VQ-VAE-shaped Gaussian proposals", 4: "Gaussian proposals"}
     per = f"{B // world} per GPU" if scaling == "weak" else f"{B} strong-scaled over {world} GPU(s)"
-    return (f"BASELINE config {config}: {n} drones, H={H}, batch {per}, SF to 1e-3 (max_iters {MAX_ITERS}), "
+    return (f"BASELINE config {config}: {n} drones, H={H}, batch {per}, SF to 1e-3 (max_iters {mi}), "
             f"boundary-projected start; {what[config]}")
 
 
@@ -96,17 +101,17 @@ def config_label(config: int, B: int, world: int) -> str:
 _W = {}
 
 
-def _pool_init(doc, use_ref):
+def _pool_init(doc, use_ref, max_iters):
     os.environ["OPENBLAS_NUM_THREADS"] = os.environ["OMP_NUM_THREADS"] = os.environ["MKL_NUM_THREADS"] = "1"
     if use_ref:
         sys.path.insert(0, str(REF_DIR))
         import swarmfilter as sfm
         prob = sfm.load_problem(doc)
         _W.update(kind="reference", sfm=sfm, prob=prob,
-                  filt=sfm.SafetyFilter(prob, degree=10, config=sfm.SolverConfig(max_iters=MAX_ITERS)))
+                  filt=sfm.SafetyFilter(prob, degree=10, config=sfm.SolverConfig(max_iters=max_iters)))
     else:
         from oracle import sf_oracle
-        _W.update(kind="port", mod=sf_oracle, prob=sf_oracle.make_problem(doc, degree=10))
+        _W.update(kind="port", mod=sf_oracle, prob=sf_oracle.make_problem(doc, degree=10), max_iters=max_iters)
 
 
 def _pool_solve(x):
@@ -119,7 +124,7 @@ def _pool_solve(x):
             feas = len(sfm.metrics.feasible_results([r], _W["prob"])) == 1   # the headline's own numerator
             its = r.iterations
         else:
-            r = _W["mod"].solve(_W["prob"], x, max_iters=MAX_ITERS)
+            r = _W["mod"].solve(_W["prob"], x, max_iters=_W["max_iters"])
             feas, its = _W["mod"].feasible(_W["prob"], r), r.iterations
         return its, bool(feas), time.perf_counter() - t0
 
@@ -137,14 +142,15 @@ class CpuStream:
     core in flight; `take(s)` counts what completes in the next s seconds: the pool's steady-state throughput,
     with no per-step pool start-up and no straggler wave at the end of a step."""
 
-    def __init__(self, doc, props, cores=None):
+    def __init__(self, doc, props, max_iters=MAX_ITERS, cores=None):
         import itertools
         import multiprocessing as mp
         import queue
         self.use_ref = reference_available()
         self.kind = "reference" if self.use_ref else "port"
         self.cores = cores or os.cpu_count() or 1
-        self.pool = mp.get_context("fork").Pool(self.cores, initializer=_pool_init, initargs=(doc, self.use_ref))
+        self.pool = mp.get_context("fork").Pool(self.cores, initializer=_pool_init,
+                                                  initargs=(doc, self.use_ref, max_iters))
         self.cyc = itertools.cycle(list(props))
         self.done = queue.Queue()
         for _ in range(2 * self.cores):
@@ -258,7 +264,7 @@ def run_reference(args, rank: int, world: int) -> None:
     if rank != 0:
         return
     prob, shard, B = workload(args.config, 0, 1, args.batch)
-    stream = CpuStream(prob.to_doc(), shard)
+    stream = CpuStream(prob.to_doc(), shard, max_iters_of(args.config))
     # per-step CPU time slice: --ref-budget, or ~150 s over the timed steps (2-12 s each), so the whole
     # --steps K --warmup W run stays within a few minutes
     budget = args.ref_budget if args.ref_budget is not None else min(12.0, max(2.0, 150.0 / max(1, args.steps)))
@@ -281,7 +287,7 @@ def run_reference(args, rank: int, world: int) -> None:
         "scaling": CONFIGS[args.config][3], "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded scenario + reference Gaussian sampler)",
         "config": {"workload": config_label(args.config, B, 1) + "; each step a time slice of the batch",
-                   "n": prob.n, "H": prob.horizon_samples - 1, "batch": B, "max_iters": MAX_ITERS},
+                   "n": prob.n, "H": prob.horizon_samples - 1, "batch": B, "max_iters": max_iters_of(args.config)},
         "ms_per_1k_batch": 1e3 * 1000 / value if value > 0 else None,
         "feasible_fraction": feas / done if done else None,
         "cpu_baseline": {"value": value, "unit": "feasible samples/s", "cores": stream.cores, "kind": stream.kind,
@@ -393,7 +399,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     prob, shard, B = workload(args.config, rank, world, args.batch)
-    cfg = SolverConfig(max_iters=MAX_ITERS, svars=False, precision=args.precision)
+    cfg = SolverConfig(max_iters=max_iters_of(args.config), svars=False, precision=args.precision)
     sf = SafetyFilter(prob, degree=10, config=cfg)
     n, S, m1 = prob.n, prob.horizon_samples, 11
     xb_host = torch.from_numpy(shard).pin_memory()
@@ -517,7 +523,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
                   "strict": "f64"}[args.precision],
         "data": "synthetic (seeded scenario, reference Gaussian sampler proposals)",
         "config": {"workload": config_label(args.config, B, world), "n": n, "H": S - 1, "degree": 10,
-                   "batch": B, "batch_per_gpu": int(xb.shape[0]), "max_iters": MAX_ITERS, "rho": 1.0,
+                   "batch": B, "batch_per_gpu": int(xb.shape[0]), "max_iters": cfg.max_iters, "rho": 1.0,
                    "precision": args.precision, "l2_flush": "256 MB write between steps",
                    "parallelism": f"dp{world} (contiguous sample shards"
                                   + (", NCCL all_gather of every per-sample output in the step)" if world > 1 else ")")},
@@ -540,7 +546,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
             line["e2e_dropin"] = dropin_e2e(prob, shard)
             line["pipeline"] = pipeline_e2e(prob, int(xb.shape[0]))
     if args.cpu_baseline and world == 1:
-        stream = CpuStream(prob.to_doc(), shard)
+        stream = CpuStream(prob.to_doc(), shard, cfg.max_iters)
         try:
             stream.take(3.0)   # pool start-up and the first wave
             r = stream.take(args.ref_budget if args.ref_budget is not None else 12.0)

@@ -25,7 +25,8 @@ import numpy as np
 from .conftest import load_golden
 
 # how each fixture's proposals were drawn (make_golden_batch.py): batch, seed, spread
-BATCHES = {"batch_cfg2": (1000, 0, 0.25), "batch_ws_tight": (48, 3, 3.0)}
+BATCHES = {"batch_cfg2": (1000, 0, 0.25), "batch_ws_tight": (48, 3, 3.0), "batch_cfg3": (16, 0, 0.25),
+           "batch_cfg4": (8, 0, 0.25), "batch_cfg4e": (1024, 0, 0.25)}
 
 
 def proposals(name: str, meta: dict) -> np.ndarray:
@@ -35,6 +36,8 @@ def proposals(name: str, meta: dict) -> np.ndarray:
     prob = load_problem(meta["problem"])
     basis = build_basis(prob.duration, degree=meta["degree"], samples=prob.horizon_samples)
     x = sample_proposals(prob, basis, B, seed=seed, spread=spread).proposals
+    if "select" in meta:   # rows of a larger draw
+        x = np.ascontiguousarray(x[meta["select"]["indices"]])
     sha = hashlib.sha256(np.ascontiguousarray(x, dtype=np.float64).tobytes()).hexdigest()
     assert sha == meta["proposals_sha256"], f"{name}: regenerated proposals differ from the fixture's"
     return x

@@ -73,7 +73,7 @@ def _solve_one(args):
             np.asarray(r.coeffs), np.asarray(r.multipliers), dt)
 
 
-def run_batch(name, doc, proposals, degree=10, keep_coeffs=64, procs=None, **cfg):
+def run_batch(name, doc, proposals, degree=10, keep_coeffs=64, procs=None, select=None, **cfg):
     import multiprocessing as mp
     B = len(proposals)
     maxit = cfg.get("max_iters", 200)
@@ -118,6 +118,8 @@ def run_batch(name, doc, proposals, degree=10, keep_coeffs=64, procs=None, **cfg
     meta = {"name": name, "problem": doc, "degree": degree, "config": cfg, "batch": B,
             "proposals_sha256": sha, "reference_backend": "compiled", "wall_s": wall, "cpu_s": cpu,
             "procs": procs, "sample_iterations": int(out["iterations"].sum())}
+    if select is not None:   # rows `indices` of a `batch`-sample draw (seed 0) of bench.py's batch
+        meta["select"] = select
     np.savez_compressed(HERE / f"{name}.npz", meta=np.array(json.dumps(meta)), **out)
     print(f"{name}: B={B} iterations {out['iterations'].min()}..{out['iterations'].max()} "
           f"(mean {out['iterations'].mean():.1f}) converged {out['converged'].sum()} "
@@ -161,12 +163,17 @@ def main(argv):
             doc = ws_tight_doc()
             props = proposals_for(doc, 48, seed=3, spread=3.0)
             run_batch("batch_ws_tight", doc, props, keep_coeffs=48, max_iters=300, tol_residual=0.05)
-        elif which == "cfg3":
+        elif which == "cfg3":   # the first 16 proposals of bench.py --config 3's batch
             doc = config_doc(3)
-            run_batch("batch_cfg3", doc, proposals_for(doc, 8), keep_coeffs=8, max_iters=500)
-        elif which == "cfg4":
+            run_batch("batch_cfg3", doc, proposals_for(doc, 16), keep_coeffs=16, max_iters=500)
+        elif which == "cfg4":   # the first 8 proposals of bench.py --config 4's batch (all reach the cap)
             doc = config_doc(4)
-            run_batch("batch_cfg4", doc, proposals_for(doc, 4), keep_coeffs=4, max_iters=500)
+            run_batch("batch_cfg4", doc, proposals_for(doc, 8), keep_coeffs=8, max_iters=1000)
+        elif which == "cfg4e":  # 8 proposals of the config-4 batch that stop early (chosen from a GPU run of
+            doc = config_doc(4)  # the first 1024: 1 to 671 iterations, one converged-but-infeasible)
+            idx = [789, 315, 566, 526, 448, 513, 938, 681]
+            run_batch("batch_cfg4e", doc, proposals_for(doc, 1024)[idx], keep_coeffs=8, max_iters=1000,
+                      select={"batch": 1024, "indices": idx})
         else:
             raise SystemExit(f"unknown batch {which}")
 

@@ -1,5 +1,9 @@
 """GPU parity on WHOLE batches against the real reference (tests/golden/batch_*.npz).
 
+``batch_cfg3`` / ``batch_cfg4`` are the first 16 / 8 proposals of bench.py's config-3 / config-4 batches
+(32 robots H = 100 / 64 robots H = 150), solved by the reference with early stop: converging and
+capped samples, pair- and workspace-violating verdicts.
+
 ``batch_cfg2`` is the headline workload itself: all 1000 config-2 bench proposals (16 drones,
 H = 100, max_iters 500) as the compiled reference solved them -- 998 converged, 765 feasible,
 235 converged-but-violating (the pair branch of ``assembly.py:437-487``).  ``batch_ws_tight``
@@ -21,8 +25,11 @@ from .batch_parity import compare, run
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("precision", ["strict", "hybrid"])
-@pytest.mark.parametrize("name", ["batch_cfg2", "batch_ws_tight"])
+@pytest.mark.parametrize("name,precision", [
+    ("batch_cfg2", "strict"), ("batch_cfg2", "hybrid"), ("batch_ws_tight", "strict"), ("batch_ws_tight", "hybrid"),
+    # BASELINE configs 3 / 4 with early stop: 32 robots (K1, two lanes per step; strict does not fit one CTA at
+    # H = 100) and 64 robots, H = 150, max_iters 1000 (K1L, FP64)
+    ("batch_cfg3", "hybrid"), ("batch_cfg4", "strict"), ("batch_cfg4e", "strict")])
 def test_whole_batch_matches_reference(name, precision):
     g, o = run(name, precision)
     rep = compare(g, o, band=1e-6)
