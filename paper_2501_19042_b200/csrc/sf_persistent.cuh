@@ -975,7 +975,11 @@ __device__ __forceinline__ StepOut<T> flagged_path(const T* __restrict__ Pnew, T
         for (int u = 0; u < L; ++u) reinterpret_cast<T*>(&z)[u] = T(0);
 #pragma unroll
         for (int c = 0; c < 3 * NB / L; ++c) reinterpret_cast<V*>(Pold)[c] = z;
+#ifndef SGSF_HY_NO_SCATTER   // (attribution experiments only: FP32 scattered residuals)
         if constexpr (HY) {   // FP64 scattered residuals (0 for terms interior in FP64), rounded once
+#else
+        if constexpr (false) {
+#endif
             act64 = hy_scatter_step<T, NB, MP>(p, Cn, t, nm, ptab, Pold);
         } else {
 #pragma unroll 1
@@ -1008,7 +1012,11 @@ __device__ __forceinline__ StepOut<T> flagged_path(const T* __restrict__ Pnew, T
     StepOut<T> r;
     r.inf = fmax(base, flmax);
     r.sq = fmax(qsq + dsq, T(0));
+#ifndef SGSF_HY_NO_SCATTER
     r.active = HY ? act64 : act_new;   // HY: a step whose flagged terms are all interior in FP64 has R = 0
+#else
+    r.active = act_new;
+#endif
     return r;
 }
 
@@ -1706,7 +1714,11 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                 }
             }
             double infd = (double)inf;
+#ifndef SGSF_HY_NO_RECOMPUTE   // (attribution experiments only: drops the FP64 stop re-evaluation)
             if constexpr (HY) {
+#else
+            if constexpr (false) {
+#endif
                 // the FP32-measured exit residual sits within hy_delta of tol_res (slot-uniform: every warp
                 // read the same partials): re-evaluate it in FP64 over every time step, so the stop decision
                 // is the one the FP64 iterates give
