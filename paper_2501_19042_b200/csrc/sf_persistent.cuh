@@ -668,11 +668,41 @@ __device__ __forceinline__ D3 resid64(bool pair, const D3& d, const D3& b, const
     return r;
 }
 
+// streamed variants (the W row through the read-only cache; pos64's order of operations)
+template <int MP>
+__device__ __forceinline__ double pos64s(const double* __restrict__ C, const double* __restrict__ Wrow, int m1,
+                                         int row) {
+    const double* c = C + row * MP;
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < MP; ++q) s = fma(c[q], q < m1 ? __ldg(Wrow + q) : 0.0, s);
+    return s;
+}
+template <int MP>
+__device__ __forceinline__ D3 term_diff64s(const SolveParams& p, const double* __restrict__ C,
+                                           const double* __restrict__ Wrow, int i, int j) {
+    const int n = p.n, m1 = p.m1;
+    D3 d;
+    if (j >= 0) {
+        d.x = pos64s<MP>(C, Wrow, m1, i) - pos64s<MP>(C, Wrow, m1, j);
+        d.y = pos64s<MP>(C, Wrow, m1, n + i) - pos64s<MP>(C, Wrow, m1, n + j);
+        d.z = pos64s<MP>(C, Wrow, m1, 2 * n + i) - pos64s<MP>(C, Wrow, m1, 2 * n + j);
+    } else {
+        d.x = pos64s<MP>(C, Wrow, m1, i) - p.cx;
+        d.y = pos64s<MP>(C, Wrow, m1, n + i) - p.cy;
+        d.z = pos64s<MP>(C, Wrow, m1, 2 * n + i) - p.cz;
+    }
+    return d;
+}
+
 // Scattered residual R of every term non-interior (guarded FP32 test) in the new iterate at step t, in
 // FP64 from C_k: W row loaded once, R accumulated into the thread's (dead) old row.  Returns whether some term
 // has a non-zero residual (is active in FP64).
+// (every HY helper that takes the kernel's SolveParams by reference must be inlined: a reference to a kernel
+// parameter passed to a real call makes the compiler copy the parameter block to local memory and read every
+// p.* field from there, on every iteration -- that cost hybrid ~15% of its samples until round 2 found it)
 template <typename T, int NB, int MP>
-__device__ __noinline__ bool hy_scatter_step(const SolveParams& p, const double* Cn, int t, const MaskPack<NB> nm,
+__device__ __forceinline__ bool hy_scatter_step(const SolveParams& p, const double* Cn, int t, const MaskPack<NB> nm,
                                              const int* __restrict__ ptab, T* Pold) {
     double w[MP];
     w64_row<MP>(p.W, t, p.m1, w);
@@ -709,7 +739,7 @@ template <typename T, int NB, int MP> struct HyStepOut {
     bool zero, active;
 };
 template <typename T, int NB, int MP>
-__device__ __noinline__ HyStepOut<T, NB, MP> hy_step_full(const SolveParams& p, const double* Cn, const double* Co,
+__device__ __forceinline__ HyStepOut<T, NB, MP> hy_step_full(const SolveParams& p, const double* Cn, const double* Co,
                                                          int t, T* Rrow, MaskPack<NB>* nmo) {
     const int n = p.n;
     double w[MP];
@@ -1110,67 +1140,127 @@ __device__ __noinline__ CarefulOut<T> careful_pass(const PosPack<T, NB> pk, T* _
 // FP64 exit residual (max |x|, sum x^2) of time step t for the stop decision near tol_res.  A term interior
 // at the old iterate (bit set in om -- the guarded FP32 test, so interior in FP64 too) has exit residual
 // Dd = D(p_i) - D(p_j) (workspace: D(p_i)), with D p = (C_k - C_{k-1}) W[t]^T: the per-axis range / max |D p|
-// of the robots, O(n).  The few terms non-interior at the old iterate take the FP64 target formula and, only
-// then, the max over the other terms is taken term by term.
+// of the robots, O(n).  The terms non-interior at the old iterate take the FP64 target formula, and the max
+// over the others comes from three-deep top / bottom selections of D p per axis (exact while at most two
+// pair terms of the step are non-interior at the old iterate; beyond that the pairs are scanned).
+// Register-light (inlined into the decision): the W row is streamed through the read-only cache and D p is
+// recomputed rather than stored.
+template <int MP>
+__device__ __forceinline__ double hy_dp_s(const double* __restrict__ Cn, const double* __restrict__ Co,
+                                          const double* __restrict__ Wrow, int m1, int row) {
+    const double* cn = Cn + row * MP;
+    const double* co = Co + row * MP;
+    double v = 0.0;
+#pragma unroll
+    for (int q = 0; q < MP; ++q) v = fma(cn[q] - co[q], q < m1 ? __ldg(Wrow + q) : 0.0, v);
+    return v;
+}
 template <int NB, int MP>
-__device__ __noinline__ double2 hy_exit64(const SolveParams& p, const double* Cn, const double* Co, int t,
-                                          const MaskPack<NB> om) {
-    const int n = p.n;
-    double w[MP];
-    w64_row<MP>(p.W, t, p.m1, w);
-    double dp[3 * NB];
-    double mx = 0.0, s2 = 0.0;
+__device__ __forceinline__ double2 hy_exit64_inline(const SolveParams& p, const double* Cn, const double* Co, int t,
+                                                    const uint32_t (&omr)[TermBits<NB>::words]) {
+    constexpr int NP = NB * (NB - 1) / 2;
+    uint32_t om[TermBits<NB>::words];   // (a copy: runtime-indexed lookups below must not pin the caller's registers)
+#pragma unroll
+    for (int u = 0; u < TermBits<NB>::words; ++u) om[u] = omr[u];
+    const int n = p.n, m1 = p.m1;
+    const double* Wrow = p.W + (size_t)t * m1;
+    // non-interior-at-old terms: count pairs and workspace terms, remember up to two pair bits
+    int npf = 0, fb0 = -1, fb1 = -1;
+    bool anyf = false;
+#pragma unroll
+    for (int u = 0; u < TermBits<NB>::words; ++u) {
+        const int rem = TermBits<NB>::count - 32 * u;
+        uint32_t f = ~om[u] & (rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u));
+        anyf = anyf || f != 0u;
+        while (f) {
+            const int b = 32 * u + __ffs(f) - 1;
+            f &= f - 1;
+            if (b < NP) {
+                ++npf;
+                fb1 = fb0;
+                fb0 = b;
+            }
+        }
+    }
+    double mx = 0.0, s2 = 0.0, base = 0.0;
+#pragma unroll 1
     for (int ax = 0; ax < 3; ++ax) {
         double lo = 0.0, hi = 0.0, s1 = 0.0, sq = 0.0;
+        double tv[3] = {-1e300, -1e300, -1e300}, bv[3] = {-1e300, -1e300, -1e300}, av[3] = {-1.0, -1.0, -1.0};
+        int ti[3] = {-1, -1, -1}, bi[3] = {-1, -1, -1}, ai[3] = {-1, -1, -1};
+#pragma unroll 1
         for (int i = 0; i < n; ++i) {
-            const double* cn = Cn + (ax * n + i) * MP;
-            const double* co = Co + (ax * n + i) * MP;
-            double v = 0.0;
-#pragma unroll
-            for (int q = 0; q < MP; ++q) v = fma(cn[q] - co[q], w[q], v);
-            dp[ax * NB + i] = v;
+            const double v = hy_dp_s<MP>(Cn, Co, Wrow, m1, ax * n + i);
             lo = i ? fmin(lo, v) : v;
             hi = i ? fmax(hi, v) : v;
             s1 += v;
             sq = fma(v, v, sq);
+            if (anyf) {
+                top3_insert(tv, ti, v, i);
+                top3_insert(bv, bi, -v, i);
+                const int wb = NP + i;
+                if ((om[wb >> 5] >> (wb & 31)) & 1u) top3_insert(av, ai, fabs(v), i);
+            }
         }
         mx = fmax(mx, fmax(hi - lo, fmax(hi, -lo)));
         s2 += fmax(fma((double)(n + 1), sq, -s1 * s1), sq);
-    }
-    constexpr int NP = NB * (NB - 1) / 2;
-    bool any = false;   // (phantom robots' terms are always interior: their bits are set)
-    for (int b = 0; b < TermBits<NB>::count; ++b) any = any || !bit_of(om.w, b);
-    if (any) {   // terms non-interior at the old iterate: exact targets, then the max over the rest
-        double base = 0.0, flmax = 0.0, adj = 0.0;
-        int b = 0;
-        for (int i = 0; i < NB; ++i) {
-            for (int j = i + 1; j < NB; ++j, ++b) {
-                if (j >= n) continue;
-                const double ex = dp[i] - dp[j], ey = dp[NB + i] - dp[NB + j], ez = dp[2 * NB + i] - dp[2 * NB + j];
-                if (bit_of(om.w, b)) {
-                    base = fmax(base, fmax(fabs(ex), fmax(fabs(ey), fabs(ez))));
-                } else {
-                    double wr[MP];
-                    w64_row<MP>(p.W, t, p.m1, wr);
-                    const D3 dn = term_diff64<MP>(p, Cn, wr, i, j), dol = term_diff64<MP>(p, Co, wr, i, j);
-                    const D3 x = resid64(true, dol, dn, family64(p, true));
-                    flmax = fmax(flmax, fmax(fabs(x.x), fmax(fabs(x.y), fabs(x.z))));
-                    adj += (x.x * x.x + x.y * x.y + x.z * x.z) - (ex * ex + ey * ey + ez * ez);
+        if (anyf) {
+            if (npf <= 2) {   // the max over pairs (a, b) not flagged lies among the top / bottom three
+#pragma unroll
+                for (int u = 0; u < 3; ++u)
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) {
+                        const int ia = ti[u], ib = bi[k];
+                        if (ia >= 0 && ib >= 0 && ia != ib) {
+                            const int pb = pair_bit<NB>(min(ia, ib), max(ia, ib));
+                            if (pb != fb0 && pb != fb1) base = fmax(base, tv[u] + bv[k]);
+                        }
+                    }
+            } else {   // many flagged pairs: scan every pair interior at the old iterate
+#pragma unroll 1
+                for (int i = 0; i < n; ++i) {
+                    const double vi = hy_dp_s<MP>(Cn, Co, Wrow, m1, ax * n + i);
+#pragma unroll 1
+                    for (int j = i + 1; j < n; ++j) {
+                        const int pb = pair_bit<NB>(i, j);
+                        if ((om[pb >> 5] >> (pb & 31)) & 1u)
+                            base = fmax(base, fabs(vi - hy_dp_s<MP>(Cn, Co, Wrow, m1, ax * n + j)));
+                    }
                 }
             }
+            if (ai[0] >= 0) base = fmax(base, av[0]);   // workspace terms interior at the old iterate
         }
-        b = NP;
-        for (int i = 0; i < n; ++i, ++b) {
-            const double ex = dp[i], ey = dp[NB + i], ez = dp[2 * NB + i];
-            if (bit_of(om.w, b)) {
-                base = fmax(base, fmax(fabs(ex), fmax(fabs(ey), fabs(ez))));
-            } else {
-                double wr[MP];
-                w64_row<MP>(p.W, t, p.m1, wr);
-                const D3 dn = term_diff64<MP>(p, Cn, wr, i, -1), dol = term_diff64<MP>(p, Co, wr, i, -1);
-                const D3 x = resid64(false, dol, dn, family64(p, false));
+    }
+    if (anyf) {   // exact residuals of the terms non-interior at the old iterate; their quiet shares leave the l2 sum
+        double flmax = 0.0, adj = 0.0;
+#pragma unroll 1
+        for (int u = 0; u < TermBits<NB>::words; ++u) {
+            const int rem = TermBits<NB>::count - 32 * u;
+            uint32_t f = ~om[u] & (rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u));
+            while (f) {
+                const int b = 32 * u + __ffs(f) - 1;
+                f &= f - 1;
+                int i, j;
+                if (b < NP) {
+                    i = 0;
+                    int rest = b;
+                    while (rest >= NB - 1 - i) rest -= NB - 1 - i, ++i;
+                    j = i + 1 + rest;
+                } else {
+                    i = b - NP;
+                    j = -1;
+                }
+                double e2 = 0.0;
+#pragma unroll 1
+                for (int ax = 0; ax < 3; ++ax) {
+                    const double e = hy_dp_s<MP>(Cn, Co, Wrow, m1, ax * n + i) -
+                                     (j >= 0 ? hy_dp_s<MP>(Cn, Co, Wrow, m1, ax * n + j) : 0.0);
+                    e2 = fma(e, e, e2);
+                }
+                const D3 dn = term_diff64s<MP>(p, Cn, Wrow, i, j), dol = term_diff64s<MP>(p, Co, Wrow, i, j);
+                const D3 x = resid64(j >= 0, dol, dn, family64(p, j >= 0));
                 flmax = fmax(flmax, fmax(fabs(x.x), fmax(fabs(x.y), fabs(x.z))));
-                adj += (x.x * x.x + x.y * x.y + x.z * x.z) - (ex * ex + ey * ey + ez * ez);
+                adj += (x.x * x.x + x.y * x.y + x.z * x.z) - e2;
             }
         }
         mx = fmax(base, flmax);
@@ -1726,10 +1816,7 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                     if (lt == 0) SGSF_COUNT(8, 1);
                     double xi = 0.0, xs = 0.0;
                     if (ts < S && owner) {
-                        MaskPack<NB> om;
-#pragma unroll
-                        for (int w = 0; w < NW; ++w) om.w[w] = imask[w];
-                        const double2 e = hy_exit64<NB, MP>(p, Ccur, Cprv, ts, om);
+                        const double2 e = hy_exit64_inline<NB, MP>(p, Ccur, Cprv, ts, imask);
                         xi = e.x;
                         xs = e.y;
                     }
