@@ -558,6 +558,36 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     print(json.dumps(line), flush=True)
 
 
+def run_stub(args, rank: int, world: int) -> None:
+    """`--stub` (CPU, gloo): the launcher, sharding, output gather and max-over-ranks reduction of the real
+    arm with the solve replaced by row-identifying fake outputs -- for tests/test_bench_launcher.py."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2501_19042_b200.distributed import gather_outputs, shard_range
+    prob, shard, B = workload(args.config, rank, world, args.batch)
+    lo, hi = shard_range(B, world, rank)
+    steps_ms, feas = [], 0
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        rows = torch.arange(lo, hi, dtype=torch.float64)
+        out = {"coeffs": torch.from_numpy(shard).clone(), "iterations": (rows % 7).to(torch.int32),
+               "feasible": (rows.to(torch.int64) % 3 == 0).to(torch.uint8)}
+        full = gather_outputs(out, B) if world > 1 else out
+        assert full["coeffs"].shape[0] == B
+        feas = int(full["feasible"].sum())
+        steps_ms.append(1e3 * (time.perf_counter() - t0))
+    t = torch.tensor([sum(steps_ms)], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": feas * args.steps / (float(t[0]) * 1e-3), "unit": "feasible samples/s",
+                          "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(t[0]) / args.steps,
+                          "scaling": CONFIGS[args.config][3], "stub": True, "feasible_per_step": feas,
+                          "config": {"workload": config_label(args.config, B, world), "batch": B,
+                                     "batch_per_gpu": hi - lo}}), flush=True)
+
+
 def ctypes_peak(native) -> float:
     import ctypes
 
@@ -595,6 +625,7 @@ def parse_args(argv=None):
                          "150 s / steps, within 2-12 s, for --impl reference)")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--quick", action="store_true", help="skip the side precisions, drop-in and pipeline numbers")
+    ap.add_argument("--stub", action="store_true", help=argparse.SUPPRESS)   # CPU/gloo launcher test (no GPU)
     return ap.parse_args(argv)
 
 
@@ -607,6 +638,16 @@ def main():
         raise SystemExit(launch_ranks(args.gpus))
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if args.stub:
+        import torch.distributed as dist
+        if world > 1:
+            dist.init_process_group("gloo")
+        try:
+            run_stub(args, rank, world)
+        finally:
+            if world > 1:
+                dist.destroy_process_group()
         return
     if world > 1:
         import torch
