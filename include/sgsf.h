@@ -18,6 +18,8 @@
  *                                                                                  _speedups.pyx:18-73
  *   sgsf_apply_F / sgsf_apply_FT PairwiseOperator.apply / apply_transpose          assembly.py:285-310
  *   sgsf_kkt_step                KktFactorization.solve                            assembly.py:186-219
+ *   sgsf_decoder_forward         the CVAE / VQ-VAE decoder forward pass feeding the SF (no reference code,
+ *                                SPEC.md:8; PAPER.md "CVAE / VQ-VAE Network Details")
  *   sgsf_unroll / _backward      K unrolled fixed-point steps and their reverse sweep: the differentiable
  *                                SF of PAPER.md "Learned Initialization for SF" (eq. NN_loss); the step is
  *                                the solve loop body solver.py:314-328 (the reference has no autodiff)
@@ -198,6 +200,30 @@ size_t sgsf_cosine_work_doubles(int count, int dim);
 int sgsf_pairwise_cosine(int count, int dim, const double* vectors, int center, double* work, double* result,
                          void* stream);
 
+/*
+ * Generative decoder forward pass (K4; BASELINE configs 1-3 sample the SF's proposals from a CVAE / VQ-VAE
+ * decoder, PAPER.md "CVAE / VQ-VAE Network Details"; the reference has no network code).  Four
+ * kernel-3 transposed convolutions of 128 channels (batch norm folded), LeakyReLU or ReLU, a 1x1 head to 3
+ * channels and a Linear L -> n (degree + 1) per axis, times `scale`: the coefficient correction to the
+ * straight line, B x 3 n (degree + 1), FP64.  Weights are device buffers in the packed layout written by
+ * paper_2501_19042_b200.generative.FusedDecoder (sgsf_decoder_pack_bytes(c0) bytes for the 4 layers).
+ */
+typedef struct {
+    int L;               /* latent positions */
+    int c0;              /* input channels of the first layer (latent + state features), <= 128 */
+    int nm1;             /* n (degree + 1): coefficients per axis */
+    int leaky;           /* 1: LeakyReLU(slope), 0: ReLU */
+    float slope, scale;
+    const void* wpack;   /* the 4 layers' weights, BN folded, tf32 hi / lo, in the kernel's operand layout */
+    const float* bias;   /* 4 x 128 folded biases */
+    const float* head_w; /* 3 x 128 */
+    const float* head_b; /* 3 */
+    const float* exp_w;  /* nm1 x L */
+    const float* exp_b;  /* nm1 */
+} sgsf_decoder_t;
+size_t sgsf_decoder_pack_bytes(int c0);
+/* h0: B x c0 x L float (device): the first layer's input; corr: B x 3 nm1 double (device) */
+int sgsf_decoder_forward(const sgsf_decoder_t* dec, int batch, const float* h0, double* corr, void* stream);
 /* FP32 FFMA throughput microbenchmark (roofline denominator); returns TFLOP/s in *tflops */
 int sgsf_fp32_peak(double* tflops, double* ms, void* stream);
 

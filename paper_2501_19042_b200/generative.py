@@ -116,6 +116,92 @@ def calibrate_batchnorm(sf, decoder: nn.Module, batches: int = 4, batch: int = 2
     return decoder.eval()
 
 
+def _tf32_split(x: torch.Tensor):
+    """(hi, lo) float32 with hi = x rounded to tf32 (nearest, ties away: cvt.rna) and lo = tf32(x - hi)."""
+    def rna(v):
+        b = v.contiguous().view(torch.int32)
+        return ((b + 0x1000) & ~0x1FFF).view(torch.float32)
+    x = x.to(torch.float32)
+    hi = rna(x)
+    return hi, rna(x - hi)
+
+
+class FusedDecoder:
+    """The decoder's eval-mode forward pass as one sm_100a kernel (K4, ``sgsf_decoder_forward``): batch norm
+    folded into the convolutions, weights packed once into the tensor-core operand layout (tf32 hi / lo per
+    32 KB stage of (tap, 32 input channels)).  ``__call__(latent, state)`` returns what
+    ``decoder(latent, state).to(float64)`` returns, computed on the tensor cores to FP32-level accuracy."""
+
+    STAGE = 32768
+
+    def __init__(self, decoder: nn.Module, device=None):
+        from . import native
+        self.decoder = decoder.eval()
+        dev = torch.device(device) if device is not None else next(decoder.parameters()).device
+        self.dev = dev
+        convs = [m for m in decoder.body if isinstance(m, nn.ConvTranspose1d)]
+        bns = [m for m in decoder.body if isinstance(m, nn.modules.batchnorm._BatchNorm)]
+        acts = [m for m in decoder.body if isinstance(m, (nn.LeakyReLU, nn.ReLU))]
+        assert len(convs) == 4 and len(bns) == 4 and all(c.kernel_size == (3,) and c.padding == (1,) for c in convs)
+        self.leaky = isinstance(acts[0], nn.LeakyReLU)
+        self.slope = float(acts[0].negative_slope) if self.leaky else 0.0
+        self.c0 = convs[0].in_channels
+        c0p = ((self.c0 + 31) // 32) * 32
+        stages, biases = [], []
+        with torch.no_grad():
+            for li, (cv, bn) in enumerate(zip(convs, bns)):
+                Wt = cv.weight.detach().double().cpu()                  # (c_in, c_out, 3)
+                Wc = Wt.flip(2).permute(1, 0, 2).contiguous()          # conv form (c_out, c_in, tap)
+                sc = bn.weight.double().cpu() / torch.sqrt(bn.running_var.double().cpu() + bn.eps)
+                Wc = Wc * sc[:, None, None]
+                b = (cv.bias.double().cpu() - bn.running_mean.double().cpu()) * sc + bn.bias.double().cpu()
+                cin = Wc.shape[1]
+                cinp = c0p if li == 0 else 128
+                Wp = torch.zeros(128, cinp, 3, dtype=torch.float64)
+                Wp[:, :cin] = Wc
+                for tap in range(3):
+                    for cg in range(cinp // 32):
+                        blk = Wp[:, cg * 32:(cg + 1) * 32, tap].reshape(128, 8, 4).permute(1, 0, 2)  # [chunk][m][4]
+                        hi, lo = _tf32_split(blk.float())
+                        stages.append(torch.cat([hi.reshape(-1), lo.reshape(-1)]))
+                biases.append(b.float())
+        self.wpack = torch.cat(stages).to(dev).contiguous()
+        assert self.wpack.numel() * 4 == native.load().sgsf_decoder_pack_bytes(self.c0)
+        self.bias = torch.cat(biases).to(dev).contiguous()
+        self.head_w = decoder.head.weight.detach().float().reshape(3, 128).to(dev).contiguous()
+        self.head_b = decoder.head.bias.detach().float().to(dev).contiguous()
+        self.exp_w = decoder.expand.weight.detach().float().to(dev).contiguous()   # (n m1, L)
+        self.exp_b = decoder.expand.bias.detach().float().to(dev).contiguous()
+        self.L, self.nm1, self.scale = decoder.L, decoder.n * decoder.m1, float(decoder.scale)
+        self.desc = native.Decoder(self.L, self.c0, self.nm1, int(self.leaky), self.slope, self.scale,
+                                   self.wpack.data_ptr(), self.bias.data_ptr(), self.head_w.data_ptr(),
+                                   self.head_b.data_ptr(), self.exp_w.data_ptr(), self.exp_b.data_ptr())
+
+    @torch.no_grad()
+    def first_layer_input(self, latent: torch.Tensor, state: torch.Tensor | None) -> torch.Tensor:
+        """(B, c0, L) float32: the latent (CVAE: with the broadcast state features; VQ-VAE: codebook vectors)."""
+        d = self.decoder
+        if isinstance(d, CVAEDecoder):
+            # one problem: the same features for all samples; full FP32 (cuDNN's default TF32 would put a 1e-3
+            # relative error into every sample's input)
+            with torch.backends.cudnn.flags(enabled=True, allow_tf32=False):
+                feat = d.state(state[:1].to(torch.float32), d.L)
+            return torch.cat([latent.to(torch.float32), feat.expand(latent.shape[0], -1, -1)], dim=1).contiguous()
+        return d.codebook(latent).transpose(1, 2).contiguous()
+
+    @torch.no_grad()
+    def __call__(self, latent: torch.Tensor, state: torch.Tensor | None = None) -> torch.Tensor:
+        from . import native
+        from .solver import _stream
+        h0 = self.first_layer_input(latent, state)
+        B = int(h0.shape[0])
+        out = torch.empty((B, 3 * self.nm1), dtype=torch.float64, device=h0.device)
+        if B:
+            native.check(native.load().sgsf_decoder_forward(native.C.byref(self.desc), B, h0.data_ptr(),
+                                                            out.data_ptr(), _stream()), "sgsf_decoder_forward")
+        return out
+
+
 def make_decoder(kind: str, n: int, m1: int = 11, **kw) -> nn.Module:
     if kind == "cvae":
         return CVAEDecoder(n, m1, **kw)

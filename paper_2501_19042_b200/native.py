@@ -47,6 +47,12 @@ class Verdict(C.Structure):
                 ("ws_margin_max", C.c_void_p), ("pair_viol", C.c_void_p), ("ws_viol", C.c_void_p)]
 
 
+class Decoder(C.Structure):
+    _fields_ = [("L", C.c_int), ("c0", C.c_int), ("nm1", C.c_int), ("leaky", C.c_int), ("slope", C.c_float),
+                ("scale", C.c_float), ("wpack", C.c_void_p), ("bias", C.c_void_p), ("head_w", C.c_void_p),
+                ("head_b", C.c_void_p), ("exp_w", C.c_void_p), ("exp_b", C.c_void_p)]
+
+
 class Timing(C.Structure):
     _fields_ = [("start", C.c_void_p), ("stop", C.c_void_p)]
 
@@ -78,6 +84,10 @@ EXPORTS = {
     "sgsf_cosine_work_doubles": (C.c_size_t, [C.c_int, C.c_int]),
     "sgsf_pairwise_cosine": (C.c_int, [C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
     "sgsf_fp32_peak": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_void_p]),
+    "sgsf_decoder_pack_bytes": (C.c_size_t, [C.c_int]),
+    "sgsf_decoder_forward": (C.c_int, [C.POINTER(Decoder), C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "sgsf_decoder_forward_dbg": (C.c_int, [C.POINTER(Decoder), C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                           C.c_int, C.c_void_p]),
 }
 
 _lib = None

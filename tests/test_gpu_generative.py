@@ -55,3 +55,30 @@ def test_pipeline_graph_replays_the_eager_pipeline():
         assert torch.equal(xb, xe)
         assert torch.equal(out.coeffs, ref.coeffs) and torch.equal(out.iterations, ref.iterations)
         assert torch.equal(out.feasible, ref.feasible)
+
+
+@pytest.mark.parametrize("kind,config,batch", [("cvae", 2, 300), ("vqvae", 3, 40), ("cvae", 1, 8)])
+def test_fused_decoder_kernel_matches_the_module(kind, config, batch):
+    """K4 (sgsf_decoder_forward: the 4 transposed convolutions on tcgen05 3xTF32, head and expansion fused)
+    equals the eval-mode PyTorch module in FP32 (TF32 off) to 1e-4 of the output scale, for the CVAE (L = 100
+    and L = 25) and the VQ-VAE, over more samples than SMs (the persistent loop)."""
+    from paper_2501_19042_b200 import SafetyFilter, SolverConfig
+    from paper_2501_19042_b200.generative import FusedDecoder, calibrate_batchnorm, make_decoder
+    from paper_2501_19042_b200.initnet import context_features
+    from paper_2501_19042_b200.scenarios import config_problem
+    prob = config_problem(config)
+    sf = SafetyFilter(prob, config=SolverConfig(max_iters=50, svars=False))
+    torch.manual_seed(11)
+    dec = calibrate_batchnorm(sf, make_decoder(kind, prob.n).cuda())
+    lat = dec.sample_latent(batch, torch.Generator(device="cuda").manual_seed(4), "cuda")
+    state = torch.as_tensor(context_features(prob), dtype=torch.float32, device="cuda").expand(batch, -1, -1)
+    with torch.no_grad(), torch.backends.cudnn.flags(enabled=True, allow_tf32=False):
+        torch.backends.cuda.matmul.allow_tf32 = False
+        ref = dec(lat, state).double()
+    fused = FusedDecoder(dec)
+    got = fused(lat, state)
+    torch.cuda.synchronize()
+    scale = float(ref.abs().max())
+    err = float((got - ref).abs().max())
+    assert err <= 1e-4 * scale, (err, scale)
+    assert got.shape == ref.shape and torch.isfinite(got).all()
