@@ -218,11 +218,20 @@ typedef struct {
     const float* bias;   /* 4 x 128 folded biases */
     const float* head_w; /* 3 x 128 */
     const float* head_b; /* 3 */
-    const float* exp_w;  /* nm1 x L */
+    const float* exp_w;  /* L x nm1: the expansion Linear's weight, transposed */
     const float* exp_b;  /* nm1 */
+    int cz;              /* channels read per sample from the input (the latent); the other c0 - cz ... */
+    const float* feat;   /* ... come from feat (c0 - cz values, constant over positions and samples), or NULL */
+    /* the boundary QP layer fused behind the decoder (projection.py:11-25), all nullable: with base set, the
+       output is xi_bar = project(base + correction) instead of the correction */
+    const double* base;  /* 3 nm1 straight-line coefficients */
+    const double* B6;    /* 6 x m1 endpoint rows */
+    const double* PBt;   /* m1 x 6  B^T (B B^T)^-1 */
+    const double* rhs;   /* 3 n x 6 endpoint values */
+    int n, m1;
 } sgsf_decoder_t;
 size_t sgsf_decoder_pack_bytes(int c0);
-/* h0: B x c0 x L float (device): the first layer's input; corr: B x 3 nm1 double (device) */
+/* h0: B x cz x L float (device): the latent (cz = c0 when feat is NULL); out: B x 3 nm1 double (device) */
 int sgsf_decoder_forward(const sgsf_decoder_t* dec, int batch, const float* h0, double* corr, void* stream);
 /* FP32 FFMA throughput microbenchmark (roofline denominator); returns TFLOP/s in *tflops */
 int sgsf_fp32_peak(double* tflops, double* ms, void* stream);

@@ -41,6 +41,14 @@ using namespace sgsf;
 constexpr int kThreads = 128;
 constexpr int kStageBytes = 32768;   // (tap, 32 input channels): 8 K-chunks x 128 rows x 16 B, tf32 hi then lo
 constexpr int kHalfStage = kStageBytes / 2;
+constexpr int kBuf = 3;              // weight stage buffers (prefetch depth)
+
+// (hi, lo) operand split: hi = x with the low 13 mantissa bits cleared (a tf32 value), lo = x - hi exactly (the
+// tensor core reads lo's top 11 significant bits: the pair carries x to ~2^-21 relative)
+__device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
+    hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+    lo = x - hi;
+}
 
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* mbar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(mbar)), "r"(bytes)
@@ -63,14 +71,19 @@ __device__ __forceinline__ void mma_tf32_ss(uint32_t d_tmem, uint64_t a_desc, ui
 }
 
 struct DecParams {
-    int batch, L, c0, c0p, nmma, nrows, nm1, leaky;
+    int batch, L, c0, c0p, nmma, nrows, nm1, leaky, cz, n, m1;
     float slope, scale;
-    const float* h0;        // B x c0 x L, the first layer's input (latent + state features)
+    const float* h0;        // B x cz x L: the per-sample channels of the first layer's input (the latent)
+    const float* feat;      // c0 - cz channels constant along L and over the batch (state features), nullable
+    const double* base;     // 3 nm1: straight-line coefficients (nullable: output the correction alone)
+    const double* B6;       // 6 x m1 endpoint rows
+    const double* PBt;      // m1 x 6 boundary projector
+    const double* rhs;      // 3 n x 6 endpoint values
     const uint8_t* wpack;   // all stages of the 4 layers, in order
     const float* bias;      // 4 x 128 (folded)
     const float* head_w;    // 3 x 128
     const float* head_b;    // 3
-    const float* exp_w;     // nm1 x L
+    const float* exp_w;     // L x nm1 (the Linear's weight, transposed)
     const float* exp_b;     // nm1
     double* corr;           // B x 3 nm1
     float* dbg;             // debug (nullable): B x 4 x 128 x L activations after each layer
@@ -86,17 +99,22 @@ __global__ void __launch_bounds__(kThreads, 1) decoder_kernel(const DecParams p)
     const int CH = p.nrows * 16;                  // bytes per 4-channel chunk of the activation operand
     unsigned char* act_hi = smem;                 // 32 chunks x nrows x 16 B
     unsigned char* act_lo = smem + 32 * CH;
-    unsigned char* wbuf = smem + 64 * CH;         // 2 x 32 KB weight stages
-    float* hbuf = (float*)(wbuf + 2 * kStageBytes);   // 3 x L head outputs
-    // [0..1] weights landed, [2..3] a stage's MMAs done, [4] a layer's MMAs done.  (The epilogue waits on its own
+    unsigned char* wbuf = smem + 64 * CH;         // kBuf x 32 KB weight stages
+    float* hbuf = (float*)(wbuf + kBuf * kStageBytes);   // 3 x L head outputs
+    float* hw_s = hbuf + 3 * ((p.L + 3) & ~3);              // 3 x 128 head weights
+    // [0, kBuf) weights landed, [kBuf, 2 kBuf) a stage's MMAs done, [2 kBuf] a layer's MMAs done.  (The epilogue waits on its own
     // barrier: warps that reach it early would otherwise wait on a stage barrier two phases ahead, which a
     // parity wait cannot tell from the previous phase -- they read TMEM before the MMAs finished.)
-    uint64_t* bars = (uint64_t*)(hbuf + 3 * ((p.L + 3) & ~3));
-    uint32_t* tslot = (uint32_t*)(bars + 5);
+    uint64_t* bars = (uint64_t*)(hw_s + 3 * 128);
+    uint32_t* tslot = (uint32_t*)(bars + 2 * kBuf + 1);
+    uint64_t* const wready = bars;
+    uint64_t* const mdone = bars + kBuf;
+    uint64_t* const ldone = bars + 2 * kBuf;
 
     for (int i = tid; i < 64 * CH / 4; i += kThreads) ((uint32_t*)smem)[i] = 0u;   // padding rows stay zero
+    for (int i = tid; i < 3 * 128; i += kThreads) hw_s[i] = p.head_w[i];
     if (tid == 0) {
-        for (int i = 0; i < 5; ++i) tc::mbar_init(&bars[i], 1);
+        for (int i = 0; i < 2 * kBuf + 1; ++i) tc::mbar_init(&bars[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     const int AS = p.nmma + 32;   // columns per tap accumulator (the epilogue reads 16 past the last row)
@@ -113,10 +131,10 @@ __global__ void __launch_bounds__(kThreads, 1) decoder_kernel(const DecParams p)
     const int my_samples = p.batch > (int)blockIdx.x ? (p.batch - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
     const long long total = (long long)my_samples * per_sample;
     auto stage_src = [&](long long g) { return p.wpack + (size_t)(g % per_sample) * kStageBytes; };
-    if (tid == 32) {   // producer: the first two stages
-        for (long long g = 0; g < 2 && g < total; ++g) {
-            mbar_expect_tx(&bars[g & 1], kStageBytes);
-            bulk_g2s(wbuf + (g & 1) * kStageBytes, stage_src(g), kStageBytes, &bars[g & 1]);
+    if (tid == 32) {   // producer: the first kBuf stages
+        for (long long g = 0; g < kBuf && g < total; ++g) {
+            mbar_expect_tx(&wready[g], kStageBytes);
+            bulk_g2s(wbuf + g * kStageBytes, stage_src(g), kStageBytes, &wready[g]);
         }
     }
 
@@ -125,13 +143,29 @@ __global__ void __launch_bounds__(kThreads, 1) decoder_kernel(const DecParams p)
     for (int s = 0; s < my_samples; ++s) {
         const int b = (int)blockIdx.x + s * (int)gridDim.x;
         // ---- the first layer's input: h0[b] -> rows 1..L, channels 0..c0-1 (c0..c0p-1 zero)
-        for (int e = tid; e < p.c0p * p.L; e += kThreads) {
-            const int c = e / p.L, t = e - c * p.L;
-            const float v = c < p.c0 ? p.h0[((size_t)b * p.c0 + c) * p.L + t] : 0.f;
-            const float hi = tc::tf32_rna(v);
-            const int off = (c >> 2) * CH + (t + 1) * 16 + (c & 3) * 4;
-            *(float*)(act_hi + off) = hi;
-            *(float*)(act_lo + off) = tc::tf32_rna(v - hi);
+        {
+            const float* src = p.h0 + (size_t)b * p.cz * p.L;
+            const int n_in = p.cz * p.L, n_feat = p.c0 * p.L, n_all = p.c0p * p.L;
+            for (int e0 = tid; e0 < n_all; e0 += 4 * kThreads) {   // four independent loads in flight
+                float v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int e = e0 + u * kThreads;
+                    v[u] = e < n_in ? __ldg(src + e) : (e < n_feat ? __ldg(p.feat + (e / p.L - p.cz)) : 0.f);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int e = e0 + u * kThreads;
+                    if (e < n_all) {
+                        const int c = e / p.L, t = e - c * p.L;
+                        float hi, lo;
+                        split_tf32(v[u], hi, lo);
+                        const int off = (c >> 2) * CH + (t + 1) * 16 + (c & 3) * 4;
+                        *(float*)(act_hi + off) = hi;
+                        *(float*)(act_lo + off) = lo;
+                    }
+                }
+            }
         }
         tc::fence_proxy_async();
         tc::fence_before_sync();
@@ -152,10 +186,10 @@ __global__ void __launch_bounds__(kThreads, 1) decoder_kernel(const DecParams p)
             }
 #endif
             for (int st = 0; st < ns; ++st, ++g) {
-                const int bi = (int)(g & 1);
-                const uint32_t ph = (uint32_t)((g >> 1) & 1);
+                const int bi = (int)(g % kBuf);
+                const uint32_t ph = (uint32_t)((g / kBuf) & 1);
                 if (tid == 0) {   // MMA issuer
-                    tc::mbar_wait(&bars[bi], ph);
+                    tc::mbar_wait(&wready[bi], ph);
 #ifdef SGSF_DEC_SLEEP
                     __nanosleep(20000);
 #endif
@@ -180,20 +214,21 @@ __global__ void __launch_bounds__(kThreads, 1) decoder_kernel(const DecParams p)
                         mma_tf32_ss(dt, a_lo, b_hi, idesc, 1u);
                         mma_tf32_ss(dt, a_hi, b_hi, idesc, 1u);
                     }
-                    tc::mma_commit(&bars[2 + bi]);
-                    if (st == ns - 1) tc::mma_commit(&bars[4]);
+                    tc::mma_commit(&mdone[bi]);
+                    if (st == ns - 1) tc::mma_commit(ldone);
                 }
-                if (tid == 32 && g + 2 < total) {   // producer: refill this buffer once its MMAs are done
-                    tc::mbar_wait(&bars[2 + bi], ph);
-                    mbar_expect_tx(&bars[bi], kStageBytes);
-                    bulk_g2s(wbuf + bi * kStageBytes, stage_src(g + 2), kStageBytes, &bars[bi]);
+                if (tid == 32 && g + kBuf < total) {   // producer: refill this buffer once its MMAs are done
+                    tc::mbar_wait(&mdone[bi], ph);
+                    mbar_expect_tx(&wready[bi], kStageBytes);
+                    bulk_g2s(wbuf + bi * kStageBytes, stage_src(g + kBuf), kStageBytes, &wready[bi]);
                 }
                 if (st == ns - 1) {   // ---- epilogue: D -> bias, activation -> the next layer's operand
-                    tc::mbar_wait(&bars[4], layers_done & 1u);
+                    tc::mbar_wait(ldone, layers_done & 1u);
                     ++layers_done;
                     tc::fence_after_sync();
                     const int c = tid;   // TMEM lane = output channel
                     const float bias = p.bias[l * 128 + c];
+                    const float slope = p.leaky ? p.slope : 0.f;
                     const uint32_t lrow = tbase + ((uint32_t)(32 * warp) << 16);
                     for (int t0 = 0; t0 < p.L; t0 += 16) {
                         // out[t] = P_0[t] + P_1[t + 1] + P_2[t + 2] (rows = positions + 1)
@@ -220,11 +255,12 @@ __global__ void __launch_bounds__(kThreads, 1) decoder_kernel(const DecParams p)
                                 const float a1 = u + 1 < 16 ? v1[u + 1] : v1n[u + 1 - 16];
                                 const float a2 = u + 2 < 16 ? v2[u + 2] : v2n[u + 2 - 16];
                                 float y = ((v0[u] + a1) + a2) + bias;
-                                y = y > 0.f ? y : (p.leaky ? p.slope * y : 0.f);
-                                const float hi = tc::tf32_rna(y);
+                                y = y > 0.f ? y : slope * y;
+                                float hi, lo;
+                                split_tf32(y, hi, lo);
                                 const int off = (c >> 2) * CH + (t + 1) * 16 + (c & 3) * 4;
                                 *(float*)(act_hi + off) = hi;
-                                *(float*)(act_lo + off) = tc::tf32_rna(y - hi);
+                                *(float*)(act_lo + off) = lo;
                                 if (p.dbg && !(p.dbg_raw && l > 0)) p.dbg[(((size_t)b * 4 + l) * 128 + c) * p.L + t] = y;
                             }
                         }
@@ -243,18 +279,55 @@ __global__ void __launch_bounds__(kThreads, 1) decoder_kernel(const DecParams p)
                 const int off = (c >> 2) * CH + (t + 1) * 16 + (c & 3) * 4;
                 const float x = *(const float*)(act_hi + off) + *(const float*)(act_lo + off);
 #pragma unroll
-                for (int ax = 0; ax < 3; ++ax) h[ax] = fmaf(__ldg(p.head_w + ax * 128 + c), x, h[ax]);
+                for (int ax = 0; ax < 3; ++ax) h[ax] = fmaf(hw_s[ax * 128 + c], x, h[ax]);
             }
 #pragma unroll
             for (int ax = 0; ax < 3; ++ax) hbuf[ax * p.L + t] = h[ax];
         }
         __syncthreads();
-        for (int o = tid; o < 3 * p.nm1; o += kThreads) {
-            const int ax = o / p.nm1, j = o - ax * p.nm1;
-            const float* e = p.exp_w + (size_t)j * p.L;
-            float acc = __ldg(p.exp_b + j);
-            for (int t = 0; t < p.L; ++t) acc = fmaf(__ldg(e + t), hbuf[ax * p.L + t], acc);
-            p.corr[(size_t)b * 3 * p.nm1 + o] = (double)(p.scale * acc);
+        for (int j = tid; j < p.nm1; j += kThreads) {   // exp_w is L x nm1 (transposed): coalesced rows
+            const float eb = __ldg(p.exp_b + j);
+            float a0 = eb, a1 = eb, a2 = eb;
+            for (int t = 0; t < p.L; ++t) {
+                const float e = __ldg(p.exp_w + (size_t)t * p.nm1 + j);
+                a0 = fmaf(e, hbuf[t], a0);
+                a1 = fmaf(e, hbuf[p.L + t], a1);
+                a2 = fmaf(e, hbuf[2 * p.L + t], a2);
+            }
+            if (p.base) {   // xi' = straight line + correction, kept in shared memory for the QP layer below
+                double* xs = (double*)act_lo;   // (free: the head has read the last activations)
+                xs[j] = p.base[j] + (double)(p.scale * a0);
+                xs[p.nm1 + j] = p.base[p.nm1 + j] + (double)(p.scale * a1);
+                xs[2 * p.nm1 + j] = p.base[2 * p.nm1 + j] + (double)(p.scale * a2);
+            } else {
+                double* o = p.corr + (size_t)b * 3 * p.nm1 + j;
+                o[0] = (double)(p.scale * a0);
+                o[p.nm1] = (double)(p.scale * a1);
+                o[2 * p.nm1] = (double)(p.scale * a2);
+            }
+        }
+        if (p.base) {   // the boundary QP layer (projection.py:11-25): C - PBt (B6 C - rhs), per robot and axis
+            __syncthreads();
+            const double* xs = (const double*)act_lo;
+            for (int r = tid; r < 3 * p.n; r += kThreads) {
+                const double* c = xs + r * p.m1;
+                double res[6];
+#pragma unroll
+                for (int k = 0; k < 6; ++k) {
+                    double e = 0.0;
+                    for (int q = 0; q < p.m1; ++q) e = fma(p.B6[k * p.m1 + q], c[q], e);
+                    res[k] = e - p.rhs[r * 6 + k];
+                }
+                double* o = p.corr + (size_t)b * 3 * p.nm1 + r * p.m1;
+                for (int q = 0; q < p.m1; ++q) {
+                    double corr = 0.0;
+#pragma unroll
+                    for (int k = 0; k < 6; ++k) corr = fma(p.PBt[q * 6 + k], res[k], corr);
+                    o[q] = c[q] - corr;
+                }
+            }
+            __syncthreads();   // restore the zero padding rows the scratch covered
+            for (int i = tid; i < 3 * p.nm1 * 2; i += kThreads) ((uint32_t*)act_lo)[i] = 0u;
         }
         __syncthreads();   // hbuf and the activation buffers are rewritten by the next sample
     }
@@ -298,6 +371,16 @@ int sgsf_decoder_forward_dbg(const sgsf_decoder_t* d, int batch, const float* h0
     p.slope = d->slope;
     p.scale = d->scale;
     p.h0 = h0;
+    p.cz = d->feat ? d->cz : d->c0;
+    p.feat = d->feat;
+    p.base = d->base;
+    p.B6 = d->B6;
+    p.PBt = d->PBt;
+    p.rhs = d->rhs;
+    p.n = d->n;
+    p.m1 = d->m1;
+    if (p.base && (!p.B6 || !p.PBt || !p.rhs || p.n * p.m1 != p.nm1))
+        return internal_fail(SGSF_ERR_INVALID, "decoder QP layer: B6, PBt, rhs and n m1 = nm1 required");
     p.wpack = (const uint8_t*)d->wpack;
     p.bias = d->bias;
     p.head_w = d->head_w;
@@ -307,7 +390,8 @@ int sgsf_decoder_forward_dbg(const sgsf_decoder_t* d, int batch, const float* h0
     p.corr = corr;
     p.dbg = dbg;
     p.dbg_raw = raw;
-    const size_t smem = (size_t)64 * p.nrows * 16 + 2 * kStageBytes + (size_t)3 * ((p.L + 3) & ~3) * 4 + 64 + 16;
+    const size_t smem = (size_t)64 * p.nrows * 16 + kBuf * kStageBytes + (size_t)3 * ((p.L + 3) & ~3) * 4 +
+                        3 * 128 * 4 + 128;
     cudaError_t e = cudaFuncSetAttribute(decoder_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return internal_fail(SGSF_ERR_CUDA, std::string("decoder smem: ") + cudaGetErrorString(e));
     int dev = 0, sms = 0;

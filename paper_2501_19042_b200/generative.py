@@ -170,12 +170,40 @@ class FusedDecoder:
         self.bias = torch.cat(biases).to(dev).contiguous()
         self.head_w = decoder.head.weight.detach().float().reshape(3, 128).to(dev).contiguous()
         self.head_b = decoder.head.bias.detach().float().to(dev).contiguous()
-        self.exp_w = decoder.expand.weight.detach().float().to(dev).contiguous()   # (n m1, L)
+        self.exp_w = decoder.expand.weight.detach().float().t().to(dev).contiguous()   # (L, n m1): transposed
         self.exp_b = decoder.expand.bias.detach().float().to(dev).contiguous()
         self.L, self.nm1, self.scale = decoder.L, decoder.n * decoder.m1, float(decoder.scale)
-        self.desc = native.Decoder(self.L, self.c0, self.nm1, int(self.leaky), self.slope, self.scale,
-                                   self.wpack.data_ptr(), self.bias.data_ptr(), self.head_w.data_ptr(),
-                                   self.head_b.data_ptr(), self.exp_w.data_ptr(), self.exp_b.data_ptr())
+        self._feat_key, self._feat = None, None
+        self._descs: dict = {}
+
+    def _desc(self, cz: int, feat, qp: dict | None):
+        key = (cz, feat.data_ptr() if feat is not None else 0, id(qp))
+        d = self._descs.get(key)
+        if d is None:
+            d = self._descs[key] = (self._make_desc(cz, feat, qp), qp)   # (qp kept alive: its id is the key)
+        return d[0]
+
+    def _make_desc(self, cz: int, feat, qp: dict | None):
+        from . import native
+        d = native.Decoder(self.L, self.c0, self.nm1, int(self.leaky), self.slope, self.scale,
+                           self.wpack.data_ptr(), self.bias.data_ptr(), self.head_w.data_ptr(),
+                           self.head_b.data_ptr(), self.exp_w.data_ptr(), self.exp_b.data_ptr(), cz,
+                           feat.data_ptr() if feat is not None else None)
+        if qp is not None:
+            d.base, d.B6, d.PBt, d.rhs = (qp[k].data_ptr() for k in ("base", "B", "PBt", "rhs"))
+            d.n, d.m1 = qp["n"], qp["m1"]
+        return d
+
+    @torch.no_grad()
+    def state_features(self, state: torch.Tensor) -> torch.Tensor:
+        """(c0 - 3,) float32: the CVAE's state-network features of one problem's start/goal context (the same
+        for every sample), cached per context tensor."""
+        key = (state.data_ptr(), tuple(state.shape))
+        if self._feat_key != key:
+            with torch.backends.cudnn.flags(enabled=True, allow_tf32=False):
+                self._feat = self.decoder.state(state[:1].to(torch.float32), 1)[0, :, 0].contiguous()
+            self._feat_key = key
+        return self._feat
 
     @torch.no_grad()
     def first_layer_input(self, latent: torch.Tensor, state: torch.Tensor | None) -> torch.Tensor:
@@ -190,15 +218,23 @@ class FusedDecoder:
         return d.codebook(latent).transpose(1, 2).contiguous()
 
     @torch.no_grad()
-    def __call__(self, latent: torch.Tensor, state: torch.Tensor | None = None) -> torch.Tensor:
+    def __call__(self, latent: torch.Tensor, state: torch.Tensor | None = None, qp: dict | None = None) -> torch.Tensor:
+        """The correction ``decoder(latent, state)`` (B, 3 n m1) FP64; with ``qp`` (the QP layer's device
+        constants: base, B, PBt, rhs, n, m1) the projected proposals boundary_projection(base + correction),
+        with the QP layer fused into the kernel."""
         from . import native
         from .solver import _stream
-        h0 = self.first_layer_input(latent, state)
+        d = self.decoder
+        if isinstance(d, CVAEDecoder):   # the latent per sample, the state features from a per-problem cache
+            h0, feat, cz = latent.to(torch.float32).contiguous(), self.state_features(state), latent.shape[1]
+        else:
+            h0, feat, cz = d.codebook(latent).transpose(1, 2).contiguous(), None, self.c0
         B = int(h0.shape[0])
         out = torch.empty((B, 3 * self.nm1), dtype=torch.float64, device=h0.device)
         if B:
-            native.check(native.load().sgsf_decoder_forward(native.C.byref(self.desc), B, h0.data_ptr(),
-                                                            out.data_ptr(), _stream()), "sgsf_decoder_forward")
+            desc = self._desc(cz, feat, qp)
+            native.check(native.load().sgsf_decoder_forward(desc, B, h0.data_ptr(), out.data_ptr(), _stream()),
+                         "sgsf_decoder_forward")
         return out
 
 
@@ -210,23 +246,28 @@ def make_decoder(kind: str, n: int, m1: int = 11, **kw) -> nn.Module:
     raise ValueError(f"decoder kind must be 'cvae' or 'vqvae', got {kind!r}")
 
 
-def decode_proposals(sf, decoder: nn.Module, latent: torch.Tensor) -> torch.Tensor:
+def decode_proposals(sf, decoder: nn.Module, latent: torch.Tensor, fused: "FusedDecoder | None" = None) -> torch.Tensor:
     """xi_bar (B, dim) float64 on the decoder's device: the straight line plus the decoder's correction,
-    through the boundary QP layer (projection.py:11-25)."""
+    through the boundary QP layer (projection.py:11-25).  With ``fused`` (a :class:`FusedDecoder` of the same
+    decoder) the correction comes from the sm_100a decoder kernel K4 instead of the PyTorch module."""
     k = device_constants_of(sf, latent.device)
     state, base = k["context"].to(torch.float32), k["base"]
-    corr = decoder(latent, state.expand(latent.shape[0], -1, -1)).to(torch.float64)
-    return boundary_projection(sf, base + corr)
+    st = state.expand(latent.shape[0], -1, -1)
+    if fused is not None:   # decoder + QP layer in one kernel
+        return fused(latent, st, qp=k)
+    return boundary_projection(sf, base + decoder(latent, st).to(torch.float64))
 
 
 @torch.no_grad()
-def generate_and_filter(sf, decoder: nn.Module, batch: int, seed: int = 0, init_net=None, config=None):
+def generate_and_filter(sf, decoder: nn.Module, batch: int, seed: int = 0, init_net=None, config=None,
+                        fused: "FusedDecoder | None" = None):
     """Sample ``batch`` proposals from the decoder and filter them, all on the current CUDA device (no host
-    round trip): latent -> decoder -> QP layer -> (init network) -> SF kernel.  Returns (xi_bar, DeviceBatch)."""
+    round trip): latent -> decoder (kernel K4 when ``fused`` is given) -> QP layer -> (init network) -> SF
+    kernel.  Returns (xi_bar, DeviceBatch)."""
     dev = torch.device("cuda", torch.cuda.current_device())
     decoder.to(dev).eval()
     gen = torch.Generator(device=dev).manual_seed(seed)
-    xb = decode_proposals(sf, decoder, decoder.sample_latent(batch, gen, dev))
+    xb = decode_proposals(sf, decoder, decoder.sample_latent(batch, gen, dev), fused)
     xi0 = lam0 = None
     if init_net is not None:
         from .initnet import initial_states
@@ -242,9 +283,10 @@ class PipelineGraph:
     same (xi_bar, DeviceBatch) tensors, overwritten."""
 
     def __init__(self, sf, decoder: nn.Module, batch: int, init_net=None, config=None, seed: int = 0,
-                 warmup: int = 2):
+                 warmup: int = 2, fused: bool = True):
         dev = torch.device("cuda", torch.cuda.current_device())
         self.sf, self.decoder, self.init_net, self.config = sf, decoder.to(dev).eval(), init_net, config
+        self.fused = FusedDecoder(self.decoder) if fused else None
         if init_net is not None:
             init_net.to(dev).eval()
         gen = torch.Generator(device=dev).manual_seed(seed)
@@ -261,7 +303,7 @@ class PipelineGraph:
 
     @torch.no_grad()
     def _run(self):
-        xb = decode_proposals(self.sf, self.decoder, self.latent)
+        xb = decode_proposals(self.sf, self.decoder, self.latent, self.fused)
         xi0 = lam0 = None
         if self.init_net is not None:
             from .initnet import initial_states

@@ -50,7 +50,9 @@ class Verdict(C.Structure):
 class Decoder(C.Structure):
     _fields_ = [("L", C.c_int), ("c0", C.c_int), ("nm1", C.c_int), ("leaky", C.c_int), ("slope", C.c_float),
                 ("scale", C.c_float), ("wpack", C.c_void_p), ("bias", C.c_void_p), ("head_w", C.c_void_p),
-                ("head_b", C.c_void_p), ("exp_w", C.c_void_p), ("exp_b", C.c_void_p)]
+                ("head_b", C.c_void_p), ("exp_w", C.c_void_p), ("exp_b", C.c_void_p), ("cz", C.c_int),
+                ("feat", C.c_void_p), ("base", C.c_void_p), ("B6", C.c_void_p), ("PBt", C.c_void_p),
+                ("rhs", C.c_void_p), ("n", C.c_int), ("m1", C.c_int)]
 
 
 class Timing(C.Structure):

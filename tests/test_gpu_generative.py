@@ -49,7 +49,7 @@ def test_pipeline_graph_replays_the_eager_pipeline():
     for latent in (g.latent.clone(), dec.sample_latent(8, torch.Generator(device="cuda").manual_seed(9), "cuda")):
         xb, out = g.replay(latent)
         with torch.no_grad():
-            xe = decode_proposals(sf, dec, latent)
+            xe = decode_proposals(sf, dec, latent, g.fused)
         ref = sf.solve_batched(xe, config=cfg)
         torch.cuda.synchronize()
         assert torch.equal(xb, xe)
@@ -82,3 +82,25 @@ def test_fused_decoder_kernel_matches_the_module(kind, config, batch):
     err = float((got - ref).abs().max())
     assert err <= 1e-4 * scale, (err, scale)
     assert got.shape == ref.shape and torch.isfinite(got).all()
+
+
+def test_fused_decoder_qp_layer_equals_boundary_projection():
+    """With the QP layer fused (decode_proposals(..., fused)), K4 returns boundary_projection(line +
+    correction) (projection.py:11-25): equal to the module path to 1e-4 of the scale, endpoint conditions
+    to 1e-9."""
+    from paper_2501_19042_b200 import SafetyFilter, SolverConfig
+    from paper_2501_19042_b200.generative import FusedDecoder, calibrate_batchnorm, decode_proposals, make_decoder
+    from paper_2501_19042_b200.scenarios import config_problem
+    prob = config_problem(2)
+    sf = SafetyFilter(prob, config=SolverConfig(max_iters=50, svars=False))
+    torch.manual_seed(2)
+    dec = calibrate_batchnorm(sf, make_decoder("cvae", prob.n).cuda())
+    lat = dec.sample_latent(200, torch.Generator(device="cuda").manual_seed(8), "cuda")
+    with torch.no_grad(), torch.backends.cudnn.flags(enabled=True, allow_tf32=False):
+        ref = decode_proposals(sf, dec, lat)
+    got = decode_proposals(sf, dec, lat, FusedDecoder(dec))
+    torch.cuda.synchronize()
+    assert float((got - ref).abs().max()) <= 1e-4 * float(ref.abs().max())
+    res = got.cpu().numpy()
+    for b in range(0, 200, 37):
+        assert abs(sf.equality.residual(res[b])).max() <= 1e-9

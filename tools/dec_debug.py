@@ -22,7 +22,7 @@ h0 = f.first_layer_input(lat, state)
 L = dec.L
 dbg = torch.zeros(B, 4, 128, L, device="cuda")
 out = torch.empty(B, 3 * f.nm1, dtype=torch.float64, device="cuda")
-native.check(native.load().sgsf_decoder_forward_dbg(native.C.byref(f.desc), B, h0.data_ptr(), out.data_ptr(),
+native.check(native.load().sgsf_decoder_forward_dbg(native.C.byref(f._desc(f.c0, None, None)), B, h0.data_ptr(), out.data_ptr(),
                                                     dbg.data_ptr(), 0, 0), "dbg")
 torch.cuda.synchronize()
 convs = [m for m in dec.body if isinstance(m, torch.nn.ConvTranspose1d)]

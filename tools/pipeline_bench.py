@@ -13,7 +13,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 from paper_2501_19042_b200 import SafetyFilter, SolverConfig  # noqa: E402
-from paper_2501_19042_b200.generative import calibrate_batchnorm, decode_proposals, make_decoder  # noqa: E402
+from paper_2501_19042_b200.generative import FusedDecoder, calibrate_batchnorm, decode_proposals, make_decoder  # noqa: E402
 from paper_2501_19042_b200.scenarios import config_problem  # noqa: E402
 
 CASES = [  # (config, decoder, batch, max_iters)
@@ -28,6 +28,7 @@ def run(config, kind, batch, max_iters, reps=3):
     prob = config_problem(config)
     sf = SafetyFilter(prob, config=SolverConfig(max_iters=max_iters, svars=False))
     dec = calibrate_batchnorm(sf, make_decoder(kind, prob.n).cuda())
+    fused = FusedDecoder(dec)   # K4
     gen = torch.Generator(device="cuda").manual_seed(0)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
     out = None
@@ -35,7 +36,7 @@ def run(config, kind, batch, max_iters, reps=3):
     for r in range(reps + 1):
         with torch.no_grad():
             ev[0].record()
-            xb = decode_proposals(sf, dec, dec.sample_latent(batch, gen, "cuda"))
+            xb = decode_proposals(sf, dec, dec.sample_latent(batch, gen, "cuda"), fused)
             ev[1].record()
             out = sf.solve_batched(xb)
             ev[2].record()
