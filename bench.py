@@ -360,12 +360,14 @@ def pipeline_e2e(prob, batch: int, reps: int = 3) -> dict:
 
     from paper_2501_19042_b200 import SafetyFilter, SolverConfig
     from paper_2501_19042_b200.generative import FusedDecoder, calibrate_batchnorm, decode_proposals, make_decoder
-    from paper_2501_19042_b200.initnet import InitNet, initial_states
+    from paper_2501_19042_b200.initnet import FoldedInitNet, InitNet, initial_states
+    from paper_2501_19042_b200.unrolled import device_constants_of
     torch.manual_seed(0)
     sf = SafetyFilter(prob, degree=10, config=SolverConfig(max_iters=MAX_ITERS, svars=False))
     dec = calibrate_batchnorm(sf, make_decoder("cvae", prob.n).cuda()).eval()
     fused = FusedDecoder(dec)   # K4: the decoder's forward pass as one sm_100a kernel
     net = InitNet(prob.n, sf.coeff_dim).cuda().eval()
+    net = FoldedInitNet(net, device_constants_of(sf, "cuda")["context"][None])   # per-problem folded GEMMs
     gen = torch.Generator(device="cuda").manual_seed(0)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     acc = [0.0, 0.0, 0.0]

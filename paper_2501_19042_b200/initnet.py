@@ -69,6 +69,48 @@ class InitNet(nn.Module):
         return xi_bar + out[:, :self.dim], out[:, self.dim:]
 
 
+class FoldedInitNet:
+    """The eval-mode init net for ONE problem as four cuBLAS GEMMs: the context encoder's output is the same
+    for every sample of a problem, so it becomes a constant bias of the first layer (W1 [c | x] = W1_x x +
+    W1_c c), and each batch norm folds into its Linear.  ``__call__(xi_bar)`` returns what
+    ``net(context, xi_bar)`` returns (eval mode) to FP32 rounding, without the per-call PointNet pass,
+    concatenation and normalisation kernels."""
+
+    def __init__(self, net: InitNet, context: torch.Tensor):
+        net = net.eval()
+        self.dim = net.dim
+        lin = [m for m in net.mlp if isinstance(m, nn.Linear)]
+        bns = [m for m in net.mlp if isinstance(m, nn.BatchNorm1d)]
+        acts = [m for m in net.mlp if isinstance(m, nn.LeakyReLU)]
+        self.slope = float(acts[0].negative_slope)
+        with torch.no_grad(), torch.backends.cudnn.flags(enabled=True, allow_tf32=False):
+            c = net.point(context[:1].to(lin[0].weight.dtype)).amax(dim=2)[0].double()   # (width,)
+            width = c.shape[0]
+            self.W, self.b = [], []
+            for i, L_ in enumerate(lin):
+                W, b = L_.weight.double(), L_.bias.double()
+                if i == 0:   # the context half of the first layer is a constant: fold it into the bias
+                    b = b + W[:, :width] @ c
+                    W = W[:, width:]
+                if i < len(bns):
+                    bn = bns[i]
+                    sc = bn.weight.double() / torch.sqrt(bn.running_var.double() + bn.eps)
+                    W = W * sc[:, None]
+                    b = (b - bn.running_mean.double()) * sc + bn.bias.double()
+                self.W.append(W.t().contiguous().float())   # (in, out) for x @ W
+                self.b.append(b.float().contiguous())
+
+    @torch.no_grad()
+    def __call__(self, xi_bar: torch.Tensor):
+        h = xi_bar.to(torch.float32)
+        for i, (W, b) in enumerate(zip(self.W, self.b)):
+            h = torch.addmm(b, h, W)
+            if i < len(self.W) - 1:
+                h = torch.nn.functional.leaky_relu(h, self.slope)
+        out = h.to(xi_bar.dtype)
+        return xi_bar + out[:, :self.dim], out[:, self.dim:]
+
+
 @dataclass
 class TrainLog:
     losses: list = field(default_factory=list)
@@ -142,6 +184,8 @@ def initial_states(sf, proposals: torch.Tensor, strategy: str, net: InitNet | No
     if strategy == "initnet":
         if net is None:
             raise ValueError("strategy 'initnet' needs a network")
+        if isinstance(net, FoldedInitNet):
+            return net(proposals)
         net.eval()
         with torch.no_grad():
             from .unrolled import device_constants_of

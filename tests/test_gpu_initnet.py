@@ -42,3 +42,33 @@ def test_multi_scenario_training_runs():
     net = InitNet(8, scen[0][0].coeff_dim)
     log = train_init_net_multi(scen, net, iters=3, steps=12, batch=96, per_step=3)
     assert log.steps == 12 and np.isfinite(log.losses).all() and log.sf_seconds > 0
+
+
+def test_folded_init_net_equals_the_module():
+    """FoldedInitNet (context encoder folded into the first layer's bias, batch norms into the Linears)
+    returns the eval-mode module's (xi_0, lambda_0) to FP32 rounding."""
+    import torch
+
+    from paper_2501_19042_b200 import SafetyFilter, SolverConfig, sample_proposals
+    from paper_2501_19042_b200.initnet import FoldedInitNet, InitNet
+    from paper_2501_19042_b200.scenarios import config_problem
+    from paper_2501_19042_b200.unrolled import device_constants_of
+    prob = config_problem(2)
+    sf = SafetyFilter(prob, config=SolverConfig(max_iters=20, svars=False))
+    torch.manual_seed(0)
+    net = InitNet(prob.n, sf.coeff_dim).cuda()
+    with torch.no_grad():   # non-trivial batch norm statistics and last layer
+        for m in net.modules():
+            if isinstance(m, torch.nn.BatchNorm1d):
+                m.running_mean.uniform_(-0.5, 0.5)
+                m.running_var.uniform_(0.5, 2.0)
+        net.mlp[-1].weight.normal_(0.0, 1e-3)
+    net.eval()
+    xb = torch.from_numpy(sample_proposals(prob, sf.basis, 64, seed=1).proposals).cuda()
+    ctx = device_constants_of(sf, "cuda")["context"][None]
+    torch.backends.cuda.matmul.allow_tf32 = False
+    with torch.no_grad(), torch.backends.cudnn.flags(enabled=True, allow_tf32=False):
+        x_ref, l_ref = net(ctx.expand(64, -1, -1), xb)
+    x_f, l_f = FoldedInitNet(net, ctx)(xb)
+    assert float((x_f - x_ref).abs().max()) <= 1e-5 * float(x_ref.abs().max())
+    assert float((l_f - l_ref).abs().max()) <= 1e-4 * max(float(l_ref.abs().max()), 1e-6) + 1e-7
