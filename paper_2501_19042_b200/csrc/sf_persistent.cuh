@@ -1430,6 +1430,40 @@ __host__ __device__ __forceinline__ int step_of(int lwarp, int lane, int wps, in
     return 8 * (lwarp + wps * (lane >> 3)) + (lane & 7);
 }
 
+// ||A xi - b||_inf over one axis' rows of the iterate C (assembly.py:198-199): E[robot][c6] = B6[c6] . C_robot -
+// rhs as FP64 tensor-core tiles, max-reduced over the warp.  Called by the axis warps at the top of the next
+// iteration, where it overlaps the wait for the position MMAs instead of lengthening the xi-step's chain.
+template <int MT, int MP>
+__device__ __forceinline__ double eq_check_axis(const double* __restrict__ C, const double* __restrict__ B6,
+                                                const double* __restrict__ rhs, int rb, int n, int lane) {
+    const int fr = lane >> 2, fc = lane & 3;
+    double eacc[MT][2];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+        const int rob = 8 * mt + fr;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int c6 = 2 * fc + e;
+            eacc[mt][e] = (rob < n && c6 < 6) ? -rhs[(rb + rob) * 6 + c6] : 0.0;
+        }
+    }
+#pragma unroll
+    for (int kk = 0; kk < MP / 4; ++kk) {
+        const int q = 4 * kk + fc;
+        const double bv = fr < 6 ? B6[fr * MP + q] : 0.0;
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+            const int rob = 8 * mt + fr;
+            const double a = rob < n ? C[(rb + rob) * MP + q] : 0.0;
+            dmma884(eacc[mt][0], eacc[mt][1], a, bv);
+        }
+    }
+    double em = 0.0;
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) em = fmax(em, fmax(fabs(eacc[mt][0]), fabs(eacc[mt][1])));
+    return warp_max_nonneg(em);
+}
+
 // ---------------------------------------------------------------- the kernel
 // TC = positions by the 3xTF32 tcgen05 GEMM (float, 16 robots, one thread per step, 4 warps per slot)
 // FULLN: 0 = both term-pass variants, chosen at run time by n == NB; 1 = only the phantom-free one
@@ -1629,6 +1663,13 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
             T* const Pbase_new = (T*)((k & 1) ? sp.P0 : sp.P1);
             T* Prow_old = (T*)((k & 1) ? sp.P1 : sp.P0) + ts * RS;
             T* Prow_new = Pbase_new + ts * RS;
+            if (k >= 1) {   // ||A xi - b|| of the iterate the previous xi-step wrote (read after the term-pass barrier)
+                constexpr int MTE = (NB + 7) / 8;
+                for (int ax = lwarp; ax < 3; ax += p.wps) {
+                    const double em = eq_check_axis<MTE, MP>(Ccur, B6, rhs, ax * n, n, lane);
+                    if (lane == 0) sp.eqerr[ax] = em;
+                }
+            }
             // ---------------- T1: positions, O(n) statistics, workspace terms, motion bound, near pairs
             bool need_scan = false;
             uint32_t nm[NW];
@@ -1759,10 +1800,6 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                     sp.psq[lwarp] = wq;
                 }
             }
-            // ||A xi - b|| of iteration k-1: written by the axis warps in MX before the previous
-            // iteration's closing barrier, rewritten in this iteration's MX -- so it is read HERE,
-            // before the term-pass barrier, where no warp can have reached the rewrite yet (WAR-safe)
-            const double emax_pre = k >= 1 ? fmax(fmax(sp.eqerr[0], sp.eqerr[1]), sp.eqerr[2]) : 0.0;
 #ifdef SGSF_PHASE_TIMING
             if (slot == 0 && lane == 0 && lwarp < 4) pt_arrive[lwarp] = clock64();   // term-pass barrier arrivals
 #endif
@@ -1782,7 +1819,9 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
 #endif
 
             // ---------------- decision (every warp, redundantly): exit residual of iteration k-1, early stop, SingularKKT
-            const double emax = emax_pre;
+            // ||A xi - b|| of the iterate C_k: written by the axis warps at the top of this iteration, before the
+            // term-pass barrier; rewritten at the top of the next one, after the closing barrier (race-free)
+            const double emax = k >= 1 ? fmax(fmax(sp.eqerr[0], sp.eqerr[1]), sp.eqerr[2]) : 0.0;
             double sqs = 0.0;
             T inf = T(0);
             if (k >= 1) {   // partials: per axis (MX of iteration k-1, read above), per warp (T3 above)
@@ -2108,36 +2147,6 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                     }
                     __syncwarp();
                     SGSF_PT(13);
-                    {   // ||A xi - b||_inf over this axis' new rows: E[robot][c6] = B6[c6] . C_robot - rhs
-                        double eacc[MT][2];
-#pragma unroll
-                        for (int mt = 0; mt < MT; ++mt) {
-                            const int rob = 8 * mt + fr;
-#pragma unroll
-                            for (int e = 0; e < 2; ++e) {
-                                const int c6 = 2 * fc + e;
-                                eacc[mt][e] = (rob < n && c6 < 6) ? -rhs[(rb + rob) * 6 + c6] : 0.0;
-                            }
-                        }
-#pragma unroll
-                        for (int kk = 0; kk < MP / 4; ++kk) {
-                            const int q = 4 * kk + fc;
-                            const double bv = fr < 6 ? B6[fr * MP + q] : 0.0;
-#pragma unroll
-                            for (int mt = 0; mt < MT; ++mt) {
-                                const int rob = 8 * mt + fr;
-                                const double a = rob < n ? Cnext[(rb + rob) * MP + q] : 0.0;
-                                dmma884(eacc[mt][0], eacc[mt][1], a, bv);
-                            }
-                        }
-                        double em = 0.0;
-#pragma unroll
-                        for (int mt = 0; mt < MT; ++mt) em = fmax(em, fmax(fabs(eacc[mt][0]), fabs(eacc[mt][1])));
-                        em = warp_max_nonneg(em);
-                        if (lane == 0) sp.eqerr[ax] = em;
-                    }
-                    __syncwarp();
-                    SGSF_PT(14);
                 }
                 prev_active = any_active;
             }
