@@ -50,7 +50,7 @@ extern "C" {
 #define SGSF_PRECISION_STRICT 1  /* FP64 everywhere */
 #define SGSF_PRECISION_HYBRID 2  /* FP32 screening with guard bands, FP64 targets/residuals/state and an FP64
                                     re-evaluation of the stop decision near tol_residual: the FP64 iteration
-                                    counts and verdicts at close to lean speed (n <= 32; n > 32 runs strict) */
+                                    counts and verdicts at close to lean speed (K1 and K1L) */
 
 typedef struct sgsf_handle_s sgsf_handle_t;
 

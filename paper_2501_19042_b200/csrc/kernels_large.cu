@@ -4,14 +4,15 @@
 
 namespace sgsf {
 
-template <typename T, int MP>
+template <typename T, int MP, bool HY = false>
 static int launch_large_t(const LaunchInfo& li, SolveParams& p, const sgsf_config_t* cfg, const sgsf_timing_t* timing,
                           cudaStream_t stream) {
-    auto kern = sf_large_kernel<T, 64, MP>;
+    auto kern = sf_large_kernel<T, 64, MP, HY>;
+    set_family_constants(p);
     int dev_smem = 0;
     cudaError_t e = cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, li.device);
     if (e != cudaSuccess) return internal_fail(SGSF_ERR_CUDA, cudaGetErrorString(e));
-    const LargeLayout L = make_large_layout<T, 64>(p.n, p.S, MP, p.want_prev);
+    const LargeLayout L = make_large_layout<T, 64>(p.n, p.S, MP, p.want_prev || HY);
     if (L.total > (size_t)dev_smem)
         return internal_fail(SGSF_ERR_UNSUPPORTED, "problem too large for one CTA: one sample needs " +
                                                        std::to_string(L.total / 1024) + " KB of shared memory, the device allows " +
@@ -45,6 +46,9 @@ static int launch_large_t(const LaunchInfo& li, SolveParams& p, const sgsf_confi
 int launch_large(const LaunchInfo& li, SolveParams& p, const sgsf_config_t* cfg, const sgsf_timing_t* timing,
                  cudaStream_t stream, bool strict) {
     const bool wide = p.m1 > 12;
+    if (cfg->precision == SGSF_PRECISION_HYBRID)
+        return wide ? launch_large_t<float, 16, true>(li, p, cfg, timing, stream)
+                    : launch_large_t<float, 12, true>(li, p, cfg, timing, stream);
     if (strict)
         return wide ? launch_large_t<double, 16>(li, p, cfg, timing, stream)
                     : launch_large_t<double, 12>(li, p, cfg, timing, stream);

@@ -44,7 +44,7 @@ struct LargeShared {
 
 struct LargeLayout {
     size_t W, KMm, KMd, cconst, B6, rhs, PBt;
-    size_t C, Cp, lam, U, xb, g, Cf, Cfo, scr, winf, wsq, eqerr, srmin, scum, sflag, snear, sncnt, sh;
+    size_t C, Cp, lam, U, xb, g, Cf, Cfo, scr, winf, wsq, winf64, eqerr, srmin, scum, sflag, snear, sncnt, sh;
     size_t total;
 };
 
@@ -72,6 +72,7 @@ __host__ __device__ inline LargeLayout make_large_layout(int n, int S, int MP, i
     L.scr = o;    o = align16(o + (size_t)kLargeWarps * 2 * 3 * NB * ts);
     L.winf = o;   o = align16(o + (size_t)kLargeWarps * ts);
     L.wsq = o;    o = align16(o + (size_t)kLargeWarps * d);
+    L.winf64 = o; o = align16(o + (size_t)kLargeWarps * d);   // hybrid: FP64 per-warp exit-residual maxima
     L.eqerr = o;  o = align16(o + (size_t)4 * d);
     L.srmin = o;  o = align16(o + (size_t)S * ts);   // per step: min normalised pair distance at the last exact pass
     L.scum = o;   o = align16(o + (size_t)S * ts);   // ... pair motion bound accumulated since
@@ -115,11 +116,100 @@ __device__ __forceinline__ void exact_term(const T (&dn)[3], const T (&dd)[3], c
     }
 }
 
-template <typename T, int NB, int MP>
+// Hybrid precision (HY, as K1's): the FP32 term pass screens with narrowed interior limits; the scattered
+// residual of every term it does not call interior is recomputed from FP64 positions of the FP64 C (and
+// rounded once into the lane's FP32 accumulators); the stop decision re-evaluates the whole exit residual in
+// FP64 when the FP32-measured one lies within hy_delta of tol_res.
+// FP64 scattered residual d - e(d) of one term (j < 0: the workspace term of robot i), positions from the
+// FP64 coefficients; out of line with explicit scalars (the cold path of the hybrid term pass)
+template <int MP>
+__device__ __noinline__ D3 large_term_r64(const double* __restrict__ C, const double* __restrict__ Wrow, int m1,
+                                         int n, int i, int j, double cx, double cy, double cz,
+                                         const Family<double> f) {
+    D3 d;
+    if (j >= 0) {
+        d.x = pos64s<MP>(C, Wrow, m1, i) - pos64s<MP>(C, Wrow, m1, j);
+        d.y = pos64s<MP>(C, Wrow, m1, n + i) - pos64s<MP>(C, Wrow, m1, n + j);
+        d.z = pos64s<MP>(C, Wrow, m1, 2 * n + i) - pos64s<MP>(C, Wrow, m1, 2 * n + j);
+    } else {
+        d.x = pos64s<MP>(C, Wrow, m1, i) - cx;
+        d.y = pos64s<MP>(C, Wrow, m1, n + i) - cy;
+        d.z = pos64s<MP>(C, Wrow, m1, 2 * n + i) - cz;
+    }
+    return resid64(j >= 0, d, d, f);
+}
+
+struct LargeExitArgs {   // by value: a non-inlined callee must not take the kernel's parameter block by reference
+    const double* W;
+    int n, S, m1;
+    double cx, cy, cz;
+    Family<double> fp, fw;
+};
+template <int MP>
+__device__ __noinline__ double2 large_exit64(const LargeExitArgs p, const double* __restrict__ C,
+                                             const double* __restrict__ Cp, int warp, int lane) {
+    // every term of this warp's steps, both iterates' FP64 positions: the lane holds robots lane and lane + 32,
+    // partners come by warp broadcast (warp-uniform j loop); each pair counted once (i < j)
+    const int n = p.n, S = p.S, m1 = p.m1;
+    const Family<double>& fp = p.fp;
+    const Family<double>& fw = p.fw;
+    double mx = 0.0, s2 = 0.0;
+    for (int t = warp; t < S; t += kLargeWarps) {
+        const double* Wrow = p.W + (size_t)t * m1;
+        double pn[2][3], po[2][3];
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+            const int i = lane + 32 * rr;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                pn[rr][a] = i < n ? pos64s<MP>(C, Wrow, m1, a * n + i) : 0.0;
+                po[rr][a] = i < n ? pos64s<MP>(Cp, Wrow, m1, a * n + i) : 0.0;
+            }
+        }
+        for (int j = 0; j < n; ++j) {
+            const int src = j & 31, sj = j >> 5;
+            double qn[3], qo[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                qn[a] = __shfl_sync(0xffffffffu, sj ? pn[1][a] : pn[0][a], src);
+                qo[a] = __shfl_sync(0xffffffffu, sj ? po[1][a] : po[0][a], src);
+            }
+#pragma unroll
+            for (int rr = 0; rr < 2; ++rr) {
+                const int i = lane + 32 * rr;
+                if (i < n && i < j) {
+                    const D3 dn{pn[rr][0] - qn[0], pn[rr][1] - qn[1], pn[rr][2] - qn[2]};
+                    const D3 dol{po[rr][0] - qo[0], po[rr][1] - qo[1], po[rr][2] - qo[2]};
+                    const D3 x = resid64(true, dol, dn, fp);
+                    mx = fmax(mx, fmax(fabs(x.x), fmax(fabs(x.y), fabs(x.z))));
+                    s2 = fma(x.x, x.x, fma(x.y, x.y, fma(x.z, x.z, s2)));
+                }
+            }
+        }
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+            const int i = lane + 32 * rr;
+            if (i < n) {
+                const D3 dn{pn[rr][0] - p.cx, pn[rr][1] - p.cy, pn[rr][2] - p.cz};
+                const D3 dol{po[rr][0] - p.cx, po[rr][1] - p.cy, po[rr][2] - p.cz};
+                const D3 x = resid64(false, dol, dn, fw);
+                mx = fmax(mx, fmax(fabs(x.x), fmax(fabs(x.y), fabs(x.z))));
+                s2 = fma(x.x, x.x, fma(x.y, x.y, fma(x.z, x.z, s2)));
+            }
+        }
+    }
+    mx = warp_max_nonneg(mx);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, off);
+    return make_double2(mx, s2);
+}
+
+template <typename T, int NB, int MP, bool HY = false>
 __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const SolveParams p) {
     static_assert(NB == 64, "K1L is laid out for 64 robots (lane l owns robots l and l + 32)");
+    static_assert(!HY || sizeof(T) == 4, "hybrid precision screens in FP32");
     extern __shared__ __align__(16) unsigned char smem[];
-    const LargeLayout L = make_large_layout<T, NB>(p.n, p.S, MP, p.want_prev);
+    const LargeLayout L = make_large_layout<T, NB>(p.n, p.S, MP, p.want_prev || HY);
     constexpr int M2P = 2 * MP;
     constexpr int MT = NB / 8;   // 8-robot DMMA tiles
     constexpr int KT = MP / 2;   // 4-column k-steps over [C | u]
@@ -145,6 +235,7 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
     T* Cfo = (T*)(smem + L.Cfo);
     T* winf = (T*)(smem + L.winf);
     double* wsq = (double*)(smem + L.wsq);
+    double* winf64 = (double*)(smem + L.winf64);
     double* eqerr = (double*)(smem + L.eqerr);
     T* srmin = (T*)(smem + L.srmin);
     T* scum = (T*)(smem + L.scum);
@@ -180,8 +271,12 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
     }
     __syncthreads();
 
-    const Family<T> fp = make_family<T>(p.lat, p.vert);
-    const Family<T> fw = make_family<T>(p.ws_lat, p.ws_vert);
+    Family<T> fp = make_family<T>(p.lat, p.vert);
+    Family<T> fw = make_family<T>(p.ws_lat, p.ws_vert);
+    if constexpr (HY) {   // guard bands: a term the FP32 test calls interior is interior in FP64
+        fp.lim = (T)p.hy_fp_lim_f;
+        fw.lim = (T)p.hy_fw_lim_f;
+    }
     const T cen[3] = {(T)p.cx, (T)p.cy, (T)p.cz};
     const double inv_n = 1.0 / n;
     const T inv_lat = T(1) / fp.lat;
@@ -234,7 +329,7 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
                 C[idx] = c[q];
                 lam[idx] = l[q];
                 g[idx] = 0.0;
-                if (p.want_prev) Cp[idx] = c[q];
+                if (p.want_prev || HY) Cp[idx] = c[q];
                 Cf[(ax * MP + q) * NB + i] = (T)c[q];
                 Cfo[(ax * MP + q) * NB + i] = (T)c[q];   // no previous iterate: "old" := "new"
             }
@@ -353,6 +448,15 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
                             dd[a] = fwd ? oi[a] - oj : oj - oi[a];
                         }
                         exact_term<T, true>(dn, dd, fp, r, x);
+                        if constexpr (HY) {   // a term not interior under the guarded FP32 test: R from FP64
+                            if (r[0] != T(0) || r[1] != T(0) || r[2] != T(0)) {
+                                const D3 r64 = large_term_r64<MP>(C, p.W + (size_t)t * m1, m1, n, fwd ? i : j, fwd ? j : i,
+                                                                  p.cx, p.cy, p.cz, family64(p, true));
+                                r[0] = (T)r64.x;
+                                r[1] = (T)r64.y;
+                                r[2] = (T)r64.z;
+                            }
+                        }
 #pragma unroll
                         for (int a = 0; a < 3; ++a) Ri[a] += fwd ? r[a] : -r[a];
                         if (fwd && count_exit) {
@@ -412,6 +516,15 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
                             dd[a] = oi[a] - cen[a];
                         }
                         exact_term<T, false>(dn, dd, fw, r, x);
+                        if constexpr (HY) {
+                            if (r[0] != T(0) || r[1] != T(0) || r[2] != T(0)) {
+                                const D3 r64 = large_term_r64<MP>(C, p.W + (size_t)t * m1, m1, n, i, -1, p.cx, p.cy, p.cz,
+                                                                  family64(p, false));
+                                r[0] = (T)r64.x;
+                                r[1] = (T)r64.y;
+                                r[2] = (T)r64.z;
+                            }
+                        }
 #pragma unroll
                         for (int a = 0; a < 3; ++a) {
                             Ri[a] += r[a];
@@ -519,13 +632,41 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
                     sqs += wsq[w];
                 }
             }
+            double infd = (double)inf;
+            if constexpr (HY) {   // near tol: the exit residual in FP64 (block-uniform: every thread read the same)
+                if (k >= 1 && p.early_stop && fabs(infd - p.tol_res) <= p.hy_delta) {
+                    LargeExitArgs xa;
+                    xa.W = p.W;
+                    xa.n = n;
+                    xa.S = S;
+                    xa.m1 = m1;
+                    xa.cx = p.cx;
+                    xa.cy = p.cy;
+                    xa.cz = p.cz;
+                    xa.fp = family64(p, true);
+                    xa.fw = family64(p, false);
+                    const double2 e = large_exit64<MP>(xa, C, Cp, warp, lane);
+                    __syncthreads();   // every thread has read winf / wsq
+                    if (lane == 0) {
+                        winf64[warp] = e.x;
+                        wsq[warp] = e.y;
+                    }
+                    __syncthreads();
+                    infd = 0.0;
+                    sqs = 0.0;
+                    for (int w = 0; w < kLargeWarps; ++w) {
+                        infd = fmax(infd, winf64[w]);
+                        sqs += wsq[w];
+                    }
+                }
+            }
             const bool failed = (k >= 1) && (emax > p.tol_eq);
             bool done = failed;
             if (k >= 1) {
-                done = done || (p.early_stop && (double)inf <= p.tol_res) || (k >= p.max_iters);
+                done = done || (p.early_stop && infd <= p.tol_res) || (k >= p.max_iters);
                 if (tid == 0) {
                     const size_t hix = (size_t)sample * p.max_iters + (k - 1);
-                    p.res_inf[hix] = (double)inf;
+                    p.res_inf[hix] = infd;
                     p.res_l2[hix] = sqrt(sqs);
                 }
             }
@@ -550,7 +691,7 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
                     for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
                     if (lane == 0) {
                         p.iterations[sample] = failed ? 0 : k;
-                        p.converged[sample] = (!failed && (double)inf <= p.tol_res) ? 1 : 0;
+                        p.converged[sample] = (!failed && infd <= p.tol_res) ? 1 : 0;
                         p.displacement[sample] = failed ? CUDART_NAN : sqrt(acc);
                         p.status[sample] = failed ? SAMPLE_SINGULAR_KKT : SAMPLE_OK;
                         p.eq_err[sample] = emax;
@@ -634,7 +775,7 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
                             dacc[mt][nt2][1] += dm[nt2][1];
                         }
                 }
-                if (p.want_prev) {
+                if (p.want_prev || HY) {
                     for (int e = lane; e < n * MP; e += 32) Cp[rb * MP + e] = C[rb * MP + e];
                 }
                 for (int e = lane; e < MP * NB; e += 32) Cfo[ax * MP * NB + e] = Cf[ax * MP * NB + e];

@@ -237,8 +237,7 @@ int sgsf_solve(sgsf_handle_t* h, int batch, const double* xi_bar, const double* 
     LaunchInfo li{h->device, h->sm_count};
     int rc = SGSF_OK;
     if (n > 32) {
-        // (K1L has no hybrid variant: hybrid runs it in FP64)
-        rc = launch_large(li, p, cfg, timing, stream, cfg->precision != SGSF_PRECISION_LEAN);
+        rc = launch_large(li, p, cfg, timing, stream, cfg->precision == SGSF_PRECISION_STRICT);
     } else {
 #define SGSF_PICK(T, NB, MAXT, TPS)                                                      \
     rc = wide ? launch_persistent<T, NB, 16, MAXT, TPS>(li, p, cfg, timing, stream) \
