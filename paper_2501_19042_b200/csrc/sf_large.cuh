@@ -553,18 +553,33 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
                     for (int off = 16; off > 0; off >>= 1) nsq += __shfl_xor_sync(0xffffffffu, nsq, off);
                     T far_max = qinf_p;
                     if (nmax >= qinf_p) {   // a near pair attains the quiet max: the far max, exactly
-                        T fm = T(0);
+                        // D p of every robot over the old-position scratch (dead for this step once the near
+                        // pairs are done), the same rounding as the quiet statistics
+                        T dpi[2][3];
 #pragma unroll
                         for (int rr = 0; rr < 2; ++rr) {
                             const int i = lane + 32 * rr;
-                            if (i >= n) continue;
-                            for (int j = i + 1; j < n; ++j) {
-                                if ((nmask[rr] >> j) & 1ull) continue;
 #pragma unroll
-                                for (int a = 0; a < 3; ++a)
-                                    fm = fmax(fm, fabs((sn[a * NB + i] - so[a * NB + i]) - (sn[a * NB + j] - so[a * NB + j])));
-                            }
+                            for (int a = 0; a < 3; ++a) dpi[rr][a] = sn[a * NB + i] - so[a * NB + i];
                         }
+                        __syncwarp();
+#pragma unroll
+                        for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+                            for (int a = 0; a < 3; ++a) so[a * NB + lane + 32 * rr] = dpi[rr][a];
+                        __syncwarp();
+                        // every unordered pair once, 63 per lane: robot lane takes partners lane+1 .. lane+32,
+                        // robot lane+32 takes lane+33 .. 63 and 0 .. lane-1
+                        T fm = T(0);
+                        auto visit = [&](int rr, int j) {
+                            const int i = lane + 32 * rr;
+                            if (i >= n || j >= n || ((nmask[rr] >> j) & 1ull)) return;
+#pragma unroll
+                            for (int a = 0; a < 3; ++a) fm = fmax(fm, fabs(dpi[rr][a] - so[a * NB + j]));
+                        };
+                        for (int j = lane + 1; j <= lane + 32; ++j) visit(0, j);
+                        for (int j = lane + 33; j < 64; ++j) visit(1, j);
+                        for (int j = 0; j < lane; ++j) visit(1, j);
                         far_max = warp_max_nonneg(fm);
                     }
                     if (lane == 0) {
