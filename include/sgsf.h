@@ -233,6 +233,10 @@ typedef struct {
 size_t sgsf_decoder_pack_bytes(int c0);
 /* h0: B x cz x L float (device): the latent (cz = c0 when feat is NULL); out: B x 3 nm1 double (device) */
 int sgsf_decoder_forward(const sgsf_decoder_t* dec, int batch, const float* h0, double* corr, void* stream);
+/* test entry point: as sgsf_decoder_forward, also writing each layer's activations (B x 4 x 128 x L floats) to
+   dbg, or with raw != 0 the first layer's three tap accumulators in slots 1..3 */
+int sgsf_decoder_forward_dbg(const sgsf_decoder_t* dec, int batch, const float* h0, double* corr, float* dbg,
+                             int raw, void* stream);
 /* FP32 FFMA throughput microbenchmark (roofline denominator); returns TFLOP/s in *tflops */
 int sgsf_fp32_peak(double* tflops, double* ms, void* stream);
 
