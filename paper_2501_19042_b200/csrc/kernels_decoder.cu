@@ -129,42 +129,41 @@ __global__ void __launch_bounds__(kThreads, 1) decoder_kernel(const DecParams p)
     int per_sample = 0;
     for (int l = 0; l < 4; ++l) per_sample += layer_stages(p, l);
     const int my_samples = p.batch > (int)blockIdx.x ? (p.batch - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-    const long long total = (long long)my_samples * per_sample;
-    auto stage_src = [&](long long g) { return p.wpack + (size_t)(g % per_sample) * kStageBytes; };
+    const int total = my_samples * per_sample;
+    auto stage_src = [&](int g) { return p.wpack + (size_t)(g % per_sample) * kStageBytes; };
     if (tid == 32) {   // producer: the first kBuf stages
-        for (long long g = 0; g < kBuf && g < total; ++g) {
+        for (int g = 0; g < kBuf && g < total; ++g) {
             mbar_expect_tx(&wready[g], kStageBytes);
             bulk_g2s(wbuf + g * kStageBytes, stage_src(g), kStageBytes, &wready[g]);
         }
     }
 
-    long long g = 0;   // global stage counter (same sequence in every role)
+    int g = 0;   // global stage counter (same sequence in every role)
     uint32_t layers_done = 0;
     for (int s = 0; s < my_samples; ++s) {
         const int b = (int)blockIdx.x + s * (int)gridDim.x;
-        // ---- the first layer's input: h0[b] -> rows 1..L, channels 0..c0-1 (c0..c0p-1 zero)
+        // ---- the first layer's input: h0[b] -> rows 1..L, channels 0..c0-1 (c0..c0p-1 zero).  One (4-channel
+        // chunk, position) per item: four loads coalesced over the positions, one 16-byte store each of hi / lo
+        // (consecutive lanes, consecutive rows: conflict-free)
         {
             const float* src = p.h0 + (size_t)b * p.cz * p.L;
-            const int n_in = p.cz * p.L, n_feat = p.c0 * p.L, n_all = p.c0p * p.L;
-            for (int e0 = tid; e0 < n_all; e0 += 4 * kThreads) {   // four independent loads in flight
+            const int items = (p.c0p >> 2) * p.L;
+            for (int it = tid; it < items; it += kThreads) {
+                const int g = it / p.L, t = it - g * p.L;
                 float v[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int e = e0 + u * kThreads;
-                    v[u] = e < n_in ? __ldg(src + e) : (e < n_feat ? __ldg(p.feat + (e / p.L - p.cz)) : 0.f);
+                for (int k = 0; k < 4; ++k) {
+                    const int c = 4 * g + k;
+                    v[k] = c < p.cz ? __ldg(src + c * p.L + t) : (c < p.c0 ? __ldg(p.feat + (c - p.cz)) : 0.f);
                 }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int e = e0 + u * kThreads;
-                    if (e < n_all) {
-                        const int c = e / p.L, t = e - c * p.L;
-                        float hi, lo;
-                        split_tf32(v[u], hi, lo);
-                        const int off = (c >> 2) * CH + (t + 1) * 16 + (c & 3) * 4;
-                        *(float*)(act_hi + off) = hi;
-                        *(float*)(act_lo + off) = lo;
-                    }
-                }
+                float4 hi, lo;
+                split_tf32(v[0], hi.x, lo.x);
+                split_tf32(v[1], hi.y, lo.y);
+                split_tf32(v[2], hi.z, lo.z);
+                split_tf32(v[3], hi.w, lo.w);
+                const int off = g * CH + (t + 1) * 16;
+                *(float4*)(act_hi + off) = hi;
+                *(float4*)(act_lo + off) = lo;
             }
         }
         tc::fence_proxy_async();
@@ -226,17 +225,18 @@ __global__ void __launch_bounds__(kThreads, 1) decoder_kernel(const DecParams p)
                     tc::mbar_wait(ldone, layers_done & 1u);
                     ++layers_done;
                     tc::fence_after_sync();
-                    const int c = tid;   // TMEM lane = output channel
+                    const int c = tid, lane = tid & 31;   // TMEM lane = output channel
                     const float bias = p.bias[l * 128 + c];
                     const float slope = p.leaky ? p.slope : 0.f;
                     const uint32_t lrow = tbase + ((uint32_t)(32 * warp) << 16);
+                    float v1[16], v2[16];   // P_1, P_2 at columns t0 .. t0 + 15 (carried over from the last chunk)
+                    tc::tmem_ld16(lrow + AS, v1);
+                    tc::tmem_ld16(lrow + 2 * AS, v2);
                     for (int t0 = 0; t0 < p.L; t0 += 16) {
                         // out[t] = P_0[t] + P_1[t + 1] + P_2[t + 2] (rows = positions + 1)
-                        float v0[16], v1[16], v1n[16], v2[16], v2n[16];
+                        float v0[16], v1n[16], v2n[16];
                         tc::tmem_ld16(lrow + t0, v0);
-                        tc::tmem_ld16(lrow + AS + t0, v1);
                         tc::tmem_ld16(lrow + AS + t0 + 16, v1n);
-                        tc::tmem_ld16(lrow + 2 * AS + t0, v2);
                         tc::tmem_ld16(lrow + 2 * AS + t0 + 16, v2n);
                         tc::tmem_wait_ld();
                         if (p.dbg && p.dbg_raw && l == 0) {
@@ -248,21 +248,44 @@ __global__ void __launch_bounds__(kThreads, 1) decoder_kernel(const DecParams p)
                                     p.dbg[(((size_t)b * 4 + 3) * 128 + c) * p.L + t0 + u] = v2[u];
                                 }
                         }
+                        uint32_t yh[16], yl[16];   // positions past L are zero (the next layer's padding rows)
+                        const int valid = p.L - t0;
 #pragma unroll
                         for (int u = 0; u < 16; ++u) {
-                            const int t = t0 + u;
-                            if (t < p.L) {
-                                const float a1 = u + 1 < 16 ? v1[u + 1] : v1n[u + 1 - 16];
-                                const float a2 = u + 2 < 16 ? v2[u + 2] : v2n[u + 2 - 16];
-                                float y = ((v0[u] + a1) + a2) + bias;
-                                y = y > 0.f ? y : slope * y;
-                                float hi, lo;
-                                split_tf32(y, hi, lo);
-                                const int off = (c >> 2) * CH + (t + 1) * 16 + (c & 3) * 4;
-                                *(float*)(act_hi + off) = hi;
-                                *(float*)(act_lo + off) = lo;
-                                if (p.dbg && !(p.dbg_raw && l > 0)) p.dbg[(((size_t)b * 4 + l) * 128 + c) * p.L + t] = y;
-                            }
+                            const float a1 = u + 1 < 16 ? v1[u + 1] : v1n[u + 1 - 16];
+                            const float a2 = u + 2 < 16 ? v2[u + 2] : v2n[u + 2 - 16];
+                            float y = ((v0[u] + a1) + a2) + bias;
+                            y = y > 0.f ? y : slope * y;
+                            y = u < valid ? y : 0.f;
+                            float hi, lo;
+                            split_tf32(y, hi, lo);
+                            yh[u] = __float_as_uint(hi);
+                            yl[u] = __float_as_uint(lo);
+                        }
+                        if (p.dbg && !(p.dbg_raw && l > 0)) {
+#pragma unroll
+                            for (int u = 0; u < 16; ++u)
+                                if (u < valid)
+                                    p.dbg[(((size_t)b * 4 + l) * 128 + c) * p.L + t0 + u] =
+                                        __uint_as_float(yh[u]) + __uint_as_float(yl[u]);
+                        }
+#pragma unroll
+                        for (int u = 0; u < 16; ++u) {
+                            v1[u] = v1n[u];
+                            v2[u] = v2n[u];
+                        }
+                        // stmatrix.x4: matrix m = position t0 + 4 q + m, its row r = chunk 8 warp + r (16 bytes:
+                        // channels of lanes 4 r .. 4 r + 3).  Lane i addresses row i % 8 of matrix i / 8.
+                        const int mrow = lane & 7, mmat = lane >> 3;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const int t = t0 + 4 * q + mmat;
+                            const int row = t < p.L ? t + 1 : p.nrows - 1;   // (a zero padding row)
+                            const uint32_t off = (uint32_t)((8 * warp + mrow) * CH + row * 16);
+                            tc::stmatrix_x4(tc::smem_u32(act_hi + off), yh[4 * q], yh[4 * q + 1], yh[4 * q + 2],
+                                            yh[4 * q + 3]);
+                            tc::stmatrix_x4(tc::smem_u32(act_lo + off), yl[4 * q], yl[4 * q + 1], yl[4 * q + 2],
+                                            yl[4 * q + 3]);
                         }
                     }
                     tc::fence_proxy_async();
@@ -272,64 +295,24 @@ __global__ void __launch_bounds__(kThreads, 1) decoder_kernel(const DecParams p)
                 }
             }
         }
-        // ---- head (1x1, 128 -> 3) over the positions, then the expansion L -> n m1 per axis
-        for (int t = tid; t < p.L; t += kThreads) {
+        // ---- head (1x1, 128 -> 3) over the positions -> h (3 x L floats), parked in the sample's output row
+        // (3 n m1 doubles, read back by decoder_tail_kernel before it writes the row)
+        float* hout = (float*)(p.corr + (size_t)b * 3 * p.nm1);
+        for (int t = tid; t < p.L; t += kThreads) {   // 16-byte reads: consecutive lanes, consecutive rows
             float h[3] = {p.head_b[0], p.head_b[1], p.head_b[2]};
-            for (int c = 0; c < 128; ++c) {
-                const int off = (c >> 2) * CH + (t + 1) * 16 + (c & 3) * 4;
-                const float x = *(const float*)(act_hi + off) + *(const float*)(act_lo + off);
+            for (int g4 = 0; g4 < 32; ++g4) {
+                const float4 xh = *(const float4*)(act_hi + g4 * CH + (t + 1) * 16);
+                const float4 xl = *(const float4*)(act_lo + g4 * CH + (t + 1) * 16);
+                const float x[4] = {xh.x + xl.x, xh.y + xl.y, xh.z + xl.z, xh.w + xl.w};
 #pragma unroll
-                for (int ax = 0; ax < 3; ++ax) h[ax] = fmaf(hw_s[ax * 128 + c], x, h[ax]);
+                for (int k = 0; k < 4; ++k)
+#pragma unroll
+                    for (int ax = 0; ax < 3; ++ax) h[ax] = fmaf(hw_s[ax * 128 + 4 * g4 + k], x[k], h[ax]);
             }
 #pragma unroll
-            for (int ax = 0; ax < 3; ++ax) hbuf[ax * p.L + t] = h[ax];
+            for (int ax = 0; ax < 3; ++ax) hout[ax * p.L + t] = h[ax];
         }
-        __syncthreads();
-        for (int j = tid; j < p.nm1; j += kThreads) {   // exp_w is L x nm1 (transposed): coalesced rows
-            const float eb = __ldg(p.exp_b + j);
-            float a0 = eb, a1 = eb, a2 = eb;
-            for (int t = 0; t < p.L; ++t) {
-                const float e = __ldg(p.exp_w + (size_t)t * p.nm1 + j);
-                a0 = fmaf(e, hbuf[t], a0);
-                a1 = fmaf(e, hbuf[p.L + t], a1);
-                a2 = fmaf(e, hbuf[2 * p.L + t], a2);
-            }
-            if (p.base) {   // xi' = straight line + correction, kept in shared memory for the QP layer below
-                double* xs = (double*)act_lo;   // (free: the head has read the last activations)
-                xs[j] = p.base[j] + (double)(p.scale * a0);
-                xs[p.nm1 + j] = p.base[p.nm1 + j] + (double)(p.scale * a1);
-                xs[2 * p.nm1 + j] = p.base[2 * p.nm1 + j] + (double)(p.scale * a2);
-            } else {
-                double* o = p.corr + (size_t)b * 3 * p.nm1 + j;
-                o[0] = (double)(p.scale * a0);
-                o[p.nm1] = (double)(p.scale * a1);
-                o[2 * p.nm1] = (double)(p.scale * a2);
-            }
-        }
-        if (p.base) {   // the boundary QP layer (projection.py:11-25): C - PBt (B6 C - rhs), per robot and axis
-            __syncthreads();
-            const double* xs = (const double*)act_lo;
-            for (int r = tid; r < 3 * p.n; r += kThreads) {
-                const double* c = xs + r * p.m1;
-                double res[6];
-#pragma unroll
-                for (int k = 0; k < 6; ++k) {
-                    double e = 0.0;
-                    for (int q = 0; q < p.m1; ++q) e = fma(p.B6[k * p.m1 + q], c[q], e);
-                    res[k] = e - p.rhs[r * 6 + k];
-                }
-                double* o = p.corr + (size_t)b * 3 * p.nm1 + r * p.m1;
-                for (int q = 0; q < p.m1; ++q) {
-                    double corr = 0.0;
-#pragma unroll
-                    for (int k = 0; k < 6; ++k) corr = fma(p.PBt[q * 6 + k], res[k], corr);
-                    o[q] = c[q] - corr;
-                }
-            }
-            __syncthreads();   // restore the zero padding rows the scratch covered
-            for (int i = tid; i < 3 * p.nm1 * 2; i += kThreads) ((uint32_t*)act_lo)[i] = 0u;
-        }
-        __syncthreads();   // hbuf and the activation buffers are rewritten by the next sample
+        __syncthreads();   // the activation buffers are rewritten by the next sample
     }
     tc::fence_before_sync();
     __syncthreads();
@@ -337,6 +320,83 @@ __global__ void __launch_bounds__(kThreads, 1) decoder_kernel(const DecParams p)
     if (warp == 0) tc::tmem_dealloc(tbase, tcols);
 }
 
+
+// ---- the expansion L -> n m1 per axis (+ the boundary QP layer) for S samples per CTA, so that each exp_w element
+// is read once per S samples: reads h (3 x L floats) from the front of each sample's output row, writes the row.
+template <int S>
+__global__ void __launch_bounds__(256) decoder_tail_kernel(const DecParams p) {
+    extern __shared__ __align__(16) unsigned char tsm[];
+    const int L = p.L, nm1 = p.nm1, tid = threadIdx.x;
+    float* hs = (float*)tsm;                                                   // S x 3 x L
+    double* xs = (double*)(tsm + (((size_t)S * 3 * L * 4 + 15) & ~(size_t)15));   // S x 3 nm1
+    double* res = xs + (size_t)S * 3 * nm1;                                    // S x 3 n x 6
+    const int b0 = blockIdx.x * S, ns = min(S, p.batch - b0);
+    for (int i = tid; i < S * 3 * L; i += blockDim.x) {
+        const int s = i / (3 * L), k = i - s * 3 * L;
+        hs[i] = s < ns ? ((const float*)(p.corr + (size_t)(b0 + s) * 3 * nm1))[k] : 0.f;
+    }
+    __syncthreads();
+    for (int j = tid; j < nm1; j += blockDim.x) {   // exp_w is L x nm1 (transposed): coalesced rows
+        const float eb = __ldg(p.exp_b + j);
+        float a[S][3];
+#pragma unroll
+        for (int s = 0; s < S; ++s) a[s][0] = a[s][1] = a[s][2] = eb;
+#pragma unroll 10
+        for (int t = 0; t < L; ++t) {
+            const float e = __ldg(p.exp_w + (size_t)t * nm1 + j);
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+#pragma unroll
+                for (int ax = 0; ax < 3; ++ax) a[s][ax] = fmaf(e, hs[(s * 3 + ax) * L + t], a[s][ax]);
+        }
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            if (s >= ns) break;
+#pragma unroll
+            for (int ax = 0; ax < 3; ++ax) {
+                const double v = (double)(p.scale * a[s][ax]);
+                if (p.base)   // xi' = straight line + correction, for the QP layer below
+                    xs[((size_t)s * 3 + ax) * nm1 + j] = p.base[(size_t)ax * nm1 + j] + v;
+                else
+                    p.corr[(size_t)(b0 + s) * 3 * nm1 + (size_t)ax * nm1 + j] = v;
+            }
+        }
+    }
+    if (!p.base) return;
+    // the boundary QP layer (projection.py:11-25): C - PBt (B6 C - rhs), per robot and axis
+    __syncthreads();
+    const int R6 = 3 * p.n * 6;
+    for (int i = tid; i < ns * R6; i += blockDim.x) {
+        const int s = i / R6, e = i - s * R6, r = e / 6, k = e - 6 * r;
+        const double* cr = xs + (size_t)s * 3 * nm1 + r * p.m1;
+        double acc = 0.0;
+        for (int q = 0; q < p.m1; ++q) acc = fma(__ldg(p.B6 + k * p.m1 + q), cr[q], acc);
+        res[i] = acc - __ldg(p.rhs + e);
+    }
+    __syncthreads();
+    for (int i = tid; i < ns * 3 * nm1; i += blockDim.x) {   // (sample, r, q): coalesced output rows
+        const int s = i / (3 * nm1), e = i - s * 3 * nm1, r = e / p.m1, q = e - r * p.m1;
+        double corr = 0.0;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) corr = fma(__ldg(p.PBt + q * 6 + k), res[s * R6 + r * 6 + k], corr);
+        p.corr[(size_t)(b0 + s) * 3 * nm1 + e] = xs[i] - corr;
+    }
+}
+
+template <int S>
+size_t tail_smem(const DecParams& p) {
+    return (((size_t)S * 3 * p.L * 4 + 15) & ~(size_t)15) + (size_t)S * 3 * p.nm1 * 8 +
+           (p.base ? (size_t)S * 3 * p.n * 6 * 8 : 0);
+}
+
+template <int S>
+cudaError_t launch_tail(const DecParams& p, cudaStream_t stream) {
+    const size_t smem = tail_smem<S>(p);
+    cudaError_t e = cudaFuncSetAttribute(decoder_tail_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    decoder_tail_kernel<S><<<(p.batch + S - 1) / S, 256, smem, stream>>>(p);
+    return cudaGetLastError();
+}
 }  // namespace
 
 extern "C" {
@@ -379,6 +439,8 @@ int sgsf_decoder_forward_dbg(const sgsf_decoder_t* d, int batch, const float* h0
     p.rhs = d->rhs;
     p.n = d->n;
     p.m1 = d->m1;
+    if (d->L > 2 * d->nm1)
+        return internal_fail(SGSF_ERR_UNSUPPORTED, "decoder: 3 L floats must fit in a sample's 3 n m1 doubles");
     if (p.base && (!p.B6 || !p.PBt || !p.rhs || p.n * p.m1 != p.nm1))
         return internal_fail(SGSF_ERR_INVALID, "decoder QP layer: B6, PBt, rhs and n m1 = nm1 required");
     p.wpack = (const uint8_t*)d->wpack;
@@ -402,6 +464,18 @@ int sgsf_decoder_forward_dbg(const sgsf_decoder_t* d, int batch, const float* h0
     internal_count_launch(1);
     e = cudaGetLastError();
     if (e != cudaSuccess) return internal_fail(SGSF_ERR_CUDA, std::string("decoder launch: ") + cudaGetErrorString(e));
+    // the expansion (+ QP) kernel: up to 8 samples per CTA (each exp_w element read once per CTA), at least
+    // about one CTA per SM, within 200 KB of shared memory
+    if (tail_smem<8>(p) <= 200 * 1024 && batch >= 8 * sms)
+        e = launch_tail<8>(p, (cudaStream_t)stream);
+    else if (tail_smem<4>(p) <= 200 * 1024 && batch >= 4 * sms / 2)
+        e = launch_tail<4>(p, (cudaStream_t)stream);
+    else if (tail_smem<2>(p) <= 200 * 1024)
+        e = launch_tail<2>(p, (cudaStream_t)stream);
+    else
+        e = launch_tail<1>(p, (cudaStream_t)stream);
+    internal_count_launch(1);
+    if (e != cudaSuccess) return internal_fail(SGSF_ERR_CUDA, std::string("decoder tail launch: ") + cudaGetErrorString(e));
     return SGSF_OK;
 }
 

@@ -55,6 +55,10 @@ int launch_persistent(const LaunchInfo& li, SolveParams& p, const sgsf_config_t*
                       : sf_persistent_kernel<T, NB, MP, MAXT, TPS, true>;
         }
     }
+    {
+        const char* nc = std::getenv("SGSF_NO_COOP");
+        p.coop = !(nc && nc[0] == '1');
+    }
     int spb = cfg->slots_per_block;
     if (spb <= 0) {
         spb = 0;

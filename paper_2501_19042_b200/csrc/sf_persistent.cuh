@@ -56,12 +56,13 @@ enum { SAMPLE_OK = 0, SAMPLE_SINGULAR_KKT = 1 };
 struct SmemLayout {
     size_t W, KMm, KMd, cconst, B6, rhs, ptab, tmem;
     size_t slot0, slot_stride;
-    size_t C, Cp, lam, U, xb, eqerr, psq, pex, P0, P1, Cf, pinf, sh, sc;
+    size_t C, Cp, lam, U, xb, eqerr, psq, pex, P0, P1, Cf, pinf, sh, sc, cp;
     size_t total;
 };
 
 struct SolveParams {
     int n, S, m1, MP, batch, max_iters, early_stop, want_prev, spb, wps;
+    int coop;   // HY, NB <= 4: warp-cooperative careful path (hy_careful_item); 0 = serial (SGSF_NO_COOP=1, tests)
     double rho, tol_res, tol_eq;
     // hybrid precision (HY kernels): FP32 screening with guard bands, FP64 values.  hy_delta = half-width of
     // the band around tol_res in which the FP32-measured exit residual is re-evaluated in FP64
@@ -206,6 +207,8 @@ __host__ __device__ inline SmemLayout make_layout(int n, int S, int MP, int spb,
     L.Cf = q;     q = align16(q + (tc ? (size_t)kTcBopBytes : (size_t)3 * MP * NB * ts));
     L.pinf = q;   q = align16(q + pw * ts);                            // per warp max of the inf partials
     L.sh = q;     q = align16(q + sizeof(SlotShared));
+    // hy, NB <= 4: per warp 32 items of the warp-cooperative careful path (hy_careful_item)
+    L.cp = q;     q = align16(q + ((hy && NB <= 4 && !tc) ? (size_t)((S + 31) / 32) * 32 * 8 * d : 0));
 #ifdef SGSF_SYNC_CHECK
     L.sc = q;     q = align16(q + pw * sizeof(int));                   // debug: per-warp decisions
 #else
@@ -220,6 +223,7 @@ struct SlotPtrs {
     double *C, *Cp, *lam, *U, *xb, *eqerr, *psq, *pex;
     void *P0, *P1, *Cf, *pinf;
     SlotShared* sh;
+    double* cp;
 };
 
 __device__ __forceinline__ SlotPtrs slot_ptrs(unsigned char* smem, const SmemLayout& L, int s) {
@@ -238,6 +242,7 @@ __device__ __forceinline__ SlotPtrs slot_ptrs(unsigned char* smem, const SmemLay
     P.Cf = (void*)(b + L.Cf);
     P.pinf = (void*)(b + L.pinf);
     P.sh = (SlotShared*)(b + L.sh);
+    P.cp = (double*)(b + L.cp);
     return P;
 }
 
@@ -668,6 +673,47 @@ __device__ __forceinline__ D3 resid64(bool pair, const D3& d, const D3& b, const
     return r;
 }
 
+// Warp-cooperative careful path (HY, NB <= 4).  A careful time step (a term with an exactly-zero component
+// now or at the previous iterate: FP64 reference trig targets, ~1.6K cycles each) is owned by one lane; a
+// symmetric scenario has few such steps -- the fixed endpoints -- and their owners would run every term's
+// FP64 positions and trig serially (with the position arrays spilled: ~13K cycles per step at n = 4, measured
+// with SGSF_CAREFUL_CLOCK) while the warp waits.  Instead the warp spreads the (careful lane, term) items over
+// its lanes: item (k, b) computes, for the k-th careful lane's step, term b's FP64 exit residual x = d_k -
+// e(d_{k-1}), its scattered residual r = d_k - e(d_k) and its flags exactly as hy_step_full does (same
+// positions, same resid64) into out[0..6]; the owner then reduces its items in term order (hy_step_coop).
+// Bit-identical to hy_step_full by construction.
+constexpr int kCoopItem = 8;   // doubles per item: x (3), r (3), flags (1: not interior or zero, 2: zero)
+template <int NB, int MP>
+__device__ __forceinline__ void hy_careful_item(const SolveParams& p, const double* Cn, const double* Co, int t, int b,
+                                                double* __restrict__ out) {
+    constexpr int NP = NB * (NB - 1) / 2;
+    int i = 0, j = -1;
+    if (b < NP) {
+        int r = b;
+        for (i = 0; i < NB; ++i) {
+            if (r < NB - 1 - i) break;
+            r -= NB - 1 - i;
+        }
+        j = i + 1 + r;
+        if (j >= p.n) return;
+    } else {
+        i = b - NP;
+        if (i >= p.n) return;
+    }
+    double w[MP];
+    w64_row<MP>(p.W, t, p.m1, w);
+    const D3 d = term_diff64<MP>(p, Cn, w, i, j), o = term_diff64<MP>(p, Co, w, i, j);
+    const bool pair = j >= 0;
+    const Family<double> f = family64(p, pair);
+    const D3 x = resid64(pair, o, d, f), r = resid64(pair, d, d, f);
+    const double q = fma(d.z * f.beta, d.z, fma(d.y, d.y, d.x * d.x));
+    const bool zero = d.x == 0.0 || d.y == 0.0 || d.z == 0.0;
+    const bool off = pair ? !(q >= f.lim) : !(q <= f.lim);
+    out[0] = x.x, out[1] = x.y, out[2] = x.z;
+    out[3] = r.x, out[4] = r.y, out[5] = r.z;
+    out[6] = (double)(((off || zero) ? 1 : 0) | (zero ? 2 : 0));
+}
+
 // streamed variants (the W row through the read-only cache; pos64's order of operations)
 template <int MP>
 __device__ __forceinline__ double pos64s(const double* __restrict__ C, const double* __restrict__ Wrow, int m1,
@@ -812,6 +858,64 @@ __device__ __forceinline__ HyStepOut<T, NB, MP> hy_step_full(const SolveParams& 
     return r;
 }
 
+
+// The owner's half of the cooperative careful path: hy_step_full's reductions over its step's items, in
+// hy_step_full's term order (same max, same FMA chain, same R sums).
+template <typename T, int NB, int MP>
+__device__ __forceinline__ HyStepOut<T, NB, MP> hy_step_coop(const double* __restrict__ it, int n, T* Rrow,
+                                                         MaskPack<NB>* nmo) {
+    double R[3 * NB];
+#pragma unroll
+    for (int q = 0; q < 3 * NB; ++q) R[q] = 0.0;
+    MaskPack<NB> nmw;
+#pragma unroll
+    for (int u = 0; u < TermBits<NB>::words; ++u) nmw.w[u] = 0xffffffffu;
+    double mx = 0.0, s2 = 0.0;
+    bool znow = false, act = false;
+    int b = 0;
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+#pragma unroll
+        for (int j = i + 1; j < NB; ++j, ++b) {
+            if (j >= n) continue;
+            const double* e = it + kCoopItem * b;
+            mx = fmax(mx, fmax(fabs(e[0]), fmax(fabs(e[1]), fabs(e[2]))));
+            s2 = fma(e[0], e[0], fma(e[1], e[1], fma(e[2], e[2], s2)));
+            R[i] += e[3], R[NB + i] += e[4], R[2 * NB + i] += e[5];
+            R[j] -= e[3], R[NB + j] -= e[4], R[2 * NB + j] -= e[5];
+            const int fl = (int)e[6];
+            znow = znow || (fl & 2);
+            if (fl & 1) {
+                nmw.w[b >> 5] &= ~(1u << (b & 31));
+                act = true;
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < NB; ++i, ++b) {
+        if (i >= n) continue;
+        const double* e = it + kCoopItem * b;
+        mx = fmax(mx, fmax(fabs(e[0]), fmax(fabs(e[1]), fabs(e[2]))));
+        s2 = fma(e[0], e[0], fma(e[1], e[1], fma(e[2], e[2], s2)));
+        R[i] += e[3], R[NB + i] += e[4], R[2 * NB + i] += e[5];
+        const int fl = (int)e[6];
+        znow = znow || (fl & 2);
+        if (fl & 1) {
+            nmw.w[b >> 5] &= ~(1u << (b & 31));
+            act = true;
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 3 * NB; ++q)
+        if ((q % NB) < n) Rrow[q] = (T)R[q];
+    *nmo = nmw;
+    HyStepOut<T, NB, MP> r;
+    r.inf = mx;
+    r.sq = s2;
+    r.zero = znow;
+    r.active = act;
+    return r;
+}
 
 // Flagged terms (active now or at the previous iterate) of one time step,
 // O(#flagged): true exit residual, scatter of d - e for terms active now,
@@ -1285,7 +1389,8 @@ __device__ __forceinline__ Partials<T> finish_step(const SolveParams& p, const S
                                             const T* __restrict__ Prow_new, T qinf, T qsq,
                                             uint32_t (&nm)[TermBits<NB>::words],
                                             T zmin, uint32_t (&imask)[TermBits<NB>::words], bool& zprev,
-                                            const Family<T>& fp, const Family<T>& fw, T cx, T cy, T cz) {
+                                            const Family<T>& fp, const Family<T>& fw, T cx, T cy, T cz,
+                                            const double* pre = nullptr) {
     constexpr int NW = TermBits<NB>::words;
     T inf = qinf, sq = qsq;
     bool active = false;
@@ -1294,7 +1399,19 @@ __device__ __forceinline__ Partials<T> finish_step(const SolveParams& p, const S
         SGSF_COUNT(3, 1);
         if constexpr (HY) {   // careful path from FP64 positions of both iterates
             MaskPack<NB> mo;
-            const HyStepOut<T, NB, MP> co = hy_step_full<T, NB, MP>(p, Ck, Ckm1, lt, Prow_old, &mo);
+#ifdef SGSF_CAREFUL_CLOCK
+            const long long hc0 = clock64();
+#endif
+            HyStepOut<T, NB, MP> co;
+            if constexpr (NB <= 4) {   // (the cooperative path exists for NB <= 4 only)
+                co = pre ? hy_step_coop<T, NB, MP>(pre, n, Prow_old, &mo)
+                         : hy_step_full<T, NB, MP>(p, Ck, Ckm1, lt, Prow_old, &mo);
+            } else {
+                co = hy_step_full<T, NB, MP>(p, Ck, Ckm1, lt, Prow_old, &mo);
+            }
+#ifdef SGSF_CAREFUL_CLOCK
+            if (blockIdx.x == 0 && lt < 64) printf("HC step %d hy_step_full %lld\n", lt, clock64() - hc0);
+#endif
 #pragma unroll
             for (int w = 0; w < NW; ++w) nm[w] = mo.w[w];
             inf = (T)co.inf;
@@ -1784,9 +1901,36 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
             SGSF_PT(6);
             // ---------------- T3: every time step finishes (quiet / flagged / careful path), by its owner lane
             Partials<T> pr{T(0), T(0)};
+            const double* pre = nullptr;
+#ifdef SGSF_CAREFUL_CLOCK
+            const long long cc0 = clock64();
+#endif
+            if constexpr (HY && NB <= 4 && TPS == 1 && !TC) {   // careful steps: spread their trig over the warp
+                constexpr int NT = NB * (NB - 1) / 2 + NB;
+                const bool car = ts < S && (fmin(zmin_ws, zmin_pairs) == T(0) || zprev);
+                const uint32_t bal = __ballot_sync(0xffffffffu, car);
+                const int nc = __popc(bal);
+                if (nc != 0 && nc * NT <= 32 && p.coop) {
+                    double* scr = sp.cp + (size_t)lwarp * 32 * kCoopItem;
+                    const int kk = lane / NT, bb = lane - kk * NT;
+                    const int src = kk < nc ? (int)__fns(bal, 0, kk + 1) : 0;
+                    const int tsrc = __shfl_sync(0xffffffffu, ts, src);
+                    if (kk < nc) hy_careful_item<NB, MP>(p, Ccur, Cprv, tsrc, bb, scr + kCoopItem * lane);
+                    __syncwarp();
+                    if (car) pre = scr + kCoopItem * NT * __popc(bal & ((1u << lane) - 1u));
+                }
+            }
+#ifdef SGSF_CAREFUL_CLOCK
+            const long long cc1 = clock64();
+            const bool was_careful = ts < S && (fmin(zmin_ws, zmin_pairs) == T(0) || zprev);
+#endif
             if (ts < S && owner)
                 pr = finish_step<T, NB, MP, HY>(p, sp, Ccur, Cprv, ptab, ts, n, par, Prow_old, Prow_new, qinf, qsq, nm, fmin(zmin_ws, zmin_pairs),
-                                        imask, zprev, fp, fw, cx, cy, cz);
+                                        imask, zprev, fp, fw, cx, cy, cz, pre);
+#ifdef SGSF_CAREFUL_CLOCK
+            if (blockIdx.x == 0 && slot == 0 && k < 6 && was_careful)
+                printf("CC k %d step %d coop %lld finish %lld pre %d\n", k, ts, cc1 - cc0, clock64() - cc1, pre != nullptr);
+#endif
             {   // per-warp exit-residual partials for the decision (fixed order: deterministic); the l2
                 // partial is summed over the warp in T (FP32 lean: the history is an l2 norm, checked to
                 // 1e-3) and across the warps in FP64

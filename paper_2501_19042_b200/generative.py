@@ -251,7 +251,7 @@ def decode_proposals(sf, decoder: nn.Module, latent: torch.Tensor, fused: "Fused
     through the boundary QP layer (projection.py:11-25).  With ``fused`` (a :class:`FusedDecoder` of the same
     decoder) the correction comes from the sm_100a decoder kernel K4 instead of the PyTorch module."""
     k = device_constants_of(sf, latent.device)
-    state, base = k["context"].to(torch.float32), k["base"]
+    state, base = k["context32"], k["base"]   # (one tensor per filter: the decoder's state-feature cache key)
     st = state.expand(latent.shape[0], -1, -1)
     if fused is not None:   # decoder + QP layer in one kernel
         return fused(latent, st, qp=k)

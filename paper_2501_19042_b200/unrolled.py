@@ -79,6 +79,7 @@ def device_constants_of(sf, device) -> dict:
             "base": torch.as_tensor(straight_line_coeffs(sf.problem, sf.basis), **f64),
             "context": torch.as_tensor(context_features(sf.problem), **f64),
         }
+        cache[key]["context32"] = cache[key]["context"].to(torch.float32)   # (the decoders' input dtype)
     return cache[key]
 
 

@@ -1,0 +1,58 @@
+"""The warp-cooperative careful path (hybrid precision, n <= 4: the FP64 reference-trig terms of the few
+careful time steps -- the fixed endpoints of symmetric scenarios -- spread over the warp's lanes,
+sf_persistent.cuh hy_careful_item / hy_step_coop) gives the serial path's results bit for bit."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _solve(sf, xb, cfg, coop: bool):
+    old = os.environ.get("SGSF_NO_COOP")
+    os.environ["SGSF_NO_COOP"] = "0" if coop else "1"
+    try:
+        out = sf.solve_batched(xb, config=cfg)
+        torch.cuda.synchronize()
+    finally:
+        if old is None:
+            del os.environ["SGSF_NO_COOP"]
+        else:
+            os.environ["SGSF_NO_COOP"] = old
+    return out
+
+
+@pytest.mark.parametrize("batch,seed", [(8, 0), (64, 3)])
+def test_cooperative_careful_path_is_bitwise_the_serial_one(batch, seed):
+    from paper_2501_19042_b200 import SafetyFilter, SolverConfig, sample_proposals
+    from paper_2501_19042_b200.scenarios import config_problem
+    prob = config_problem(1)   # 4 robots crossing at one altitude: every endpoint step is careful
+    cfg = SolverConfig(max_iters=100, svars=False, precision="hybrid")
+    sf = SafetyFilter(prob, degree=10, config=cfg)
+    xb = torch.from_numpy(sample_proposals(prob, sf.basis, batch, seed=seed).proposals).cuda()
+    a, b = _solve(sf, xb, cfg, True), _solve(sf, xb, cfg, False)
+    for k in ("coeffs", "iterations", "converged", "residual_inf", "residual_l2", "multipliers", "feasible", "status"):
+        ta, tb = getattr(a, k), getattr(b, k)
+        if ta is None:
+            continue
+        assert torch.equal(ta, tb), k
+    assert (a.status == 0).all()
+
+
+def test_cooperative_careful_path_on_the_reference_goldens():
+    """crossing4_cfg1 (the real reference's output, n = 4, symmetric): identical counts, coefficients to the
+    hybrid parity tolerance, with the cooperative path taken."""
+    from paper_2501_19042_b200 import SafetyFilter, SolverConfig, load_problem
+
+    from .conftest import load_golden
+    case = load_golden("crossing4_cfg1")
+    meta = case["meta"]
+    cfg = SolverConfig(precision="hybrid", svars=False, **meta["config"])
+    sf = SafetyFilter(load_problem(meta["problem"]), degree=meta["degree"], config=cfg)
+    xb = torch.from_numpy(np.ascontiguousarray(case["proposals"], dtype=np.float64)).cuda()
+    out = _solve(sf, xb, cfg, True)
+    assert out.iterations.cpu().numpy().tolist() == case["iterations"].astype(int).tolist()
+    err = np.abs(out.coeffs.cpu().numpy() - case["coeffs"]).max() / max(1.0, np.abs(case["coeffs"]).max())
+    assert err <= 1e-6
