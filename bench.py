@@ -16,9 +16,13 @@ re-evaluation of the stop decision near tol -- the precision whose iteration cou
 reference's on all 1000 headline samples (tests/test_gpu_batch_parity.py).  At N = 1 the line also carries
 device-timed numbers of "lean" (FP32 terms) and "strict" (FP64 everywhere) from the same run.
 
-`value` is device-timed (CUDA events, inputs resident in HBM, a 256 MB write flushes L2 between steps, max
-over ranks); `e2e` is the same metric through the public API with pinned host buffers, the H2D copy of the
-proposals and the D2H copy of every per-sample output inside the timed region.  At N = 1 two more end-to-end
+`value` is device-timed (CUDA events, inputs resident in HBM, max over ranks) over K batches submitted with
+two in flight (`SafetyFilter.solve_pipelined`: the next batch starts on the SMs the previous batch's tail
+frees); `pipelining.batch_latency_ms` times the same K batches one after another, and the roofline takes the
+kernel's per-launch time from that run.  The steps' inputs rotate over device copies of the batch totalling
+>= 256 MB (inputs larger than L2: no step finds its proposals cached).  `e2e` is the same metric through the
+public API with pinned host buffers, the H2D copy of the proposals and the D2H copy of every per-sample output
+of each batch on its own stream inside the timed region.  At N = 1 two more end-to-end
 numbers: `e2e_dropin` (the reference-compatible `SafetyFilter.batch_solve` on a list of numpy proposals at its
 defaults, plus `feasible_results`) and `pipeline` (config 2 as BASELINE states it: CVAE samples -> boundary QP
 -> init-network warm start -> SF -> verdict, all on the device).
@@ -309,8 +313,9 @@ def _timed(fn, reps: int = 1):
     return r, a.elapsed_time(b) / reps
 
 
-def side_precisions(sf, xb, cfg, flush, steps: int = 3) -> dict:
-    """Device-timed step of the other precisions on the same batch (N = 1 only)."""
+def side_precisions(sf, ring, cfg, steps: int = 3) -> dict:
+    """Device-timed step of the other precisions on the same batch (N = 1 only; one batch at a time, the
+    inputs rotating over the copies in `ring`)."""
     import torch
     from dataclasses import replace
     out = {}
@@ -318,11 +323,12 @@ def side_precisions(sf, xb, cfg, flush, steps: int = 3) -> dict:
         if prec == cfg.precision:
             continue
         c = replace(cfg, precision=prec)
+        xb = ring[0]
         sf.solve_batched(xb, config=c)
         torch.cuda.synchronize()
         step_ms, kern_ms, feas, its = [], [], 0, 0
         for k in range(steps):
-            flush.fill_(float(k))
+            xb = ring[(k + 1) % len(ring)]
             kev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
             o, ms = _timed(lambda: sf.solve_batched(xb, config=c, timing=kev))
             step_ms.append(ms)
@@ -412,7 +418,9 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     xb_host = torch.from_numpy(shard).pin_memory()
     xb = xb_host.to(dev)
     dim = xb.shape[1]
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # 256 MB > 126 MB L2
+    # inputs larger than L2 instead of a flush: the steps rotate over R device copies of the batch, >= 256 MB
+    # in all (2x the 126 MB L2), so no step finds its proposals L2-resident from an earlier step
+    ring = [xb] + [xb.clone() for _ in range(max(2, -(-256 * 2**20 // max(1, xb.numel() * 8))) - 1)]
     peak_tflops = ctypes_peak(native)
 
     def step(x, timing=None):
@@ -426,24 +434,50 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         clocks.__enter__()
     for _ in range(max(3, args.warmup)):
         step(xb)
+    # (and the two-in-flight submission: its side streams and their allocator pools, outside the timed region)
+    sf.solve_pipelined((ring[k % len(ring)] for k in range(max(4, args.warmup))), config=cfg,
+                       finish=(lambda k, out: gather_outputs(out, B)) if world > 1 else None)
     torch.cuda.synchronize()
     if clocks:
         clocks.wait_first()
 
-    # ---- device-timed region: inputs resident in HBM
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    # ---- device-timed region (the headline value): inputs resident in HBM, K batches with two in flight
+    # (SafetyFilter.solve_pipelined: batch k on side stream k % 2, so the next batch's CTAs start on the SMs
+    # the previous batch's tail frees); each batch is still its own launch with its own outputs
+    def gather(k, out):
+        if world > 1:
+            gather_outputs(out, B)
+
     launches0 = native.launch_count()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     if clocks:
         clocks.mark()
+    a0, b0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a0.record()
+    pouts = sf.solve_pipelined((ring[k % len(ring)] for k in range(args.steps)), config=cfg, finish=gather)
+    b0.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = native.launch_count() - launches0
+    pipe_ms = a0.elapsed_time(b0)
+    pfeas = sum(int(o.feasible.sum().item()) for o in pouts)
+    pits = sum(int(o.iterations.sum().item()) for o in pouts)
+    del pouts
+
+    # ---- the same K batches one after another (one stream): the per-batch latency and the per-launch
+    # kernel time of the roofline (the kernel alone on the GPU)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
     outs = []
     for k in range(args.steps):
-        flush.fill_(float(k))
         ev[k][0].record()
-        out, full = step(xb, timing=kev[k])
+        out, full = step(ring[k % len(ring)], timing=kev[k])
         ev[k][1].record()
         outs.append((out.feasible, out.iterations))   # the rest is freed: the next step reuses its blocks
         del out, full
@@ -454,47 +488,56 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         time.sleep(0.15)   # one more sample after the last step
         clocks.mark()
         clocks.__exit__()
-    launches = native.launch_count() - launches0
     step_ms = [a.elapsed_time(b) for a, b in ev]
     kern_ms = [a.elapsed_time(b) for a, b in kev]
     feas_counts = [int(f.sum().item()) for f, _ in outs]
     its_total = [int(i.sum().item()) for _, i in outs]
-    t = torch.tensor([sum(step_ms), float(sum(feas_counts)), float(sum(its_total))], dtype=torch.float64, device=dev)
+    if pfeas != sum(feas_counts) or pits != sum(its_total):
+        raise SystemExit(f"pipelined batches disagree with the sequential ones: {pfeas} vs {sum(feas_counts)} feasible")
+    t = torch.tensor([pipe_ms, sum(step_ms), float(pfeas), float(pits)], dtype=torch.float64, device=dev)
     if world > 1:
         tmax = t.clone()
-        dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
-        dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
-        total_ms_max = float(tmax[0])
+        dist.all_reduce(tmax[:2], op=dist.ReduceOp.MAX)
+        dist.all_reduce(t[2:], op=dist.ReduceOp.SUM)
+        total_ms_max, seq_ms_max = float(tmax[0]), float(tmax[1])
     else:
-        total_ms_max = float(t[0])
-    feas_all, its_all = float(t[1]), float(t[2])
+        total_ms_max, seq_ms_max = float(t[0]), float(t[1])
+    feas_all, its_all = float(t[2]), float(t[3])
     value = feas_all / (total_ms_max * 1e-3)
 
-    # ---- end to end through the public API: pinned host proposals in, every per-sample output out
-    host = {}
+    # ---- end to end through the public API: pinned host proposals in, every per-sample output out, the
+    # same two-in-flight submission (H2D, solve, D2H of batch k on its stream; no host sync between batches)
     probe, _ = step(xb)
+    host = [{}, {}]
     for k in GATHERED_FIELDS + ("eq_err",):
         v = getattr(probe, k, None)
         if v is not None:
-            host[k] = torch.empty(tuple(v.shape), dtype=v.dtype).pin_memory()
+            for hb in host:
+                hb[k] = torch.empty(tuple(v.shape), dtype=v.dtype).pin_memory()
     del probe
+
+    def h2d(k, _):
+        return xb_host.to(dev, non_blocking=True)
+
+    def d2h(k, out):
+        for key, h in host[k % 2].items():
+            h.copy_(getattr(out, key), non_blocking=True)
+
     e2e_ms = []
-    for k in range(args.steps + 1):
+    for rep in range(2):   # the first one is a warm-up
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        xd = xb_host.to(dev, non_blocking=True)
-        out = sf.solve_batched(xd, config=cfg)
-        for key, h in host.items():
-            h.copy_(getattr(out, key), non_blocking=True)
+        eo = sf.solve_pipelined(range(args.steps), config=cfg, prepare=h2d, finish=d2h)
         b.record()
         b.synchronize()
-        if k:   # the first one is a warm-up
+        del eo
+        if rep:
             e2e_ms.append(a.elapsed_time(b))
-    e2e_feas = int(host["feasible"].numpy().sum())
-    te = torch.tensor([sum(e2e_ms), float(e2e_feas * len(e2e_ms))], dtype=torch.float64, device=dev)
+    e2e_feas = int(host[(args.steps - 1) % 2]["feasible"].numpy().sum())
+    te = torch.tensor([sum(e2e_ms), float(e2e_feas * args.steps)], dtype=torch.float64, device=dev)
     if world > 1:
         temax = te.clone()
         dist.all_reduce(temax[:1], op=dist.ReduceOp.MAX)
@@ -502,8 +545,8 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         e2e_value = float(te[1]) / (float(temax[0]) * 1e-3)
     else:
         e2e_value = float(te[1]) / (float(te[0]) * 1e-3)
-    h2d = xb_host.numel() * 8
-    d2h = sum(h.numel() * h.element_size() for h in host.values())
+    h2d_bytes = xb_host.numel() * 8
+    d2h_bytes = sum(h.numel() * h.element_size() for h in host[0].values())
 
     if rank != 0:
         return
@@ -531,24 +574,31 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         "data": "synthetic (seeded scenario, reference Gaussian sampler proposals)",
         "config": {"workload": config_label(args.config, B, world), "n": n, "H": S - 1, "degree": 10,
                    "batch": B, "batch_per_gpu": int(xb.shape[0]), "max_iters": cfg.max_iters, "rho": 1.0,
-                   "precision": args.precision, "l2_flush": "256 MB write between steps",
+                   "precision": args.precision, "l2_flush": f"no flush kernel: inputs larger than L2 (the steps rotate over {len(ring)} device copies of the batch, {len(ring) * xb.numel() * 8 / 2**20:.0f} MB)",
                    "parallelism": f"dp{world} (contiguous sample shards"
                                   + (", NCCL all_gather of every per-sample output in the step)" if world > 1 else ")")},
         "ms_per_1k_batch": (total_ms_max / args.steps) * 1000.0 / B,
         "feasible_fraction": feas_all / (args.steps * B),
         "mean_iterations": its_all / (args.steps * B),
         "gpu_launches": int(round(launches / args.steps)),
-        "e2e": {"value": e2e_value, "unit": "feasible samples/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "outputs": sorted(host)},
+        "e2e": {"value": e2e_value, "unit": "feasible samples/s", "h2d_bytes_per_step": h2d_bytes,
+                "d2h_bytes_per_step": d2h_bytes, "outputs": sorted(host[0])},
+        "pipelining": {"batches_in_flight": 2, "batch_latency_ms": seq_ms_max / args.steps,
+                       "sequential_value": feas_all / (seq_ms_max * 1e-3),
+                       "note": "value / ms_per_step: the K batches submitted with two in flight "
+                               "(SafetyFilter.solve_pipelined); batch_latency_ms / sequential_value: the same "
+                               "K batches one after another; roofline: per-launch kernel time of the latter"},
         "roofline": {"bound": "fp32_cuda_core", "achieved": achieved, "peak": peak_tflops,
                      "unit": "TFLOP/s", "frac": achieved / peak_tflops if peak_tflops else None,
+                     # the same algorithmic FLOPs over the two-in-flight region (the tail's idle SMs filled)
+                     "frac_pipelined": (pits * fps / (pipe_ms * 1e-3) / 1e12) / peak_tflops if peak_tflops else None,
                      "traffic": traffic, "kernel": kname, "kernel_ms": kern_avg_ms, "flop_per_si": fps,
                      "peak_source": "FFMA microbenchmark (sgsf_fp32_peak) run live in this process; "
                                     "MEASURED_PEAKS.json has no FP32 figure"},
         "clocks": clocks.summary(local_rank) if clocks else None,
     }
     if world == 1 and not args.quick:
-        line["precisions"] = side_precisions(sf, xb, cfg, flush)
+        line["precisions"] = side_precisions(sf, ring, cfg)
         if args.config == 2:
             line["e2e_dropin"] = dropin_e2e(prob, shard)
             line["pipeline"] = pipeline_e2e(prob, int(xb.shape[0]))

@@ -372,6 +372,46 @@ class SafetyFilter:
             native.check(rc, "sgsf_solve")
         return out
 
+    def solve_pipelined(self, batches, config: SolverConfig | None = None, streams: int = 2, prepare=None,
+                        finish=None, **solve_kw) -> list:
+        """Filter a sequence of (B, dim) proposal batches with ``streams`` of them in flight.
+
+        Batch k is one :meth:`solve_batched` launch on side stream k % streams.  A batch's last samples
+        run on a few slots while most SMs idle (the tail); with two batches in flight the
+        next batch's CTAs start on the SMs the previous one frees.  Each batch keeps its own launch and
+        outputs, and a sample's result does not depend on scheduling, so the results equal
+        ``[solve_batched(x) for x in batches]`` bit for bit.  ``prepare(k, x) -> x`` and
+        ``finish(k, out)`` run on batch k's stream (host-to-device copies of the proposals in, copies of
+        the results out).  The caller's stream waits for every batch before this returns.
+        """
+        if streams < 1:
+            raise ValueError("streams must be >= 1")
+        cur = torch.cuda.current_stream()
+        key = (cur.device, streams)
+        side = self.__dict__.setdefault("_side_streams", {}).get(key)
+        if side is None:
+            side = self._side_streams[key] = [torch.cuda.Stream(device=cur.device) for _ in range(streams)]
+        for st in side:
+            st.wait_stream(cur)
+        outs = []
+        for k, x in enumerate(batches):
+            st = side[k % streams]
+            with torch.cuda.stream(st):
+                if prepare is not None:
+                    x = prepare(k, x)
+                if x.is_cuda:
+                    x.record_stream(st)
+                out = self.solve_batched(x, config=config, **solve_kw)
+                if finish is not None:
+                    finish(k, out)
+            for t in vars(out).values():   # consumed on the caller's stream: keep the blocks until it is done
+                if isinstance(t, torch.Tensor):
+                    t.record_stream(cur)
+            outs.append(out)
+        for st in side:
+            cur.wait_stream(st)
+        return outs
+
     def svars_of(self, coeffs: torch.Tensor) -> list:
         """Spherical variables of positions C W^T for each row (K2b), as SphericalVars."""
         B = int(coeffs.shape[0])

@@ -1,4 +1,4 @@
-"""(box) One fused decoder + QP launch at the config-2 size (for ncu -k regex:decoder_kernel)."""
+"""(box) Fused decoder + QP launches: python tools/dec_prof.py [config [cvae|vqvae [batch]]] (for ncu -k regex:decoder)."""
 import sys
 from pathlib import Path
 
@@ -10,11 +10,13 @@ from paper_2501_19042_b200.generative import FusedDecoder, calibrate_batchnorm, 
 from paper_2501_19042_b200.scenarios import config_problem  # noqa: E402
 
 prob = config_problem(int(sys.argv[1]) if len(sys.argv) > 1 else 2)
+kind = sys.argv[2] if len(sys.argv) > 2 else "cvae"
+B = int(sys.argv[3]) if len(sys.argv) > 3 else 1000
 sf = SafetyFilter(prob, config=SolverConfig(max_iters=50, svars=False))
 torch.manual_seed(0)
-dec = calibrate_batchnorm(sf, make_decoder("cvae", prob.n).cuda()).eval()
+dec = calibrate_batchnorm(sf, make_decoder(kind, prob.n).cuda()).eval()
 fused = FusedDecoder(dec)
-lat = dec.sample_latent(1000, torch.Generator(device="cuda").manual_seed(0), "cuda")
+lat = dec.sample_latent(B, torch.Generator(device="cuda").manual_seed(0), "cuda")
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 for _ in range(3):
     decode_proposals(sf, dec, lat, fused)
