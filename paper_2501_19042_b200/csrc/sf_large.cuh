@@ -341,8 +341,17 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
         if (tid == 0) sh->g_ticket = 0;
         __syncthreads();
 
+#ifdef SGSF_LARGE_PT
+        __shared__ long long lpt_dur[kLargeWarps];
+        __shared__ int lpt_ex[kLargeWarps];
+        double lpt_max = 0, lpt_mean = 0, lpt_exmax = 0, lpt_exmean = 0;
+#endif
         for (int k = 0;; ++k) {
             const int par = k & 1;
+#ifdef SGSF_LARGE_PT
+            const long long lpt0 = clock64();
+            int lpt_nex = 0;
+#endif
             if (tid == 0) sh->active[par ^ 1] = 0;   // last read before the previous closing barrier
             // ---------------- term pass
             T gacc[2][3][MP];
@@ -421,6 +430,9 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
                 // there) are provably interior now and were before; the near pairs are evaluated exactly
                 const bool quiet = k > 0 && ncnt >= 0 && sflag[t] != 0 && srmin[t] - cum_t > T(1) + T(1e-3);
                 if (lane == 0) SGSF_COUNT(quiet ? 6 : 5, 1);   // diagnostics: quiet / exact steps
+#ifdef SGSF_LARGE_PT
+                lpt_nex += quiet ? 0 : 1;
+#endif
                 const uint16_t* nl = snear + (size_t)t * kNearCap;
                 T farmin = T(1e30);    // exact pass: min q over the far pairs of this lane's robots
                 bool zfar = false;     // ... a zero component in a far pair
@@ -614,6 +626,12 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
             {
                 const bool wact = __any_sync(0xffffffffu, lact);
                 const int ticket = k * kLargeWarps + warp;
+#ifdef SGSF_LARGE_PT
+                if (lane == 0) {
+                    lpt_dur[warp] = clock64() - lpt0;
+                    lpt_ex[warp] = lpt_nex;
+                }
+#endif
                 if (lane == 0)
                     while (*(volatile int*)&sh->g_ticket != ticket) __nanosleep(32);
                 __syncwarp();
@@ -636,6 +654,22 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
                 if (lane == 0) *(volatile int*)&sh->g_ticket = ticket + 1;
             }
             __syncthreads();
+#ifdef SGSF_LARGE_PT
+            if (tid == 0) {
+                long long mx = 0, sm = 0;
+                int exm = 0, exs = 0;
+                for (int w = 0; w < kLargeWarps; ++w) {
+                    mx = max(mx, lpt_dur[w]);
+                    sm += lpt_dur[w];
+                    exm = max(exm, lpt_ex[w]);
+                    exs += lpt_ex[w];
+                }
+                lpt_max += (double)mx;
+                lpt_mean += (double)sm / kLargeWarps;
+                lpt_exmax += exm;
+                lpt_exmean += (double)exs / kLargeWarps;
+            }
+#endif
 
             // ---------------- decision (every thread): exit residual of iteration k-1, early stop, SingularKKT
             double emax = 0.0, sqs = 0.0;
@@ -710,6 +744,12 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
                         p.displacement[sample] = failed ? CUDART_NAN : sqrt(acc);
                         p.status[sample] = failed ? SAMPLE_SINGULAR_KKT : SAMPLE_OK;
                         p.eq_err[sample] = emax;
+#ifdef SGSF_LARGE_PT
+                        if (blockIdx.x < 4)
+                            printf("LPT cta %d sample %d iters %d term-pass cycles: slowest warp %.0f mean %.0f | exact steps per warp: max %.2f mean %.2f\n",
+                                   blockIdx.x, sample, k, lpt_max / (k + 1), lpt_mean / (k + 1), lpt_exmax / (k + 1), lpt_exmean / (k + 1));
+                        lpt_max = lpt_mean = lpt_exmax = lpt_exmean = 0;
+#endif
                         sh->sample = next_sample(p);
                         sh->active[0] = sh->active[1] = 0;
                     }

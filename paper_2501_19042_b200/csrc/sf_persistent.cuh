@@ -56,7 +56,7 @@ enum { SAMPLE_OK = 0, SAMPLE_SINGULAR_KKT = 1 };
 struct SmemLayout {
     size_t W, KMm, KMd, cconst, B6, rhs, ptab, tmem;
     size_t slot0, slot_stride;
-    size_t C, Cp, lam, U, xb, eqerr, psq, pex, P0, P1, Cf, pinf, sh, sc, cp;
+    size_t C, Cp, lam, U, xb, eqerr, psq, pex, P0, P1, Cf, pinf, sh, sc, cp, ct;
     size_t total;
 };
 
@@ -209,6 +209,9 @@ __host__ __device__ inline SmemLayout make_layout(int n, int S, int MP, int spb,
     L.sh = q;     q = align16(q + sizeof(SlotShared));
     // hy, NB <= 4: per warp 32 items of the warp-cooperative careful path (hy_careful_item)
     L.cp = q;     q = align16(q + ((hy && NB <= 4 && !tc) ? (size_t)((S + 31) / 32) * 32 * 8 * d : 0));
+    // ... and the FP64 trig targets e(d_k) of its zero-component terms per (step, term), tagged (sample, k): the
+    // next iteration's e(d_{k-1}) (hy_careful_item)
+    L.ct = q;     q = align16(q + ((hy && NB <= 4 && !tc) ? (size_t)S * (NB * (NB - 1) / 2 + NB) * (3 * d + 8) : 0));
 #ifdef SGSF_SYNC_CHECK
     L.sc = q;     q = align16(q + pw * sizeof(int));                   // debug: per-warp decisions
 #else
@@ -224,6 +227,7 @@ struct SlotPtrs {
     void *P0, *P1, *Cf, *pinf;
     SlotShared* sh;
     double* cp;
+    double* ct;
 };
 
 __device__ __forceinline__ SlotPtrs slot_ptrs(unsigned char* smem, const SmemLayout& L, int s) {
@@ -243,6 +247,7 @@ __device__ __forceinline__ SlotPtrs slot_ptrs(unsigned char* smem, const SmemLay
     P.pinf = (void*)(b + L.pinf);
     P.sh = (SlotShared*)(b + L.sh);
     P.cp = (double*)(b + L.cp);
+    P.ct = (double*)(b + L.ct);
     return P;
 }
 
@@ -682,10 +687,13 @@ __device__ __forceinline__ D3 resid64(bool pair, const D3& d, const D3& b, const
 // e(d_{k-1}), its scattered residual r = d_k - e(d_k) and its flags exactly as hy_step_full does (same
 // positions, same resid64) into out[0..6]; the owner then reduces its items in term order (hy_step_coop).
 // Bit-identical to hy_step_full by construction.
+__device__ __forceinline__ bool has_zero(const D3& d) { return d.x == 0.0 || d.y == 0.0 || d.z == 0.0; }
+// b - (a target computed earlier): resid's operation for a zero-component term
+__device__ __forceinline__ D3 minus(const D3& b, const double* __restrict__ t) { return D3{b.x - t[0], b.y - t[1], b.z - t[2]}; }
 constexpr int kCoopItem = 8;   // doubles per item: x (3), r (3), flags (1: not interior or zero, 2: zero)
 template <int NB, int MP>
 __device__ __forceinline__ void hy_careful_item(const SolveParams& p, const double* Cn, const double* Co, int t, int b,
-                                                double* __restrict__ out) {
+                                                double* __restrict__ out, double* __restrict__ ct, long long tag) {
     constexpr int NP = NB * (NB - 1) / 2;
     int i = 0, j = -1;
     if (b < NP) {
@@ -705,7 +713,24 @@ __device__ __forceinline__ void hy_careful_item(const SolveParams& p, const doub
     const D3 d = term_diff64<MP>(p, Cn, w, i, j), o = term_diff64<MP>(p, Co, w, i, j);
     const bool pair = j >= 0;
     const Family<double> f = family64(p, pair);
-    const D3 x = resid64(pair, o, d, f), r = resid64(pair, d, d, f);
+    // e(d_{k-1}) of a zero-component term is the e(d_k) this item stored one iteration earlier (the same FP64
+    // positions of the same C_{k-1}: the same bits); a trig target is computed once per iterate
+    constexpr int NT = NB * (NB - 1) / 2 + NB;
+    double* ce = ct + ((size_t)t * NT + b) * 3;
+    long long* cs = (long long*)(ct + (size_t)p.S * NT * 3) + (size_t)t * NT + b;
+    D3 x, r;
+    if (has_zero(o) && *cs == tag - 1) x = minus(d, ce);
+    else x = resid64(pair, o, d, f);
+    if (has_zero(d)) {
+        double e[3];
+        if (pair) target<double, true>(d.x, d.y, d.z, f, e[0], e[1], e[2]);
+        else target<double, false>(d.x, d.y, d.z, f, e[0], e[1], e[2]);
+        r = minus(d, e);
+        ce[0] = e[0], ce[1] = e[1], ce[2] = e[2];
+        *cs = tag;
+    } else {
+        r = resid64(pair, d, d, f);
+    }
     const double q = fma(d.z * f.beta, d.z, fma(d.y, d.y, d.x * d.x));
     const bool zero = d.x == 0.0 || d.y == 0.0 || d.z == 0.0;
     const bool off = pair ? !(q >= f.lim) : !(q <= f.lim);
@@ -1700,6 +1725,11 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
     const int r0 = h * RH;
     const bool owner = h == 0;
     const unsigned smask = __ballot_sync(0xffffffffu, ts < S);   // lanes of this warp with a step
+    if constexpr (HY && NB <= 4 && TPS == 1 && !TC) {   // careful-path target cache: no entry valid yet
+        constexpr int NT = NB * (NB - 1) / 2 + NB;
+        long long* tags = (long long*)(sp.ct + (size_t)S * NT * 3);
+        for (int e = lt; e < S * NT; e += gsize) tags[e] = -1;
+    }
 
     constexpr int NP = NB * (NB - 1) / 2;
     constexpr int NPW = (NP + 31) / 32;   // words holding pair bits
@@ -1915,7 +1945,9 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                     const int kk = lane / NT, bb = lane - kk * NT;
                     const int src = kk < nc ? (int)__fns(bal, 0, kk + 1) : 0;
                     const int tsrc = __shfl_sync(0xffffffffu, ts, src);
-                    if (kk < nc) hy_careful_item<NB, MP>(p, Ccur, Cprv, tsrc, bb, scr + kCoopItem * lane);
+                    if (kk < nc)
+                        hy_careful_item<NB, MP>(p, Ccur, Cprv, tsrc, bb, scr + kCoopItem * lane, sp.ct,
+                                                ((long long)sample << 32) | (unsigned)k);
                     __syncwarp();
                     if (car) pre = scr + kCoopItem * NT * __popc(bal & ((1u << lane) - 1u));
                 }
@@ -1997,6 +2029,9 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                 // is the one the FP64 iterates give
                 if (k >= 1 && p.early_stop && fabs(infd - p.tol_res) <= p.hy_delta) {
                     if (lt == 0) SGSF_COUNT(8, 1);
+#ifdef SGSF_HY_CLOCK
+                    const long long hyc0 = clock64();
+#endif
                     double xi = 0.0, xs = 0.0;
                     if (ts < S && owner) {
                         const double2 e = hy_exit64_inline<NB, MP>(p, Ccur, Cprv, ts, imask);
@@ -2018,6 +2053,9 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                         infd = fmax(infd, sp.pex[w]);
                         sqs += sp.pex[pw + w];
                     }
+#ifdef SGSF_HY_CLOCK
+                    if (lt == 0 && blockIdx.x < 2) printf("HYC cta %d slot %d k %d cycles %lld\n", blockIdx.x, slot, k, clock64() - hyc0);
+#endif
                 }
             }
             if (ts < S && owner) {   // interior bits of this iterate: the "old" ones of the next
