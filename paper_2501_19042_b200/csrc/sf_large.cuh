@@ -45,6 +45,7 @@ struct LargeShared {
 struct LargeLayout {
     size_t W, KMm, KMd, cconst, B6, rhs, PBt;
     size_t C, Cp, lam, U, xb, g, Cf, Cfo, scr, winf, wsq, winf64, eqerr, srmin, scum, sflag, snear, sncnt, sh;
+    size_t sdefer, xr, xnl, xcnt, xfm, xzf;   // the cooperative exact steps (phase B), double-buffered partials
     size_t total;
 };
 
@@ -80,6 +81,15 @@ __host__ __device__ inline LargeLayout make_large_layout(int n, int S, int MP, i
     L.snear = o;  o = align16(o + (size_t)S * kNearCap * 2);   // ... the near pairs (i | j << 8), i < j
     L.sncnt = o;  o = align16(o + (size_t)S * 4);    // ... how many (-1: none recorded / overflow)
     L.sh = o;     o = align16(o + sizeof(LargeShared));
+    // phase B (T = float: lean and hybrid; FP64 "strict" keeps the one-warp exact pass -- its buffers would
+    // not fit next to the FP64 state at H = 150)
+    const size_t pb = sizeof(T) == 4 ? 1 : 0;
+    L.sdefer = o; o = align16(o + pb * S * 4);    // per step: 1 = exact this iteration, taken by phase B
+    L.xr = o;     o = align16(o + pb * 2 * kLargeWarps * 2 * 32 * 3 * ts);   // [buf][warp][rr][lane][axis] R parts
+    L.xnl = o;    o = align16(o + pb * 2 * kLargeWarps * 2 * kNearCap * 2);  // [buf][warp][rr] near sublists
+    L.xcnt = o;   o = align16(o + pb * 2 * kLargeWarps * 2 * 4);             // ... their lengths
+    L.xfm = o;    o = align16(o + pb * 2 * kLargeWarps * ts);                // [buf][warp] min far q
+    L.xzf = o;    o = align16(o + pb * 2 * kLargeWarps * 4);                 // ... a far zero component
     L.total = o;
     return L;
 }
@@ -243,6 +253,13 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
     uint16_t* snear = (uint16_t*)(smem + L.snear);
     int* sncnt = (int*)(smem + L.sncnt);
     LargeShared* sh = (LargeShared*)(smem + L.sh);
+    constexpr bool kCoopExact = sizeof(T) == 4;   // phase B: exact steps taken by all warps together
+    int* sdefer = (int*)(smem + L.sdefer);
+    T* xr = (T*)(smem + L.xr);
+    uint16_t* xnl = (uint16_t*)(smem + L.xnl);
+    int* xcnt = (int*)(smem + L.xcnt);
+    T* xfm = (T*)(smem + L.xfm);
+    int* xzf = (int*)(smem + L.xzf);
 
     // shared constants (as K1), zero-padded to MP columns
     for (int i = tid; i < S * MP; i += nt) {
@@ -337,6 +354,7 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
         for (int t = tid; t < S; t += nt) {   // the first iterate takes the exact pass everywhere
             sflag[t] = 0;
             sncnt[t] = -1;
+            if (kCoopExact) sdefer[t] = 0;
         }
         if (tid == 0) sh->g_ticket = 0;
         __syncthreads();
@@ -344,13 +362,16 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
 #ifdef SGSF_LARGE_PT
         __shared__ long long lpt_dur[kLargeWarps];
         __shared__ int lpt_ex[kLargeWarps];
-        double lpt_max = 0, lpt_mean = 0, lpt_exmax = 0, lpt_exmean = 0;
+        __shared__ long long lpt_exq[kLargeWarps];
+        long long lqa[5] = {0, 0, 0, 0, 0};   // CTA 0 warp 0 quiet steps: positions, statistics, near pairs + ws, far
+        double lpt_max = 0, lpt_mean = 0, lpt_exmax = 0, lpt_exmean = 0, lpt_qmax = 0, lpt_excyc = 0;
 #endif
         for (int k = 0;; ++k) {
             const int par = k & 1;
 #ifdef SGSF_LARGE_PT
             const long long lpt0 = clock64();
             int lpt_nex = 0;
+            long long lpt_exc = 0;   // cycles in exact steps (phase B: all of it)
 #endif
             if (tid == 0) sh->active[par ^ 1] = 0;   // last read before the previous closing barrier
             // ---------------- term pass
@@ -365,6 +386,9 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
             double lsq = 0.0;
             bool lact = false;
             for (int t = warp; t < S; t += kLargeWarps) {
+#ifdef SGSF_LARGE_PT
+                const long long lq0 = clock64();
+#endif
                 T w[MP];
                 load_row16<T, MP>(Wt + t * MP, w);
 #pragma unroll
@@ -383,6 +407,9 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
                     }
                 }
                 __syncwarp();
+#ifdef SGSF_LARGE_PT
+                const long long lq1 = clock64();
+#endif
                 // O(n) statistics of the position change (lane: robots lane, lane + 32) and the pair
                 // motion bound: while rmin - cum > 1 + margin, every pair of this step is provably
                 // interior now, and if it was interior (and free of zero components) at the last exact
@@ -424,6 +451,9 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
                         s2[a] += __shfl_xor_sync(0xffffffffu, s2[a], off);
                     }
                 }
+#ifdef SGSF_LARGE_PT
+                const long long lq2 = clock64();
+#endif
                 const T cum_t = scum[t] + T(2) * sqrt(dmv) * inv_lat;
                 const int ncnt = sncnt[t];
                 // quiet: the far pairs (distance >= rmin >= skin at the last exact pass, no zero component
@@ -432,7 +462,13 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
                 if (lane == 0) SGSF_COUNT(quiet ? 6 : 5, 1);   // diagnostics: quiet / exact steps
 #ifdef SGSF_LARGE_PT
                 lpt_nex += quiet ? 0 : 1;
+                const long long lpt_s0 = clock64();
 #endif
+                if (kCoopExact && !quiet) {   // an exact step: all eight warps take it together below (phase B)
+                    if (lane == 0) sdefer[t] = 1;
+                    __syncwarp();   // the scratch is rewritten for the next step
+                    continue;
+                }
                 const uint16_t* nl = snear + (size_t)t * kNearCap;
                 T farmin = T(1e30);    // exact pass: min q over the far pairs of this lane's robots
                 bool zfar = false;     // ... a zero component in a far pair
@@ -481,9 +517,26 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
                         return fma_t<T>(dn[2] * fp.beta, dn[2], fma_t<T>(dn[1], dn[1], dn[0] * dn[0]));
                     };
                     if (quiet) {
-                        for (int e = 0; e < ncnt; ++e) {
+                        // the near pairs of robot i, in list order: a byte compare (__vcmpeq4 against i in every
+                        // byte) of 8 entries per 16-byte load marks the entries that name i, then one pass over
+                        // the marks (the per-entry test was ~3K cycles of a ~7K-cycle quiet step)
+                        uint64_t hits = 0ull;
+                        const uint32_t key = (uint32_t)i * 0x01010101u;
+                        for (int c8 = 0; iv && c8 < ncnt; c8 += 8) {
+                            const uint4 v = *reinterpret_cast<const uint4*>(nl + c8);
+                            const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                            for (int h = 0; h < 4; ++h) {
+                                const uint32_t mt = __vcmpeq4(w4[h], key);
+                                const uint64_t two = ((mt & 0xffffu) ? 1ull : 0ull) | ((mt >> 16) ? 2ull : 0ull);
+                                hits |= two << (c8 + 2 * h);
+                            }
+                        }
+                        if (ncnt < 64) hits &= (1ull << ncnt) - 1ull;
+                        while (hits) {
+                            const int e = __ffsll((long long)hits) - 1;
+                            hits &= hits - 1ull;
                             const int code = nl[e], pa = code & 0xff, pb = code >> 8;
-                            if (!iv || (pa != i && pb != i)) continue;
                             const int j = pa == i ? pb : pa;
                             nmask[rr] |= 1ull << j;
                             pair_exact(j, true);
@@ -552,6 +605,9 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
                             for (int q = 0; q < MP; ++q) gacc[rr][a][q] = fma_t<T>(Ri[a], w[q], gacc[rr][a][q]);
                     }
                 }
+#ifdef SGSF_LARGE_PT
+                const long long lq3 = clock64();
+#endif
                 if (quiet) {   // far pairs: the O(n) statistics without the near pairs' share
                     T qinf_p = T(0), qsq_p = T(0);
 #pragma unroll
@@ -610,6 +666,205 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
                     }
                 }
                 __syncwarp();   // the scratch is rewritten for the next step
+#ifdef SGSF_LARGE_PT
+                if (!quiet) lpt_exc += clock64() - lpt_s0;
+                if (quiet && blockIdx.x == 0 && warp == 0 && lane == 0) {
+                    lqa[0] += lq1 - lq0;
+                    lqa[1] += lq2 - lq1;
+                    lqa[2] += lq3 - lq2;
+                    lqa[3] += clock64() - lq3;
+                    lqa[4] += 1;
+                }
+#endif
+            }
+            // ---------------- phase B: the exact steps of this iteration, in ascending order, each taken by all
+            // eight warps at once (warp u: partners 8u .. 8u + 7 of every robot; warp 0 also the workspace
+            // terms).  A step's partial R rows, near sublists and far minima go to double-buffered shared
+            // memory; after a barrier warp e % 8 combines them in warp order (R into its g accumulators, the
+            // near list in the serial pass's (robot half, partner, lane) order) while the others start the
+            // next step.  An exact pass costs ~93K cycles on one warp, and an iteration has fewer of them than
+            // warps, so the serial pass left seven warps waiting.
+            if constexpr (kCoopExact) {
+                __syncthreads();   // every warp's deferred steps are marked
+#ifdef SGSF_LARGE_PT
+                const long long lpt_b0 = clock64();
+#endif
+                int e = 0;
+                for (int base = 0; base < S; base += 32) {
+                    uint32_t bal = __ballot_sync(0xffffffffu, base + lane < S && sdefer[base + lane] != 0);
+                    while (bal) {
+                        const int t = base + __ffs(bal) - 1;
+                        bal &= bal - 1;
+                        const int buf = e & 1;
+                        {   // this warp's partners of step t
+                            T w[MP];
+                            load_row16<T, MP>(Wt + t * MP, w);
+#pragma unroll
+                            for (int rr = 0; rr < 2; ++rr) {
+                                const int i = lane + 32 * rr;
+#pragma unroll
+                                for (int a = 0; a < 3; ++a) {
+                                    T pn = T(0), po = T(0);
+#pragma unroll
+                                    for (int q = 0; q < MP; ++q) {
+                                        pn = fma_t<T>(Cf[(a * MP + q) * NB + i], w[q], pn);
+                                        po = fma_t<T>(Cfo[(a * MP + q) * NB + i], w[q], po);
+                                    }
+                                    sn[a * NB + i] = pn;
+                                    so[a * NB + i] = po;
+                                }
+                            }
+                            __syncwarp();
+                            const int j0 = 8 * warp, j1 = min(j0 + 8, n);
+                            T farmin = T(1e30);
+                            bool zfar = false;
+#pragma unroll
+                            for (int rr = 0; rr < 2; ++rr) {
+                                const int i = lane + 32 * rr;
+                                const bool iv = i < n;
+                                T Ri[3] = {T(0), T(0), T(0)};
+                                T ni[3], oi[3];
+#pragma unroll
+                                for (int a = 0; a < 3; ++a) {
+                                    ni[a] = sn[a * NB + i];
+                                    oi[a] = so[a * NB + i];
+                                }
+                                int nb = 0;
+                                for (int j = j0; j < j1; ++j) {   // warp-uniform: the near sublist is built with ballots
+                                    bool is_near = false;
+                                    if (iv && j != i) {
+                                        const bool fwd = i < j;
+                                        T dn[3], dd[3], r[3], x[3];
+#pragma unroll
+                                        for (int a = 0; a < 3; ++a) {
+                                            const T nj = sn[a * NB + j], oj = so[a * NB + j];
+                                            dn[a] = fwd ? ni[a] - nj : nj - ni[a];
+                                            dd[a] = fwd ? oi[a] - oj : oj - oi[a];
+                                        }
+                                        exact_term<T, true>(dn, dd, fp, r, x);
+                                        if constexpr (HY) {   // not interior under the guarded FP32 test: R from FP64
+                                            if (r[0] != T(0) || r[1] != T(0) || r[2] != T(0)) {
+                                                const D3 r64 = large_term_r64<MP>(C, p.W + (size_t)t * m1, m1, n, fwd ? i : j,
+                                                                                  fwd ? j : i, p.cx, p.cy, p.cz, family64(p, true));
+                                                r[0] = (T)r64.x;
+                                                r[1] = (T)r64.y;
+                                                r[2] = (T)r64.z;
+                                            }
+                                        }
+#pragma unroll
+                                        for (int a = 0; a < 3; ++a) Ri[a] += fwd ? r[a] : -r[a];
+                                        if (fwd) {
+#pragma unroll
+                                            for (int a = 0; a < 3; ++a) {
+                                                linf = fmax(linf, fabs(x[a]));
+                                                lsq = fma((double)x[a], (double)x[a], lsq);
+                                            }
+                                        }
+                                        const T qn = fma_t<T>(dn[2] * fp.beta, dn[2], fma_t<T>(dn[1], dn[1], dn[0] * dn[0]));
+                                        const bool zero = (sn[j] == ni[0]) || (sn[NB + j] == ni[1]) || (sn[2 * NB + j] == ni[2]);
+                                        if (qn < skin_lim) {
+                                            is_near = i < j;
+                                        } else {
+                                            farmin = fmin(farmin, qn);
+                                            zfar = zfar || zero;
+                                        }
+                                    }
+                                    const uint32_t bm = __ballot_sync(0xffffffffu, is_near);
+                                    if (bm) {
+                                        const int pos = nb + __popc(bm & lanemask_lt);
+                                        if (is_near && pos < kNearCap)
+                                            xnl[((buf * kLargeWarps + warp) * 2 + rr) * kNearCap + pos] = (uint16_t)(i | (j << 8));
+                                        nb += __popc(bm);
+                                    }
+                                }
+                                if (warp == 0 && iv) {   // workspace term of robot i
+                                    T dn[3], dd[3], r[3], x[3];
+#pragma unroll
+                                    for (int a = 0; a < 3; ++a) {
+                                        dn[a] = ni[a] - cen[a];
+                                        dd[a] = oi[a] - cen[a];
+                                    }
+                                    exact_term<T, false>(dn, dd, fw, r, x);
+                                    if constexpr (HY) {
+                                        if (r[0] != T(0) || r[1] != T(0) || r[2] != T(0)) {
+                                            const D3 r64 = large_term_r64<MP>(C, p.W + (size_t)t * m1, m1, n, i, -1, p.cx, p.cy,
+                                                                              p.cz, family64(p, false));
+                                            r[0] = (T)r64.x;
+                                            r[1] = (T)r64.y;
+                                            r[2] = (T)r64.z;
+                                        }
+                                    }
+#pragma unroll
+                                    for (int a = 0; a < 3; ++a) {
+                                        Ri[a] += r[a];
+                                        linf = fmax(linf, fabs(x[a]));
+                                        lsq = fma((double)x[a], (double)x[a], lsq);
+                                    }
+                                }
+#pragma unroll
+                                for (int a = 0; a < 3; ++a)
+                                    xr[(((buf * kLargeWarps + warp) * 2 + rr) * 32 + lane) * 3 + a] = Ri[a];
+                                if (lane == 0) xcnt[(buf * kLargeWarps + warp) * 2 + rr] = nb;
+                            }
+                            const T qm = warp_min_nonneg(farmin);
+                            const bool zf = __any_sync(0xffffffffu, zfar);
+                            if (lane == 0) {
+                                xfm[buf * kLargeWarps + warp] = qm;
+                                xzf[buf * kLargeWarps + warp] = zf ? 1 : 0;
+                            }
+                            __syncwarp();   // the scratch is rewritten for the next step
+                        }
+                        __syncthreads();   // step t's partials are complete
+                        if (warp == (e & (kLargeWarps - 1))) {   // combine them, in warp order
+                            T w[MP];
+                            load_row16<T, MP>(Wt + t * MP, w);
+#pragma unroll
+                            for (int rr = 0; rr < 2; ++rr) {
+                                T Ri[3] = {T(0), T(0), T(0)};
+#pragma unroll
+                                for (int u = 0; u < kLargeWarps; ++u)
+#pragma unroll
+                                    for (int a = 0; a < 3; ++a) Ri[a] += xr[(((buf * kLargeWarps + u) * 2 + rr) * 32 + lane) * 3 + a];
+                                if (Ri[0] != T(0) || Ri[1] != T(0) || Ri[2] != T(0)) {
+                                    lact = true;
+#pragma unroll
+                                    for (int a = 0; a < 3; ++a)
+#pragma unroll
+                                        for (int q = 0; q < MP; ++q) gacc[rr][a][q] = fma_t<T>(Ri[a], w[q], gacc[rr][a][q]);
+                                }
+                            }
+                            int total = 0;   // the near list: (robot half, warp) sublists in order, up to kNearCap
+#pragma unroll
+                            for (int rr = 0; rr < 2; ++rr) {
+                                for (int u = 0; u < kLargeWarps; ++u) {
+                                    const int c = xcnt[(buf * kLargeWarps + u) * 2 + rr];
+                                    for (int q = lane; q < c && q < kNearCap; q += 32)
+                                        if (total + q < kNearCap)
+                                            snear[(size_t)t * kNearCap + total + q] =
+                                                xnl[((buf * kLargeWarps + u) * 2 + rr) * kNearCap + q];
+                                    total += c;
+                                }
+                            }
+                            T qm = T(1e30);
+                            int zf = 0;
+                            for (int u = 0; u < kLargeWarps; ++u) {
+                                qm = fmin(qm, xfm[buf * kLargeWarps + u]);
+                                zf |= xzf[buf * kLargeWarps + u];
+                            }
+                            if (lane == 0) {   // refresh the step's state from the exact pass
+                                srmin[t] = sqrt(qm) * inv_lat;
+                                scum[t] = T(0);
+                                sflag[t] = zf ? 0 : 1;
+                                sncnt[t] = total <= kNearCap ? total : -1;
+                                sdefer[t] = 0;
+                            }
+                        }
+                        ++e;
+                    }
+                }
+#ifdef SGSF_LARGE_PT
+                lpt_exc += clock64() - lpt_b0;
+#endif
             }
             // per-warp partials of the exit norm, fixed order
             {
@@ -630,6 +885,7 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
                 if (lane == 0) {
                     lpt_dur[warp] = clock64() - lpt0;
                     lpt_ex[warp] = lpt_nex;
+                    lpt_exq[warp] = lpt_exc;
                 }
 #endif
                 if (lane == 0)
@@ -656,14 +912,18 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
             __syncthreads();
 #ifdef SGSF_LARGE_PT
             if (tid == 0) {
-                long long mx = 0, sm = 0;
+                long long mx = 0, sm = 0, qm = 0, exc = 0;
                 int exm = 0, exs = 0;
                 for (int w = 0; w < kLargeWarps; ++w) {
                     mx = max(mx, lpt_dur[w]);
                     sm += lpt_dur[w];
                     exm = max(exm, lpt_ex[w]);
                     exs += lpt_ex[w];
+                    qm = max(qm, lpt_dur[w] - lpt_exq[w]);
+                    exc += lpt_exq[w];
                 }
+                lpt_qmax += (double)qm;
+                lpt_excyc += (double)exc;
                 lpt_max += (double)mx;
                 lpt_mean += (double)sm / kLargeWarps;
                 lpt_exmax += exm;
@@ -745,10 +1005,14 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
                         p.status[sample] = failed ? SAMPLE_SINGULAR_KKT : SAMPLE_OK;
                         p.eq_err[sample] = emax;
 #ifdef SGSF_LARGE_PT
+                        if (blockIdx.x == 0 && lqa[4])
+                            printf("LQ quiet steps %lld: positions %lld statistics %lld near+ws %lld far %lld cycles each\n", lqa[4],
+                                   lqa[0] / lqa[4], lqa[1] / lqa[4], lqa[2] / lqa[4], lqa[3] / lqa[4]);
                         if (blockIdx.x < 4)
-                            printf("LPT cta %d sample %d iters %d term-pass cycles: slowest warp %.0f mean %.0f | exact steps per warp: max %.2f mean %.2f\n",
-                                   blockIdx.x, sample, k, lpt_max / (k + 1), lpt_mean / (k + 1), lpt_exmax / (k + 1), lpt_exmean / (k + 1));
-                        lpt_max = lpt_mean = lpt_exmax = lpt_exmean = 0;
+                            printf("LPT cta %d sample %d iters %d term-pass cycles: slowest warp %.0f mean %.0f slowest-without-exact %.0f | exact steps per warp: max %.2f mean %.2f, exact-step cycles per iteration (all warps) %.0f\n",
+                                   blockIdx.x, sample, k, lpt_max / (k + 1), lpt_mean / (k + 1), lpt_qmax / (k + 1), lpt_exmax / (k + 1),
+                                   lpt_exmean / (k + 1), lpt_excyc / (k + 1));
+                        lpt_max = lpt_mean = lpt_exmax = lpt_exmean = lpt_qmax = lpt_excyc = 0;
 #endif
                         sh->sample = next_sample(p);
                         sh->active[0] = sh->active[1] = 0;
