@@ -45,7 +45,8 @@ struct LargeShared {
 struct LargeLayout {
     size_t W, KMm, KMd, cconst, B6, rhs, PBt;
     size_t C, Cp, lam, U, xb, g, Cf, Cfo, scr, winf, wsq, winf64, eqerr, srmin, scum, sflag, snear, sncnt, sh;
-    size_t sdefer, xr, xnl, xcnt, xfm, xzf;   // the cooperative exact steps (phase B), double-buffered partials
+    size_t sdefer, xr, xnl, xcnt, xfm, xzf;
+    size_t ner;   // per warp: the R of each near pair of the quiet step at hand (evaluated once per pair)   // the cooperative exact steps (phase B), double-buffered partials
     size_t total;
 };
 
@@ -71,6 +72,7 @@ __host__ __device__ inline LargeLayout make_large_layout(int n, int S, int MP, i
     L.Cf = o;     o = align16(o + (size_t)3 * MP * NB * ts);   // C of the current iterate, robot-minor
     L.Cfo = o;    o = align16(o + (size_t)3 * MP * NB * ts);   // ... of the previous iterate
     L.scr = o;    o = align16(o + (size_t)kLargeWarps * 2 * 3 * NB * ts);
+    L.ner = o;    o = align16(o + (size_t)kLargeWarps * kNearCap * 3 * ts);
     L.winf = o;   o = align16(o + (size_t)kLargeWarps * ts);
     L.wsq = o;    o = align16(o + (size_t)kLargeWarps * d);
     L.winf64 = o; o = align16(o + (size_t)kLargeWarps * d);   // hybrid: FP64 per-warp exit-residual maxima
@@ -301,6 +303,7 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
     const unsigned lanemask_lt = (1u << lane) - 1u;
     T* sn = (T*)(smem + L.scr) + warp * 2 * 3 * NB;   // this warp's positions at the step: new [3][NB] ...
     T* so = sn + 3 * NB;                              // ... and old [3][NB]
+    T* ner = (T*)(smem + L.ner) + warp * kNearCap * 3;   // this warp's near-pair R rows of the quiet step
     int sample = sh->sample;
     bool prev_active = false;
 
@@ -475,6 +478,42 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
                 int nbase = 0;         // ... near pairs recorded so far (warp-uniform)
                 T nq_sq = T(0), nq_max = T(0);   // quiet: near pairs' share of the O(n) statistics
                 uint64_t nmask[2] = {0ull, 0ull};  // quiet: near partners of this lane's robots
+                if (quiet) {   // every near pair once, lane e -> entry e: its R (kept for both robots), its exit
+                    // residual and its share of the O(n) statistics; the robots then add their pairs' R in list
+                    // order below (bitwise what the per-robot evaluation gave: the same d = p_min - p_max)
+                    for (int e = lane; e < ncnt; e += 32) {
+                        const int code = nl[e], pa = code & 0xff, pb = code >> 8;   // pa < pb
+                        T dn[3], dd[3], r[3], x[3];
+#pragma unroll
+                        for (int a = 0; a < 3; ++a) {
+                            dn[a] = sn[a * NB + pa] - sn[a * NB + pb];
+                            dd[a] = so[a * NB + pa] - so[a * NB + pb];
+                        }
+                        exact_term<T, true>(dn, dd, fp, r, x);
+                        if constexpr (HY) {   // not interior under the guarded FP32 test: R from FP64
+                            if (r[0] != T(0) || r[1] != T(0) || r[2] != T(0)) {
+                                const D3 r64 = large_term_r64<MP>(C, p.W + (size_t)t * m1, m1, n, pa, pb, p.cx, p.cy, p.cz,
+                                                                  family64(p, true));
+                                r[0] = (T)r64.x;
+                                r[1] = (T)r64.y;
+                                r[2] = (T)r64.z;
+                            }
+                        }
+                        T m = T(0), q2 = T(0);
+#pragma unroll
+                        for (int a = 0; a < 3; ++a) {
+                            ner[e * 3 + a] = r[a];
+                            linf = fmax(linf, fabs(x[a]));
+                            lsq = fma((double)x[a], (double)x[a], lsq);
+                            const T xq = (sn[a * NB + pa] - so[a * NB + pa]) - (sn[a * NB + pb] - so[a * NB + pb]);
+                            m = fmax(m, fabs(xq));
+                            q2 = fma_t<T>(xq, xq, q2);
+                        }
+                        nq_max = fmax(nq_max, m);
+                        nq_sq += q2;
+                    }
+                    __syncwarp();
+                }
 #pragma unroll
                 for (int rr = 0; rr < 2; ++rr) {
                     const int i = lane + 32 * rr;
@@ -537,20 +576,10 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
                             const int e = __ffsll((long long)hits) - 1;
                             hits &= hits - 1ull;
                             const int code = nl[e], pa = code & 0xff, pb = code >> 8;
-                            const int j = pa == i ? pb : pa;
-                            nmask[rr] |= 1ull << j;
-                            pair_exact(j, true);
-                            if (i < j) {
-                                T m = T(0), q2 = T(0);
+                            const bool fwd = pa == i;
+                            nmask[rr] |= 1ull << (fwd ? pb : pa);
 #pragma unroll
-                                for (int a = 0; a < 3; ++a) {
-                                    const T xq = (ni[a] - oi[a]) - (sn[a * NB + j] - so[a * NB + j]);
-                                    m = fmax(m, fabs(xq));
-                                    q2 = fma_t<T>(xq, xq, q2);
-                                }
-                                nq_max = fmax(nq_max, m);
-                                nq_sq += q2;
-                            }
+                            for (int a = 0; a < 3; ++a) Ri[a] += fwd ? ner[e * 3 + a] : -ner[e * 3 + a];
                         }
                     } else {
                         for (int j = 0; j < n; ++j) {   // warp-uniform: the near list is built with ballots
