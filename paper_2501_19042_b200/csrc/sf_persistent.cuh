@@ -56,7 +56,7 @@ enum { SAMPLE_OK = 0, SAMPLE_SINGULAR_KKT = 1 };
 struct SmemLayout {
     size_t W, KMm, KMd, cconst, B6, rhs, ptab, tmem;
     size_t slot0, slot_stride;
-    size_t C, Cp, lam, U, xb, eqerr, psq, pex, P0, P1, Cf, pinf, sh, sc, cp, ct;
+    size_t C, Cp, lam, U, xb, eqerr, psq, pex, P0, P1, Cf, pinf, sh, sc, cp, ct, cw;
     size_t total;
 };
 
@@ -172,6 +172,8 @@ template <typename T, int NB> struct RowStride {
 // TC: the FP32 copy of C becomes the 3xTF32 B operand of the position GEMM, [axis][hi, lo] blocks of
 // 16 robots x 16 k in the UMMA K-major layout (tc::kmajor16_offset)
 constexpr int kTcBopBytes = 3 * 2 * 1024;
+// round-based cooperative careful path (hy_careful_rounds): per warp 32 items of 8 doubles + 32 owners x 12
+constexpr int kCoopWarpDoubles = 32 * 8 + 32 * 12;
 
 // hy: hybrid precision keeps the previous iterate's FP64 coefficients (Cp) and FP64 exit-residual partials
 // (pex).  The per-warp partial arrays are sized for the slot's warps: 4 on the tensor-core path.
@@ -212,6 +214,8 @@ __host__ __device__ inline SmemLayout make_layout(int n, int S, int MP, int spb,
     // ... and the FP64 trig targets e(d_k) of its zero-component terms per (step, term), tagged (sample, k): the
     // next iteration's e(d_{k-1}) (hy_careful_item)
     L.ct = q;     q = align16(q + ((hy && NB <= 4 && !tc) ? (size_t)S * (NB * (NB - 1) / 2 + NB) * (3 * d + 8) : 0));
+    // hy, NB = 32: per warp 32 items + 32 owners' outputs of the round-based cooperative careful path
+    L.cw = q;     q = align16(q + ((hy && NB >= 32 && !tc) ? (size_t)((S + 15) / 16) * kCoopWarpDoubles * d : 0));
 #ifdef SGSF_SYNC_CHECK
     L.sc = q;     q = align16(q + pw * sizeof(int));                   // debug: per-warp decisions
 #else
@@ -228,6 +232,7 @@ struct SlotPtrs {
     SlotShared* sh;
     double* cp;
     double* ct;
+    double* cw;
 };
 
 __device__ __forceinline__ SlotPtrs slot_ptrs(unsigned char* smem, const SmemLayout& L, int s) {
@@ -248,6 +253,7 @@ __device__ __forceinline__ SlotPtrs slot_ptrs(unsigned char* smem, const SmemLay
     P.sh = (SlotShared*)(b + L.sh);
     P.cp = (double*)(b + L.cp);
     P.ct = (double*)(b + L.ct);
+    P.cw = (double*)(b + L.cw);
     return P;
 }
 
@@ -942,6 +948,108 @@ __device__ __forceinline__ HyStepOut<T, NB, MP> hy_step_coop(const double* __res
     return r;
 }
 
+// Round-based cooperative careful path (HY, NB = 32: 528 terms per step; the serial hy_step_full of one
+// careful step costs ~300K cycles there, with its position arrays in local memory, and stalls its slot).
+// The warp takes the careful owner's step 32 terms per round: lane b evaluates term 32 r + b exactly as
+// hy_step_full (FP64 positions of both iterates, resid64, the interior flags); then every lane adds, for its
+// (robot, axis) entries of the R row, the round's terms in term order (bitwise hy_step_full's sums), and a
+// ballot gives the round's word of interior bits.  Only the step's l2 exit partial is summed in another
+// (fixed) order.
+template <int NB, int MP>
+__device__ __forceinline__ bool hy_careful_item2(const SolveParams& p, const double* Cn, const double* Co, int t,
+                                                 int b, double* __restrict__ out, bool& off, bool& zero) {
+    constexpr int NP = NB * (NB - 1) / 2;
+    int i = 0, j = -1;
+    if (b < NP) {
+        int r = b;
+        for (i = 0; i < NB; ++i) {
+            if (r < NB - 1 - i) break;
+            r -= NB - 1 - i;
+        }
+        j = i + 1 + r;
+        if (j >= p.n) return false;
+    } else {
+        i = b - NP;
+        if (i >= p.n) return false;
+    }
+    double w[MP];
+    w64_row<MP>(p.W, t, p.m1, w);
+    const D3 d = term_diff64<MP>(p, Cn, w, i, j), o = term_diff64<MP>(p, Co, w, i, j);
+    const bool pair = j >= 0;
+    const Family<double> f = family64(p, pair);
+    const D3 x = resid64(pair, o, d, f), r = resid64(pair, d, d, f);
+    const double q = fma(d.z * f.beta, d.z, fma(d.y, d.y, d.x * d.x));
+    zero = d.x == 0.0 || d.y == 0.0 || d.z == 0.0;
+    off = pair ? !(q >= f.lim) : !(q <= f.lim);
+    out[0] = x.x, out[1] = x.y, out[2] = x.z;
+    out[3] = r.x, out[4] = r.y, out[5] = r.z;
+    out[6] = (double)(i | ((pair ? j : 255) << 8));
+    return true;
+}
+
+// outs: [0] inf, [1] sq, [2] flags (1 zero, 2 active), [3..] the interior-bit words
+template <typename T, int NB, int MP>
+__device__ __forceinline__ void hy_careful_rounds(const SolveParams& p, const double* Cn, const double* Co, int t,
+                                                  double* __restrict__ items, double* __restrict__ outs,
+                                                  T* __restrict__ Rrow, int lane) {
+    constexpr int NP = NB * (NB - 1) / 2, NT = NP + NB, R3 = 3 * NB, RPL = (R3 + 31) / 32;
+    double R[RPL];
+#pragma unroll
+    for (int u = 0; u < RPL; ++u) R[u] = 0.0;
+    double mx = 0.0, s2 = 0.0;
+    bool zn = false, ac = false;
+    uint32_t* nmo = (uint32_t*)(outs + 3);
+    for (int r0 = 0; r0 < NT; r0 += 32) {
+        const int b = r0 + lane;
+        double* it = items + 8 * lane;
+        bool off = false, zero = false, valid = false;
+        if (b < NT) valid = hy_careful_item2<NB, MP>(p, Cn, Co, t, b, it, off, zero);
+        if (!valid) it[6] = -1.0;
+        if (valid) {
+            mx = fmax(mx, fmax(fabs(it[0]), fmax(fabs(it[1]), fabs(it[2]))));
+            s2 = fma(it[0], it[0], fma(it[1], it[1], fma(it[2], it[2], s2)));
+        }
+        const uint32_t offw = __ballot_sync(0xffffffffu, valid && (off || zero));
+        zn = zn || __any_sync(0xffffffffu, valid && zero);
+        ac = ac || offw != 0u;
+        if (lane == 0) nmo[r0 >> 5] = ~offw;
+        __syncwarp();
+        const int cnt = min(32, NT - r0);
+        for (int e = 0; e < cnt; ++e) {   // term order: R[i] += r (first robot / workspace), R[j] -= r
+            const double* ie = items + 8 * e;
+            const int code = (int)ie[6];
+            if (code < 0) continue;
+            const int ci = code & 0xff, cj = code >> 8;
+#pragma unroll
+            for (int u = 0; u < RPL; ++u) {
+                const int q = lane + 32 * u;
+                if (q < R3) {
+                    const int rob = q % NB, ax = q / NB;
+                    if (rob == ci) R[u] += ie[3 + ax];
+                    else if (rob == cj) R[u] -= ie[3 + ax];
+                }
+            }
+        }
+        __syncwarp();   // the items are rewritten next round
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+        s2 += __shfl_xor_sync(0xffffffffu, s2, off);
+    }
+#pragma unroll
+    for (int u = 0; u < RPL; ++u) {
+        const int q = lane + 32 * u;
+        if (q < R3 && (q % NB) < p.n) Rrow[q] = (T)R[u];
+    }
+    if (lane == 0) {
+        outs[0] = mx;
+        outs[1] = s2;
+        outs[2] = (double)((zn ? 1 : 0) | (ac ? 2 : 0));
+    }
+    __syncwarp();
+}
+
 // Flagged terms (active now or at the previous iterate) of one time step,
 // O(#flagged): true exit residual, scatter of d - e for terms active now,
 // and the corrections of the quiet statistics (qinf, qsq).  The quiet
@@ -1428,9 +1536,22 @@ __device__ __forceinline__ Partials<T> finish_step(const SolveParams& p, const S
             const long long hc0 = clock64();
 #endif
             HyStepOut<T, NB, MP> co;
-            if constexpr (NB <= 4) {   // (the cooperative path exists for NB <= 4 only)
+            if constexpr (NB <= 4) {   // (the cooperative paths: item lists for NB <= 4, rounds for NB = 32)
                 co = pre ? hy_step_coop<T, NB, MP>(pre, n, Prow_old, &mo)
                          : hy_step_full<T, NB, MP>(p, Ck, Ckm1, lt, Prow_old, &mo);
+            } else if constexpr (NB >= 32) {
+                if (pre) {   // the warp has run hy_careful_rounds for this step: R row written, outputs here
+                    const uint32_t* w = (const uint32_t*)(pre + 3);
+#pragma unroll
+                    for (int u = 0; u < NW; ++u) mo.w[u] = w[u];
+                    const int fl = (int)pre[2];
+                    co.inf = pre[0];
+                    co.sq = pre[1];
+                    co.zero = (fl & 1) != 0;
+                    co.active = (fl & 2) != 0;
+                } else {
+                    co = hy_step_full<T, NB, MP>(p, Ck, Ckm1, lt, Prow_old, &mo);
+                }
             } else {
                 co = hy_step_full<T, NB, MP>(p, Ck, Ckm1, lt, Prow_old, &mo);
             }
@@ -1950,6 +2071,21 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                                                 ((long long)sample << 32) | (unsigned)k);
                     __syncwarp();
                     if (car) pre = scr + kCoopItem * NT * __popc(bal & ((1u << lane) - 1u));
+                }
+            }
+            if constexpr (HY && NB >= 32 && !TC) {   // careful steps: the warp takes each in rounds of 32 terms
+                const bool car = ts < S && owner && (fmin(zmin_ws, zmin_pairs) == T(0) || zprev);
+                uint32_t bal = __ballot_sync(0xffffffffu, car);
+                if (bal && p.coop) {
+                    double* wbase = sp.cw + (size_t)lwarp * kCoopWarpDoubles;
+                    while (bal) {
+                        const int src = __ffs(bal) - 1;
+                        bal &= bal - 1;
+                        const int tso = __shfl_sync(0xffffffffu, ts, src);
+                        T* rowo = (T*)((k & 1) ? sp.P1 : sp.P0) + tso * RS;
+                        hy_careful_rounds<T, NB, MP>(p, Ccur, Cprv, tso, wbase, wbase + 256 + 12 * src, rowo, lane);
+                    }
+                    if (car) pre = wbase + 256 + 12 * lane;
                 }
             }
 #ifdef SGSF_CAREFUL_CLOCK

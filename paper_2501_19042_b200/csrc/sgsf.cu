@@ -10,6 +10,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -221,7 +222,8 @@ int sgsf_solve(sgsf_handle_t* h, int batch, const double* xi_bar, const double* 
     p.coeffs_prev = out->coeffs_prev;
     p.queue = (int*)workspace;
     CUDA_TRY(cudaMemsetAsync(workspace, 0, sizeof(int), stream));
-    if (batch > 1 && h->n <= 32) {   // longest-first queue order (sf_order.cuh)
+    const char* no_order = std::getenv("SGSF_NO_ORDER");   // (experiments: index order)
+    if (batch > 1 && h->n <= 32 && !(no_order && no_order[0] == '1')) {   // longest-first queue order (sf_order.cuh)
         float* score = (float*)((char*)workspace + 256);
         int* order = (int*)((char*)workspace + 256 + align256((size_t)batch * 4));
         const int rc = launch_order(p, score, order, stream);

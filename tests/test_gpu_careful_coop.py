@@ -57,3 +57,23 @@ def test_cooperative_careful_path_on_the_reference_goldens():
     assert out.iterations.cpu().numpy().tolist() == case["iterations"].astype(int).tolist()
     err = np.abs(out.coeffs.cpu().numpy() - case["coeffs"]).max() / max(1.0, np.abs(case["coeffs"]).max())
     assert err <= 1e-6
+
+
+def test_round_based_careful_path_n32():
+    """n = 32 (config 3's last 512-sample shard has ~100 careful step-finishes): the warp-cooperative rounds
+    (hy_careful_rounds) give the serial path's R rows, interior bits and stop decisions bit for bit; only the
+    careful steps' l2 exit partials are summed in another order."""
+    import bench
+    from paper_2501_19042_b200 import SafetyFilter, SolverConfig
+    prob, shard, _ = bench.workload(3, 7, 8, None)
+    cfg = SolverConfig(max_iters=500, svars=False, precision="hybrid")
+    sf = SafetyFilter(prob, degree=10, config=cfg)
+    xb = torch.from_numpy(shard).cuda()
+    a, b = _solve(sf, xb, cfg, True), _solve(sf, xb, cfg, False)
+    for k in ("coeffs", "iterations", "converged", "multipliers", "feasible", "status"):
+        assert torch.equal(getattr(a, k), getattr(b, k)), k
+    ha, hb = a.residual_inf.cpu(), b.residual_inf.cpu()
+    la, lb = a.residual_l2.cpu(), b.residual_l2.cpu()
+    for s, it in enumerate(a.iterations.tolist()):
+        assert torch.equal(ha[s, :it], hb[s, :it]), s
+        assert torch.allclose(la[s, :it], lb[s, :it], rtol=1e-12, atol=0), s
