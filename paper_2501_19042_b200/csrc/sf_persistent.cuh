@@ -173,7 +173,7 @@ template <typename T, int NB> struct RowStride {
 // 16 robots x 16 k in the UMMA K-major layout (tc::kmajor16_offset)
 constexpr int kTcBopBytes = 3 * 2 * 1024;
 // round-based cooperative careful path (hy_careful_rounds): per warp 32 items of 8 doubles + 32 owners x 12
-constexpr int kCoopWarpDoubles = 32 * 8 + 32 * 12;
+constexpr int kCoopWarpDoubles = 32 * 8 + 32 * 12 + 2 * 3 * 32;   // + both iterates' FP64 positions
 
 // hy: hybrid precision keeps the previous iterate's FP64 coefficients (Cp) and FP64 exit-residual partials
 // (pex).  The per-warp partial arrays are sized for the slot's warps: 4 on the tensor-core path.
@@ -547,8 +547,9 @@ __device__ __forceinline__ PartStats<T> quiet_part(const T (&pos)[3 * RH], const
 // component is exactly zero (FULL: the product of the three components,
 // which can only underflow to a false "zero" -- that just takes the exact
 // careful path), and the non-interior workspace bits cleared in nm (combined
-// over the step's lanes; h = this lane's half)
-template <typename T, int NB, int RH, int TPS, bool FULL>
+// over the step's lanes; h = this lane's half).  COINC (hybrid): only non-interior terms count -- an interior
+// term's reference-trig target differs from d by an ulp-level leak, which the hybrid kernels take as d
+template <typename T, int NB, int RH, int TPS, bool FULL, bool COINC = false>
 __device__ __forceinline__ T ws_part(const T (&pos)[3 * RH], int r0, int h, int n, const Family<T>& fw, T cx, T cy,
                                      T cz, uint32_t (&nm)[TermBits<NB>::words], unsigned m) {
     T zm = T(1), qw = T(0);
@@ -557,8 +558,8 @@ __device__ __forceinline__ T ws_part(const T (&pos)[3 * RH], int r0, int h, int 
 #pragma unroll
         for (int i = 0; i < RH; ++i) {
             const T rx = pos[i] - cx, ry = pos[RH + i] - cy, rz = pos[2 * RH + i] - cz;
-            zv[i] = fabs(rx * ry * rz);
             qv[i] = fma_t<T>(rz * fw.beta, rz, fma_t<T>(ry, ry, rx * rx));
+            zv[i] = (COINC && qv[i] <= fw.lim) ? T(1) : fabs(rx * ry * rz);
         }
         zm = tree_reduce(zv, OpMin());
         qw = tree_reduce(qv, OpMax());
@@ -567,8 +568,9 @@ __device__ __forceinline__ T ws_part(const T (&pos)[3 * RH], int r0, int h, int 
         for (int i = 0; i < RH; ++i) {
             if (r0 + i < n) {
                 const T rx = pos[i] - cx, ry = pos[RH + i] - cy, rz = pos[2 * RH + i] - cz;
-                zm = fmin(zm, fmin(fabs(rx), fmin(fabs(ry), fabs(rz))));
-                qw = fmax(qw, fma_t<T>(rz * fw.beta, rz, fma_t<T>(ry, ry, rx * rx)));
+                const T qi = fma_t<T>(rz * fw.beta, rz, fma_t<T>(ry, ry, rx * rx));
+                zm = fmin(zm, (COINC && qi <= fw.lim) ? T(1) : fmin(fabs(rx), fmin(fabs(ry), fabs(rz))));
+                qw = fmax(qw, qi);
             }
         }
     }
@@ -738,8 +740,8 @@ __device__ __forceinline__ void hy_careful_item(const SolveParams& p, const doub
         r = resid64(pair, d, d, f);
     }
     const double q = fma(d.z * f.beta, d.z, fma(d.y, d.y, d.x * d.x));
-    const bool zero = d.x == 0.0 || d.y == 0.0 || d.z == 0.0;
     const bool off = pair ? !(q >= f.lim) : !(q <= f.lim);
+    const bool zero = (d.x == 0.0 || d.y == 0.0 || d.z == 0.0) && off;   // (hybrid: non-interior)
     out[0] = x.x, out[1] = x.y, out[2] = x.z;
     out[3] = r.x, out[4] = r.y, out[5] = r.z;
     out[6] = (double)(((off || zero) ? 1 : 0) | (zero ? 2 : 0));
@@ -847,7 +849,7 @@ __device__ __forceinline__ HyStepOut<T, NB, MP> hy_step_full(const SolveParams& 
                 R[i] += r.x, R[NB + i] += r.y, R[2 * NB + i] += r.z;
                 R[j] -= r.x, R[NB + j] -= r.y, R[2 * NB + j] -= r.z;
                 const double q = fma(d.z * fp.beta, d.z, fma(d.y, d.y, d.x * d.x));
-                const bool zero = d.x == 0.0 || d.y == 0.0 || d.z == 0.0;
+                const bool zero = (d.x == 0.0 || d.y == 0.0 || d.z == 0.0) && !(q >= fp.lim);   // (hybrid: non-interior)
                 znow = znow || zero;
                 if (!(q >= fp.lim) || zero) {
                     nmw.w[b >> 5] &= ~(1u << (b & 31));
@@ -868,7 +870,7 @@ __device__ __forceinline__ HyStepOut<T, NB, MP> hy_step_full(const SolveParams& 
             const D3 r = resid64(false, d, d, fw);
             R[i] += r.x, R[NB + i] += r.y, R[2 * NB + i] += r.z;
             const double q = fma(d.z * fw.beta, d.z, fma(d.y, d.y, d.x * d.x));
-            const bool zero = d.x == 0.0 || d.y == 0.0 || d.z == 0.0;
+            const bool zero = (d.x == 0.0 || d.y == 0.0 || d.z == 0.0) && !(q <= fw.lim);   // (hybrid: non-interior)
             znow = znow || zero;
             if (!(q <= fw.lim) || zero) {
                 nmw.w[b >> 5] &= ~(1u << (b & 31));
@@ -956,8 +958,8 @@ __device__ __forceinline__ HyStepOut<T, NB, MP> hy_step_coop(const double* __res
 // ballot gives the round's word of interior bits.  Only the step's l2 exit partial is summed in another
 // (fixed) order.
 template <int NB, int MP>
-__device__ __forceinline__ bool hy_careful_item2(const SolveParams& p, const double* Cn, const double* Co, int t,
-                                                 int b, double* __restrict__ out, bool& off, bool& zero) {
+__device__ __forceinline__ bool hy_careful_item2(const SolveParams& p, const double* __restrict__ pos, int b,
+                                                 double* __restrict__ out, bool& off, bool& zero) {
     constexpr int NP = NB * (NB - 1) / 2;
     int i = 0, j = -1;
     if (b < NP) {
@@ -972,15 +974,23 @@ __device__ __forceinline__ bool hy_careful_item2(const SolveParams& p, const dou
         i = b - NP;
         if (i >= p.n) return false;
     }
-    double w[MP];
-    w64_row<MP>(p.W, t, p.m1, w);
-    const D3 d = term_diff64<MP>(p, Cn, w, i, j), o = term_diff64<MP>(p, Co, w, i, j);
+    // term_diff64's differences, from the step's FP64 positions (pos: [iterate][axis][robot], pos64's bits)
+    const double* pn = pos;
+    const double* po = pos + 3 * NB;
+    D3 d, o;
+    if (j >= 0) {
+        d = D3{pn[i] - pn[j], pn[NB + i] - pn[NB + j], pn[2 * NB + i] - pn[2 * NB + j]};
+        o = D3{po[i] - po[j], po[NB + i] - po[NB + j], po[2 * NB + i] - po[2 * NB + j]};
+    } else {
+        d = D3{pn[i] - p.cx, pn[NB + i] - p.cy, pn[2 * NB + i] - p.cz};
+        o = D3{po[i] - p.cx, po[NB + i] - p.cy, po[2 * NB + i] - p.cz};
+    }
     const bool pair = j >= 0;
     const Family<double> f = family64(p, pair);
     const D3 x = resid64(pair, o, d, f), r = resid64(pair, d, d, f);
     const double q = fma(d.z * f.beta, d.z, fma(d.y, d.y, d.x * d.x));
-    zero = d.x == 0.0 || d.y == 0.0 || d.z == 0.0;
     off = pair ? !(q >= f.lim) : !(q <= f.lim);
+    zero = (d.x == 0.0 || d.y == 0.0 || d.z == 0.0) && off;   // (hybrid: non-interior)
     out[0] = x.x, out[1] = x.y, out[2] = x.z;
     out[3] = r.x, out[4] = r.y, out[5] = r.z;
     out[6] = (double)(i | ((pair ? j : 255) << 8));
@@ -999,11 +1009,22 @@ __device__ __forceinline__ void hy_careful_rounds(const SolveParams& p, const do
     double mx = 0.0, s2 = 0.0;
     bool zn = false, ac = false;
     uint32_t* nmo = (uint32_t*)(outs + 3);
+    double* pos = items + 32 * 8 + 32 * 12;   // [iterate][axis][robot]: each robot's FP64 positions, once
+    {
+        double w[MP];
+        w64_row<MP>(p.W, t, p.m1, w);
+        for (int q = lane; q < 3 * NB; q += 32) {
+            const int ax = q / NB, i = q % NB;
+            pos[q] = i < p.n ? pos64<MP>(Cn, w, ax * p.n + i) : 0.0;
+            pos[3 * NB + q] = i < p.n ? pos64<MP>(Co, w, ax * p.n + i) : 0.0;
+        }
+    }
+    __syncwarp();
     for (int r0 = 0; r0 < NT; r0 += 32) {
         const int b = r0 + lane;
         double* it = items + 8 * lane;
         bool off = false, zero = false, valid = false;
-        if (b < NT) valid = hy_careful_item2<NB, MP>(p, Cn, Co, t, b, it, off, zero);
+        if (b < NT) valid = hy_careful_item2<NB, MP>(p, pos, b, it, off, zero);
         if (!valid) it[6] = -1.0;
         if (valid) {
             mx = fmax(mx, fmax(fabs(it[0]), fmax(fabs(it[1]), fabs(it[2]))));
@@ -1980,9 +2001,9 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                 cum += T(2) * sqrt(st.dmax2) * inv_lat;
                 need_scan = (k == 0) || zprev || !(rmin - cum > T(1) + T(1e-3));
                 if (FULLN == 1 || (FULLN == 0 && full))
-                    zmin_ws = ws_part<T, NB, RH, TPS, FULLN != 2>(pos, r0, h, n, fw, cx, cy, cz, nm, smask);
+                    zmin_ws = ws_part<T, NB, RH, TPS, FULLN != 2, HY>(pos, r0, h, n, fw, cx, cy, cz, nm, smask);
                 else
-                    zmin_ws = ws_part<T, NB, RH, TPS, false>(pos, r0, h, n, fw, cx, cy, cz, nm, smask);
+                    zmin_ws = ws_part<T, NB, RH, TPS, false, HY>(pos, r0, h, n, fw, cx, cy, cz, nm, smask);
             }
             __syncwarp();   // both halves of every row written before the owners and the scans read them
             if (ts < S && owner && !need_scan) {   // near pairs of the last scan, exactly (a pair active before is near)
@@ -1996,8 +2017,9 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                         const int ij = ptab[w * 32 + bit], i = ij & 0xff, j = ij >> 8;
                         const T dx = Prow_new[i] - Prow_new[j], dy = Prow_new[NB + i] - Prow_new[NB + j];
                         const T dz = Prow_new[2 * NB + i] - Prow_new[2 * NB + j];
-                        zmin_ws = fmin(zmin_ws, fmin(fabs(dx), fmin(fabs(dy), fabs(dz))));
                         const T q = fma_t<T>(dz * fp.beta, dz, fma_t<T>(dy, dy, dx * dx));
+                        // (HY: zero components of interior terms do not send the step to the careful path)
+                        zmin_ws = fmin(zmin_ws, (HY && q >= fp.lim) ? T(1) : fmin(fabs(dx), fmin(fabs(dy), fabs(dz))));
                         if (!(q >= fp.lim)) nm[w] &= ~(1u << bit);
                     }
                 }
@@ -2025,8 +2047,8 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                         if (j < n) {
                             const T dx = row[i] - row[j], dy = row[NB + i] - row[NB + j];
                             const T dz = row[2 * NB + i] - row[2 * NB + j];
-                            zm = fmin(zm, fmin(fabs(dx), fmin(fabs(dy), fabs(dz))));
                             const T q = fma_t<T>(dz * fp.beta, dz, fma_t<T>(dy, dy, dx * dx));
+                            zm = fmin(zm, (HY && q >= fp.lim) ? T(1) : fmin(fabs(dx), fmin(fabs(dy), fabs(dz))));
                             is_near = !(q >= skin_lim);
                             if (!is_near) qm = fmin(qm, q);
                             outside = !(q >= fp.lim);
