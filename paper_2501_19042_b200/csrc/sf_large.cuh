@@ -591,7 +591,7 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
                                     is_near = i < j;
                                 } else {
                                     farmin = fmin(farmin, qn);
-                                    zfar = zfar || zero;
+                                    zfar = zfar || (!HY && zero);   // (HY: an interior pair's zero component does not block quiet steps)
                                 }
                             }
                             const uint32_t bm = __ballot_sync(0xffffffffu, is_near);
@@ -795,7 +795,7 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
                                             is_near = i < j;
                                         } else {
                                             farmin = fmin(farmin, qn);
-                                            zfar = zfar || zero;
+                                            zfar = zfar || (!HY && zero);   // (HY: an interior pair's zero component does not block quiet steps)
                                         }
                                     }
                                     const uint32_t bm = __ballot_sync(0xffffffffu, is_near);
