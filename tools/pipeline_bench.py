@@ -30,20 +30,26 @@ def run(config, kind, batch, max_iters, reps=3):
     dec = calibrate_batchnorm(sf, make_decoder(kind, prob.n).cuda())
     fused = FusedDecoder(dec)   # K4
     gen = torch.Generator(device="cuda").manual_seed(0)
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    # one warm-up pass (cuDNN plans, allocator blocks), then `reps` passes enqueued back to back: the stage
+    # times are the device's, not the host's launch latency after a synchronisation
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(reps + 1)]
     out = None
     t_dec = t_sf = 0.0
+    keep = []
     for r in range(reps + 1):
         with torch.no_grad():
-            ev[0].record()
+            ev[r][0].record()
             xb = decode_proposals(sf, dec, dec.sample_latent(batch, gen, "cuda"), fused)
-            ev[1].record()
+            ev[r][1].record()
             out = sf.solve_batched(xb)
-            ev[2].record()
-        ev[2].synchronize()
-        if r > 0:   # the first pass warms up cuDNN and the handle
-            t_dec += ev[0].elapsed_time(ev[1]) / reps
-            t_sf += ev[1].elapsed_time(ev[2]) / reps
+            ev[r][2].record()
+        keep.append((xb, out))
+        if r == 0:
+            ev[0][2].synchronize()
+    ev[reps][2].synchronize()
+    for r in range(1, reps + 1):
+        t_dec += ev[r][0].elapsed_time(ev[r][1]) / reps
+        t_sf += ev[r][1].elapsed_time(ev[r][2]) / reps
     its = out.iterations.double()
     return {"config": config, "decoder": kind, "batch": batch, "n": prob.n, "H": prob.horizon_samples - 1,
             "max_iters": max_iters, "decode_qp_ms": t_dec, "sf_verdict_ms": t_sf, "total_ms": t_dec + t_sf,
