@@ -547,8 +547,9 @@ __device__ __forceinline__ PartStats<T> quiet_part(const T (&pos)[3 * RH], const
 // component is exactly zero (FULL: the product of the three components,
 // which can only underflow to a false "zero" -- that just takes the exact
 // careful path), and the non-interior workspace bits cleared in nm (combined
-// over the step's lanes; h = this lane's half).  COINC (hybrid): only non-interior terms count -- an interior
-// term's reference-trig target differs from d by an ulp-level leak, which the hybrid kernels take as d
+// over the step's lanes; h = this lane's half).  COINC (hybrid): the zeros count only when one of the lane's
+// workspace terms is non-interior -- an interior term's reference-trig target is d up to an ulp-level leak,
+// which the hybrid kernels take as d (conservative: a non-interior term keeps the lane's zeros)
 template <typename T, int NB, int RH, int TPS, bool FULL, bool COINC = false>
 __device__ __forceinline__ T ws_part(const T (&pos)[3 * RH], int r0, int h, int n, const Family<T>& fw, T cx, T cy,
                                      T cz, uint32_t (&nm)[TermBits<NB>::words], unsigned m) {
@@ -558,8 +559,8 @@ __device__ __forceinline__ T ws_part(const T (&pos)[3 * RH], int r0, int h, int 
 #pragma unroll
         for (int i = 0; i < RH; ++i) {
             const T rx = pos[i] - cx, ry = pos[RH + i] - cy, rz = pos[2 * RH + i] - cz;
+            zv[i] = fabs(rx * ry * rz);
             qv[i] = fma_t<T>(rz * fw.beta, rz, fma_t<T>(ry, ry, rx * rx));
-            zv[i] = (COINC && qv[i] <= fw.lim) ? T(1) : fabs(rx * ry * rz);
         }
         zm = tree_reduce(zv, OpMin());
         qw = tree_reduce(qv, OpMax());
@@ -568,12 +569,12 @@ __device__ __forceinline__ T ws_part(const T (&pos)[3 * RH], int r0, int h, int 
         for (int i = 0; i < RH; ++i) {
             if (r0 + i < n) {
                 const T rx = pos[i] - cx, ry = pos[RH + i] - cy, rz = pos[2 * RH + i] - cz;
-                const T qi = fma_t<T>(rz * fw.beta, rz, fma_t<T>(ry, ry, rx * rx));
-                zm = fmin(zm, (COINC && qi <= fw.lim) ? T(1) : fmin(fabs(rx), fmin(fabs(ry), fabs(rz))));
-                qw = fmax(qw, qi);
+                zm = fmin(zm, fmin(fabs(rx), fmin(fabs(ry), fabs(rz))));
+                qw = fmax(qw, fma_t<T>(rz * fw.beta, rz, fma_t<T>(ry, ry, rx * rx)));
             }
         }
     }
+    if (COINC && qw <= fw.lim) zm = T(1);   // (this lane's workspace terms are all interior)
 #pragma unroll
     for (int w = 0; w < TermBits<NB>::words; ++w) nm[w] = 0xffffffffu;
     if (__builtin_expect(__any_sync(m, !(qw <= fw.lim)), 0)) {
@@ -2019,8 +2020,11 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                         const T dz = Prow_new[2 * NB + i] - Prow_new[2 * NB + j];
                         const T q = fma_t<T>(dz * fp.beta, dz, fma_t<T>(dy, dy, dx * dx));
                         // (HY: zero components of interior terms do not send the step to the careful path)
-                        zmin_ws = fmin(zmin_ws, (HY && q >= fp.lim) ? T(1) : fmin(fabs(dx), fmin(fabs(dy), fabs(dz))));
-                        if (!(q >= fp.lim)) nm[w] &= ~(1u << bit);
+                        if (!HY) zmin_ws = fmin(zmin_ws, fmin(fabs(dx), fmin(fabs(dy), fabs(dz))));
+                        if (!(q >= fp.lim)) {
+                            nm[w] &= ~(1u << bit);
+                            if (HY) zmin_ws = fmin(zmin_ws, fmin(fabs(dx), fmin(fabs(dy), fabs(dz))));
+                        }
                     }
                 }
             }
