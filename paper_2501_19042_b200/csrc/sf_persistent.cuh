@@ -1414,6 +1414,17 @@ __device__ __forceinline__ double hy_dp_s(const double* __restrict__ Cn, const d
     for (int q = 0; q < MP; ++q) v = fma(cn[q] - co[q], q < m1 ? __ldg(Wrow + q) : 0.0, v);
     return v;
 }
+// hy_dp_s with the W row in registers (the same operations)
+template <int MP>
+__device__ __forceinline__ double hy_dp_w(const double* __restrict__ Cn, const double* __restrict__ Co,
+                                          const double (&w)[MP], int row) {
+    const double* cn = Cn + row * MP;
+    const double* co = Co + row * MP;
+    double v = 0.0;
+#pragma unroll
+    for (int q = 0; q < MP; ++q) v = fma(cn[q] - co[q], w[q], v);
+    return v;
+}
 template <int NB, int MP>
 __device__ __forceinline__ double2 hy_exit64_inline(const SolveParams& p, const double* Cn, const double* Co, int t,
                                                     const uint32_t (&omr)[TermBits<NB>::words]) {
@@ -1423,6 +1434,8 @@ __device__ __forceinline__ double2 hy_exit64_inline(const SolveParams& p, const 
     for (int u = 0; u < TermBits<NB>::words; ++u) om[u] = omr[u];
     const int n = p.n, m1 = p.m1;
     const double* Wrow = p.W + (size_t)t * m1;
+    double wr[MP];   // the W row, once
+    w64_row<MP>(p.W, t, m1, wr);
     // non-interior-at-old terms: count pairs and workspace terms, remember up to two pair bits
     int npf = 0, fb0 = -1, fb1 = -1;
     bool anyf = false;
@@ -1447,18 +1460,27 @@ __device__ __forceinline__ double2 hy_exit64_inline(const SolveParams& p, const 
         double lo = 0.0, hi = 0.0, s1 = 0.0, sq = 0.0;
         double tv[3] = {-1e300, -1e300, -1e300}, bv[3] = {-1e300, -1e300, -1e300}, av[3] = {-1.0, -1.0, -1.0};
         int ti[3] = {-1, -1, -1}, bi[3] = {-1, -1, -1}, ai[3] = {-1, -1, -1};
+        // four rows' D p at a time (independent FMA chains), consumed in row order
 #pragma unroll 1
-        for (int i = 0; i < n; ++i) {
-            const double v = hy_dp_s<MP>(Cn, Co, Wrow, m1, ax * n + i);
-            lo = i ? fmin(lo, v) : v;
-            hi = i ? fmax(hi, v) : v;
-            s1 += v;
-            sq = fma(v, v, sq);
-            if (anyf) {
-                top3_insert(tv, ti, v, i);
-                top3_insert(bv, bi, -v, i);
-                const int wb = NP + i;
-                if ((om[wb >> 5] >> (wb & 31)) & 1u) top3_insert(av, ai, fabs(v), i);
+        for (int i0 = 0; i0 < n; i0 += 4) {
+            double v4[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v4[u] = i0 + u < n ? hy_dp_w<MP>(Cn, Co, wr, ax * n + i0 + u) : 0.0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = i0 + u;
+                if (i >= n) break;
+                const double v = v4[u];
+                lo = i ? fmin(lo, v) : v;
+                hi = i ? fmax(hi, v) : v;
+                s1 += v;
+                sq = fma(v, v, sq);
+                if (anyf) {
+                    top3_insert(tv, ti, v, i);
+                    top3_insert(bv, bi, -v, i);
+                    const int wb = NP + i;
+                    if ((om[wb >> 5] >> (wb & 31)) & 1u) top3_insert(av, ai, fabs(v), i);
+                }
             }
         }
         mx = fmax(mx, fmax(hi - lo, fmax(hi, -lo)));
@@ -1478,12 +1500,12 @@ __device__ __forceinline__ double2 hy_exit64_inline(const SolveParams& p, const 
             } else {   // many flagged pairs: scan every pair interior at the old iterate
 #pragma unroll 1
                 for (int i = 0; i < n; ++i) {
-                    const double vi = hy_dp_s<MP>(Cn, Co, Wrow, m1, ax * n + i);
+                    const double vi = hy_dp_w<MP>(Cn, Co, wr, ax * n + i);
 #pragma unroll 1
                     for (int j = i + 1; j < n; ++j) {
                         const int pb = pair_bit<NB>(i, j);
                         if ((om[pb >> 5] >> (pb & 31)) & 1u)
-                            base = fmax(base, fabs(vi - hy_dp_s<MP>(Cn, Co, Wrow, m1, ax * n + j)));
+                            base = fmax(base, fabs(vi - hy_dp_w<MP>(Cn, Co, wr, ax * n + j)));
                     }
                 }
             }
@@ -1512,8 +1534,8 @@ __device__ __forceinline__ double2 hy_exit64_inline(const SolveParams& p, const 
                 double e2 = 0.0;
 #pragma unroll 1
                 for (int ax = 0; ax < 3; ++ax) {
-                    const double e = hy_dp_s<MP>(Cn, Co, Wrow, m1, ax * n + i) -
-                                     (j >= 0 ? hy_dp_s<MP>(Cn, Co, Wrow, m1, ax * n + j) : 0.0);
+                    const double e = hy_dp_w<MP>(Cn, Co, wr, ax * n + i) -
+                                     (j >= 0 ? hy_dp_w<MP>(Cn, Co, wr, ax * n + j) : 0.0);
                     e2 = fma(e, e, e2);
                 }
                 const D3 dn = term_diff64s<MP>(p, Cn, Wrow, i, j), dol = term_diff64s<MP>(p, Co, Wrow, i, j);
