@@ -650,7 +650,8 @@ __device__ __forceinline__ double pos64(const double* __restrict__ C, const doub
     return s;
 }
 
-__device__ __forceinline__ Family<double> family64(const SolveParams& p, bool pair) {
+template <typename P>
+__device__ __forceinline__ Family<double> family64(const P& p, bool pair) {
     Family<double> f;
     f.lat = pair ? p.lat : p.ws_lat;
     f.lim = pair ? p.fp_lim_d : p.fw_lim_d;
@@ -758,8 +759,8 @@ __device__ __forceinline__ double pos64s(const double* __restrict__ C, const dou
     for (int q = 0; q < MP; ++q) s = fma(c[q], q < m1 ? __ldg(Wrow + q) : 0.0, s);
     return s;
 }
-template <int MP>
-__device__ __forceinline__ D3 term_diff64s(const SolveParams& p, const double* __restrict__ C,
+template <int MP, typename P>
+__device__ __forceinline__ D3 term_diff64s(const P& p, const double* __restrict__ C,
                                            const double* __restrict__ Wrow, int i, int j) {
     const int n = p.n, m1 = p.m1;
     D3 d;
@@ -1425,8 +1426,8 @@ __device__ __forceinline__ double hy_dp_w(const double* __restrict__ Cn, const d
     for (int q = 0; q < MP; ++q) v = fma(cn[q] - co[q], w[q], v);
     return v;
 }
-template <int NB, int MP>
-__device__ __forceinline__ double2 hy_exit64_inline(const SolveParams& p, const double* Cn, const double* Co, int t,
+template <int NB, int MP, typename P>
+__device__ __forceinline__ double2 hy_exit64_inline(const P& p, const double* Cn, const double* Co, int t,
                                                     const uint32_t (&omr)[TermBits<NB>::words]) {
     constexpr int NP = NB * (NB - 1) / 2;
     uint32_t om[TermBits<NB>::words];   // (a copy: runtime-indexed lookups below must not pin the caller's registers)
@@ -1548,6 +1549,30 @@ __device__ __forceinline__ double2 hy_exit64_inline(const SolveParams& p, const 
         s2 = fmax(s2 + adj, 0.0);
     }
     return make_double2(mx, s2);
+}
+
+// The FP64 stop re-evaluation out of line (it runs ~2 times per sample): the fields it reads, by value -- a
+// non-inlined callee must not take the kernel's parameter block by reference (its local copy turns every p.*
+// read into a local-memory load); inlined, its code and registers weighed on the whole kernel
+struct HyExitArgs {
+    const double* W;
+    int n, m1;
+    double cx, cy, cz, lat, vert, ws_lat, ws_vert, fp_lim_d, fp_beta_d, fw_lim_d, fw_beta_d;
+};
+__device__ __forceinline__ HyExitArgs hy_exit_args(const SolveParams& p) {
+    HyExitArgs a;
+    a.W = p.W;
+    a.n = p.n;
+    a.m1 = p.m1;
+    a.cx = p.cx, a.cy = p.cy, a.cz = p.cz;
+    a.lat = p.lat, a.vert = p.vert, a.ws_lat = p.ws_lat, a.ws_vert = p.ws_vert;
+    a.fp_lim_d = p.fp_lim_d, a.fp_beta_d = p.fp_beta_d, a.fw_lim_d = p.fw_lim_d, a.fw_beta_d = p.fw_beta_d;
+    return a;
+}
+template <int NB, int MP>
+__device__ __noinline__ double2 hy_exit64_call(const HyExitArgs a, const double* Cn, const double* Co, int t,
+                                               const MaskPack<NB> om) {
+    return hy_exit64_inline<NB, MP>(a, Cn, Co, t, om.w);
 }
 
 // ---------------------------------------------------------------- finishing a time step
@@ -2218,7 +2243,10 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
 #endif
                     double xi = 0.0, xs = 0.0;
                     if (ts < S && owner) {
-                        const double2 e = hy_exit64_inline<NB, MP>(p, Ccur, Cprv, ts, imask);
+                        MaskPack<NB> om;
+#pragma unroll
+                        for (int w = 0; w < NW; ++w) om.w[w] = imask[w];
+                        const double2 e = hy_exit64_call<NB, MP>(hy_exit_args(p), Ccur, Cprv, ts, om);
                         xi = e.x;
                         xs = e.y;
                     }
