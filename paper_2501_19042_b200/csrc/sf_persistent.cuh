@@ -635,6 +635,25 @@ struct D3 {
     double x, y, z;
 };
 
+// The FP64 stop re-evaluation and scatter out of line: the fields they read, by value -- a
+// non-inlined callee must not take the kernel's parameter block by reference (its local copy turns every p.*
+// read into a local-memory load); inlined, its code and registers weighed on the whole kernel
+struct HyExitArgs {
+    const double* W;
+    int n, m1;
+    double cx, cy, cz, lat, vert, ws_lat, ws_vert, fp_lim_d, fp_beta_d, fw_lim_d, fw_beta_d;
+};
+__device__ __forceinline__ HyExitArgs hy_exit_args(const SolveParams& p) {
+    HyExitArgs a;
+    a.W = p.W;
+    a.n = p.n;
+    a.m1 = p.m1;
+    a.cx = p.cx, a.cy = p.cy, a.cz = p.cz;
+    a.lat = p.lat, a.vert = p.vert, a.ws_lat = p.ws_lat, a.ws_vert = p.ws_vert;
+    a.fp_lim_d = p.fp_lim_d, a.fp_beta_d = p.fp_beta_d, a.fw_lim_d = p.fw_lim_d, a.fw_beta_d = p.fw_beta_d;
+    return a;
+}
+
 template <int MP>
 __device__ __forceinline__ void w64_row(const double* __restrict__ W, int t, int m1, double (&w)[MP]) {
 #pragma unroll
@@ -662,8 +681,8 @@ __device__ __forceinline__ Family<double> family64(const P& p, bool pair) {
 }
 
 // difference vector of term (i, j) (j < 0: workspace term of robot i, relative to the centre) at step t of C
-template <int MP>
-__device__ __forceinline__ D3 term_diff64(const SolveParams& p, const double* __restrict__ C, const double (&w)[MP],
+template <int MP, typename P>
+__device__ __forceinline__ D3 term_diff64(const P& p, const double* __restrict__ C, const double (&w)[MP],
                                           int i, int j) {
     const int n = p.n;
     D3 d;
@@ -782,8 +801,8 @@ __device__ __forceinline__ D3 term_diff64s(const P& p, const double* __restrict_
 // (every HY helper that takes the kernel's SolveParams by reference must be inlined: a reference to a kernel
 // parameter passed to a real call makes the compiler copy the parameter block to local memory and read every
 // p.* field from there, on every iteration -- that cost hybrid ~15% of its samples until round 2 found it)
-template <typename T, int NB, int MP>
-__device__ __forceinline__ bool hy_scatter_step(const SolveParams& p, const double* Cn, int t, const MaskPack<NB> nm,
+template <typename T, int NB, int MP, typename P>
+__device__ __forceinline__ bool hy_scatter_step(const P& p, const double* Cn, int t, const MaskPack<NB> nm,
                                              const int* __restrict__ ptab, T* Pold) {
     double w[MP];
     w64_row<MP>(p.W, t, p.m1, w);
@@ -1270,7 +1289,7 @@ __device__ __forceinline__ StepOut<T> flagged_path(const T* __restrict__ Pnew, T
 #else
         if constexpr (false) {
 #endif
-            act64 = hy_scatter_step<T, NB, MP>(p, Cn, t, nm, ptab, Pold);
+            act64 = hy_scatter_step<T, NB, MP>(p, Cn, t, nm, ptab, Pold);   // (inline: out of line measured 0.5% slower)
         } else {
 #pragma unroll 1
         for (int w = 0; w < NWD; ++w) {
@@ -1551,24 +1570,6 @@ __device__ __forceinline__ double2 hy_exit64_inline(const P& p, const double* Cn
     return make_double2(mx, s2);
 }
 
-// The FP64 stop re-evaluation out of line (it runs ~2 times per sample): the fields it reads, by value -- a
-// non-inlined callee must not take the kernel's parameter block by reference (its local copy turns every p.*
-// read into a local-memory load); inlined, its code and registers weighed on the whole kernel
-struct HyExitArgs {
-    const double* W;
-    int n, m1;
-    double cx, cy, cz, lat, vert, ws_lat, ws_vert, fp_lim_d, fp_beta_d, fw_lim_d, fw_beta_d;
-};
-__device__ __forceinline__ HyExitArgs hy_exit_args(const SolveParams& p) {
-    HyExitArgs a;
-    a.W = p.W;
-    a.n = p.n;
-    a.m1 = p.m1;
-    a.cx = p.cx, a.cy = p.cy, a.cz = p.cz;
-    a.lat = p.lat, a.vert = p.vert, a.ws_lat = p.ws_lat, a.ws_vert = p.ws_vert;
-    a.fp_lim_d = p.fp_lim_d, a.fp_beta_d = p.fp_beta_d, a.fw_lim_d = p.fw_lim_d, a.fw_beta_d = p.fw_beta_d;
-    return a;
-}
 template <int NB, int MP>
 __device__ __noinline__ double2 hy_exit64_call(const HyExitArgs a, const double* Cn, const double* Co, int t,
                                                const MaskPack<NB> om) {
