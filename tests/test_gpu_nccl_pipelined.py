@@ -1,0 +1,41 @@
+"""The bench's N-GPU step shape on one GPU: an NCCL process group of size 1, the per-sample outputs gathered
+with gather_outputs inside SafetyFilter.solve_pipelined's finish hook (NCCL collectives issued from the side
+streams, two batches in flight).  Exercises the stream / collective interplay the driver's multi-GPU bench runs;
+with one rank the gather is an identity, so the results must equal solve_batched's."""
+import os
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def test_pipelined_solve_with_nccl_gather_world1():
+    import torch.distributed as dist
+
+    from paper_2501_19042_b200 import SafetyFilter, SolverConfig, sample_proposals
+    from paper_2501_19042_b200.distributed import gather_outputs
+    from paper_2501_19042_b200.scenarios import config_problem
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29531")
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        prob = config_problem(2)
+        cfg = SolverConfig(max_iters=100, svars=False)
+        sf = SafetyFilter(prob, degree=10, config=cfg)
+        xs = [torch.from_numpy(sample_proposals(prob, sf.basis, 200, seed=s).proposals).cuda() for s in range(4)]
+        gathered = {}
+
+        def finish(k, out):
+            gathered[k] = gather_outputs(out, out.coeffs.shape[0])
+
+        outs = sf.solve_pipelined(iter(xs), config=cfg, finish=finish)
+        torch.cuda.synchronize()
+        for k, x in enumerate(xs):
+            ref = sf.solve_batched(x, config=cfg)
+            assert torch.equal(gathered[k]["coeffs"], ref.coeffs)
+            assert torch.equal(gathered[k]["iterations"], ref.iterations)
+            assert torch.equal(outs[k].feasible, ref.feasible)
+    finally:
+        dist.destroy_process_group()
