@@ -46,7 +46,8 @@ struct LargeLayout {
     size_t W, KMm, KMd, cconst, B6, rhs, PBt;
     size_t C, Cp, lam, U, xb, g, Cf, Cfo, scr, winf, wsq, winf64, eqerr, srmin, scum, sflag, snear, sncnt, sh;
     size_t sdefer, xr, xnl, xcnt, xfm, xzf;
-    size_t ner;   // per warp: the R of each near pair of the quiet step at hand (evaluated once per pair)   // the cooperative exact steps (phase B), double-buffered partials
+    size_t ner;   // per warp: the R of each near pair of the quiet step at hand (evaluated once per pair)
+    size_t gwords;   // doubles of the g region (g itself, or the larger term-pass scratch aliased on it)   // the cooperative exact steps (phase B), double-buffered partials
     size_t total;
 };
 
@@ -68,11 +69,29 @@ __host__ __device__ inline LargeLayout make_large_layout(int n, int S, int MP, i
     L.lam = o;    o = align16(o + dimp * d);
     L.U = o;      o = align16(o + dimp * d);
     L.xb = o;     o = align16(o + dimp * d);
-    L.g = o;      o = align16(o + dimp * d);
+    // g is all-zero during the term pass (it is accumulated after it, and cleared by the xi-step), so the term
+    // pass's scratch -- the near-pair R rows of phase A and the partials of phase B -- lives in it; the kernel
+    // clears it again before the g accumulation.  (As separate buffers they pushed 64 robots at degree >= 12
+    // past the 227 KB of shared memory.)
+    const size_t pb = sizeof(T) == 4 ? 1 : 0;   // phase B: T = float (lean, hybrid); FP64 "strict" keeps the one-warp pass
+    const size_t xr_b = align16(pb * 2 * kLargeWarps * 2 * 32 * 3 * ts);   // [buf][warp][rr][lane][axis] R parts
+    const size_t xnl_b = align16(pb * 2 * kLargeWarps * 2 * kNearCap * 2);  // [buf][warp][rr] near sublists
+    const size_t xcnt_b = align16(pb * 2 * kLargeWarps * 2 * 4);             // ... their lengths
+    const size_t xfm_b = align16(pb * 2 * kLargeWarps * ts);                 // [buf][warp] min far q
+    const size_t xzf_b = align16(pb * 2 * kLargeWarps * 4);                  // ... a far zero component
+    const size_t ner_b = align16((size_t)kLargeWarps * kNearCap * 3 * ts);   // phase A: per warp, the near pairs' R
+    const size_t scratch = xr_b + xnl_b + xcnt_b + xfm_b + xzf_b > ner_b ? xr_b + xnl_b + xcnt_b + xfm_b + xzf_b : ner_b;
+    L.g = o;      o = align16(o + (dimp * d > scratch ? dimp * d : scratch));
+    L.gwords = (o - L.g) / d;
+    L.ner = L.g;
+    L.xr = L.g;
+    L.xnl = L.xr + xr_b;
+    L.xcnt = L.xnl + xnl_b;
+    L.xfm = L.xcnt + xcnt_b;
+    L.xzf = L.xfm + xfm_b;
     L.Cf = o;     o = align16(o + (size_t)3 * MP * NB * ts);   // C of the current iterate, robot-minor
     L.Cfo = o;    o = align16(o + (size_t)3 * MP * NB * ts);   // ... of the previous iterate
     L.scr = o;    o = align16(o + (size_t)kLargeWarps * 2 * 3 * NB * ts);
-    L.ner = o;    o = align16(o + (size_t)kLargeWarps * kNearCap * 3 * ts);
     L.winf = o;   o = align16(o + (size_t)kLargeWarps * ts);
     L.wsq = o;    o = align16(o + (size_t)kLargeWarps * d);
     L.winf64 = o; o = align16(o + (size_t)kLargeWarps * d);   // hybrid: FP64 per-warp exit-residual maxima
@@ -83,15 +102,7 @@ __host__ __device__ inline LargeLayout make_large_layout(int n, int S, int MP, i
     L.snear = o;  o = align16(o + (size_t)S * kNearCap * 2);   // ... the near pairs (i | j << 8), i < j
     L.sncnt = o;  o = align16(o + (size_t)S * 4);    // ... how many (-1: none recorded / overflow)
     L.sh = o;     o = align16(o + sizeof(LargeShared));
-    // phase B (T = float: lean and hybrid; FP64 "strict" keeps the one-warp exact pass -- its buffers would
-    // not fit next to the FP64 state at H = 150)
-    const size_t pb = sizeof(T) == 4 ? 1 : 0;
     L.sdefer = o; o = align16(o + pb * S * 4);    // per step: 1 = exact this iteration, taken by phase B
-    L.xr = o;     o = align16(o + pb * 2 * kLargeWarps * 2 * 32 * 3 * ts);   // [buf][warp][rr][lane][axis] R parts
-    L.xnl = o;    o = align16(o + pb * 2 * kLargeWarps * 2 * kNearCap * 2);  // [buf][warp][rr] near sublists
-    L.xcnt = o;   o = align16(o + pb * 2 * kLargeWarps * 2 * 4);             // ... their lengths
-    L.xfm = o;    o = align16(o + pb * 2 * kLargeWarps * ts);                // [buf][warp] min far q
-    L.xzf = o;    o = align16(o + pb * 2 * kLargeWarps * 4);                 // ... a far zero component
     L.total = o;
     return L;
 }
@@ -906,6 +917,10 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
                     wsq[warp] = wq;
                 }
             }
+            // the term-pass scratch aliased on g is cleared before g accumulates (after every warp is done with it)
+            __syncthreads();
+            for (int e = tid; e < (int)L.gwords; e += nt) g[e] = 0.0;
+            __syncthreads();
             // g = sum over the warps of their partial R W, in warp order
             {
                 const bool wact = __any_sync(0xffffffffu, lact);

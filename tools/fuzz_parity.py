@@ -2,7 +2,7 @@
 
 Random (n, H, degree, precision, seed) cases; each solves a few proposals for 10 iterations with early
 stop off and compares coefficients and residual histories with oracle/sf_oracle.py (lean 1e-5 / 1e-3,
-strict 1e-9 / 1e-7 relative; histories with the tests' 1e-9 absolute floor).  Prints one line per case and a summary; exit code 1 on any failure.
+hybrid 1e-6 / 1e-3, strict 1e-9 / 1e-7 relative; histories with the tests' 1e-9 absolute floor).  Prints one line per case and a summary; exit code 1 on any failure.
 
     python tools/fuzz_parity.py [cases] [seed] [large]
 """
@@ -29,7 +29,8 @@ def main():
         n = int(rng.integers(17, 65)) if large else int(rng.integers(2, 17))
         H = int(rng.choice([20, 40])) if large else int(rng.choice([20, 50, 96, 100, 127]))
         degree = int(rng.integers(7, 16))
-        precision = "strict" if rng.random() < 0.3 else "lean"
+        u = rng.random()
+        precision = "strict" if u < 0.3 else ("hybrid" if u < 0.65 else "lean")
         if precision == "strict" and H > 100:
             H = 100
         seed = int(rng.integers(0, 1000))
@@ -39,9 +40,13 @@ def main():
         cfg = SolverConfig(max_iters=10, early_stop=False, svars=False, precision=precision)
         sf = SafetyFilter(prob, degree=degree, config=cfg)
         props = sample_proposals(prob, sf.basis, 2, seed=seed, spread=spread).proposals
-        out = sf.solve_batched(torch.from_numpy(props).cuda(), config=cfg)
+        try:
+            out = sf.solve_batched(torch.from_numpy(props).cuda(), config=cfg)
+        except NotImplementedError as e:   # shared-memory limits (64 robots at degree >= 12, long horizons)
+            print(f"case {c:2d} n={n:2d} H={H:3d} deg={degree:2d} {precision:6s}: skipped ({e})", flush=True)
+            continue
         op = sf_oracle.make_problem(doc, degree=degree)
-        ctol, htol = (1e-5, 1e-3) if precision == "lean" else (1e-9, 1e-7)
+        ctol, htol = {"lean": (1e-5, 1e-3), "hybrid": (1e-6, 1e-3), "strict": (1e-9, 1e-7)}[precision]
         worst_c = worst_h = 0.0
         for b, x in enumerate(props):
             r = sf_oracle.solve(op, x, max_iters=10, early_stop=False)
