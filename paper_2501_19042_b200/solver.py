@@ -488,6 +488,9 @@ class SafetyFilter:
                           ("coeffs", "multipliers", "residual_inf", "residual_l2", "iterations", "converged",
                            "displacement", "status", "eq_err")})
             per = (time.perf_counter() - t0) / max(1, len(rows))
+            # one private copy per output array (the pinned staging buffers are reused by the next call); the
+            # results hold disjoint row views of it (4 large copies instead of 4 per result)
+            own = {k: h[k].copy() for k in ("coeffs", "multipliers", "residual_inf", "residual_l2")}
             for r, idx in enumerate(rows):
                 if h["status"][r] == native.SAMPLE_SINGULAR_KKT:
                     msg = (f"endpoint conditions missed by {h['eq_err'][r]:.3e} after refinement "
@@ -498,8 +501,8 @@ class SafetyFilter:
                     continue
                 its = int(h["iterations"][r])
                 results[idx] = SolveResult(
-                    coeffs=h["coeffs"][r].copy(), multipliers=h["multipliers"][r].copy(),
-                    residual_inf=h["residual_inf"][r, :its].copy(), residual_l2=h["residual_l2"][r, :its].copy(),
+                    coeffs=own["coeffs"][r], multipliers=own["multipliers"][r],
+                    residual_inf=own["residual_inf"][r, :its], residual_l2=own["residual_l2"][r, :its],
                     iterations=its, converged=bool(h["converged"][r]), displacement=float(h["displacement"][r]),
                     solve_time=per, svars=svars[r])
         return results

@@ -18,4 +18,4 @@ pr.enable()
 res = sf.batch_solve(props)
 feasible_results(res.results, prob)
 pr.disable()
-pstats.Stats(pr).sort_stats("cumulative").print_stats(25)
+pstats.Stats(pr).sort_stats("cumulative").print_stats(14)
