@@ -377,7 +377,7 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
         __shared__ long long lpt_dur[kLargeWarps];
         __shared__ int lpt_ex[kLargeWarps];
         __shared__ long long lpt_exq[kLargeWarps];
-        long long lqa[5] = {0, 0, 0, 0, 0};   // CTA 0 warp 0 quiet steps: positions, statistics, near pairs + ws, far
+        long long lqa[7] = {0, 0, 0, 0, 0, 0, 0};   // CTA 0 warp 0 quiet steps: positions, statistics, near pairs + ws, far
         double lpt_max = 0, lpt_mean = 0, lpt_exmax = 0, lpt_exmean = 0, lpt_qmax = 0, lpt_excyc = 0;
 #endif
         for (int k = 0;; ++k) {
@@ -660,6 +660,9 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
 #pragma unroll
                     for (int off = 16; off > 0; off >>= 1) nsq += __shfl_xor_sync(0xffffffffu, nsq, off);
                     T far_max = qinf_p;
+#ifdef SGSF_LARGE_PT
+                    const long long lqf0 = clock64();
+#endif
                     if (nmax >= qinf_p) {   // a near pair attains the quiet max: the far max, exactly
                         // D p of every robot over the old-position scratch (dead for this step once the near
                         // pairs are done), the same rounding as the quiet statistics
@@ -678,17 +681,38 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
                         __syncwarp();
                         // every unordered pair once, 63 per lane: robot lane takes partners lane+1 .. lane+32,
                         // robot lane+32 takes lane+33 .. 63 and 0 .. lane-1
-                        T fm = T(0);
-                        auto visit = [&](int rr, int j) {
-                            const int i = lane + 32 * rr;
-                            if (i >= n || j >= n || ((nmask[rr] >> j) & 1ull)) return;
+                        // fixed trip counts and selects instead of early returns, so the loads pipeline (the
+                        // branchy form took ~8.4K cycles, 12% of quiet steps); max is exact in any order
+                        T fa = T(0), fb = T(0);
+                        const bool v0 = lane < n, v1 = lane + 32 < n;
+#pragma unroll 8
+                        for (int jj = 1; jj <= 32; ++jj) {   // robot lane: partners lane + 1 .. lane + 32
+                            const int j = lane + jj;
+                            const bool ok = v0 && j < n && !((nmask[0] >> j) & 1ull);
+                            T m = T(0);
 #pragma unroll
-                            for (int a = 0; a < 3; ++a) fm = fmax(fm, fabs(dpi[rr][a] - so[a * NB + j]));
-                        };
-                        for (int j = lane + 1; j <= lane + 32; ++j) visit(0, j);
-                        for (int j = lane + 33; j < 64; ++j) visit(1, j);
-                        for (int j = 0; j < lane; ++j) visit(1, j);
+                            for (int a = 0; a < 3; ++a) m = fmax(m, fabs(dpi[0][a] - so[a * NB + j]));
+                            if (jj & 1) fa = fmax(fa, ok ? m : T(0));
+                            else fb = fmax(fb, ok ? m : T(0));
+                        }
+#pragma unroll 8
+                        for (int jj = 1; jj <= 31; ++jj) {   // robot lane + 32: partners lane + 33 .. 63, 0 .. lane - 1
+                            const int j = (lane + 32 + jj) & 63;
+                            const bool ok = v1 && j < n && !((nmask[1] >> j) & 1ull);
+                            T m = T(0);
+#pragma unroll
+                            for (int a = 0; a < 3; ++a) m = fmax(m, fabs(dpi[1][a] - so[a * NB + j]));
+                            if (jj & 1) fa = fmax(fa, ok ? m : T(0));
+                            else fb = fmax(fb, ok ? m : T(0));
+                        }
+                        const T fm = fmax(fa, fb);
                         far_max = warp_max_nonneg(fm);
+#ifdef SGSF_LARGE_PT
+                        if (blockIdx.x == 0 && warp == 0 && lane == 0) {
+                            lqa[5] += 1;
+                            lqa[6] += clock64() - lqf0;
+                        }
+#endif
                     }
                     if (lane == 0) {
                         scum[t] = cum_t;
@@ -1050,8 +1074,8 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
                         p.eq_err[sample] = emax;
 #ifdef SGSF_LARGE_PT
                         if (blockIdx.x == 0 && lqa[4])
-                            printf("LQ quiet steps %lld: positions %lld statistics %lld near+ws %lld far %lld cycles each\n", lqa[4],
-                                   lqa[0] / lqa[4], lqa[1] / lqa[4], lqa[2] / lqa[4], lqa[3] / lqa[4]);
+                            printf("LQ quiet steps %lld: positions %lld statistics %lld near+ws %lld far %lld cycles each; far-max fallback %lld times, %lld cycles each\n", lqa[4],
+                                   lqa[0] / lqa[4], lqa[1] / lqa[4], lqa[2] / lqa[4], lqa[3] / lqa[4], lqa[5], lqa[5] ? lqa[6] / lqa[5] : 0);
                         if (blockIdx.x < 4)
                             printf("LPT cta %d sample %d iters %d term-pass cycles: slowest warp %.0f mean %.0f slowest-without-exact %.0f | exact steps per warp: max %.2f mean %.2f, exact-step cycles per iteration (all warps) %.0f\n",
                                    blockIdx.x, sample, k, lpt_max / (k + 1), lpt_mean / (k + 1), lpt_qmax / (k + 1), lpt_exmax / (k + 1),
