@@ -377,7 +377,7 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
         __shared__ long long lpt_dur[kLargeWarps];
         __shared__ int lpt_ex[kLargeWarps];
         __shared__ long long lpt_exq[kLargeWarps];
-        long long lqa[7] = {0, 0, 0, 0, 0, 0, 0};   // CTA 0 warp 0 quiet steps: positions, statistics, near pairs + ws, far
+        long long lqa[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // CTA 0 warp 0 quiet steps: positions, statistics, near pairs + ws, far
         double lpt_max = 0, lpt_mean = 0, lpt_exmax = 0, lpt_exmean = 0, lpt_qmax = 0, lpt_excyc = 0;
 #endif
         for (int k = 0;; ++k) {
@@ -525,6 +525,9 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
                     }
                     __syncwarp();
                 }
+#ifdef SGSF_LARGE_PT
+                const long long lq2b = clock64();
+#endif
 #pragma unroll
                 for (int rr = 0; rr < 2; ++rr) {
                     const int i = lane + 32 * rr;
@@ -736,6 +739,7 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
                     lqa[0] += lq1 - lq0;
                     lqa[1] += lq2 - lq1;
                     lqa[2] += lq3 - lq2;
+                    lqa[7] += lq2b - lq2;
                     lqa[3] += clock64() - lq3;
                     lqa[4] += 1;
                 }
@@ -1074,8 +1078,8 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
                         p.eq_err[sample] = emax;
 #ifdef SGSF_LARGE_PT
                         if (blockIdx.x == 0 && lqa[4])
-                            printf("LQ quiet steps %lld: positions %lld statistics %lld near+ws %lld far %lld cycles each; far-max fallback %lld times, %lld cycles each\n", lqa[4],
-                                   lqa[0] / lqa[4], lqa[1] / lqa[4], lqa[2] / lqa[4], lqa[3] / lqa[4], lqa[5], lqa[5] ? lqa[6] / lqa[5] : 0);
+                            printf("LQ quiet steps %lld: positions %lld statistics %lld near+ws %lld far %lld cycles each; far-max fallback %lld times, %lld cycles each; near stage 1 %lld\n", lqa[4],
+                                   lqa[0] / lqa[4], lqa[1] / lqa[4], lqa[2] / lqa[4], lqa[3] / lqa[4], lqa[5], lqa[5] ? lqa[6] / lqa[5] : 0, lqa[7] / lqa[4]);
                         if (blockIdx.x < 4)
                             printf("LPT cta %d sample %d iters %d term-pass cycles: slowest warp %.0f mean %.0f slowest-without-exact %.0f | exact steps per warp: max %.2f mean %.2f, exact-step cycles per iteration (all warps) %.0f\n",
                                    blockIdx.x, sample, k, lpt_max / (k + 1), lpt_mean / (k + 1), lpt_qmax / (k + 1), lpt_exmax / (k + 1),
