@@ -59,38 +59,38 @@ __global__ void __launch_bounds__(128) start_score_kernel(const SolveParams p, f
     __syncthreads();
     const float ia2 = (float)(1.0 / (p.lat * p.lat)), ib2 = (float)(1.0 / (p.vert * p.vert));
     const float iw2 = (float)(1.0 / (p.ws_lat * p.ws_lat)), iv2 = (float)(1.0 / (p.ws_vert * p.ws_vert));
+    // thread = (step slot, robot): its robot's position into shared memory, then its pairs (i, j > i) and its
+    // workspace term (few registers: many CTAs per SM; the thread-per-step form held 48 positions in 255
+    // registers and took 65 us per 1000 samples)
+    constexpr int SPR = 128 / NB;   // steps per round
+    __shared__ float Pt[SPR][3 * NB];
+    const int sl = threadIdx.x / NB, i = threadIdx.x % NB;
     float v = 0.f;
-    for (int t = threadIdx.x; t < S; t += blockDim.x) {
-        float w[MP];
+    for (int t0 = 0; t0 < S; t0 += SPR) {
+        const int t = t0 + sl;
+        if (t < S && i < n) {
+            float w[MP];
 #pragma unroll
-        for (int q = 0; q < MP; ++q) w[q] = q < m1 ? (float)p.W[t * m1 + q] : 0.f;
-        float pos[3 * NB];
+            for (int q = 0; q < MP; ++q) w[q] = q < m1 ? (float)p.W[t * m1 + q] : 0.f;
 #pragma unroll
-        for (int a = 0; a < 3 * NB; ++a) {
-            const int ax = a / NB, i = a % NB;
-            float acc = 0.f;
-            if (i < n) {
+            for (int ax = 0; ax < 3; ++ax) {
+                float acc = 0.f;
 #pragma unroll
                 for (int q = 0; q < MP; ++q) acc = fmaf(Cs[(ax * n + i) * MP + q], w[q], acc);
-            }
-            pos[a] = acc;
-        }
-#pragma unroll
-        for (int i = 0; i < NB; ++i) {
-            if (i < n) {
-#pragma unroll
-                for (int j = 0; j < NB; ++j) {
-                    if (j > i && j < n) {
-                        const float dx = pos[i] - pos[j], dy = pos[NB + i] - pos[NB + j];
-                        const float dz = pos[2 * NB + i] - pos[2 * NB + j];
-                        v += fmaxf(0.f, 1.f - sqrtf((dx * dx + dy * dy) * ia2 + dz * dz * ib2));
-                    }
-                }
-                const float rx = pos[i] - (float)p.cx, ry = pos[NB + i] - (float)p.cy;
-                const float rz = pos[2 * NB + i] - (float)p.cz;
-                v += fmaxf(0.f, sqrtf((rx * rx + ry * ry) * iw2 + rz * rz * iv2) - 1.f);
+                Pt[sl][ax * NB + i] = acc;
             }
         }
+        __syncthreads();
+        if (t < S && i < n) {
+            const float xi = Pt[sl][i], yi = Pt[sl][NB + i], zi = Pt[sl][2 * NB + i];
+            for (int j = i + 1; j < n; ++j) {
+                const float dx = xi - Pt[sl][j], dy = yi - Pt[sl][NB + j], dz = zi - Pt[sl][2 * NB + j];
+                v += fmaxf(0.f, 1.f - sqrtf((dx * dx + dy * dy) * ia2 + dz * dz * ib2));
+            }
+            const float rx = xi - (float)p.cx, ry = yi - (float)p.cy, rz = zi - (float)p.cz;
+            v += fmaxf(0.f, sqrtf((rx * rx + ry * ry) * iw2 + rz * rz * iv2) - 1.f);
+        }
+        __syncthreads();
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
