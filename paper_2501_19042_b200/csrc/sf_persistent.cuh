@@ -1947,6 +1947,10 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
 #endif
     uint32_t imask[NW];
     bool zprev = false;
+#ifdef SGSF_NEAR_CLOCK
+    long long near_cyc = 0;   // this warp's cycles in the T1 near-pair checks (diagnostics)
+    int near_its = 0;
+#endif
     // Verlet-style pair list: the last scan of this time step split the pairs
     // into "near" (normalised distance < kSkin; their bits in `near`, checked
     // exactly every iteration) and "far" (distance >= rmin >= kSkin).  Since
@@ -1989,6 +1993,9 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
         }
 
         for (int k = 0;; ++k) {
+#ifdef SGSF_NEAR_CLOCK
+            ++near_its;
+#endif
             SGSF_PT(0);
             const int par = k & 1;
             // HY: C_k and C_{k-1} alternate between the C and Cp buffers (the xi-step writes C_{k+1} over C_{k-1});
@@ -2055,6 +2062,9 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                     zmin_ws = ws_part<T, NB, RH, TPS, false, HY>(pos, r0, h, n, fw, cx, cy, cz, nm, smask);
             }
             __syncwarp();   // both halves of every row written before the owners and the scans read them
+#ifdef SGSF_NEAR_CLOCK
+            const long long nc0 = clock64();
+#endif
             if (ts < S && owner && !need_scan) {   // near pairs of the last scan, exactly (a pair active before is near)
 #pragma unroll
                 for (int w = 0; w < NPW; ++w) {
@@ -2077,6 +2087,10 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                 }
             }
 
+#ifdef SGSF_NEAR_CLOCK
+            __syncwarp();
+            if (lane == 0) near_cyc += clock64() - nc0;
+#endif
             SGSF_PT(5);
             // ---------------- T2: warp-local O(n^2) pair scans of this warp's queued time steps: all 32 lanes
             // take 1/32 of the pairs of one step; ballots give the non-interior pair bits, REDUX the minima
@@ -2549,6 +2563,11 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
             SGSF_PT(4);
         }
     }
+#ifdef SGSF_NEAR_CLOCK
+    if (blockIdx.x < 2 && lane == 0)
+        printf("NEAR cta %d slot %d warp %d iterations %d near-check cycles per iteration %.0f\n", blockIdx.x, slot, lwarp,
+               near_its, (double)near_cyc / (near_its > 0 ? near_its : 1));
+#endif
     if constexpr (TC) {   // the last slot to finish frees the TMEM
         tc::fence_before_sync();
         if (lwarp == 0) {
