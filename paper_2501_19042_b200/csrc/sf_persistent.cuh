@@ -172,8 +172,10 @@ template <typename T, int NB> struct RowStride {
 // TC: the FP32 copy of C becomes the 3xTF32 B operand of the position GEMM, [axis][hi, lo] blocks of
 // 16 robots x 16 k in the UMMA K-major layout (tc::kmajor16_offset)
 constexpr int kTcBopBytes = 3 * 2 * 1024;
-// round-based cooperative careful path (hy_careful_rounds): per warp 32 items of 8 doubles + 32 owners x 12
-constexpr int kCoopWarpDoubles = 32 * 8 + 32 * 12 + 2 * 3 * 32;   // + both iterates' FP64 positions
+// round-based cooperative careful path (hy_careful_rounds): per warp 32 items of 8 doubles + 16 owners x 12
+// (outputs for the 16 owner lanes of a two-lane-per-step warp; + both iterates' FP64 positions)
+constexpr int kCoopOwners = 16;
+constexpr int kCoopWarpDoubles = 32 * 8 + kCoopOwners * 12 + 2 * 3 * 32;
 
 // hy: hybrid precision keeps the previous iterate's FP64 coefficients (Cp) and FP64 exit-residual partials
 // (pex).  The per-warp partial arrays are sized for the slot's warps: 4 on the tensor-core path.
@@ -1030,7 +1032,7 @@ __device__ __forceinline__ void hy_careful_rounds(const SolveParams& p, const do
     double mx = 0.0, s2 = 0.0;
     bool zn = false, ac = false;
     uint32_t* nmo = (uint32_t*)(outs + 3);
-    double* pos = items + 32 * 8 + 32 * 12;   // [iterate][axis][robot]: each robot's FP64 positions, once
+    double* pos = items + 32 * 8 + kCoopOwners * 12;   // [iterate][axis][robot]: each robot's FP64 positions, once
     {
         double w[MP];
         w64_row<MP>(p.W, t, p.m1, w);
@@ -2164,7 +2166,7 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
             if constexpr (HY && NB >= 32 && !TC) {   // careful steps: the warp takes each in rounds of 32 terms
                 const bool car = ts < S && owner && (fmin(zmin_ws, zmin_pairs) == T(0) || zprev);
                 uint32_t bal = __ballot_sync(0xffffffffu, car);
-                if (bal && p.coop) {
+                if (bal && p.coop && (bal >> kCoopOwners) == 0u) {   // (owners are lanes 0..15: two lanes per step)
                     double* wbase = sp.cw + (size_t)lwarp * kCoopWarpDoubles;
                     while (bal) {
                         const int src = __ffs(bal) - 1;

@@ -79,3 +79,17 @@ def test_full_size_config3_properties():
     sub = dataclasses.replace(cfg)
     alt = sf.solve_batched(xb[:300], config=sub, grid=37)
     assert torch.equal(alt.coeffs, out.coeffs[:300]) and torch.equal(alt.iterations, out.iterations[:300])
+
+
+@pytest.mark.parametrize("precision", ["hybrid", "lean"])
+def test_n32_longest_horizon_fits_one_cta(precision):
+    """32 robots at H = 127 (128 time steps, eight two-lane warps): the slot, including hybrid's
+    warp-cooperative careful-path scratch, fits the 227 KB of shared memory."""
+    from paper_2501_19042_b200 import SafetyFilter, SolverConfig, load_problem, sample_proposals
+    from paper_2501_19042_b200.scenarios import random_swarm_doc
+    prob = load_problem(random_swarm_doc(32, 127, 3))
+    cfg = SolverConfig(max_iters=20, svars=False, precision=precision)
+    sf = SafetyFilter(prob, degree=10, config=cfg)
+    x = torch.from_numpy(sample_proposals(prob, sf.basis, 4, seed=1).proposals).cuda()
+    out = sf.solve_batched(x, config=cfg)
+    assert (out.status == 0).all() and out.eq_err.max().item() <= 1e-8
