@@ -175,6 +175,7 @@ constexpr int kTcBopBytes = 3 * 2 * 1024;
 // round-based cooperative careful path (hy_careful_rounds): per warp 32 items of 8 doubles + 16 owners x 12
 // (outputs for the 16 owner lanes of a two-lane-per-step warp; + both iterates' FP64 positions)
 constexpr int kCoopOwners = 16;
+constexpr int kCoopMaxS = 128;   // n <= 4: the cooperative careful path's scratch and target cache up to this horizon
 constexpr int kCoopWarpDoubles = 32 * 8 + kCoopOwners * 12 + 2 * 3 * 32;
 
 // hy: hybrid precision keeps the previous iterate's FP64 coefficients (Cp) and FP64 exit-residual partials
@@ -212,10 +213,12 @@ __host__ __device__ inline SmemLayout make_layout(int n, int S, int MP, int spb,
     L.pinf = q;   q = align16(q + pw * ts);                            // per warp max of the inf partials
     L.sh = q;     q = align16(q + sizeof(SlotShared));
     // hy, NB <= 4: per warp 32 items of the warp-cooperative careful path (hy_careful_item)
-    L.cp = q;     q = align16(q + ((hy && NB <= 4 && !tc) ? (size_t)((S + 31) / 32) * 32 * 8 * d : 0));
+    // (horizons up to kCoopMaxS steps: past that the careful steps stay serial, so long horizons keep fitting)
+    const bool coop4 = hy && NB <= 4 && !tc && S <= kCoopMaxS;
+    L.cp = q;     q = align16(q + (coop4 ? (size_t)((S + 31) / 32) * 32 * 8 * d : 0));
     // ... and the FP64 trig targets e(d_k) of its zero-component terms per (step, term), tagged (sample, k): the
     // next iteration's e(d_{k-1}) (hy_careful_item)
-    L.ct = q;     q = align16(q + ((hy && NB <= 4 && !tc) ? (size_t)S * (NB * (NB - 1) / 2 + NB) * (3 * d + 8) : 0));
+    L.ct = q;     q = align16(q + (coop4 ? (size_t)S * (NB * (NB - 1) / 2 + NB) * (3 * d + 8) : 0));
     // hy, NB = 32: per warp 32 items + 32 owners' outputs of the round-based cooperative careful path
     L.cw = q;     q = align16(q + ((hy && NB >= 32 && !tc) ? (size_t)((S + 15) / 16) * kCoopWarpDoubles * d : 0));
 #ifdef SGSF_SYNC_CHECK
@@ -1920,8 +1923,10 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
     const unsigned smask = __ballot_sync(0xffffffffu, ts < S);   // lanes of this warp with a step
     if constexpr (HY && NB <= 4 && TPS == 1 && !TC) {   // careful-path target cache: no entry valid yet
         constexpr int NT = NB * (NB - 1) / 2 + NB;
-        long long* tags = (long long*)(sp.ct + (size_t)S * NT * 3);
-        for (int e = lt; e < S * NT; e += gsize) tags[e] = -1;
+        if (S <= kCoopMaxS) {
+            long long* tags = (long long*)(sp.ct + (size_t)S * NT * 3);
+            for (int e = lt; e < S * NT; e += gsize) tags[e] = -1;
+        }
     }
 
     constexpr int NP = NB * (NB - 1) / 2;
@@ -2151,7 +2156,7 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                 const bool car = ts < S && (fmin(zmin_ws, zmin_pairs) == T(0) || zprev);
                 const uint32_t bal = __ballot_sync(0xffffffffu, car);
                 const int nc = __popc(bal);
-                if (nc != 0 && nc * NT <= 32 && p.coop) {
+                if (nc != 0 && nc * NT <= 32 && p.coop && S <= kCoopMaxS) {
                     double* scr = sp.cp + (size_t)lwarp * 32 * kCoopItem;
                     const int kk = lane / NT, bb = lane - kk * NT;
                     const int src = kk < nc ? (int)__fns(bal, 0, kk + 1) : 0;
