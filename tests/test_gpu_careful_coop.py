@@ -77,3 +77,17 @@ def test_round_based_careful_path_n32():
     for s, it in enumerate(a.iterations.tolist()):
         assert torch.equal(ha[s, :it], hb[s, :it]), s
         assert torch.allclose(la[s, :it], lb[s, :it], rtol=1e-12, atol=0), s
+
+
+@pytest.mark.parametrize("precision", ["hybrid", "lean", "strict"])
+def test_long_horizon_n4_fits(precision):
+    """Four robots at H = 300: past 128 steps the cooperative careful path's scratch is not laid out, so the
+    slot still fits one CTA (the serial careful path takes the rare careful steps)."""
+    from paper_2501_19042_b200 import SafetyFilter, SolverConfig, load_problem, sample_proposals
+    from paper_2501_19042_b200.scenarios import random_swarm_doc
+    prob = load_problem(random_swarm_doc(4, 300, 3))
+    cfg = SolverConfig(max_iters=20, svars=False, precision=precision)
+    sf = SafetyFilter(prob, degree=10, config=cfg)
+    x = torch.from_numpy(sample_proposals(prob, sf.basis, 4, seed=1).proposals).cuda()
+    out = sf.solve_batched(x, config=cfg)
+    assert (out.status == 0).all() and out.eq_err.max().item() <= 1e-8
