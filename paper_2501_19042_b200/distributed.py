@@ -58,6 +58,36 @@ def gather_outputs(out, batch: int, group=None) -> dict:
     return res
 
 
+def gather_outputs_async(out, batch: int, group=None):
+    """gather_outputs without blocking the calling stream: NCCL all-gathers issued with async_op=True (their
+    kernels run on the process group's stream; the caller's stream does not wait for them, so the next batch
+    on it is not queued behind a collective that needs an SM).  Returns finish() -> the gathered dict, which
+    makes the current stream wait for the collectives.  Equal shards only (batch divisible by the world size:
+    no padding kernel); otherwise it gathers synchronously."""
+    world = dist.get_world_size(group)
+    if dist.get_backend(group) != "nccl" or batch % world:
+        res = gather_outputs(out, batch, group)
+        return lambda: res
+    get = (lambda k: out[k]) if isinstance(out, dict) else (lambda k: getattr(out, k))
+    pend = []
+    for k in GATHERED_FIELDS:
+        try:
+            t = get(k)
+        except (KeyError, AttributeError):
+            continue
+        if t is None:
+            continue
+        t = t.contiguous()
+        full = torch.empty((batch,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        pend.append((k, full, dist.all_gather_into_tensor(full, t, group=group, async_op=True)))
+
+    def finish() -> dict:
+        for _, _, work in pend:
+            work.wait()
+        return {k: full for k, full, _ in pend}
+    return finish
+
+
 def sharded_solve(sf, xi_bar: torch.Tensor, config=None, group=None, **kw) -> dict:
     """Filter a full (B, dim) batch across the ranks of `group`; every rank returns the full outputs.
 

@@ -373,7 +373,7 @@ class SafetyFilter:
         return out
 
     def solve_pipelined(self, batches, config: SolverConfig | None = None, streams: int = 2, prepare=None,
-                        finish=None, **solve_kw) -> list:
+                        finish=None, keep: bool = True, **solve_kw) -> list:
         """Filter a sequence of (B, dim) proposal batches with ``streams`` of them in flight.
 
         Batch k is one :meth:`solve_batched` launch on side stream k % streams.  A batch's last samples
@@ -382,7 +382,8 @@ class SafetyFilter:
         outputs, and a sample's result does not depend on scheduling, so the results equal
         ``[solve_batched(x) for x in batches]`` bit for bit.  ``prepare(k, x) -> x`` and
         ``finish(k, out)`` run on batch k's stream (host-to-device copies of the proposals in, copies of
-        the results out).  The caller's stream waits for every batch before this returns.
+        the results out).  The caller's stream waits for every batch before this returns.  ``keep=False``
+        returns no outputs (``finish`` consumes them), so each batch's blocks are reused by a later one.
         """
         if streams < 1:
             raise ValueError("streams must be >= 1")
@@ -404,10 +405,11 @@ class SafetyFilter:
                 out = self.solve_batched(x, config=config, **solve_kw)
                 if finish is not None:
                     finish(k, out)
-            for t in vars(out).values():   # consumed on the caller's stream: keep the blocks until it is done
-                if isinstance(t, torch.Tensor):
-                    t.record_stream(cur)
-            outs.append(out)
+            if keep:
+                for t in vars(out).values():   # consumed on the caller's stream: keep the blocks until it is done
+                    if isinstance(t, torch.Tensor):
+                        t.record_stream(cur)
+                outs.append(out)
         for st in side:
             cur.wait_stream(st)
         return outs

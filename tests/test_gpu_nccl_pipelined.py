@@ -10,14 +10,15 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
-def test_pipelined_solve_with_nccl_gather_world1():
+@pytest.mark.parametrize("asynchronous", [False, True])
+def test_pipelined_solve_with_nccl_gather_world1(asynchronous):
     import torch.distributed as dist
 
     from paper_2501_19042_b200 import SafetyFilter, SolverConfig, sample_proposals
-    from paper_2501_19042_b200.distributed import gather_outputs
+    from paper_2501_19042_b200.distributed import gather_outputs, gather_outputs_async
     from paper_2501_19042_b200.scenarios import config_problem
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-    os.environ.setdefault("MASTER_PORT", "29531")
+    os.environ["MASTER_PORT"] = "29531" if not asynchronous else "29532"
     torch.cuda.set_device(0)
     dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
     try:
@@ -28,9 +29,15 @@ def test_pipelined_solve_with_nccl_gather_world1():
         gathered = {}
 
         def finish(k, out):
-            gathered[k] = gather_outputs(out, out.coeffs.shape[0])
+            if asynchronous:   # (the bench's N-GPU step: collectives not waited for on the batch's stream)
+                gathered[k] = gather_outputs_async(out, out.coeffs.shape[0])
+            else:
+                gathered[k] = gather_outputs(out, out.coeffs.shape[0])
 
         outs = sf.solve_pipelined(iter(xs), config=cfg, finish=finish)
+        if asynchronous:
+            for k in list(gathered):
+                gathered[k] = gathered[k]()
         torch.cuda.synchronize()
         for k, x in enumerate(xs):
             ref = sf.solve_batched(x, config=cfg)
