@@ -384,6 +384,9 @@ class SafetyFilter:
         ``finish(k, out)`` run on batch k's stream (host-to-device copies of the proposals in, copies of
         the results out).  The caller's stream waits for every batch before this returns.  ``keep=False``
         returns no outputs (``finish`` consumes them), so each batch's blocks are reused by a later one.
+        Keep ``prepare`` / ``finish`` to copies (copy engines): a kernel there waits for a free SM behind the
+        other stream's batch, and the next batch on its stream waits for it (bench.py measured 7.1 against
+        6.9 ms per batch with two small reductions per batch).
         """
         if streams < 1:
             raise ValueError("streams must be >= 1")
