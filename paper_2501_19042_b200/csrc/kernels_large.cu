@@ -12,7 +12,12 @@ static int launch_large_t(const LaunchInfo& li, SolveParams& p, const sgsf_confi
     int dev_smem = 0;
     cudaError_t e = cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, li.device);
     if (e != cudaSuccess) return internal_fail(SGSF_ERR_CUDA, cudaGetErrorString(e));
-    const LargeLayout L = make_large_layout<T, 64>(p.n, p.S, MP, p.want_prev || HY);
+    p.large_coop = 1;
+    LargeLayout L = make_large_layout<T, 64>(p.n, p.S, MP, p.want_prev || HY, 1);
+    if (L.total > (size_t)dev_smem) {   // phase B's partials do not fit: the one-warp exact pass
+        p.large_coop = 0;
+        L = make_large_layout<T, 64>(p.n, p.S, MP, p.want_prev || HY, 0);
+    }
     if (L.total > (size_t)dev_smem)
         return internal_fail(SGSF_ERR_UNSUPPORTED, "problem too large for one CTA: one sample needs " +
                                                        std::to_string(L.total / 1024) + " KB of shared memory, the device allows " +

@@ -52,7 +52,7 @@ struct LargeLayout {
 };
 
 template <typename T, int NB>
-__host__ __device__ inline LargeLayout make_large_layout(int n, int S, int MP, int want_prev) {
+__host__ __device__ inline LargeLayout make_large_layout(int n, int S, int MP, int want_prev, int coop = 1) {
     LargeLayout L;
     size_t o = 0;
     const size_t d = sizeof(double), ts = sizeof(T);
@@ -73,7 +73,9 @@ __host__ __device__ inline LargeLayout make_large_layout(int n, int S, int MP, i
     // pass's scratch -- the near-pair R rows of phase A and the partials of phase B -- lives in it; the kernel
     // clears it again before the g accumulation.  (As separate buffers they pushed 64 robots at degree >= 12
     // past the 227 KB of shared memory.)
-    const size_t pb = sizeof(T) == 4 ? 1 : 0;   // phase B: T = float (lean, hybrid); FP64 "strict" keeps the one-warp pass
+    // phase B (its partials live in the g region) unless that does not fit: the launcher then retries with coop = 0
+    // and the kernel keeps the one-warp exact pass (FP64 "strict" at long horizons)
+    const size_t pb = coop ? 1 : 0;
     const size_t xr_b = align16(pb * 2 * kLargeWarps * 2 * 32 * 3 * ts);   // [buf][warp][rr][lane][axis] R parts
     const size_t xnl_b = align16(pb * 2 * kLargeWarps * 2 * kNearCap * 2);  // [buf][warp][rr] near sublists
     const size_t xcnt_b = align16(pb * 2 * kLargeWarps * 2 * 4);             // ... their lengths
@@ -232,7 +234,7 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
     static_assert(NB == 64, "K1L is laid out for 64 robots (lane l owns robots l and l + 32)");
     static_assert(!HY || sizeof(T) == 4, "hybrid precision screens in FP32");
     extern __shared__ __align__(16) unsigned char smem[];
-    const LargeLayout L = make_large_layout<T, NB>(p.n, p.S, MP, p.want_prev || HY);
+    const LargeLayout L = make_large_layout<T, NB>(p.n, p.S, MP, p.want_prev || HY, p.large_coop);
     constexpr int M2P = 2 * MP;
     constexpr int MT = NB / 8;   // 8-robot DMMA tiles
     constexpr int KT = MP / 2;   // 4-column k-steps over [C | u]
@@ -266,7 +268,7 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
     uint16_t* snear = (uint16_t*)(smem + L.snear);
     int* sncnt = (int*)(smem + L.sncnt);
     LargeShared* sh = (LargeShared*)(smem + L.sh);
-    constexpr bool kCoopExact = sizeof(T) == 4;   // phase B: exact steps taken by all warps together
+    const bool kCoopExact = p.large_coop != 0;   // phase B: exact steps taken by all warps together
     int* sdefer = (int*)(smem + L.sdefer);
     T* xr = (T*)(smem + L.xr);
     uint16_t* xnl = (uint16_t*)(smem + L.xnl);
@@ -752,7 +754,7 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
             // near list in the serial pass's (robot half, partner, lane) order) while the others start the
             // next step.  An exact pass costs ~93K cycles on one warp, and an iteration has fewer of them than
             // warps, so the serial pass left seven warps waiting.
-            if constexpr (kCoopExact) {
+            if (kCoopExact) {
                 __syncthreads();   // every warp's deferred steps are marked
 #ifdef SGSF_LARGE_PT
                 const long long lpt_b0 = clock64();

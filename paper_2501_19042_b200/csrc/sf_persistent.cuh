@@ -63,6 +63,7 @@ struct SmemLayout {
 struct SolveParams {
     int n, S, m1, MP, batch, max_iters, early_stop, want_prev, spb, wps;
     int coop;   // HY, NB <= 4: warp-cooperative careful path (hy_careful_item); 0 = serial (SGSF_NO_COOP=1, tests)
+    int large_coop;   // K1L: phase B (exact steps by all warps) laid out and taken (0: it did not fit)
     double rho, tol_res, tol_eq;
     // hybrid precision (HY kernels): FP32 screening with guard bands, FP64 values.  hy_delta = half-width of
     // the band around tol_res in which the FP32-measured exit residual is re-evaluated in FP64
