@@ -82,3 +82,17 @@ def test_large_n_long_run_matches_oracle():
         assert np.abs(coeffs[b] - r.coeffs).max() <= 1e-5 * np.abs(r.coeffs).max(), b
         np.testing.assert_allclose(rinf[b], r.residual_inf, rtol=1e-3, atol=1e-9)
         np.testing.assert_allclose(rl2[b], r.residual_l2, rtol=1e-3, atol=1e-9)
+
+
+@pytest.mark.parametrize("precision", ["strict", "hybrid"])
+def test_k1l_long_horizon_layout_fallback(precision):
+    """64 robots at H = 170: in FP64 phase B's partials do not fit next to the state, so the launcher lays
+    out the one-warp exact pass (SolveParams.large_coop = 0); both layouts solve."""
+    from paper_2501_19042_b200 import SafetyFilter, SolverConfig, load_problem, sample_proposals
+    from paper_2501_19042_b200.scenarios import random_swarm_doc
+    prob = load_problem(random_swarm_doc(64, 170, 5))
+    cfg = SolverConfig(max_iters=10, svars=False, precision=precision)
+    sf = SafetyFilter(prob, degree=10, config=cfg)
+    x = torch.from_numpy(sample_proposals(prob, sf.basis, 2, seed=1).proposals).cuda()
+    out = sf.solve_batched(x, config=cfg)
+    assert (out.status == 0).all() and out.eq_err.max().item() <= 1e-8
