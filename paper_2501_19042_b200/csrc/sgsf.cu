@@ -253,7 +253,12 @@ int sgsf_solve(sgsf_handle_t* h, int batch, const double* xi_bar, const double* 
             if (n <= 4) SGSF_PICK(double, 4, 384, 1);
             else if (n <= 8) SGSF_PICK(double, 8, 256, 1);
             else if (n <= 16) SGSF_PICK(double, 16, 256, 1);
-            else SGSF_PICK(double, 32, 256, 2);
+            else {
+                SGSF_PICK(double, 32, 256, 2);
+                // FP64 17..32 robots at long horizons: one K1 slot does not fit (two FP64 position buffers);
+                // K1L (one CTA of eight warps per sample, positions per step in a per-warp scratch) does
+                if (rc == SGSF_ERR_UNSUPPORTED) rc = launch_large(li, p, cfg, timing, stream, true);
+            }
         }
 #undef SGSF_PICK
     }

@@ -49,11 +49,18 @@ def test_n32_matches_oracle_fixed_iterations(precision, horizon, rtol):
     assert out.eq_err.max().item() <= 1e-8
 
 
-def test_n32_strict_full_horizon_reports_smem_limit():
-    """Strict (FP64 positions) at 32 robots and H=100 does not fit one CTA: a clean error, no launch."""
-    doc, sf, cfg, props = _setup(32, 100, 3, 2, 5, "strict")
-    with pytest.raises(NotImplementedError, match="shared memory"):
-        sf.solve_batched(torch.from_numpy(props).cuda(), config=cfg)
+def test_n32_strict_full_horizon_runs_on_k1l():
+    """Strict (FP64 positions) at 32 robots and H = 100 does not fit one K1 slot; the launcher hands it to K1L
+    (one CTA of eight warps per sample), which matches the oracle at fixed iterations."""
+    doc, sf, cfg, props = _setup(32, 100, 3, 2, 12, "strict")
+    out = sf.solve_batched(torch.from_numpy(props).cuda(), config=cfg)
+    ref = _oracle(doc, props, 12)
+    coeffs = out.coeffs.cpu().numpy()
+    rinf = out.residual_inf.cpu().numpy()
+    for b, r in enumerate(ref):
+        assert np.abs(coeffs[b] - r.coeffs).max() <= 1e-9 * np.abs(r.coeffs).max(), b
+        np.testing.assert_allclose(rinf[b], r.residual_inf, rtol=1e-7, atol=1e-9)
+    assert out.eq_err.max().item() <= 1e-8
 
 
 def test_full_size_config3_properties():
