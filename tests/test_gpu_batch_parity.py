@@ -27,9 +27,9 @@ pytestmark = pytest.mark.gpu
 
 @pytest.mark.parametrize("name,precision", [
     ("batch_cfg2", "strict"), ("batch_cfg2", "hybrid"), ("batch_ws_tight", "strict"), ("batch_ws_tight", "hybrid"),
-    # BASELINE configs 3 / 4 with early stop: 32 robots (K1, two lanes per step; strict does not fit one CTA at
-    # H = 100) and 64 robots, H = 150, max_iters 1000 (K1L, FP64)
-    ("batch_cfg3", "hybrid"), ("batch_cfg4", "strict"), ("batch_cfg4e", "strict"), ("batch_cfg4", "hybrid"),
+    # BASELINE configs 3 / 4 with early stop: 32 robots (K1, two lanes per step; strict does not fit one K1 slot
+    # at H = 100 and runs on K1L) and 64 robots, H = 150, max_iters 1000 (K1L)
+    ("batch_cfg3", "hybrid"), ("batch_cfg3", "strict"), ("batch_cfg4", "strict"), ("batch_cfg4e", "strict"), ("batch_cfg4", "hybrid"),
     ("batch_cfg4e", "hybrid")])
 def test_whole_batch_matches_reference(name, precision):
     g, o = run(name, precision)
