@@ -17,8 +17,12 @@ def test_pipelined_solve_with_nccl_gather_world1(asynchronous):
     from paper_2501_19042_b200 import SafetyFilter, SolverConfig, sample_proposals
     from paper_2501_19042_b200.distributed import gather_outputs, gather_outputs_async
     from paper_2501_19042_b200.scenarios import config_problem
-    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-    os.environ["MASTER_PORT"] = "29531" if not asynchronous else "29532"
+    import socket
+    with socket.socket() as sk:   # a free port (127.0.0.1 rendezvous)
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(0)
     dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
     try:
