@@ -2399,6 +2399,37 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                             for (int w = 0; w < SWT; ++w) na += __popc(am[w]);
                         }
                         const T* Rb = (const T*)(par ? sp.P1 : sp.P0) + ax * NB;   // the old rows hold R
+                        if constexpr (TC) {
+                            // TC: k-steps over 4-step chunks with an active step (steps 4c .. 4c + 3, inactive
+                            // ones as zero rows) -- a warp-uniform walk over a chunk mask instead of a __fns per
+                            // lane and k-step
+                            uint32_t cm = 0u;   // bit c: chunk c (steps 4c .. 4c + 3) holds an active step
+#pragma unroll
+                            for (int w = 0; w < 4; ++w) {
+#pragma unroll
+                                for (int c = 0; c < 8; ++c)
+                                    if ((am[w] >> (4 * c)) & 0xfu) cm |= 1u << (8 * w + c);
+                            }
+                            while (cm) {
+                                const int c = __ffs(cm) - 1;
+                                cm &= cm - 1;
+                                const int t = 4 * c + fc;
+                                const bool act = t < S && ((am[t >> 5] >> (t & 31)) & 1u);
+                                double bw[2];
+#pragma unroll
+                                for (int nt = 0; nt < 2; ++nt) {
+                                    const int qb = 8 * nt + fr;
+                                    bw[nt] = (act && qb < MP) ? (double)Wt[t * MP + qb] : 0.0;
+                                }
+#pragma unroll
+                                for (int mt = 0; mt < MT; ++mt) {
+                                    const int rob = 8 * mt + fr;
+                                    const double a = (act && rob < n) ? (double)Rb[t * RS + rob] : 0.0;
+#pragma unroll
+                                    for (int nt = 0; nt < 2; ++nt) dmma884(gq[mt][nt][0], gq[mt][nt][1], a, bw[nt]);
+                                }
+                            }
+                        } else
                         for (int kk = 0; 4 * kk < na; ++kk) {
                             int rem = 4 * kk + fc, t = -1;   // this lane's k = active step number
                             if (rem < na) {
