@@ -379,7 +379,8 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
         __shared__ long long lpt_dur[kLargeWarps];
         __shared__ int lpt_ex[kLargeWarps];
         __shared__ long long lpt_exq[kLargeWarps];
-        long long lqa[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // CTA 0 warp 0 quiet steps: positions, statistics, near pairs + ws, far
+        long long lqa[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        long long lmx = 0;   // thread 0: cycles from the U step through the xi-step barrier   // CTA 0 warp 0 quiet steps: positions, statistics, near pairs + ws, far
         double lpt_max = 0, lpt_mean = 0, lpt_exmax = 0, lpt_exmean = 0, lpt_qmax = 0, lpt_excyc = 0;
 #endif
         for (int k = 0;; ++k) {
@@ -1086,6 +1087,8 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
                             printf("LPT cta %d sample %d iters %d term-pass cycles: slowest warp %.0f mean %.0f slowest-without-exact %.0f | exact steps per warp: max %.2f mean %.2f, exact-step cycles per iteration (all warps) %.0f\n",
                                    blockIdx.x, sample, k, lpt_max / (k + 1), lpt_mean / (k + 1), lpt_qmax / (k + 1), lpt_exmax / (k + 1),
                                    lpt_exmean / (k + 1), lpt_excyc / (k + 1));
+                        if (blockIdx.x < 4) printf("LMX cta %d: xi-step phase %lld cycles per iteration\n", blockIdx.x, lmx / (k + 1));
+                        lmx = 0;
                         lpt_max = lpt_mean = lpt_exmax = lpt_exmean = lpt_qmax = lpt_excyc = 0;
 #endif
                         sh->sample = next_sample(p);
@@ -1108,6 +1111,9 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
             }
             __syncthreads();
 
+#ifdef SGSF_LARGE_PT
+            const long long lmx0 = clock64();
+#endif
             // ---------------- xi-step per axis (K1's DMMA formulation), equality check, commit
             const int fr = lane >> 2, fc = lane & 3;
             for (int ax = warp; ax < 3; ax += kLargeWarps) {
@@ -1225,6 +1231,9 @@ __global__ void __launch_bounds__(32 * kLargeWarps, 1) sf_large_kernel(const Sol
                 }
             }
             prev_active = any_active;
+#ifdef SGSF_LARGE_PT
+            if (tid == 0) lmx += clock64() - lmx0;
+#endif
             __syncthreads();
         }
     }
