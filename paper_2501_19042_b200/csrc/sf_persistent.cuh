@@ -2046,7 +2046,11 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                 }
             }
             if (ts < S) {
+#ifndef SGSF_NO_POS   // (timing experiments only: positions from the first iterate, results wrong)
                 if constexpr (!TC) positions_part<T, NB, RH, MP>(Wt, (const T*)sp.Cf, ts, r0, n, pos);
+#else
+                if constexpr (!TC) if (k == 0) positions_part<T, NB, RH, MP>(Wt, (const T*)sp.Cf, ts, r0, n, pos);
+#endif
                 store_part<T, NB, RH>(Prow_new, r0, pos);
                 if (k == 0) {
                     store_part<T, NB, RH>(Prow_old, r0, pos);   // no previous iterate: "old" := "new"
