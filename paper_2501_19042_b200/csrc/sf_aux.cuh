@@ -47,7 +47,9 @@ __device__ __forceinline__ double eval_pos(const double* __restrict__ C, const d
 // ---------------------------------------------------------------- K2: verdict
 // check_original_constraints (assembly.py:437-487): margins of problem.py:113-137
 // in FP64 on C W^T; block per sample, fixed-order reductions.
-__global__ void verdict_kernel(AuxParams a, int batch, const double* __restrict__ coeffs,
+// MP (compile-time padded degree + 1, 0 = runtime m1): the position dot products unroll
+template <int MP = 0>
+__global__ void __launch_bounds__(256) verdict_kernel(AuxParams a, int batch, const double* __restrict__ coeffs,
                                const uint8_t* __restrict__ converged, double tol, uint8_t* ok,
                                uint8_t* feasible, double* pmin_out, double* wmax_out, int* pcount,
                                int* wcount) {
@@ -81,12 +83,26 @@ __global__ void verdict_kernel(AuxParams a, int batch, const double* __restrict_
         __syncthreads();
         for (int e = threadIdx.x; e < 3 * n * tc; e += blockDim.x) {
             const int row = e / tc, t = e - row * tc;
-            pos[row * AUX_TCH + t] = eval_pos(C + row * m1, Ww + t * m1, m1);
+            if constexpr (MP > 0) {   // the same fma order as eval_pos (q ascending from 0)
+                const double* c = C + row * m1;
+                const double* w = Ww + t * m1;
+                double sacc = 0.0;
+#pragma unroll
+                for (int q = 0; q < MP; ++q)
+                    if (q < m1) sacc = fma(c[q], w[q], sacc);
+                pos[row * AUX_TCH + t] = sacc;
+            } else {
+                pos[row * AUX_TCH + t] = eval_pos(C + row * m1, Ww + t * m1, m1);
+            }
         }
         __syncthreads();
-        for (int e = threadIdx.x; e < (P + n) * AUX_TCH; e += blockDim.x) {
-            const int term = e / AUX_TCH, t = e - term * AUX_TCH;   // t = lane: a warp takes one term
-            if (t >= tc) continue;
+        // a warp pass takes tpw terms x tc steps (lane -> (term offset, step)): the last, partial window of
+        // the horizon packs several terms per warp instead of idling the lanes past tc
+        const int tpw = AUX_TCH / tc, lane = threadIdx.x & 31, sub = lane / tc, t = lane - sub * tc;
+        const int nwarps = (int)(blockDim.x >> 5), wid = (int)(threadIdx.x >> 5);
+        for (int term0 = wid * tpw; term0 < P + n; term0 += nwarps * tpw) {
+            const int term = term0 + sub;
+            if (sub >= tpw || term >= P + n) continue;
             double dx, dy, dz, a2, b2;
             if (term < P) {
                 const int ij = ptab[term], i = ij & 0xff, j = ij >> 8;

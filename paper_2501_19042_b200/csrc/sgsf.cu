@@ -276,8 +276,9 @@ int sgsf_verdict(sgsf_handle_t* h, int batch, const double* coeffs, const uint8_
     const int threads = 256;
     const size_t smem = (size_t)(3 * h->n * h->m1 + 3 * h->n * AUX_TCH + AUX_TCH * h->m1) * sizeof(double) +
                         threads * (2 * sizeof(double) + 2 * sizeof(int)) + (size_t)h->P * sizeof(int);
-    CUDA_TRY(cudaFuncSetAttribute(verdict_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    verdict_kernel<<<batch, threads, smem, (cudaStream_t)stream>>>(aux_params(h), batch, coeffs, converged, tol,
+    auto kern = h->m1 <= 12 ? verdict_kernel<12> : (h->m1 <= 16 ? verdict_kernel<16> : verdict_kernel<0>);
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<batch, threads, smem, (cudaStream_t)stream>>>(aux_params(h), batch, coeffs, converged, tol,
                                                                     out->ok, out->feasible, out->pair_margin_min,
                                                                     out->ws_margin_max, out->pair_viol,
                                                                     out->ws_viol);
