@@ -6,7 +6,7 @@ namespace sgsf {
 
 template <int NB, int MP>
 static int launch_score(const SolveParams& p, float* score, cudaStream_t stream) {
-    start_score_kernel<NB, MP><<<p.batch, 128, 0, stream>>>(p, score);
+    start_score_kernel<NB, MP><<<p.batch, kScoreThreads, 0, stream>>>(p, score);
     internal_count_launch(1);
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? SGSF_OK : internal_fail(SGSF_ERR_CUDA, std::string("start_score: ") + cudaGetErrorString(e));

@@ -19,11 +19,13 @@
 
 namespace sgsf {
 
-// one CTA per sample, thread t = time step; FP32 is plenty for a heuristic
+constexpr int kScoreThreads = 128;   // (8 steps per round at 16 robots; 256 measured slower)
+
+// one CTA per sample; FP32 is plenty for a heuristic
 template <int NB, int MP>
-__global__ void __launch_bounds__(128) start_score_kernel(const SolveParams p, float* __restrict__ score) {
+__global__ void __launch_bounds__(kScoreThreads) start_score_kernel(const SolveParams p, float* __restrict__ score) {
     __shared__ float Cs[3 * NB * MP];
-    __shared__ float red[4];
+    __shared__ float red[kScoreThreads / 32];
     const int b = blockIdx.x;
     const int n = p.n, m1 = p.m1, S = p.S, R3 = 3 * n;
     const int dim = R3 * m1;
@@ -62,7 +64,7 @@ __global__ void __launch_bounds__(128) start_score_kernel(const SolveParams p, f
     // thread = (step slot, robot): its robot's position into shared memory, then its pairs (i, j > i) and its
     // workspace term (few registers: many CTAs per SM; the thread-per-step form held 48 positions in 255
     // registers and took 65 us per 1000 samples)
-    constexpr int SPR = 128 / NB;   // steps per round
+    constexpr int SPR = kScoreThreads / NB;   // steps per round
     __shared__ float Pt[SPR][3 * NB];
     const int sl = threadIdx.x / NB, i = threadIdx.x % NB;
     float v = 0.f;
