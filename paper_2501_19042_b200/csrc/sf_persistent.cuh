@@ -1523,6 +1523,18 @@ __device__ __forceinline__ double2 hy_exit64_inline(const P& p, const double* Cn
                             if (pb != fb0 && pb != fb1) base = fmax(base, tv[u] + bv[k]);
                         }
                     }
+            } else if constexpr (NB <= 16) {   // many flagged pairs: every pair interior at the old iterate, with
+                // each robot's D p evaluated once (registers: this runs out of line, hy_exit64_call)
+                double dv[NB];
+#pragma unroll
+                for (int i = 0; i < NB; ++i) dv[i] = i < n ? hy_dp_w<MP>(Cn, Co, wr, ax * n + i) : 0.0;
+#pragma unroll
+                for (int i = 0; i < NB; ++i)
+#pragma unroll
+                    for (int j = i + 1; j < NB; ++j) {
+                        const int pb = pair_bit<NB>(i, j);
+                        if (j < n && ((om[pb >> 5] >> (pb & 31)) & 1u)) base = fmax(base, fabs(dv[i] - dv[j]));
+                    }
             } else {   // many flagged pairs: scan every pair interior at the old iterate
 #pragma unroll 1
                 for (int i = 0; i < n; ++i) {
