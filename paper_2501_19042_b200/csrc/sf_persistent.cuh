@@ -1576,7 +1576,7 @@ __device__ __forceinline__ double2 hy_exit64_inline(const P& p, const double* Cn
                                      (j >= 0 ? hy_dp_w<MP>(Cn, Co, wr, ax * n + j) : 0.0);
                     e2 = fma(e, e, e2);
                 }
-                const D3 dn = term_diff64s<MP>(p, Cn, Wrow, i, j), dol = term_diff64s<MP>(p, Co, Wrow, i, j);
+                const D3 dn = term_diff64<MP>(p, Cn, wr, i, j), dol = term_diff64<MP>(p, Co, wr, i, j);   // (the W row in registers: pos64s's values)
                 const D3 x = resid64(j >= 0, dol, dn, family64(p, j >= 0));
                 flmax = fmax(flmax, fmax(fabs(x.x), fmax(fabs(x.y), fabs(x.z))));
                 adj += (x.x * x.x + x.y * x.y + x.z * x.z) - e2;
