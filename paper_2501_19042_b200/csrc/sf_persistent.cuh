@@ -2421,10 +2421,13 @@ __global__ void __launch_bounds__(MAXT, 1) sf_persistent_kernel(const SolveParam
                             // lane and k-step
                             uint32_t cm = 0u;   // bit c: chunk c (steps 4c .. 4c + 3) holds an active step
 #pragma unroll
-                            for (int w = 0; w < 4; ++w) {
-#pragma unroll
-                                for (int c = 0; c < 8; ++c)
-                                    if ((am[w] >> (4 * c)) & 0xfu) cm |= 1u << (8 * w + c);
+                            for (int w = 0; w < 4; ++w) {   // nonzero nibbles of the word, compacted to a byte
+                                uint32_t x = am[w];
+                                x = (x | (x >> 1) | (x >> 2) | (x >> 3)) & 0x11111111u;
+                                x = (x | (x >> 3)) & 0x03030303u;
+                                x = (x | (x >> 6)) & 0x000F000Fu;
+                                x = (x | (x >> 12)) & 0xFFu;
+                                cm |= x << (8 * w);
                             }
                             while (cm) {
                                 const int c = __ffs(cm) - 1;
