@@ -3,6 +3,7 @@
     python tests/golden/make_golden_batch.py cfg2        # all 1000 config-2 bench proposals
     python tests/golden/make_golden_batch.py ws_tight    # converged-but-violating workspace case
     python tests/golden/make_golden_batch.py cfg3 cfg4   # early-stop subsets at n = 32 / 64
+    python tests/golden/make_golden_batch.py fuzz        # 64 random scenarios x 8 proposals, early stop
 
 Like ``make_golden.py`` this builds the reference's own Cython kernel in a
 scratch copy of ``/root/reference/pkg`` and imports ``swarmfilter`` from it
@@ -73,7 +74,7 @@ def _solve_one(args):
             np.asarray(r.coeffs), np.asarray(r.multipliers), dt)
 
 
-def run_batch(name, doc, proposals, degree=10, keep_coeffs=64, procs=None, select=None, **cfg):
+def run_batch(name, doc, proposals, degree=10, keep_coeffs=64, procs=None, select=None, save=True, **cfg):
     import multiprocessing as mp
     B = len(proposals)
     maxit = cfg.get("max_iters", 200)
@@ -120,6 +121,8 @@ def run_batch(name, doc, proposals, degree=10, keep_coeffs=64, procs=None, selec
             "procs": procs, "sample_iterations": int(out["iterations"].sum())}
     if select is not None:   # rows `indices` of a `batch`-sample draw (seed 0) of bench.py's batch
         meta["select"] = select
+    if not save:
+        return out, meta
     np.savez_compressed(HERE / f"{name}.npz", meta=np.array(json.dumps(meta)), **out)
     print(f"{name}: B={B} iterations {out['iterations'].min()}..{out['iterations'].max()} "
           f"(mean {out['iterations'].mean():.1f}) converged {out['converged'].sum()} "
@@ -151,6 +154,76 @@ def ws_tight_doc():
             "boundary": [{"start": {"p": list(s)}, "goal": {"p": list(g)}} for s, g in zip(starts, goals)]}
 
 
+FUZZ_MAXIT = 300
+
+
+def fuzz_cases(count=64, seed=2026):
+    """Random scenarios for the early-stop fuzz fixture: robots 2..40 (every K1 template, the tensor-core
+    n = 16 slot, the two-lane n = 17..32 slot and K1L), horizons 20..127, degrees 7..15, rho, tol_residual and
+    proposal spread varied; 8 proposals each."""
+    from paper_2501_19042_b200.scenarios import random_swarm_doc
+    rng = np.random.default_rng(seed)
+    cases = []
+    for c in range(count):
+        u = rng.random()
+        if u < 0.55:
+            n = int(rng.choice([2, 3, 4, 5, 6, 7, 8, 9, 11, 12]))
+            H = int(rng.choice([20, 40, 60, 100, 120]))
+        elif u < 0.85:
+            n = int(rng.choice([13, 14, 15, 16]))
+            H = int(rng.choice([40, 60, 96, 100, 110, 127]))
+        elif u < 0.95:
+            n = int(rng.integers(17, 33))
+            H = int(rng.choice([20, 30, 40]))
+        else:
+            n = int(rng.integers(33, 41))
+            H = int(rng.choice([20, 30]))
+        cases.append({"n": n, "H": H, "scenario_seed": int(rng.integers(0, 10000)),
+                      "degree": int(rng.integers(7, 16)), "rho": float(rng.choice([0.5, 1.0, 2.0])),
+                      "tol_residual": float(rng.choice([1e-3, 1e-3, 3e-3, 1e-2])),
+                      "spread": float(rng.choice([0.25, 0.6, 1.0])), "seed": int(rng.integers(0, 1000)), "batch": 8})
+    return cases
+
+
+def fuzz_doc(case):
+    from paper_2501_19042_b200.scenarios import random_swarm_doc
+    return random_swarm_doc(case["n"], case["H"], case["scenario_seed"])
+
+
+def run_fuzz(name="batch_fuzz", count=64, seed=2026):
+    """One fixture of many small random scenarios (early stop on), concatenated; meta["cases"] says how each
+    slice was made (problem, degree, solver config, proposal seed / spread, SHA-256 of the proposals)."""
+    parts, cases = [], []
+    off = 0
+    todo = fuzz_cases(count, seed)
+    dmax = max(3 * c["n"] * (c["degree"] + 1) for c in todo)   # subset rows NaN-padded to the widest case
+    for case in todo:
+        doc = fuzz_doc(case)
+        x = proposals_for(doc, case["batch"], seed=case["seed"], degree=case["degree"], spread=case["spread"])
+        out, meta = run_batch(f"{name}[{len(cases)}]", doc, x, degree=case["degree"], keep_coeffs=case["batch"],
+                              save=False, max_iters=FUZZ_MAXIT, rho=case["rho"], tol_residual=case["tol_residual"])
+        out["tol"] = np.full(case["batch"], case["tol_residual"])
+        for k in ("coeffs_subset", "multipliers_subset"):
+            pad = np.full((case["batch"], dmax), np.nan)
+            pad[:, :out[k].shape[1]] = out[k]
+            out[k] = pad
+        parts.append(out)
+        cases.append({**case, "problem": doc, "offset": off, "proposals_sha256": meta["proposals_sha256"],
+                      "config": meta["config"]})
+        off += case["batch"]
+        print(f"  case {len(cases) - 1}: n={case['n']} H={case['H']} deg={case['degree']} rho={case['rho']} "
+              f"tol={case['tol_residual']} its {out['iterations'].tolist()} feasible {int(out['feasible'].sum())}",
+              flush=True)
+    full = {k: np.concatenate([p[k] for p in parts]) for k in parts[0]}
+    meta = {"name": name, "cases": cases, "batch": off, "reference_backend": "compiled", "degree": None,
+            "config": {"max_iters": FUZZ_MAXIT}}
+    np.savez_compressed(HERE / f"{name}.npz", meta=np.array(json.dumps(meta)), **full)
+    it = full["iterations"]
+    print(f"{name}: {len(cases)} scenarios, {off} samples, iterations {it.min()}..{it.max()} "
+          f"converged {full['converged'].sum()} feasible {full['feasible'].sum()} "
+          f"pair_viol>0 {(full['pair_viol'] > 0).sum()} ws_viol>0 {(full['ws_viol'] > 0).sum()}", flush=True)
+
+
 def main(argv):
     from make_golden import import_reference
     from paper_2501_19042_b200.scenarios import config_doc
@@ -174,6 +247,8 @@ def main(argv):
             idx = [789, 315, 566, 526, 448, 513, 938, 681]
             run_batch("batch_cfg4e", doc, proposals_for(doc, 1024)[idx], keep_coeffs=8, max_iters=1000,
                       select={"batch": 1024, "indices": idx})
+        elif which == "fuzz":   # random small scenarios with early stop (every kernel family)
+            run_fuzz()
         else:
             raise SystemExit(f"unknown batch {which}")
 

@@ -20,7 +20,7 @@ Bars (tolerances written here):
 """
 import pytest
 
-from .batch_parity import compare, run
+from .batch_parity import compare, run, run_fuzz
 
 pytestmark = pytest.mark.gpu
 
@@ -42,6 +42,32 @@ def test_whole_batch_matches_reference(name, precision):
     assert rep["margin_err_max"] <= tol
     assert rep["viol_count_equal"] == rep["same_iterate"]
     assert rep["coeff_rel_err_max"] is not None and rep["coeff_rel_err_max"] <= tol
+
+
+@pytest.mark.parametrize("precision", ["strict", "hybrid"])
+def test_fuzz_scenarios_match_reference(precision):
+    """``batch_fuzz``: 64 random scenarios x 8 proposals solved by the real reference with early stop -- 2 to 40
+    robots (every K1 template incl. the tensor-core n = 16 slot, the two-lane slot and K1L), horizons 20 to 127,
+    degrees 7 to 15, rho 0.5 / 1 / 2, tol_residual 1e-3 to 1e-2; 443 converged, 329 feasible, 130 with pair and 12
+    with workspace violations, 70 stop at the 300-iteration cap.  The strict bar on every sample."""
+    g, o = run_fuzz(precision)
+    rep = compare(g, o, band=1e-6)
+    tol = 1e-9 if precision == "strict" else 1e-6
+    assert rep["status_ok"] == rep["batch"]
+    assert rep["iter_flip_nonborderline"] == 0, rep["iter_flips"]
+    assert rep["verdict_flip_nonborderline"] == 0, rep["verdict_flips"]
+    assert rep["iter_flip_count"] + rep["verdict_flip_count"] <= max(1, rep["batch"] // 200)
+    assert rep["margin_err_max"] <= tol
+    assert rep["viol_count_equal"] == rep["same_iterate"]
+    assert rep["coeff_rel_err_max"] is not None and rep["coeff_rel_err_max"] <= tol
+
+
+def test_fuzz_scenarios_lean_flip_rate():
+    g, o = run_fuzz("lean")
+    rep = compare(g, o, band=1e-6)
+    assert rep["status_ok"] == rep["batch"]
+    assert rep["iter_flip_count"] <= 0.10 * rep["batch"]
+    assert abs(rep["feasible_gpu"] - rep["feasible_ref"]) <= 0.05 * rep["batch"]
 
 
 @pytest.mark.parametrize("name", ["batch_cfg2", "batch_ws_tight"])

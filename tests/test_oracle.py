@@ -84,3 +84,34 @@ def test_oracle_step_functions():
         np.testing.assert_allclose(so.multiplier_update(prob, lam, xi, e, rho), st["mult_update"][c], atol=1e-12)
         np.testing.assert_allclose(so.coefficient_step(prob, xi, e, lam, rho), st["coef_step"][c], atol=1e-10)
         np.testing.assert_allclose(so.project_boundary(prob, xi), st["projected"][c], atol=1e-12)
+
+
+def test_oracle_matches_reference_fuzz_fixture():
+    """``batch_fuzz`` (64 random scenarios with early stop, made by the real reference): the proposals regenerate
+    bit for bit (SHA-256), and the oracle reproduces the reference's iteration counts, converged flags and
+    feasible verdicts on its small scenarios (n <= 6, H <= 60: the rest are the GPU tests' job)."""
+    import hashlib
+
+    from paper_2501_19042_b200 import load_problem, sample_proposals
+    from paper_2501_19042_b200.basis import build_basis
+    g = load_golden("batch_fuzz")
+    cases = g["meta"]["cases"]
+    assert len(cases) == 64 and g["meta"]["batch"] == len(g["iterations"])
+    checked = 0
+    for case in cases:
+        prob = load_problem(case["problem"])
+        basis = build_basis(prob.duration, degree=case["degree"], samples=prob.horizon_samples)
+        x = sample_proposals(prob, basis, case["batch"], seed=case["seed"], spread=case["spread"]).proposals
+        assert hashlib.sha256(np.ascontiguousarray(x, dtype=np.float64).tobytes()).hexdigest() == case["proposals_sha256"]
+        if case["n"] > 6 or case["H"] > 60:
+            continue
+        oprob = so.make_problem(case["problem"], degree=case["degree"])
+        c = case["config"]
+        for s in range(case["batch"]):
+            r = so.solve(oprob, x[s], rho=c["rho"], max_iters=c["max_iters"], tol_residual=c["tol_residual"])
+            i = case["offset"] + s
+            assert r.iterations == g["iterations"][i], (case["offset"], s)
+            assert bool(r.converged) == bool(g["converged"][i])
+            assert bool(so.feasible(oprob, r)) == bool(g["feasible"][i])
+            checked += 1
+    assert checked >= 64

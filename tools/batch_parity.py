@@ -1,6 +1,6 @@
 """Report whole-batch parity against the real reference's frozen outputs (GPU box).
 
-    python tools/batch_parity.py [batch_cfg2|batch_ws_tight ...] [--precision lean strict]
+    python tools/batch_parity.py [batch_cfg2|batch_ws_tight|batch_fuzz ...] [--precision lean strict]
 
 Writes gpurun_out/batch_parity_<name>_<precision>.json (see tests/batch_parity.py for the
 classification of iteration-count and verdict flips).
@@ -14,7 +14,7 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 
-from tests.batch_parity import compare, run  # noqa: E402
+from tests.batch_parity import compare, run, run_fuzz  # noqa: E402
 
 
 def main():
@@ -27,7 +27,7 @@ def main():
     for name in a.names:
         for prec in a.precision:
             t0 = time.perf_counter()
-            g, o = run(name, prec)
+            g, o = run_fuzz(prec, name) if name.startswith("batch_fuzz") else run(name, prec)
             rep = compare(g, o, a.band)
             rep.update(name=name, precision=prec, band=a.band, wall_s=time.perf_counter() - t0)
             (ROOT / "gpurun_out" / f"batch_parity_{name}_{prec}.json").write_text(json.dumps(rep, indent=1))
