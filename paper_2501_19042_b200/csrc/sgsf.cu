@@ -248,7 +248,11 @@ int sgsf_solve(sgsf_handle_t* h, int batch, const double* xi_bar, const double* 
             if (n <= 4) SGSF_PICK(float, 4, 512, 1);
             else if (n <= 8) SGSF_PICK(float, 8, 384, 1);
             else if (n <= 16) SGSF_PICK(float, 16, 384, 1);
-            else SGSF_PICK(float, 32, 256, 2);
+            else {
+                SGSF_PICK(float, 32, 256, 2);
+                // 17..32 robots past one two-lane slot (H >= 128, or hybrid at H = 127 with degree > 11): K1L
+                if (rc == SGSF_ERR_UNSUPPORTED) rc = launch_large(li, p, cfg, timing, stream, false);
+            }
         } else {
             if (n <= 4) SGSF_PICK(double, 4, 384, 1);
             else if (n <= 8) SGSF_PICK(double, 8, 256, 1);

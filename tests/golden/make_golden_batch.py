@@ -4,6 +4,7 @@
     python tests/golden/make_golden_batch.py ws_tight    # converged-but-violating workspace case
     python tests/golden/make_golden_batch.py cfg3 cfg4   # early-stop subsets at n = 32 / 64
     python tests/golden/make_golden_batch.py fuzz        # 64 random scenarios x 8 proposals, early stop
+    python tests/golden/make_golden_batch.py fuzz_large  # 24 random 17..64-robot scenarios x 4 proposals
 
 Like ``make_golden.py`` this builds the reference's own Cython kernel in a
 scratch copy of ``/root/reference/pkg`` and imports ``swarmfilter`` from it
@@ -157,6 +158,21 @@ def ws_tight_doc():
 FUZZ_MAXIT = 300
 
 
+def fuzz_cases_large(count=24, seed=4242):
+    """Random scenarios for the large-swarm fuzz fixture: 17..64 robots (the two-lane K1 slot and K1L, FP64 K1L
+    for strict), horizons 20..100, degrees 7..15, rho and tol_residual varied; 4 proposals each."""
+    rng = np.random.default_rng(seed)
+    cases = []
+    for c in range(count):
+        n = int(rng.integers(17, 33)) if c % 2 == 0 else int(rng.integers(33, 65))
+        H = int(rng.choice([20, 40, 60, 100]))
+        cases.append({"n": n, "H": H, "scenario_seed": int(rng.integers(0, 10000)),
+                      "degree": int(rng.integers(7, 16)), "rho": float(rng.choice([0.5, 1.0, 2.0])),
+                      "tol_residual": float(rng.choice([1e-3, 3e-3, 1e-2])),
+                      "spread": float(rng.choice([0.25, 0.6])), "seed": int(rng.integers(0, 1000)), "batch": 4})
+    return cases
+
+
 def fuzz_cases(count=64, seed=2026):
     """Random scenarios for the early-stop fuzz fixture: robots 2..40 (every K1 template, the tensor-core
     n = 16 slot, the two-lane n = 17..32 slot and K1L), horizons 20..127, degrees 7..15, rho, tol_residual and
@@ -190,12 +206,12 @@ def fuzz_doc(case):
     return random_swarm_doc(case["n"], case["H"], case["scenario_seed"])
 
 
-def run_fuzz(name="batch_fuzz", count=64, seed=2026):
+def run_fuzz(name="batch_fuzz", count=64, seed=2026, large=False):
     """One fixture of many small random scenarios (early stop on), concatenated; meta["cases"] says how each
     slice was made (problem, degree, solver config, proposal seed / spread, SHA-256 of the proposals)."""
     parts, cases = [], []
     off = 0
-    todo = fuzz_cases(count, seed)
+    todo = fuzz_cases_large(count, seed) if large else fuzz_cases(count, seed)
     dmax = max(3 * c["n"] * (c["degree"] + 1) for c in todo)   # subset rows NaN-padded to the widest case
     for case in todo:
         doc = fuzz_doc(case)
@@ -249,6 +265,8 @@ def main(argv):
                       select={"batch": 1024, "indices": idx})
         elif which == "fuzz":   # random small scenarios with early stop (every kernel family)
             run_fuzz()
+        elif which == "fuzz_large":   # random 17..64-robot scenarios with early stop (two-lane K1, K1L)
+            run_fuzz("batch_fuzz_large", count=24, seed=4242, large=True)
         else:
             raise SystemExit(f"unknown batch {which}")
 

@@ -44,13 +44,16 @@ def test_whole_batch_matches_reference(name, precision):
     assert rep["coeff_rel_err_max"] is not None and rep["coeff_rel_err_max"] <= tol
 
 
+@pytest.mark.parametrize("name", ["batch_fuzz", "batch_fuzz_large"])
 @pytest.mark.parametrize("precision", ["strict", "hybrid"])
-def test_fuzz_scenarios_match_reference(precision):
+def test_fuzz_scenarios_match_reference(name, precision):
     """``batch_fuzz``: 64 random scenarios x 8 proposals solved by the real reference with early stop -- 2 to 40
     robots (every K1 template incl. the tensor-core n = 16 slot, the two-lane slot and K1L), horizons 20 to 127,
     degrees 7 to 15, rho 0.5 / 1 / 2, tol_residual 1e-3 to 1e-2; 443 converged, 329 feasible, 130 with pair and 12
-    with workspace violations, 70 stop at the 300-iteration cap.  The strict bar on every sample."""
-    g, o = run_fuzz(precision)
+    with workspace violations, 70 stop at the 300-iteration cap.  ``batch_fuzz_large``: 24 scenarios x 4
+    proposals of 17 to 64 robots (two-lane K1, K1L in every precision), horizons 20 to 100.  The strict bar on
+    every sample."""
+    g, o = run_fuzz(precision, name)
     rep = compare(g, o, band=1e-6)
     tol = 1e-9 if precision == "strict" else 1e-6
     assert rep["status_ok"] == rep["batch"]

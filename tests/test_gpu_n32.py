@@ -88,6 +88,30 @@ def test_full_size_config3_properties():
     assert torch.equal(alt.coeffs, out.coeffs[:300]) and torch.equal(alt.iterations, out.iterations[:300])
 
 
+@pytest.mark.parametrize("precision,n,horizon,degree", [("hybrid", 24, 150, 10), ("lean", 20, 160, 10),
+                                                        ("hybrid", 32, 127, 15)])
+def test_n32_past_one_slot_runs_on_k1l(precision, n, horizon, degree):
+    """17..32 robots where one two-lane K1 slot does not fit (more than 128 time steps, or hybrid's scratch at
+    H = 127 with degree 15): the launcher hands the batch to K1L, which matches the oracle at fixed iterations."""
+    from paper_2501_19042_b200 import SafetyFilter, SolverConfig, sample_proposals
+    from paper_2501_19042_b200.problem import load_problem
+    from paper_2501_19042_b200.scenarios import random_swarm_doc
+    doc = random_swarm_doc(n, horizon, 5)
+    prob = load_problem(doc)
+    cfg = SolverConfig(max_iters=10, early_stop=False, svars=False, precision=precision)
+    sf = SafetyFilter(prob, degree=degree, config=cfg)
+    props = sample_proposals(prob, sf.basis, 2, seed=5).proposals
+    out = sf.solve_batched(torch.from_numpy(props).cuda(), config=cfg)
+    op = sf_oracle.make_problem(doc, degree=degree)
+    rtol = 1e-5 if precision == "lean" else 1e-7
+    assert (out.status == 0).all() and out.eq_err.max().item() <= 1e-8
+    coeffs, rinf = out.coeffs.cpu().numpy(), out.residual_inf.cpu().numpy()
+    for b, x in enumerate(props):
+        r = sf_oracle.solve(op, x, max_iters=10, early_stop=False)
+        assert np.abs(coeffs[b] - r.coeffs).max() <= rtol * np.abs(r.coeffs).max(), b
+        np.testing.assert_allclose(rinf[b], r.residual_inf, rtol=1e-3, atol=1e-9)
+
+
 @pytest.mark.parametrize("precision", ["hybrid", "lean"])
 def test_n32_longest_horizon_fits_one_cta(precision):
     """32 robots at H = 127 (128 time steps, eight two-lane warps): the slot, including hybrid's

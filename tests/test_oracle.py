@@ -115,3 +115,20 @@ def test_oracle_matches_reference_fuzz_fixture():
             assert bool(so.feasible(oprob, r)) == bool(g["feasible"][i])
             checked += 1
     assert checked >= 64
+
+
+def test_fuzz_large_fixture_proposals_regenerate():
+    """``batch_fuzz_large`` (24 random 17..64-robot scenarios from the real reference): every case's proposals
+    regenerate bit for bit from its recorded sampler seed (the GPU tests re-solve them)."""
+    import hashlib
+
+    from paper_2501_19042_b200 import load_problem, sample_proposals
+    from paper_2501_19042_b200.basis import build_basis
+    g = load_golden("batch_fuzz_large")
+    assert len(g["meta"]["cases"]) == 24 and g["meta"]["batch"] == len(g["iterations"]) == 96
+    for case in g["meta"]["cases"]:
+        assert 17 <= case["n"] <= 64
+        prob = load_problem(case["problem"])
+        basis = build_basis(prob.duration, degree=case["degree"], samples=prob.horizon_samples)
+        x = sample_proposals(prob, basis, case["batch"], seed=case["seed"], spread=case["spread"]).proposals
+        assert hashlib.sha256(np.ascontiguousarray(x, dtype=np.float64).tobytes()).hexdigest() == case["proposals_sha256"]
