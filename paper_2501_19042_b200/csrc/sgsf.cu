@@ -248,23 +248,18 @@ int sgsf_solve(sgsf_handle_t* h, int batch, const double* xi_bar, const double* 
             if (n <= 4) SGSF_PICK(float, 4, 512, 1);
             else if (n <= 8) SGSF_PICK(float, 8, 384, 1);
             else if (n <= 16) SGSF_PICK(float, 16, 384, 1);
-            else {
-                SGSF_PICK(float, 32, 256, 2);
-                // 17..32 robots past one two-lane slot (H >= 128, or hybrid at H = 127 with degree > 11): K1L
-                if (rc == SGSF_ERR_UNSUPPORTED) rc = launch_large(li, p, cfg, timing, stream, false);
-            }
+            else SGSF_PICK(float, 32, 256, 2);
         } else {
             if (n <= 4) SGSF_PICK(double, 4, 384, 1);
             else if (n <= 8) SGSF_PICK(double, 8, 256, 1);
             else if (n <= 16) SGSF_PICK(double, 16, 256, 1);
-            else {
-                SGSF_PICK(double, 32, 256, 2);
-                // FP64 17..32 robots at long horizons: one K1 slot does not fit (two FP64 position buffers);
-                // K1L (one CTA of eight warps per sample, positions per step in a per-warp scratch) does
-                if (rc == SGSF_ERR_UNSUPPORTED) rc = launch_large(li, p, cfg, timing, stream, true);
-            }
+            else SGSF_PICK(double, 32, 256, 2);
         }
 #undef SGSF_PICK
+        // a K1 slot that does not fit (its two position buffers grow with the horizon: FP64 17..32 robots at
+        // H = 100, 17..32 robots past 128 time steps, long horizons in FP64): K1L, one CTA of eight warps per
+        // sample with the positions of a step in a per-warp scratch
+        if (rc == SGSF_ERR_UNSUPPORTED) rc = launch_large(li, p, cfg, timing, stream, strict);
     }
     // the feasible verdict of the returned iterates, right behind the solve on the same stream (fusing it
     // into K1's per-sample epilogue was exact but slowed the iteration loop: +3% to +15%)

@@ -89,10 +89,12 @@ def test_full_size_config3_properties():
 
 
 @pytest.mark.parametrize("precision,n,horizon,degree", [("hybrid", 24, 150, 10), ("lean", 20, 160, 10),
-                                                        ("hybrid", 32, 127, 15)])
+                                                        ("hybrid", 32, 127, 15), ("strict", 16, 260, 10),
+                                                        ("hybrid", 8, 420, 10)])
 def test_n32_past_one_slot_runs_on_k1l(precision, n, horizon, degree):
-    """17..32 robots where one two-lane K1 slot does not fit (more than 128 time steps, or hybrid's scratch at
-    H = 127 with degree 15): the launcher hands the batch to K1L, which matches the oracle at fixed iterations."""
+    """Shapes where one K1 slot does not fit -- 17..32 robots past 128 time steps or with hybrid's scratch at
+    H = 127 and degree 15; FP64 16 robots at H = 260; 8 robots past 384 time steps: the launcher hands the
+    batch to K1L, which matches the oracle at fixed iterations."""
     from paper_2501_19042_b200 import SafetyFilter, SolverConfig, sample_proposals
     from paper_2501_19042_b200.problem import load_problem
     from paper_2501_19042_b200.scenarios import random_swarm_doc
