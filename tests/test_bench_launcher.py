@@ -24,3 +24,23 @@ def test_gpus_flag_launches_ranks(config, gpus, per_gpu):
     # weak scaling for config 2 (1000 per GPU), strong for config 3 (4096 over the ranks)
     assert d["config"]["batch"] == (1000 * gpus if config == 2 else 4096)
     assert d["scaling"] == ("weak" if config == 2 else "strong")
+
+
+def test_cpu_stream_counts_until_min_samples():
+    """The CPU baseline's pool (bench.CpuStream): a slice keeps counting past its time budget until `min_samples`
+    proposals have completed (the 64-robot legs wait for a full wave), and reports the sample-iterations it saw."""
+    sys.path.insert(0, str(REPO))
+    import bench
+    from paper_2501_19042_b200 import load_problem, sample_proposals
+    from paper_2501_19042_b200.basis import build_basis
+    from paper_2501_19042_b200.scenarios import random_swarm_doc
+    doc = random_swarm_doc(2, 20, 1)
+    prob = load_problem(doc)
+    basis = build_basis(prob.duration, degree=10, samples=prob.horizon_samples)
+    props = sample_proposals(prob, basis, 4, seed=0, spread=0.6).proposals
+    stream = bench.CpuStream(doc, props, max_iters=30, cores=2)
+    try:
+        r = stream.take(0.0, min_samples=5)
+    finally:
+        stream.close()
+    assert r["samples"] >= 5 and r["sample_iterations"] >= r["samples"] and r["wall_s"] > 0
